@@ -1,0 +1,293 @@
+/*
+ * amlt_gpu.h — C-ABI of the B200 (sm_100a) backend for AMULET's
+ * matrix-multiplication-like task (MMLT):
+ *
+ *     R[i][j] (+)= sum_k body(A[i][k], B[k][j], per-column vectors[j])
+ *
+ * This is the drop-in boundary for the reference engine's executor and tuner
+ * (reference = /root/reference/proj, "amlt"). Plain C types only: pointers,
+ * sizes, enums. No CUDA, C++ or torch types appear in any signature; device
+ * buffers are passed as raw device pointers, streams as `void*`.
+ *
+ * Reference interfaces replaced (file:line in /root/reference/proj):
+ *   amlt_gpu_run_subtask       <- run_subtask(plan, kernel, ops, TileParams,
+ *                                 Bounds, Clock&, ExecLog*)
+ *                                 include/amlt/tiled_executor.hpp:42-44,
+ *                                 src/tiled_executor.cpp:9-77
+ *   amlt_gpu_adaptive_execute  <- adaptive_execute(plan, kernel, ops, Bounds,
+ *                                 pack, Clock&, ExecLog*) -> TuneReport
+ *                                 include/amlt/autotuner.hpp:68-70,
+ *                                 src/autotuner.cpp:103-151
+ *   amlt_gpu_run_host          <- run_fixed / run_adaptive over host-resident
+ *                                 MatrixBuffers (src/engine.cpp:165-175)
+ *   amlt_gpu_plan_create       <- compile_task(...) -> CompiledTask
+ *                                 (src/engine.cpp:86-102): the recognised
+ *                                 body, its leaf roles and operand layouts
+ *   amlt_body_desc             <- Mmlt + ExprDag identity (recognize.hpp:28-42,
+ *                                 expr_dag.hpp:26) reduced to the five bodies
+ *   amlt_operands / amlt_matrix<- Operands (kernel_exec.hpp:17-24) over
+ *                                 MatrixBuffer (matrix.hpp:14-59)
+ *   amlt_bounds                <- Bounds (tiled_executor.hpp:17-21)
+ *   amlt_tile_params           <- TileParams (tiled_executor.hpp:11-15)
+ *   amlt_exec_record           <- ExecRecord (tiled_executor.hpp:25-34)
+ *   amlt_trial / amlt_cover_rect / amlt_tune_report
+ *                              <- Trial / CoverRect / TuneReport
+ *                                 (autotuner.hpp:11-34)
+ *   amlt_clock_fn              <- Clock::now() (clock.hpp:12-16)
+ *   amlt_status                <- EngineError hierarchy (errors.hpp:10-60)
+ *   amlt_spr                   <- spr (engine.hpp:83-85, src/engine.cpp:212-216)
+ *
+ * Threading: one caller thread per context. Every call that
+ * returns an elapsed time is synchronous; amlt_gpu_enqueue is the
+ * asynchronous form (stream-ordered, no clock reads).
+ */
+#ifndef AMLT_GPU_H
+#define AMLT_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AMLT_GPU_ABI_VERSION 1
+
+/* Error codes; the C++ shim (amlt_gpu.hpp) rethrows the matching
+ * EngineError subclass (errors.hpp:10-60). */
+typedef enum {
+    AMLT_OK = 0,
+    AMLT_ERR_ENGINE = 1,             /* EngineError                          */
+    AMLT_ERR_UNSUPPORTED = 2,        /* UnsupportedExpression                */
+    AMLT_ERR_MISSING_BINDING = 3,    /* MissingBinding (absent aux operand)  */
+    AMLT_ERR_NO_FEASIBLE_KERNEL = 4, /* NoFeasibleKernel                     */
+    AMLT_ERR_NON_POSITIVE_TIME = 5,  /* NonPositiveTime                      */
+    AMLT_ERR_INVALID_ARGUMENT = 6,   /* bad pointer / bounds / shape         */
+    AMLT_ERR_CUDA = 7,               /* CUDA runtime error                   */
+    AMLT_ERR_NO_DEVICE = 8           /* no usable sm_100 device              */
+} amlt_status;
+
+/* The five BASELINE bodies (+ q3's threshold count):
+ *   GEMM      R += A*B                                  preset matmul
+ *   DISCOUNT  R += A*B - (A*B > T)*A*B*dis[j]           preset q1
+ *   BOOST     R += A*B + (A*B > T)*(A*B - T)            preset q2
+ *   SQDIFF    R += (A - B)*(A - B)
+ *   EQCOUNT   R += A == B
+ *   THRCOUNT  R += A*B > T                              preset q3           */
+typedef enum {
+    AMLT_BODY_GEMM = 0,
+    AMLT_BODY_DISCOUNT = 1,
+    AMLT_BODY_BOOST = 2,
+    AMLT_BODY_SQDIFF = 3,
+    AMLT_BODY_EQCOUNT = 4,
+    AMLT_BODY_THRCOUNT = 5
+} amlt_body;
+
+typedef enum { AMLT_F64 = 0, AMLT_F32 = 1, AMLT_I32 = 2 } amlt_dtype;
+
+/* MatrixBuffer storage order (matrix.hpp:10). */
+typedef enum { AMLT_ROW_MAJOR = 0, AMLT_COL_MAJOR = 1 } amlt_order;
+
+/* Statement-side operand layout (recognize.hpp:19): NORMAL is A[i][k] /
+ * B[k][j]; TRANSPOSED is A[k][i] / B[j][k]. */
+typedef enum { AMLT_LAYOUT_NORMAL = 0, AMLT_LAYOUT_TRANSPOSED = 1 } amlt_layout;
+
+/* Leaf class of the threshold operand (recognize.hpp:14). */
+typedef enum {
+    AMLT_LEAF_CONSTANT = 0,
+    AMLT_LEAF_VEC_I = 1,
+    AMLT_LEAF_VEC_J = 2,
+    AMLT_LEAF_MAT_IJ = 3
+} amlt_leaf_class;
+
+typedef struct {
+    int32_t body;        /* amlt_body                                        */
+    int32_t dtype;       /* amlt_dtype: storage AND arithmetic type           */
+    int32_t accumulate;  /* 1 for "+=", 0 for "=" (last k wins)               */
+    int32_t layout_a;    /* amlt_layout                                       */
+    int32_t layout_b;    /* amlt_layout                                       */
+    int32_t thres_class; /* amlt_leaf_class of T (DISCOUNT/BOOST/THRCOUNT)    */
+    double thres_value;  /* T when thres_class == AMLT_LEAF_CONSTANT          */
+} amlt_body_desc;
+
+/* A dense matrix in DEVICE memory, described like a MatrixBuffer: (rows,
+ * cols) are the buffer's own dimensions, `ld` its leading stride in
+ * elements (row-major: >= cols; col-major: >= rows). Vectors are len x 1. */
+typedef struct {
+    void* data;
+    int64_t rows;
+    int64_t cols;
+    int64_t ld;
+    int32_t order; /* amlt_order */
+    int32_t dtype; /* amlt_dtype; must equal the plan's dtype                 */
+} amlt_matrix;
+
+/* Operands (kernel_exec.hpp:17-24). `thres` and `dis` are the aux leaves the
+ * body names; a body that needs one which is absent -> MISSING_BINDING. */
+typedef struct {
+    amlt_matrix a;
+    amlt_matrix b;
+    amlt_matrix r;
+    amlt_matrix thres; /* data == NULL when unbound */
+    amlt_matrix dis;   /* data == NULL when unbound */
+} amlt_operands;
+
+/* Half-open index rectangle (tiled_executor.hpp:17-21). */
+typedef struct {
+    int64_t i0, i1;
+    int64_t j0, j1;
+    int64_t k0, k1;
+} amlt_bounds;
+
+/* TileParams (tiled_executor.hpp:11-15) on the GPU:
+ *   kc      K-segment depth. kc <= 0 or kc >= K: one pass over K. Otherwise
+ *           the K range is cut into ceil(K/kc) segments computed in parallel
+ *           (split-K) and added to R in ascending segment order
+ *           (deterministic), the GPU form of the reference's kc loop.
+ *   nc      column-tile width: picks the registered tile variant whose CTA
+ *           width is the largest <= nc (nc <= 0: planner default).
+ *   pack    accepted for interface parity; operands are always staged
+ *           through shared memory, so it has no effect (bit-neutral, as the
+ *           reference's packing is, acceptance c8).
+ *   variant explicit tile-variant index (>= 0) overriding nc; -1 = by nc. */
+typedef struct {
+    int64_t kc;
+    int64_t nc;
+    int32_t pack;
+    int32_t variant;
+} amlt_tile_params;
+
+/* One launch the executor made (ExecRecord, tiled_executor.hpp:25-34). */
+typedef struct {
+    int32_t variant;
+    int32_t splits; /* K segments of this dispatch */
+    int64_t i0, i1, j0, j1, k0, k1;
+} amlt_exec_record;
+
+/* Caller-owned dispatch log: the library appends while count < capacity and
+ * always increments `total`. */
+typedef struct {
+    amlt_exec_record* records;
+    int32_t capacity;
+    int32_t count;
+    int32_t total;
+} amlt_exec_log;
+
+/* Tile-variant description (the GPU analogue of KernelShape + ledger). */
+typedef struct {
+    int32_t index;
+    int32_t body;
+    int32_t dtype;
+    int32_t block_m;      /* CTA tile rows                                   */
+    int32_t block_n;      /* CTA tile columns                                */
+    int32_t block_k;      /* K depth per shared-memory stage                 */
+    int32_t thread_m;     /* register micro-tile rows per thread             */
+    int32_t thread_n;     /* register micro-tile columns per thread          */
+    int32_t threads;      /* threads per CTA                                 */
+    int32_t stages;       /* cp.async pipeline depth                         */
+    int32_t smem_bytes;   /* dynamic shared memory per CTA                   */
+    int32_t tensor_core;  /* 1: DMMA (mma.sync f64) tensor-core variant      */
+    char name[48];
+} amlt_variant_info;
+
+/* Clock seam (clock.hpp:12-16): seconds, monotonic. When given, it is read
+ * exactly twice per subtask, immediately around the synchronous GPU work
+ * (tiled_executor.cpp:40,75); when NULL, CUDA events on the context stream
+ * time the subtask. */
+typedef double (*amlt_clock_fn)(void* user);
+
+#define AMLT_MAX_TRIALS 32
+#define AMLT_MAX_COVER 64
+
+typedef struct {
+    int64_t value;  /* variant index tried                                   */
+    int64_t rows;   /* row band the trial computed (its share of the output) */
+    double elapsed; /* seconds                                               */
+    double score;   /* elapsed / rows: lower is better                       */
+} amlt_trial;
+
+/* A completed output region (CoverRect, autotuner.hpp:19-24, extended with
+ * the row range because the GPU tuner lays candidates on row bands). */
+typedef struct {
+    int64_t i0, i1;
+    int64_t k0, k1;
+    int64_t j0, j1;
+} amlt_cover_rect;
+
+typedef struct {
+    int32_t n_trials;
+    amlt_trial trials[AMLT_MAX_TRIALS];
+    int32_t best_variant;
+    int64_t best_kc;
+    int32_t tuned;      /* 0: too small to tune, ran whole with the default */
+    int32_t from_cache; /* 1: winner reused from an earlier tuning          */
+    int32_t n_cover;
+    amlt_cover_rect coverage[AMLT_MAX_COVER]; /* disjoint, union = bounds   */
+    double tuning_fraction;                   /* tuned rows / M             */
+    double total_seconds;                     /* sum over all subtasks      */
+} amlt_tune_report;
+
+typedef struct amlt_ctx amlt_ctx;
+typedef struct amlt_plan amlt_plan;
+
+/* Context flags. DRY_RUN: no device is touched; dispatches are planned,
+ * logged and "timed" through the clock seam only (tests of the host logic
+ * on machines without a GPU). Results are never produced in this mode. */
+#define AMLT_CTX_DRY_RUN 1
+
+int amlt_gpu_abi_version(void);
+
+amlt_status amlt_gpu_ctx_create(int device, int flags, amlt_ctx** out);
+void amlt_gpu_ctx_destroy(amlt_ctx* ctx);
+/* Message of the last failing call on this context (or of ctx creation when
+ * ctx == NULL). Never NULL. */
+const char* amlt_gpu_last_error(const amlt_ctx* ctx);
+/* Launch on the caller's CUDA stream (cudaStream_t as void*); NULL restores
+ * the context's own stream. */
+amlt_status amlt_gpu_set_stream(amlt_ctx* ctx, void* stream);
+/* Forget tuning winners cached by amlt_gpu_adaptive_execute. */
+void amlt_gpu_clear_tuning_cache(amlt_ctx* ctx);
+
+amlt_status amlt_gpu_plan_create(amlt_ctx* ctx, const amlt_body_desc* desc, amlt_plan** out);
+void amlt_gpu_plan_destroy(amlt_plan* plan);
+int amlt_gpu_plan_num_variants(const amlt_plan* plan);
+amlt_status amlt_gpu_plan_variant(const amlt_plan* plan, int idx, amlt_variant_info* info);
+/* Variant the planner uses when no tuning result applies. */
+int amlt_gpu_plan_default_variant(const amlt_plan* plan, int64_t M, int64_t N, int64_t K);
+
+/* run_subtask: R(bounds) (+)= body over bounds, synchronously. Returns the
+ * elapsed seconds between the two clock reads in *elapsed_s. */
+amlt_status amlt_gpu_run_subtask(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops,
+                                 const amlt_tile_params* tile, const amlt_bounds* bounds,
+                                 amlt_clock_fn clock, void* clock_user, amlt_exec_log* log,
+                                 double* elapsed_s);
+
+/* Asynchronous form of run_subtask: enqueues on the context stream and
+ * returns; no clock reads, no synchronisation. */
+amlt_status amlt_gpu_enqueue(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops,
+                             const amlt_tile_params* tile, const amlt_bounds* bounds);
+
+/* adaptive_execute: measured choice of the tile variant on row bands of the
+ * real task (each band contributes its rows of R; coverage exactly once),
+ * then the remainder with the winner. */
+amlt_status amlt_gpu_adaptive_execute(amlt_ctx* ctx, const amlt_plan* plan,
+                                      const amlt_operands* ops, const amlt_bounds* bounds,
+                                      int pack, amlt_clock_fn clock, void* clock_user,
+                                      amlt_exec_log* log, amlt_tune_report* report);
+
+/* Host-buffer entry (the reference's callers hold host MatrixBuffers):
+ * operands' `data` are HOST pointers (pinned or pageable). Copies A, B, aux
+ * and R to the device, runs (tile == NULL: adaptive; else that tile), copies
+ * R back. *elapsed_s covers copies + compute (the clock, if any, is read
+ * exactly twice around all of it). */
+amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* host_ops,
+                              const amlt_tile_params* tile, const amlt_bounds* bounds,
+                              amlt_clock_fn clock, void* clock_user, double* elapsed_s);
+
+/* Scaled processing rate M*K*N / (1e9 * seconds) (engine.cpp:212-216). */
+amlt_status amlt_spr(int64_t M, int64_t K, int64_t N, double seconds, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AMLT_GPU_H */

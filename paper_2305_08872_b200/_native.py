@@ -1,0 +1,148 @@
+"""ctypes binding of the C-ABI in ``include/amlt_gpu.h`` (lib/libamlt_gpu.so).
+
+This is the Python side of the drop-in boundary: every structure below is a
+field-for-field mirror of the header. The library is required — there is no
+CPU fallback; importing a missing or stale library raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "lib", "libamlt_gpu.so")
+
+ABI_VERSION = 1
+
+# amlt_status
+OK, ERR_ENGINE, ERR_UNSUPPORTED, ERR_MISSING_BINDING, ERR_NO_FEASIBLE_KERNEL, \
+    ERR_NON_POSITIVE_TIME, ERR_INVALID_ARGUMENT, ERR_CUDA, ERR_NO_DEVICE = range(9)
+
+# amlt_body
+BODY_GEMM, BODY_DISCOUNT, BODY_BOOST, BODY_SQDIFF, BODY_EQCOUNT, BODY_THRCOUNT = range(6)
+# amlt_dtype
+F64, F32, I32 = range(3)
+ROW_MAJOR, COL_MAJOR = 0, 1
+LAYOUT_NORMAL, LAYOUT_TRANSPOSED = 0, 1
+LEAF_CONSTANT, LEAF_VEC_I, LEAF_VEC_J, LEAF_MAT_IJ = range(4)
+CTX_DRY_RUN = 1
+MAX_TRIALS = 32
+MAX_COVER = 64
+
+
+class BodyDesc(C.Structure):
+    _fields_ = [("body", C.c_int32), ("dtype", C.c_int32), ("accumulate", C.c_int32),
+                ("layout_a", C.c_int32), ("layout_b", C.c_int32), ("thres_class", C.c_int32),
+                ("thres_value", C.c_double)]
+
+
+class Matrix(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("rows", C.c_int64), ("cols", C.c_int64),
+                ("ld", C.c_int64), ("order", C.c_int32), ("dtype", C.c_int32)]
+
+
+class OperandsC(C.Structure):
+    _fields_ = [("a", Matrix), ("b", Matrix), ("r", Matrix), ("thres", Matrix), ("dis", Matrix)]
+
+
+class BoundsC(C.Structure):
+    _fields_ = [("i0", C.c_int64), ("i1", C.c_int64), ("j0", C.c_int64), ("j1", C.c_int64),
+                ("k0", C.c_int64), ("k1", C.c_int64)]
+
+
+class TileParamsC(C.Structure):
+    _fields_ = [("kc", C.c_int64), ("nc", C.c_int64), ("pack", C.c_int32), ("variant", C.c_int32)]
+
+
+class ExecRecordC(C.Structure):
+    _fields_ = [("variant", C.c_int32), ("splits", C.c_int32), ("i0", C.c_int64),
+                ("i1", C.c_int64), ("j0", C.c_int64), ("j1", C.c_int64), ("k0", C.c_int64),
+                ("k1", C.c_int64)]
+
+
+class ExecLogC(C.Structure):
+    _fields_ = [("records", C.POINTER(ExecRecordC)), ("capacity", C.c_int32),
+                ("count", C.c_int32), ("total", C.c_int32)]
+
+
+class VariantInfoC(C.Structure):
+    _fields_ = [("index", C.c_int32), ("body", C.c_int32), ("dtype", C.c_int32),
+                ("block_m", C.c_int32), ("block_n", C.c_int32), ("block_k", C.c_int32),
+                ("thread_m", C.c_int32), ("thread_n", C.c_int32), ("threads", C.c_int32),
+                ("stages", C.c_int32), ("smem_bytes", C.c_int32), ("tensor_core", C.c_int32),
+                ("name", C.c_char * 48)]
+
+
+class TrialC(C.Structure):
+    _fields_ = [("value", C.c_int64), ("rows", C.c_int64), ("elapsed", C.c_double),
+                ("score", C.c_double)]
+
+
+class CoverRectC(C.Structure):
+    _fields_ = [("i0", C.c_int64), ("i1", C.c_int64), ("k0", C.c_int64), ("k1", C.c_int64),
+                ("j0", C.c_int64), ("j1", C.c_int64)]
+
+
+class TuneReportC(C.Structure):
+    _fields_ = [("n_trials", C.c_int32), ("trials", TrialC * MAX_TRIALS),
+                ("best_variant", C.c_int32), ("best_kc", C.c_int64), ("tuned", C.c_int32),
+                ("from_cache", C.c_int32), ("n_cover", C.c_int32),
+                ("coverage", CoverRectC * MAX_COVER), ("tuning_fraction", C.c_double),
+                ("total_seconds", C.c_double)]
+
+
+CLOCK_FN = C.CFUNCTYPE(C.c_double, C.c_void_p)
+
+EXPORTS = [
+    "amlt_gpu_abi_version", "amlt_gpu_ctx_create", "amlt_gpu_ctx_destroy", "amlt_gpu_last_error",
+    "amlt_gpu_set_stream", "amlt_gpu_clear_tuning_cache", "amlt_gpu_plan_create",
+    "amlt_gpu_plan_destroy", "amlt_gpu_plan_num_variants", "amlt_gpu_plan_variant",
+    "amlt_gpu_plan_default_variant", "amlt_gpu_run_subtask", "amlt_gpu_enqueue",
+    "amlt_gpu_adaptive_execute", "amlt_gpu_run_host", "amlt_spr",
+]
+
+_lib = None
+
+
+def lib():
+    """Loads lib/libamlt_gpu.so once. Raises if it is missing (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2305_08872_b200.build` "
+            "(there is no CPU fallback for the MMLT kernels)")
+    L = C.CDLL(LIB_PATH)
+    P = C.c_void_p
+    L.amlt_gpu_abi_version.restype = C.c_int
+    L.amlt_gpu_ctx_create.argtypes = [C.c_int, C.c_int, C.POINTER(P)]
+    L.amlt_gpu_ctx_destroy.argtypes = [P]
+    L.amlt_gpu_ctx_destroy.restype = None
+    L.amlt_gpu_last_error.argtypes = [P]
+    L.amlt_gpu_last_error.restype = C.c_char_p
+    L.amlt_gpu_set_stream.argtypes = [P, P]
+    L.amlt_gpu_clear_tuning_cache.argtypes = [P]
+    L.amlt_gpu_clear_tuning_cache.restype = None
+    L.amlt_gpu_plan_create.argtypes = [P, C.POINTER(BodyDesc), C.POINTER(P)]
+    L.amlt_gpu_plan_destroy.argtypes = [P]
+    L.amlt_gpu_plan_destroy.restype = None
+    L.amlt_gpu_plan_num_variants.argtypes = [P]
+    L.amlt_gpu_plan_variant.argtypes = [P, C.c_int, C.POINTER(VariantInfoC)]
+    L.amlt_gpu_plan_default_variant.argtypes = [P, C.c_int64, C.c_int64, C.c_int64]
+    L.amlt_gpu_run_subtask.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(TileParamsC),
+                                       C.POINTER(BoundsC), CLOCK_FN, P, C.POINTER(ExecLogC),
+                                       C.POINTER(C.c_double)]
+    L.amlt_gpu_enqueue.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(TileParamsC),
+                                   C.POINTER(BoundsC)]
+    L.amlt_gpu_adaptive_execute.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(BoundsC),
+                                            C.c_int, CLOCK_FN, P, C.POINTER(ExecLogC),
+                                            C.POINTER(TuneReportC)]
+    L.amlt_gpu_run_host.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(TileParamsC),
+                                    C.POINTER(BoundsC), CLOCK_FN, P, C.POINTER(C.c_double)]
+    L.amlt_spr.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_double, C.POINTER(C.c_double)]
+    v = L.amlt_gpu_abi_version()
+    if v != ABI_VERSION:
+        raise ImportError(f"libamlt_gpu ABI {v} != expected {ABI_VERSION}; rebuild")
+    _lib = L
+    return L

@@ -1,0 +1,830 @@
+// amlt_gpu.cu — host side of the C-ABI in include/amlt_gpu.h.
+//
+// The executor (run_subtask), the runtime tuner (adaptive_execute) and the
+// host-buffer entry of the B200 backend. Reference counterparts:
+//   run_subtask        src/tiled_executor.cpp:9-77
+//   adaptive_execute   src/autotuner.cpp:103-151 (find_kc :18-68, find_nc :70-101)
+//   run_fixed/run_adaptive over host buffers   src/engine.cpp:165-175
+// Errors are C++ exceptions internally (mirroring errors.hpp:10-60) and are
+// mapped to amlt_status at the C boundary; the message is kept per context.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/amlt_gpu.h"
+#include "variants.h"
+
+using namespace amltk;
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// errors (errors.hpp:10-60)
+
+struct EngineError : std::runtime_error {
+    amlt_status code;
+    EngineError(amlt_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void fail(amlt_status c, const std::string& m) { throw EngineError(c, m); }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(AMLT_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+thread_local std::string g_create_error = "";
+
+const char* body_name(int b) {
+    switch (b) {
+        case AMLT_BODY_GEMM: return "gemm";
+        case AMLT_BODY_DISCOUNT: return "discount";
+        case AMLT_BODY_BOOST: return "boost";
+        case AMLT_BODY_SQDIFF: return "sqdiff";
+        case AMLT_BODY_EQCOUNT: return "eqcount";
+        case AMLT_BODY_THRCOUNT: return "thrcount";
+    }
+    return "?";
+}
+const char* dtype_name(int d) { return d == AMLT_F64 ? "f64" : d == AMLT_F32 ? "f32" : "i32"; }
+int dtype_size(int d) { return d == AMLT_F64 ? 8 : 4; }
+
+// ---------------------------------------------------------------------------
+// registry of compiled variants (variants.h)
+
+const Registry& registry() {
+    static Registry reg;
+    static std::once_flag once;
+    std::call_once(once, [] { register_all(reg); });
+    return reg;
+}
+
+const BodyAux* find_aux(int body, int dtype) {
+    for (const auto& a : registry().aux)
+        if (a.body == body && a.dtype == dtype) return &a;
+    return nullptr;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// context and plan
+
+struct amlt_ctx {
+    int device = 0;
+    int flags = 0;
+    int num_sms = 148;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    void* work = nullptr;
+    size_t work_bytes = 0;
+    // device staging for amlt_gpu_run_host
+    void* hbuf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    size_t hbuf_bytes[5] = {0, 0, 0, 0, 0};
+    std::vector<int> occupancy;  // resident CTAs per SM, per registry variant
+    // tuning winners: (body, dtype, M, N, K) -> variant index
+    std::map<std::tuple<int, int, int64_t, int64_t, int64_t>, int> tune_cache;
+    std::string err;
+    bool dry() const { return (flags & AMLT_CTX_DRY_RUN) != 0; }
+};
+
+struct amlt_plan {
+    amlt_body_desc desc{};
+    std::vector<int> variants;  // registry indices usable for this body/dtype
+    const BodyAux* aux = nullptr;
+    const amlt_ctx* ctx = nullptr;
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// operand validation (the GPU analogue of make_operands / find_aux,
+// src/engine.cpp:153-163, src/kernel_exec.cpp:48-52)
+
+struct Resolved {
+    KParams kp{};
+    int64_t M = 0, N = 0, K = 0;
+    bool aligned = true;  // 16-byte staging possible
+};
+
+// Element (r, c) of a statement operand with the given layout: returns the
+// pointer of element (r0, c0) plus the strides along r and c, in elements.
+void stmt_addr(const amlt_matrix& m, int layout, int64_t r0, int64_t c0, const char* what,
+               char** ptr, int64_t* sr, int64_t* sc) {
+    // statement (r, c) -> buffer (row, col)
+    const bool tr = layout == AMLT_LAYOUT_TRANSPOSED;
+    const int64_t brow = tr ? c0 : r0, bcol = tr ? r0 : c0;
+    const int64_t es = dtype_size(m.dtype);
+    const bool rowmaj = m.order == AMLT_ROW_MAJOR;
+    const int64_t step_rows = rowmaj ? m.ld : 1;  // buffer row step
+    const int64_t step_cols = rowmaj ? 1 : m.ld;
+    *ptr = static_cast<char*>(m.data) + (brow * step_rows + bcol * step_cols) * es;
+    *sr = tr ? step_cols : step_rows;
+    *sc = tr ? step_rows : step_cols;
+    (void)what;
+}
+
+void check_matrix(const amlt_matrix& m, int dtype, const char* what) {
+    if (!m.data) fail(AMLT_ERR_MISSING_BINDING, std::string("missing binding for '") + what + "'");
+    if (m.dtype != dtype)
+        fail(AMLT_ERR_INVALID_ARGUMENT, std::string(what) + " has dtype " + dtype_name(m.dtype) +
+                                            ", plan expects " + dtype_name(dtype));
+    if (m.rows < 0 || m.cols < 0) fail(AMLT_ERR_INVALID_ARGUMENT, std::string(what) + ": negative shape");
+    const int64_t minld = m.order == AMLT_ROW_MAJOR ? m.cols : m.rows;
+    if (m.ld < std::max<int64_t>(minld, 1))
+        fail(AMLT_ERR_INVALID_ARGUMENT, std::string(what) + ": leading dimension too small");
+}
+
+Resolved resolve(const amlt_plan* plan, const amlt_operands* ops, const amlt_bounds* b) {
+    const amlt_body_desc& d = plan->desc;
+    Resolved rv;
+    KParams& kp = rv.kp;
+    if (!ops || !b) fail(AMLT_ERR_INVALID_ARGUMENT, "null operands or bounds");
+    rv.M = b->i1 - b->i0;
+    rv.N = b->j1 - b->j0;
+    rv.K = b->k1 - b->k0;
+    if (rv.M < 0 || rv.N < 0 || rv.K < 0 || b->i0 < 0 || b->j0 < 0 || b->k0 < 0)
+        fail(AMLT_ERR_INVALID_ARGUMENT, "bounds must be non-negative half-open ranges");
+    check_matrix(ops->a, d.dtype, "A");
+    check_matrix(ops->b, d.dtype, "B");
+    check_matrix(ops->r, d.dtype, "R");
+    const bool at = d.layout_a == AMLT_LAYOUT_TRANSPOSED, bt = d.layout_b == AMLT_LAYOUT_TRANSPOSED;
+    // statement extents of each operand
+    const int64_t a_i = at ? ops->a.cols : ops->a.rows, a_k = at ? ops->a.rows : ops->a.cols;
+    const int64_t b_k = bt ? ops->b.cols : ops->b.rows, b_j = bt ? ops->b.rows : ops->b.cols;
+    if (b->i1 > a_i || b->k1 > a_k || b->k1 > b_k || b->j1 > b_j || b->i1 > ops->r.rows ||
+        b->j1 > ops->r.cols)
+        fail(AMLT_ERR_INVALID_ARGUMENT, "bounds exceed an operand's extent");
+
+    char *pa, *pb, *pr;
+    int64_t sai, sak, sbk, sbj, sri, srj;
+    stmt_addr(ops->a, d.layout_a, b->i0, b->k0, "A", &pa, &sai, &sak);
+    stmt_addr(ops->b, d.layout_b, b->k0, b->j0, "B", &pb, &sbk, &sbj);
+    stmt_addr(ops->r, AMLT_LAYOUT_NORMAL, b->i0, b->j0, "R", &pr, &sri, &srj);
+    // The staged kernels read A along k and B/R along j contiguously.
+    if (sak != 1 && rv.K > 1)
+        fail(AMLT_ERR_UNSUPPORTED, "A operand with non-contiguous k (A[k][i] row-major or "
+                                   "A[i][k] col-major) is not supported by the GPU kernels yet");
+    if (sbj != 1 && rv.N > 1)
+        fail(AMLT_ERR_UNSUPPORTED, "B operand with non-contiguous j (B[j][k] row-major or "
+                                   "B[k][j] col-major) is not supported by the GPU kernels yet");
+    if (srj != 1 && rv.N > 1)
+        fail(AMLT_ERR_UNSUPPORTED, "column-major R is not supported by the GPU kernels yet");
+    kp.A = pa;
+    kp.B = pb;
+    kp.R = pr;
+    kp.lda = sai;
+    kp.ldb = sbk;
+    kp.ldr = sri;
+    kp.M = rv.M;
+    kp.N = rv.N;
+    kp.K = rv.K;
+
+    // aux leaves
+    const bool needs_t = d.body == AMLT_BODY_DISCOUNT || d.body == AMLT_BODY_BOOST ||
+                         d.body == AMLT_BODY_THRCOUNT;
+    const bool needs_d = d.body == AMLT_BODY_DISCOUNT;
+    kp.thres = nullptr;
+    kp.tconst = d.thres_value;
+    if (needs_t && d.thres_class == AMLT_LEAF_CONSTANT && ops->thres.data) {
+        // named scalar threshold (a 1 x 1 buffer): broadcast from device memory
+        check_matrix(ops->thres, d.dtype, "thres");
+        kp.thres = ops->thres.data;
+        kp.t_sj = 0;
+    } else if (needs_t && d.thres_class != AMLT_LEAF_CONSTANT) {
+        if (d.thres_class != AMLT_LEAF_VEC_J)
+            fail(AMLT_ERR_UNSUPPORTED,
+                 "threshold operands indexed [i] or [i][j] are not supported by the GPU kernels yet");
+        check_matrix(ops->thres, d.dtype, "thres");
+        const amlt_matrix& t = ops->thres;
+        // VecJ leaves are N x 1 buffers (kernel_exec.hpp:13-16)
+        if (t.rows * t.cols < b->j1) fail(AMLT_ERR_INVALID_ARGUMENT, "thres shorter than j1");
+        const int64_t step = (t.cols == 1) ? (t.order == AMLT_ROW_MAJOR ? t.ld : 1)
+                                           : (t.order == AMLT_ROW_MAJOR ? 1 : t.ld);
+        kp.thres = static_cast<const char*>(t.data) + b->j0 * step * dtype_size(d.dtype);
+        kp.t_sj = step;
+    }
+    kp.dis = nullptr;
+    if (needs_d) {
+        check_matrix(ops->dis, d.dtype, "dis");
+        const amlt_matrix& t = ops->dis;
+        if (t.rows * t.cols < b->j1) fail(AMLT_ERR_INVALID_ARGUMENT, "dis shorter than j1");
+        const int64_t step = (t.cols == 1) ? (t.order == AMLT_ROW_MAJOR ? t.ld : 1)
+                                           : (t.order == AMLT_ROW_MAJOR ? 1 : t.ld);
+        kp.dis = static_cast<const char*>(t.data) + b->j0 * step * dtype_size(d.dtype);
+        kp.d_sj = step;
+    }
+
+    const int es = dtype_size(d.dtype);
+    const int vn = 16 / es;
+    auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    rv.aligned = al16(kp.A) && al16(kp.B) && (kp.lda % vn == 0 || rv.M <= 1) &&
+                 (kp.ldb % vn == 0 || rv.K <= 1);
+    kp.r_vec_ok = al16(kp.R) && (kp.ldr % vn == 0 || rv.M <= 1);
+    return rv;
+}
+
+// ---------------------------------------------------------------------------
+// variant choice
+
+const VariantDesc& vdesc(int idx) { return registry().variants.at(static_cast<size_t>(idx)); }
+
+int64_t ctas_for(const VariantDesc& v, int64_t M, int64_t N) {
+    return ((M + v.bm - 1) / v.bm) * ((N + v.bn - 1) / v.bn);
+}
+
+// The planner's default: the largest tile that still fills every SM with at
+// least two resident CTAs' worth of work; otherwise the variant with the most
+// CTAs per wave slot (smallest tile).
+int default_variant(const amlt_ctx* ctx, const amlt_plan* plan, int64_t M, int64_t N, bool aligned) {
+    int best = -1;
+    double best_key = -1;
+    int fallback = -1;
+    double fb_key = 1e300;
+    for (int idx : plan->variants) {
+        const VariantDesc& v = vdesc(idx);
+        if (v.vec != aligned) continue;
+        if (v.tc) continue;
+        const int occ = ctx && !ctx->occupancy.empty() ? std::max(1, ctx->occupancy[idx]) : v.minb;
+        const int sms = ctx ? ctx->num_sms : 148;
+        const double waves = double(ctas_for(v, M, N)) / double(sms * occ);
+        const double area = double(v.bm) * v.bn;
+        if (waves >= 2.0) {
+            if (area > best_key) {
+                best_key = area;
+                best = idx;
+            }
+        }
+        if (area < fb_key) {
+            fb_key = area;
+            fallback = idx;
+        }
+    }
+    if (best >= 0) return best;
+    if (fallback >= 0) return fallback;
+    fail(AMLT_ERR_NO_FEASIBLE_KERNEL, std::string("no compiled tile variant for ") +
+                                          body_name(plan->desc.body) + "/" +
+                                          dtype_name(plan->desc.dtype));
+}
+
+int choose_variant(const amlt_ctx* ctx, const amlt_plan* plan, const amlt_tile_params* tile,
+                   const Resolved& rv) {
+    if (tile && tile->variant >= 0) {
+        if (tile->variant >= (int)plan->variants.size())
+            fail(AMLT_ERR_INVALID_ARGUMENT, "tile variant index out of range");
+        int idx = plan->variants[static_cast<size_t>(tile->variant)];
+        if (vdesc(idx).vec && !rv.aligned)
+            fail(AMLT_ERR_INVALID_ARGUMENT,
+                 "variant needs 16-byte aligned operands with vector-multiple strides");
+        return idx;
+    }
+    if (tile && tile->nc > 0) {
+        int best = -1;
+        for (int idx : plan->variants) {
+            const VariantDesc& v = vdesc(idx);
+            if (v.vec != rv.aligned || v.tc) continue;
+            if (v.bn > tile->nc) continue;
+            if (best < 0 || v.bn > vdesc(best).bn ||
+                (v.bn == vdesc(best).bn && v.bm * v.tm > vdesc(best).bm * vdesc(best).tm))
+                best = idx;
+        }
+        if (best >= 0) return best;
+    }
+    return default_variant(ctx, plan, rv.M, rv.N, rv.aligned);
+}
+
+int plan_local_index(const amlt_plan* plan, int reg_idx) {
+    for (size_t i = 0; i < plan->variants.size(); ++i)
+        if (plan->variants[i] == reg_idx) return static_cast<int>(i);
+    return -1;
+}
+
+// ---------------------------------------------------------------------------
+// launch
+
+void ensure_work(amlt_ctx* ctx, size_t bytes) {
+    if (bytes <= ctx->work_bytes) return;
+    if (ctx->work) cudaFree(ctx->work);
+    ctx->work = nullptr;
+    ctx->work_bytes = 0;
+    cuda_check(cudaMalloc(&ctx->work, bytes), "cudaMalloc(split-K workspace)");
+    ctx->work_bytes = bytes;
+}
+
+struct Dispatch {
+    int variant = -1;
+    int splits = 1;
+    int64_t kslice = 0;
+};
+
+Dispatch plan_dispatch(const amlt_ctx* ctx, const amlt_plan* plan, const amlt_tile_params* tile,
+                       const Resolved& rv) {
+    Dispatch dp;
+    dp.variant = choose_variant(ctx, plan, tile, rv);
+    dp.kslice = rv.K;
+    if (tile && tile->kc > 0 && tile->kc < rv.K) {
+        dp.splits = static_cast<int>((rv.K + tile->kc - 1) / tile->kc);
+        dp.kslice = tile->kc;
+        if (dp.splits > 65535) fail(AMLT_ERR_INVALID_ARGUMENT, "kc too small: more than 65535 K segments");
+    }
+    return dp;
+}
+
+void enqueue(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch& dp) {
+    if (rv.M == 0 || rv.N == 0) return;
+    if (rv.K == 0) return;  // empty k range: R untouched
+    if (ctx->dry()) return;
+    KParams kp = rv.kp;
+    if (!plan->desc.accumulate) {
+        // "=": only the last k term reaches R.
+        const int64_t total = rv.M * rv.N;
+        const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 32));
+        cuda_check(plan->aux->assign(kp, dim3(blocks), ctx->stream), "assign kernel launch");
+        return;
+    }
+    const VariantDesc& v = vdesc(dp.variant);
+    kp.tiles_m = static_cast<int32_t>((rv.M + v.bm - 1) / v.bm);
+    kp.tiles_n = static_cast<int32_t>((rv.N + v.bn - 1) / v.bn);
+    const int64_t tiles = int64_t(kp.tiles_m) * kp.tiles_n;
+    if (tiles > 0x7fffffffLL) fail(AMLT_ERR_INVALID_ARGUMENT, "problem too large for one launch");
+    kp.splits = dp.splits;
+    kp.kslice = dp.kslice;
+    kp.work = nullptr;
+    if (dp.splits > 1) {
+        ensure_work(ctx, size_t(dp.splits) * size_t(rv.M) * size_t(rv.N) * dtype_size(plan->desc.dtype));
+        kp.work = ctx->work;
+    }
+    cuda_check(v.launch(kp, dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(dp.splits)),
+                        ctx->stream),
+               "tile kernel launch");
+    if (dp.splits > 1) {
+        const int64_t total = rv.M * rv.N;
+        const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+        cuda_check(plan->aux->reduce(kp, dim3(blocks), ctx->stream), "split-K reduce launch");
+    }
+}
+
+void log_dispatch(amlt_exec_log* log, const amlt_plan* plan, const Dispatch& dp,
+                  const amlt_bounds& b) {
+    if (!log) return;
+    if (log->records && log->count < log->capacity) {
+        amlt_exec_record& r = log->records[log->count++];
+        r.variant = plan_local_index(plan, dp.variant);
+        r.splits = dp.splits;
+        r.i0 = b.i0; r.i1 = b.i1; r.j0 = b.j0; r.j1 = b.j1; r.k0 = b.k0; r.k1 = b.k1;
+    }
+    log->total++;
+}
+
+// One synchronous subtask, timed like run_subtask: exactly two clock reads
+// around the work when a clock is given, CUDA events otherwise.
+double timed_subtask(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch& dp,
+                     const amlt_bounds& b, amlt_clock_fn clock, void* user, amlt_exec_log* log) {
+    double el = 0.0;
+    if (clock) {
+        const double t0 = clock(user);
+        enqueue(ctx, plan, rv, dp);
+        if (!ctx->dry()) cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+        const double t1 = clock(user);
+        el = t1 - t0;
+    } else if (ctx->dry()) {
+        el = 0.0;
+    } else {
+        cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
+        enqueue(ctx, plan, rv, dp);
+        cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
+        cuda_check(cudaEventSynchronize(ctx->ev1), "cudaEventSynchronize");
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "cudaEventElapsedTime");
+        el = ms * 1e-3;
+    }
+    log_dispatch(log, plan, dp, b);
+    return el;
+}
+
+Resolved resolve_sub(const amlt_plan* plan, const amlt_operands* ops, const amlt_bounds& b) {
+    return resolve(plan, ops, &b);
+}
+
+// ---------------------------------------------------------------------------
+// adaptive execution (autotuner.cpp:103-151, re-derived for a GPU)
+//
+// Candidates are the plan's tile variants (+ split-K forms when the output is
+// too small to fill the GPU). Each candidate runs ONE row band of the real
+// task (full N, full K), large enough to keep every SM busy for >= 2 waves,
+// and is scored by elapsed / rows. The rest of the rows run with the winner.
+// Every band writes its rows of R, so no work is repeated, and the coverage
+// ledger proves every output is produced exactly once. A problem too small to
+// give each candidate a full band runs whole with the planner default (or a
+// winner cached from an earlier tuning of the same shape), like the
+// reference's untuned small-task path (autotuner.cpp:112-122).
+
+void add_cover(amlt_tune_report* rep, const amlt_bounds& b) {
+    if (rep->n_cover < AMLT_MAX_COVER) {
+        amlt_cover_rect& c = rep->coverage[rep->n_cover++];
+        c.i0 = b.i0; c.i1 = b.i1; c.j0 = b.j0; c.j1 = b.j1; c.k0 = b.k0; c.k1 = b.k1;
+    }
+}
+
+void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, const amlt_bounds& b,
+              amlt_clock_fn clock, void* user, amlt_exec_log* log, amlt_tune_report* rep) {
+    std::memset(rep, 0, sizeof(*rep));
+    rep->best_variant = -1;
+    Resolved whole = resolve(plan, ops, &b);
+    const auto key = std::make_tuple(plan->desc.body, plan->desc.dtype, whole.M, whole.N, whole.K);
+
+    // candidate list
+    std::vector<int> cands;
+    for (int idx : plan->variants) {
+        const VariantDesc& v = vdesc(idx);
+        if (v.vec == whole.aligned && (!v.tc || whole.aligned)) cands.push_back(idx);
+    }
+    // band height per candidate: >= 2 full waves of CTAs across all SMs
+    std::vector<int64_t> band(cands.size());
+    int64_t need = 0;
+    for (size_t c = 0; c < cands.size(); ++c) {
+        const VariantDesc& v = vdesc(cands[c]);
+        const int occ = ctx->occupancy.empty() ? v.minb : std::max(1, ctx->occupancy[cands[c]]);
+        const int64_t tiles_n = (whole.N + v.bn - 1) / v.bn;
+        const int64_t want_ctas = int64_t(2) * ctx->num_sms * occ;
+        const int64_t tiles_m = std::max<int64_t>(1, (want_ctas + tiles_n - 1) / tiles_n);
+        band[c] = tiles_m * v.bm;
+        need += band[c];
+    }
+    const bool tunable = plan->desc.accumulate && !cands.empty() && whole.K > 0 && whole.N > 0 &&
+                         need * 4 <= whole.M;  // tuning <= 25% of the rows
+
+    auto run_rect = [&](const amlt_bounds& rb, int variant, int64_t kc) {
+        amlt_tile_params tp{kc, 0, 0, plan_local_index(plan, variant)};
+        Resolved rv = resolve_sub(plan, ops, rb);
+        Dispatch dp = plan_dispatch(ctx, plan, &tp, rv);
+        double el = timed_subtask(ctx, plan, rv, dp, rb, clock, user, log);
+        rep->total_seconds += el;
+        add_cover(rep, rb);
+        return el;
+    };
+
+    if (!tunable) {
+        rep->tuned = 0;
+        auto it = ctx->tune_cache.find(key);
+        int v;
+        int64_t kc = 0;
+        if (it != ctx->tune_cache.end()) {
+            v = it->second;
+            rep->from_cache = 1;
+        } else if (!plan->desc.accumulate) {
+            v = plan->variants.empty() ? -1 : plan->variants[0];
+        } else {
+            v = default_variant(ctx, plan, whole.M, whole.N, whole.aligned);
+            // Output too small to fill the GPU: split K so every SM has work
+            // (per-segment partials are reduced in order: deterministic).
+            const VariantDesc& vd = vdesc(v);
+            const int occ = ctx->occupancy.empty() ? vd.minb : std::max(1, ctx->occupancy[v]);
+            const int64_t ctas = ctas_for(vd, whole.M, whole.N);
+            const int64_t slots = int64_t(ctx->num_sms) * occ;
+            if (ctas > 0 && ctas < slots && whole.K >= 512) {
+                int64_t splits = std::min<int64_t>((slots + ctas - 1) / ctas, whole.K / 256);
+                if (splits > 1) kc = (whole.K + splits - 1) / splits;
+            }
+        }
+        rep->best_variant = v >= 0 ? plan_local_index(plan, v) : -1;
+        rep->best_kc = kc > 0 ? kc : whole.K;
+        if (whole.M > 0 && whole.N > 0) run_rect(b, v < 0 ? plan->variants[0] : v, kc);
+        else add_cover(rep, b);
+        rep->tuning_fraction = 0.0;
+        return;
+    }
+
+    rep->tuned = 1;
+    int64_t cur = b.i0;
+    int best = -1;
+    double best_score = 0.0;
+    for (size_t c = 0; c < cands.size() && rep->n_trials < AMLT_MAX_TRIALS; ++c) {
+        amlt_bounds rb{cur, cur + band[c], b.j0, b.j1, b.k0, b.k1};
+        double el = run_rect(rb, cands[c], 0);
+        amlt_trial& t = rep->trials[rep->n_trials++];
+        t.value = plan_local_index(plan, cands[c]);
+        t.rows = band[c];
+        t.elapsed = el;
+        t.score = el / double(band[c]);
+        if (best < 0 || t.score < best_score) {
+            best = cands[c];
+            best_score = t.score;
+        }
+        cur += band[c];
+    }
+    rep->best_variant = plan_local_index(plan, best);
+    rep->best_kc = whole.K;
+    rep->tuning_fraction = double(cur - b.i0) / double(whole.M);
+    ctx->tune_cache[key] = best;
+    if (cur < b.i1) run_rect(amlt_bounds{cur, b.i1, b.j0, b.j1, b.k0, b.k1}, best, 0);
+}
+
+// ---------------------------------------------------------------------------
+// boundary helpers
+
+template <class F>
+amlt_status guarded(amlt_ctx* ctx, F&& f) {
+    try {
+        f();
+        if (ctx) ctx->err.clear();
+        return AMLT_OK;
+    } catch (const EngineError& e) {
+        if (ctx) ctx->err = e.what();
+        else g_create_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        else g_create_error = e.what();
+        return AMLT_ERR_ENGINE;
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+
+extern "C" {
+
+int amlt_gpu_abi_version(void) { return AMLT_GPU_ABI_VERSION; }
+
+const char* amlt_gpu_last_error(const amlt_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+amlt_status amlt_gpu_ctx_create(int device, int flags, amlt_ctx** out) {
+    if (!out) return AMLT_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    amlt_ctx* ctx = new amlt_ctx();
+    ctx->device = device;
+    ctx->flags = flags;
+    const auto& reg = registry();
+    amlt_status st = guarded(nullptr, [&] {
+        if (ctx->dry()) {
+            ctx->occupancy.assign(reg.variants.size(), 0);
+            for (size_t i = 0; i < reg.variants.size(); ++i) ctx->occupancy[i] = reg.variants[i].minb;
+            return;
+        }
+        int n = 0;
+        cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess || n == 0)
+            fail(AMLT_ERR_NO_DEVICE, std::string("no CUDA device: ") + cudaGetErrorString(e));
+        if (device < 0 || device >= n) fail(AMLT_ERR_NO_DEVICE, "device index out of range");
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major != 10 || prop.minor != 0)
+            fail(AMLT_ERR_NO_DEVICE, std::string("device is sm_") + std::to_string(prop.major) +
+                                         std::to_string(prop.minor) +
+                                         "; this build targets sm_100a (B200) only");
+        ctx->num_sms = prop.multiProcessorCount;
+        cuda_check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        ctx->stream = ctx->own_stream;
+        cuda_check(cudaEventCreate(&ctx->ev0), "cudaEventCreate");
+        cuda_check(cudaEventCreate(&ctx->ev1), "cudaEventCreate");
+        // Load every kernel now (lazy module loading would otherwise charge
+        // the first tuning trial) and size its occupancy.
+        ctx->occupancy.assign(reg.variants.size(), 1);
+        for (size_t i = 0; i < reg.variants.size(); ++i) {
+            const VariantDesc& v = reg.variants[i];
+            cuda_check(cudaFuncSetAttribute(v.func, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem),
+                       "cudaFuncSetAttribute");
+            int occ = 0;
+            cuda_check(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, v.func, v.threads, v.smem),
+                       "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+            if (occ < 1) fail(AMLT_ERR_NO_FEASIBLE_KERNEL, std::string("variant ") + v.name + " cannot be resident");
+            ctx->occupancy[i] = occ;
+        }
+        for (const auto& a : reg.aux) {
+            cudaFuncAttributes fa;
+            cuda_check(cudaFuncGetAttributes(&fa, a.assign_func), "cudaFuncGetAttributes");
+            cuda_check(cudaFuncGetAttributes(&fa, a.reduce_func), "cudaFuncGetAttributes");
+        }
+    });
+    if (st != AMLT_OK) {
+        if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+        delete ctx;
+        return st;
+    }
+    *out = ctx;
+    return AMLT_OK;
+}
+
+void amlt_gpu_ctx_destroy(amlt_ctx* ctx) {
+    if (!ctx) return;
+    if (!ctx->dry()) {
+        cudaSetDevice(ctx->device);
+        if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
+        if (ctx->work) cudaFree(ctx->work);
+        for (void* p : ctx->hbuf)
+            if (p) cudaFree(p);
+        if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+        if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+        if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    }
+    delete ctx;
+}
+
+amlt_status amlt_gpu_set_stream(amlt_ctx* ctx, void* stream) {
+    if (!ctx) return AMLT_ERR_INVALID_ARGUMENT;
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return AMLT_OK;
+}
+
+void amlt_gpu_clear_tuning_cache(amlt_ctx* ctx) {
+    if (ctx) ctx->tune_cache.clear();
+}
+
+amlt_status amlt_gpu_plan_create(amlt_ctx* ctx, const amlt_body_desc* desc, amlt_plan** out) {
+    if (!ctx || !desc || !out) return AMLT_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    amlt_plan* plan = new amlt_plan();
+    amlt_status st = guarded(ctx, [&] {
+        const amlt_body_desc& d = *desc;
+        if (d.body < AMLT_BODY_GEMM || d.body > AMLT_BODY_THRCOUNT)
+            fail(AMLT_ERR_UNSUPPORTED, "unknown body " + std::to_string(d.body));
+        if (d.dtype < AMLT_F64 || d.dtype > AMLT_I32)
+            fail(AMLT_ERR_INVALID_ARGUMENT, "unknown dtype " + std::to_string(d.dtype));
+        if ((d.layout_a != AMLT_LAYOUT_NORMAL && d.layout_a != AMLT_LAYOUT_TRANSPOSED) ||
+            (d.layout_b != AMLT_LAYOUT_NORMAL && d.layout_b != AMLT_LAYOUT_TRANSPOSED))
+            fail(AMLT_ERR_INVALID_ARGUMENT, "unknown operand layout");
+        plan->desc = d;
+        plan->ctx = ctx;
+        plan->aux = find_aux(d.body, d.dtype);
+        if (!plan->aux)
+            fail(AMLT_ERR_UNSUPPORTED, std::string("no GPU kernel for body ") + body_name(d.body) +
+                                           " in " + dtype_name(d.dtype));
+        const auto& reg = registry();
+        for (size_t i = 0; i < reg.variants.size(); ++i)
+            if (reg.variants[i].body == d.body && reg.variants[i].dtype == d.dtype)
+                plan->variants.push_back(static_cast<int>(i));
+        if (plan->variants.empty())
+            fail(AMLT_ERR_NO_FEASIBLE_KERNEL, "no tile variant compiled for this body/dtype");
+    });
+    if (st != AMLT_OK) {
+        delete plan;
+        return st;
+    }
+    *out = plan;
+    return AMLT_OK;
+}
+
+void amlt_gpu_plan_destroy(amlt_plan* plan) { delete plan; }
+
+int amlt_gpu_plan_num_variants(const amlt_plan* plan) {
+    return plan ? static_cast<int>(plan->variants.size()) : 0;
+}
+
+amlt_status amlt_gpu_plan_variant(const amlt_plan* plan, int idx, amlt_variant_info* info) {
+    if (!plan || !info || idx < 0 || idx >= (int)plan->variants.size()) return AMLT_ERR_INVALID_ARGUMENT;
+    const VariantDesc& v = vdesc(plan->variants[static_cast<size_t>(idx)]);
+    std::memset(info, 0, sizeof(*info));
+    info->index = idx;
+    info->body = v.body;
+    info->dtype = v.dtype;
+    info->block_m = v.bm;
+    info->block_n = v.bn;
+    info->block_k = v.bk;
+    info->thread_m = v.tm;
+    info->thread_n = v.tn;
+    info->threads = v.threads;
+    info->stages = v.stages;
+    info->smem_bytes = v.smem;
+    info->tensor_core = v.tc ? 1 : 0;
+    std::snprintf(info->name, sizeof(info->name), "%s_%s_%dx%d_%s", body_name(v.body),
+                  dtype_name(v.dtype), v.bm, v.bn, v.name);
+    return AMLT_OK;
+}
+
+int amlt_gpu_plan_default_variant(const amlt_plan* plan, int64_t M, int64_t N, int64_t K) {
+    (void)K;
+    if (!plan) return -1;
+    try {
+        return plan_local_index(plan, default_variant(plan->ctx, plan, M, N, true));
+    } catch (...) {
+        return -1;
+    }
+}
+
+amlt_status amlt_gpu_run_subtask(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops,
+                                 const amlt_tile_params* tile, const amlt_bounds* bounds,
+                                 amlt_clock_fn clock, void* clock_user, amlt_exec_log* log,
+                                 double* elapsed_s) {
+    if (!ctx || !plan) return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (!ctx->dry()) cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        Resolved rv = resolve(plan, ops, bounds);
+        Dispatch dp = plan_dispatch(ctx, plan, tile, rv);
+        double el = timed_subtask(ctx, plan, rv, dp, *bounds, clock, clock_user, log);
+        if (elapsed_s) *elapsed_s = el;
+    });
+}
+
+amlt_status amlt_gpu_enqueue(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops,
+                             const amlt_tile_params* tile, const amlt_bounds* bounds) {
+    if (!ctx || !plan) return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        Resolved rv = resolve(plan, ops, bounds);
+        Dispatch dp = plan_dispatch(ctx, plan, tile, rv);
+        enqueue(ctx, plan, rv, dp);
+    });
+}
+
+amlt_status amlt_gpu_adaptive_execute(amlt_ctx* ctx, const amlt_plan* plan,
+                                      const amlt_operands* ops, const amlt_bounds* bounds,
+                                      int pack, amlt_clock_fn clock, void* clock_user,
+                                      amlt_exec_log* log, amlt_tune_report* report) {
+    (void)pack;
+    if (!ctx || !plan || !bounds) return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (!ctx->dry()) cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        amlt_tune_report local;
+        adaptive(ctx, plan, ops, *bounds, clock, clock_user, log, report ? report : &local);
+    });
+}
+
+amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* host_ops,
+                              const amlt_tile_params* tile, const amlt_bounds* bounds,
+                              amlt_clock_fn clock, void* clock_user, double* elapsed_s) {
+    if (!ctx || !plan || !host_ops || !bounds) return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (ctx->dry()) fail(AMLT_ERR_NO_DEVICE, "amlt_gpu_run_host needs a device context");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const int dt = plan->desc.dtype;
+        const int es = dtype_size(dt);
+        // validate against the host description first (same rules)
+        (void)resolve(plan, host_ops, bounds);
+        amlt_operands dev = *host_ops;
+        const amlt_matrix* src[5] = {&host_ops->a, &host_ops->b, &host_ops->r, &host_ops->thres,
+                                     &host_ops->dis};
+        amlt_matrix* dst[5] = {&dev.a, &dev.b, &dev.r, &dev.thres, &dev.dis};
+        size_t bytes[5];
+        for (int s = 0; s < 5; ++s) {
+            const amlt_matrix& m = *src[s];
+            bytes[s] = 0;
+            if (!m.data) continue;
+            const int64_t outer = m.order == AMLT_ROW_MAJOR ? m.rows : m.cols;
+            bytes[s] = size_t(std::max<int64_t>(outer, 1)) * size_t(m.ld) * es;
+            if (bytes[s] > ctx->hbuf_bytes[s]) {
+                if (ctx->hbuf[s]) cudaFree(ctx->hbuf[s]);
+                ctx->hbuf[s] = nullptr;
+                ctx->hbuf_bytes[s] = 0;
+                cuda_check(cudaMalloc(&ctx->hbuf[s], bytes[s]), "cudaMalloc(host staging)");
+                ctx->hbuf_bytes[s] = bytes[s];
+            }
+            dst[s]->data = ctx->hbuf[s];
+        }
+        auto body = [&] {
+            for (int s = 0; s < 5; ++s)
+                if (bytes[s])
+                    cuda_check(cudaMemcpyAsync(ctx->hbuf[s], src[s]->data, bytes[s],
+                                               cudaMemcpyHostToDevice, ctx->stream),
+                               "cudaMemcpyAsync H2D");
+            if (tile) {
+                Resolved rv = resolve(plan, &dev, bounds);
+                Dispatch dp = plan_dispatch(ctx, plan, tile, rv);
+                enqueue(ctx, plan, rv, dp);
+            } else {
+                amlt_tune_report rep;
+                adaptive(ctx, plan, &dev, *bounds, nullptr, nullptr, nullptr, &rep);
+            }
+            cuda_check(cudaMemcpyAsync(host_ops->r.data, ctx->hbuf[2], bytes[2],
+                                       cudaMemcpyDeviceToHost, ctx->stream),
+                       "cudaMemcpyAsync D2H");
+        };
+        double el = 0;
+        if (clock) {
+            double t0 = clock(clock_user);
+            body();
+            cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+            el = clock(clock_user) - t0;
+        } else {
+            cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
+            body();
+            cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
+            cuda_check(cudaEventSynchronize(ctx->ev1), "cudaEventSynchronize");
+            float ms = 0;
+            cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "cudaEventElapsedTime");
+            el = ms * 1e-3;
+        }
+        if (elapsed_s) *elapsed_s = el;
+    });
+}
+
+amlt_status amlt_spr(int64_t M, int64_t K, int64_t N, double seconds, double* out) {
+    if (!out) return AMLT_ERR_INVALID_ARGUMENT;
+    if (!(seconds > 0.0)) return AMLT_ERR_NON_POSITIVE_TIME;
+    *out = double(M) * double(K) * double(N) / (1e9 * seconds);
+    return AMLT_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,556 @@
+// mmlt_kernel.cuh — sm_100a CUDA-core kernels for the MMLT loop nest
+//
+//     R[i][j] (+)= sum_{k in [k0,k1)} body(A[i][k], B[k][j], col_vectors[j])
+//
+// This is the B200 replacement for the reference's register-blocked kernel
+// execute_block / exec_block_t (reference src/kernel_exec.cpp:128-313) and
+// its interpreter run_instrs (src/kernel_exec.cpp:63-126), fused per body at
+// compile time instead of interpreted per pseudo-instruction.
+//
+// Structure (one CTA = BM x BN output tile, one thread = TM x TN micro-tile):
+//  * A (BM x BK) and B (BK x BN) tiles are staged into shared memory with a
+//    STAGES-deep cp.async (LDGSTS) ring: the reference's packing
+//    (src/packing.cpp:5-45) becomes the SMEM copy.
+//  * Every lane of a warp owns the SAME TM rows, so each A read is a 16-byte
+//    shared-memory broadcast (one wavefront, no bank conflicts); B reads are
+//    16-byte vectors, lane-interleaved so a warp touches contiguous bytes.
+//  * The per-j vectors (thres[j], dis[j]) are loaded once into registers.
+//  * The body is fused into the accumulate chain on CUDA cores (tensor cores
+//    cannot evaluate a per-product predicate); see the Body structs below for
+//    the exact per-iteration instruction mix each one compiles to.
+//  * K tail tiles run a guarded loop (operands past k1 are never applied, so
+//    bodies like A == B do not count zero padding).
+//  * Split-K (TileParams.kc < K) writes per-segment partials to a workspace
+//    reduced in segment order by mmlt_splitk_reduce: deterministic.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace amltk {
+
+// --------------------------------------------------------------------------
+// Launch parameters (plain data, passed by value)
+
+struct KParams {
+    const void* A;  // A(i, k) at A[i * lda + k], already offset to (i0, k0)
+    const void* B;  // B(k, j) at B[k * ldb + j], already offset to (k0, j0)
+    void* R;        // R(i, j) at R[i * ldr + j], already offset to (i0, j0)
+    const void* thres;  // T(j) at thres[j * t_sj] (t_sj == 0: broadcast scalar)
+    const void* dis;    // dis(j) at dis[j * d_sj]
+    void* work;         // split-K workspace: [splits][M][N] of T
+    int64_t lda, ldb, ldr;
+    int64_t t_sj, d_sj;
+    int64_t M, N, K;   // extents of the bounds rectangle
+    int64_t kslice;    // K depth per split (== K when splits == 1)
+    int32_t splits;
+    int32_t tiles_m, tiles_n;
+    int32_t r_vec_ok;  // R base 16B aligned and ldr a multiple of the vector width
+    double tconst;     // threshold when thres == nullptr
+};
+
+// --------------------------------------------------------------------------
+// cp.async helpers (LDGSTS). src_bytes < size zero-fills the remainder.
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+                 "r"(src_bytes));
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async_elem(void* smem, const void* gmem, int src_bytes) {
+    unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(s), "l"(gmem),
+                 "n"(BYTES), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// 16-byte vector of T
+template <typename T>
+struct V16;
+template <>
+struct V16<double> {
+    using type = double2;
+    static constexpr int n = 2;
+    __device__ static __forceinline__ double get(const double2& v, int e) { return e == 0 ? v.x : v.y; }
+};
+template <>
+struct V16<float> {
+    using type = float4;
+    static constexpr int n = 4;
+    __device__ static __forceinline__ float get(const float4& v, int e) {
+        return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+    }
+};
+template <>
+struct V16<int> {
+    using type = int4;
+    static constexpr int n = 4;
+    __device__ static __forceinline__ int get(const int4& v, int e) {
+        return e == 0 ? v.x : e == 1 ? v.y : e == 2 ? v.z : v.w;
+    }
+};
+
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
+template <typename T>
+__device__ __forceinline__ T ldg_elem(const void* base, int64_t idx) {
+    return __ldg(static_cast<const T*>(base) + idx);
+}
+
+// --------------------------------------------------------------------------
+// Bodies. Each gives the per-(i,j,k) update on the accumulators of one
+// output element, the per-column state it needs, and the final value added
+// to R. The reference statement, its compiled pseudo-program (schedule.cpp
+// output) and the B200 instruction mix are listed per body.
+
+// GEMM — `R[i][j] += A[i][k]*B[k][j]` (preset matmul; ref program
+// `mul REG0 A B; add R R REG0`, fused FMA path kernel_exec.cpp:161-178).
+// B200: 1 FFMA/DFMA per iteration.
+template <typename T>
+struct BodyGemm {
+    using Acc = T;
+    static constexpr int NACC = 1;
+    static constexpr bool TWO_LEVEL = sizeof(T) == 4;
+    struct Col {};
+    __device__ static Col col(const KParams&, int64_t) { return {}; }
+    __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col&) {
+        acc[0] = fma_rn(a, b, acc[0]);
+    }
+    __device__ static __forceinline__ T finish(const Acc* acc, const Col&, int64_t) { return acc[0]; }
+};
+
+// DISCOUNT — preset q1: `R += A*B - (A*B > thres[j])*A*B*dis[j]`
+// (presets.cpp:66-67; ref program `mul; gtcmp; mul; masksub; add`).
+// Per product p = A*B (rounded exactly as the reference rounds it, so the
+// mask never flips): acc += p * (p > t ? 1 - dis : 1).
+// B200: DMUL + DSETP + DFMA on the FP64 pipe, 2 FSEL on the ALU pipe.
+template <typename T>
+struct BodyDiscount {
+    using Acc = T;
+    static constexpr int NACC = 1;
+    static constexpr bool TWO_LEVEL = sizeof(T) == 4;
+    struct Col {
+        T t, c1;
+    };
+    __device__ static Col col(const KParams& p, int64_t j) {
+        Col c;
+        c.t = p.thres ? ldg_elem<T>(p.thres, j * p.t_sj) : static_cast<T>(p.tconst);
+        c.c1 = T(1) - ldg_elem<T>(p.dis, j * p.d_sj);
+        return c;
+    }
+    __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col& c) {
+        T pr = mul_rn(a, b);
+        T f = pr > c.t ? c.c1 : T(1);
+        acc[0] = fma_rn(pr, f, acc[0]);
+    }
+    __device__ static __forceinline__ T finish(const Acc* acc, const Col&, int64_t) { return acc[0]; }
+};
+
+// BOOST — preset q2: `R += A*B + (A*B > thres[j])*(A*B - thres[j])`
+// (presets.cpp:68-69; ref program `mul; gtcmp; sub; maskadd; add`).
+// The mask term is relu(p - t) = ((p - t) + |p - t|) / 2, continuous at the
+// threshold. Summed over the K segment:
+//   sum relu(u_k) = (sum_k (a b - t) + sum_k |u_k|) / 2
+//                 = (acc0 - kcount*t + acc1) / 2
+// with acc0 = sum a*b (FMA) and acc1 = sum |fma(a, b, -t)|; |.| is a free
+// operand modifier. B200: 3 FP pipe ops per iteration (FMA, FMA, ADD), no ALU
+// selects at all.
+template <typename T>
+struct BodyBoost {
+    using Acc = T;
+    static constexpr int NACC = 2;
+    static constexpr bool TWO_LEVEL = sizeof(T) == 4;
+    struct Col {
+        T t, nt;
+    };
+    __device__ static Col col(const KParams& p, int64_t j) {
+        Col c;
+        c.t = p.thres ? ldg_elem<T>(p.thres, j * p.t_sj) : static_cast<T>(p.tconst);
+        c.nt = -c.t;
+        return c;
+    }
+    __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col& c) {
+        acc[0] = fma_rn(a, b, acc[0]);
+        T u = fma_rn(a, b, c.nt);
+        acc[1] = add_rn(acc[1], fabs(u));
+    }
+    __device__ static __forceinline__ T finish(const Acc* acc, const Col& c, int64_t kcount) {
+        T s = acc[0] - static_cast<T>(kcount) * c.t;  // sum of (a*b - t)
+        return acc[0] + T(0.5) * (s + acc[1]);
+    }
+};
+
+// SQDIFF — `R += (A - B)*(A - B)`: FADD + FFMA per iteration.
+template <typename T>
+struct BodySqdiff {
+    using Acc = T;
+    static constexpr int NACC = 1;
+    static constexpr bool TWO_LEVEL = sizeof(T) == 4;
+    struct Col {};
+    __device__ static Col col(const KParams&, int64_t) { return {}; }
+    __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col&) {
+        T d = a - b;
+        acc[0] = fma_rn(d, d, acc[0]);
+    }
+    __device__ static __forceinline__ T finish(const Acc* acc, const Col&, int64_t) { return acc[0]; }
+};
+
+// EQCOUNT — `R += A == B` (ref program `eqcmp; maskadd $0 $1; add`).
+// Integer accumulator: ISETP + predicated add. Float/double inputs count in
+// int32 too (the count is exact; K < 2^31) and convert at the end.
+template <typename T>
+struct BodyEqcount {
+    using Acc = int;
+    static constexpr int NACC = 1;
+    static constexpr bool TWO_LEVEL = false;
+    struct Col {};
+    __device__ static Col col(const KParams&, int64_t) { return {}; }
+    __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col&) {
+        acc[0] += (a == b) ? 1 : 0;
+    }
+    __device__ static __forceinline__ T finish(const Acc* acc, const Col&, int64_t) {
+        return static_cast<T>(acc[0]);
+    }
+};
+
+// THRCOUNT — preset q3: `R += (A*B > 100)` (presets.cpp:70-71).
+template <typename T>
+struct BodyThrcount {
+    using Acc = int;
+    static constexpr int NACC = 1;
+    static constexpr bool TWO_LEVEL = false;
+    struct Col {
+        T t;
+    };
+    __device__ static Col col(const KParams& p, int64_t j) {
+        Col c;
+        c.t = p.thres ? ldg_elem<T>(p.thres, j * p.t_sj) : static_cast<T>(p.tconst);
+        return c;
+    }
+    __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col& c) {
+        acc[0] += (mul_rn(a, b) > c.t) ? 1 : 0;
+    }
+    __device__ static __forceinline__ T finish(const Acc* acc, const Col&, int64_t) {
+        return static_cast<T>(acc[0]);
+    }
+};
+template <>
+__device__ __forceinline__ void BodyThrcount<int>::step(int* acc, int a, int b, const Col& c) {
+    acc[0] += (a * b > c.t) ? 1 : 0;
+}
+
+// --------------------------------------------------------------------------
+// The tiled kernel
+
+template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, bool VEC,
+          int MINB>
+struct MmltTile {
+    static constexpr int VN = V16<T>::n;
+    static constexpr int THREADS = 32 * WR * WC;
+    static constexpr int BM = TM * WR;
+    static constexpr int BN = 32 * TN * WC;
+    static constexpr int SMEM_A = BM * BK;  // elements per stage
+    static constexpr int SMEM_B = BK * BN;
+    static constexpr int SMEM_BYTES = STAGES * (SMEM_A + SMEM_B) * (int)sizeof(T);
+    static_assert(TN % VN == 0, "TN must be a multiple of the 16B vector width");
+    static_assert(BK % VN == 0, "BK must be a multiple of the 16B vector width");
+    static_assert(STAGES >= 2, "need at least double buffering");
+};
+
+template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, bool VEC,
+          int MINB>
+__global__ void __launch_bounds__(32 * WR * WC, MINB) mmlt_tile_kernel(const KParams p) {
+    using Cfg = MmltTile<Body, T, TM, TN, WR, WC, BK, STAGES, VEC, MINB>;
+    constexpr int VN = Cfg::VN;
+    constexpr int THREADS = Cfg::THREADS;
+    constexpr int BM = Cfg::BM;
+    constexpr int BN = Cfg::BN;
+    using Vec = typename V16<T>::type;
+    using Acc = typename Body::Acc;
+    constexpr int NACC = Body::NACC;
+
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* As = reinterpret_cast<T*>(smem_raw);
+    T* Bs = As + STAGES * Cfg::SMEM_A;
+
+    // ---- tile coordinates: grouped raster (8 row-tiles per group) so the B
+    // column panels of concurrently resident CTAs are shared through L2.
+    constexpr int G = 8;
+    const int bid = blockIdx.x;
+    const int per_group = G * p.tiles_n;
+    const int group = bid / per_group;
+    const int first_m = group * G;
+    const int gsize = min(p.tiles_m - first_m, G);
+    const int in_group = bid - group * per_group;
+    const int tile_m = first_m + in_group % gsize;
+    const int tile_n = in_group / gsize;
+    const int64_t m0 = static_cast<int64_t>(tile_m) * BM;
+    const int64_t n0 = static_cast<int64_t>(tile_n) * BN;
+
+    const int split = blockIdx.y;
+    const int64_t kbeg = static_cast<int64_t>(split) * p.kslice;
+    const int64_t kspan = min(p.kslice, p.K - kbeg);
+
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int warp = tid >> 5;
+    const int wr = warp / WC;
+    const int wc = warp - wr * WC;
+
+    const T* __restrict__ Ag = static_cast<const T*>(p.A);
+    const T* __restrict__ Bg = static_cast<const T*>(p.B);
+
+    // ---- stage loader
+    auto load_tile = [&](int stage, int64_t k0) {
+        T* as = As + stage * Cfg::SMEM_A;
+        T* bs = Bs + stage * Cfg::SMEM_B;
+        const int64_t kend = kbeg + kspan;
+        if constexpr (VEC) {
+            constexpr int ACH = BK / VN;  // 16B chunks per A tile row
+            for (int c = tid; c < BM * ACH; c += THREADS) {
+                const int row = c / ACH;
+                const int kc = (c - row * ACH) * VN;
+                const int64_t gi = m0 + row;
+                const int64_t gk = k0 + kc;
+                int64_t rem = (gi < p.M) ? (kend - gk) : 0;
+                rem = rem < 0 ? 0 : (rem > VN ? VN : rem);
+                const T* src = rem > 0 ? Ag + gi * p.lda + gk : Ag;
+                cp_async16(as + row * BK + kc, src, static_cast<int>(rem * sizeof(T)));
+            }
+            constexpr int BCH = BN / VN;
+            for (int c = tid; c < BK * BCH; c += THREADS) {
+                const int kr = c / BCH;
+                const int cc = (c - kr * BCH) * VN;
+                const int64_t gk = k0 + kr;
+                const int64_t gj = n0 + cc;
+                int64_t rem = (gk < kend) ? (p.N - gj) : 0;
+                rem = rem < 0 ? 0 : (rem > VN ? VN : rem);
+                const T* src = rem > 0 ? Bg + gk * p.ldb + gj : Bg;
+                cp_async16(bs + kr * BN + cc, src, static_cast<int>(rem * sizeof(T)));
+            }
+        } else {
+            for (int c = tid; c < BM * BK; c += THREADS) {
+                const int row = c / BK;
+                const int kc = c - row * BK;
+                const int64_t gi = m0 + row;
+                const int64_t gk = k0 + kc;
+                const bool ok = gi < p.M && gk < kend;
+                cp_async_elem<sizeof(T)>(as + row * BK + kc, ok ? Ag + gi * p.lda + gk : Ag,
+                                         ok ? (int)sizeof(T) : 0);
+            }
+            for (int c = tid; c < BK * BN; c += THREADS) {
+                const int kr = c / BN;
+                const int cc = c - kr * BN;
+                const int64_t gk = k0 + kr;
+                const int64_t gj = n0 + cc;
+                const bool ok = gk < kend && gj < p.N;
+                cp_async_elem<sizeof(T)>(bs + kr * BN + cc, ok ? Bg + gk * p.ldb + gj : Bg,
+                                         ok ? (int)sizeof(T) : 0);
+            }
+        }
+    };
+
+    // ---- per-thread columns: local col of element (q, e) is
+    //      wc*32*TN + q*32*VN + lane*VN + e
+    typename Body::Col colst[TN];
+#pragma unroll
+    for (int q = 0; q < TN / VN; ++q)
+#pragma unroll
+        for (int e = 0; e < VN; ++e) {
+            const int64_t gj = n0 + wc * 32 * TN + q * 32 * VN + lane * VN + e;
+            colst[q * VN + e] = Body::col(p, gj < p.N ? gj : 0);
+        }
+
+    Acc acc[TM][TN][NACC];
+    Acc part[Body::TWO_LEVEL ? TM : 1][Body::TWO_LEVEL ? TN : 1][NACC];
+#pragma unroll
+    for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int c = 0; c < TN; ++c)
+#pragma unroll
+            for (int n = 0; n < NACC; ++n) acc[r][c][n] = Acc(0);
+    if constexpr (Body::TWO_LEVEL) {
+#pragma unroll
+        for (int r = 0; r < TM; ++r)
+#pragma unroll
+            for (int c = 0; c < TN; ++c)
+#pragma unroll
+                for (int n = 0; n < NACC; ++n) part[r][c][n] = Acc(0);
+    }
+
+    const int nkt = static_cast<int>((kspan + BK - 1) / BK);
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+        if (s < nkt) load_tile(s, kbeg + static_cast<int64_t>(s) * BK);
+        cp_async_commit();
+    }
+
+    for (int kt = 0; kt < nkt; ++kt) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+        {
+            const int nxt = kt + STAGES - 1;
+            if (nxt < nkt) load_tile(nxt % STAGES, kbeg + static_cast<int64_t>(nxt) * BK);
+            cp_async_commit();
+        }
+        const int stage = kt % STAGES;
+        const T* as = As + stage * Cfg::SMEM_A + (wr * TM) * BK;
+        const T* bs = Bs + stage * Cfg::SMEM_B + wc * 32 * TN + lane * VN;
+        const int kcount = static_cast<int>(min(static_cast<int64_t>(BK), kspan - static_cast<int64_t>(kt) * BK));
+
+        auto* work = Body::TWO_LEVEL ? &part[0][0][0] : &acc[0][0][0];
+        (void)work;
+        if (kcount == BK) {
+#pragma unroll
+            for (int kk = 0; kk < BK; kk += VN) {
+                Vec av[TM];
+#pragma unroll
+                for (int r = 0; r < TM; ++r) av[r] = *reinterpret_cast<const Vec*>(as + r * BK + kk);
+#pragma unroll
+                for (int v = 0; v < VN; ++v) {
+                    T b[TN];
+#pragma unroll
+                    for (int q = 0; q < TN / VN; ++q) {
+                        Vec bv = *reinterpret_cast<const Vec*>(bs + (kk + v) * BN + q * 32 * VN);
+#pragma unroll
+                        for (int e = 0; e < VN; ++e) b[q * VN + e] = V16<T>::get(bv, e);
+                    }
+#pragma unroll
+                    for (int r = 0; r < TM; ++r) {
+                        const T a = V16<T>::get(av[r], v);
+#pragma unroll
+                        for (int c = 0; c < TN; ++c) {
+                            if constexpr (Body::TWO_LEVEL)
+                                Body::step(part[r][c], a, b[c], colst[c]);
+                            else
+                                Body::step(acc[r][c], a, b[c], colst[c]);
+                        }
+                    }
+                }
+            }
+        } else {
+            for (int k = 0; k < kcount; ++k) {
+                T b[TN];
+#pragma unroll
+                for (int q = 0; q < TN / VN; ++q) {
+                    Vec bv = *reinterpret_cast<const Vec*>(bs + k * BN + q * 32 * VN);
+#pragma unroll
+                    for (int e = 0; e < VN; ++e) b[q * VN + e] = V16<T>::get(bv, e);
+                }
+#pragma unroll
+                for (int r = 0; r < TM; ++r) {
+                    const T a = as[r * BK + k];
+#pragma unroll
+                    for (int c = 0; c < TN; ++c) {
+                        if constexpr (Body::TWO_LEVEL)
+                            Body::step(part[r][c], a, b[c], colst[c]);
+                        else
+                            Body::step(acc[r][c], a, b[c], colst[c]);
+                    }
+                }
+            }
+        }
+        if constexpr (Body::TWO_LEVEL) {
+#pragma unroll
+            for (int r = 0; r < TM; ++r)
+#pragma unroll
+                for (int c = 0; c < TN; ++c)
+#pragma unroll
+                    for (int n = 0; n < NACC; ++n) {
+                        acc[r][c][n] += part[r][c][n];
+                        part[r][c][n] = Acc(0);
+                    }
+        }
+    }
+    cp_async_wait<0>();
+
+    // ---- epilogue: R (+)= value, or the split-K workspace
+    T* Rg = static_cast<T*>(p.R);
+    T* Wg = static_cast<T*>(p.work);
+#pragma unroll
+    for (int r = 0; r < TM; ++r) {
+        const int64_t gi = m0 + wr * TM + r;
+        if (gi >= p.M) continue;
+#pragma unroll
+        for (int q = 0; q < TN / VN; ++q) {
+            const int64_t gj0 = n0 + wc * 32 * TN + q * 32 * VN + lane * VN;
+            T val[VN];
+#pragma unroll
+            for (int e = 0; e < VN; ++e) val[e] = Body::finish(acc[r][q * VN + e], colst[q * VN + e], kspan);
+            if (p.splits > 1) {
+                T* dst = Wg + (static_cast<int64_t>(split) * p.M + gi) * p.N + gj0;
+#pragma unroll
+                for (int e = 0; e < VN; ++e)
+                    if (gj0 + e < p.N) dst[e] = val[e];
+            } else {
+                T* dst = Rg + gi * p.ldr + gj0;
+                if (p.r_vec_ok && gj0 + VN <= p.N) {
+                    Vec o = *reinterpret_cast<const Vec*>(dst);
+                    T* op = reinterpret_cast<T*>(&o);
+#pragma unroll
+                    for (int e = 0; e < VN; ++e) op[e] = op[e] + val[e];
+                    *reinterpret_cast<Vec*>(dst) = o;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < VN; ++e)
+                        if (gj0 + e < p.N) dst[e] = dst[e] + val[e];
+                }
+            }
+        }
+    }
+}
+
+// R[i][j] (+)= sum over splits s = 0..S-1 (ascending) of work[s][i][j].
+template <typename T>
+__global__ void mmlt_splitk_reduce(const KParams p) {
+    const int64_t total = p.M * p.N;
+    const T* W = static_cast<const T*>(p.work);
+    T* R = static_cast<T*>(p.R);
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / p.N;
+        const int64_t j = idx - i * p.N;
+        T v = R[i * p.ldr + j];
+        for (int s = 0; s < p.splits; ++s) v = v + W[static_cast<int64_t>(s) * total + idx];
+        R[i * p.ldr + j] = v;
+    }
+}
+
+}  // namespace amltk
+
+namespace amltk {
+
+// Assignment statements (`R[i][j] = ...`): the reference's "last k wins"
+// semantics (kernel_exec.cpp:299-312, test_exec.cpp:159-171) — only the
+// k = k1-1 term reaches R. One thread per output element.
+template <class Body, typename T>
+__global__ void mmlt_assign_kernel(const KParams p) {
+    const int64_t total = p.M * p.N;
+    const T* A = static_cast<const T*>(p.A);
+    const T* B = static_cast<const T*>(p.B);
+    T* R = static_cast<T*>(p.R);
+    const int64_t k = p.K - 1;
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / p.N;
+        const int64_t j = idx - i * p.N;
+        typename Body::Acc acc[Body::NACC];
+#pragma unroll
+        for (int n = 0; n < Body::NACC; ++n) acc[n] = typename Body::Acc(0);
+        const typename Body::Col c = Body::col(p, j);
+        Body::step(acc, A[i * p.lda + k], B[k * p.ldb + j], c);
+        R[i * p.ldr + j] = Body::finish(acc, c, 1);
+    }
+}
+
+}  // namespace amltk

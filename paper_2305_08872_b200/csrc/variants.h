@@ -1,0 +1,101 @@
+// variants.h — registry of compiled tile variants (host side).
+//
+// One entry per (body, dtype, tile shape) kernel instantiation. This is the
+// GPU counterpart of the reference's kernel planner (choose_kernel_shape /
+// register_ledger, src/kernel_plan.cpp:45-104): instead of one register
+// footprint picked from a CPU register budget, every feasible CTA/thread tile
+// is compiled ahead of time and the runtime tuner measures among them.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "mmlt_kernel.cuh"
+
+namespace amltk {
+
+using LaunchFn = cudaError_t (*)(const KParams&, dim3 grid, cudaStream_t);
+
+struct VariantDesc {
+    int body = 0;
+    int dtype = 0;
+    int bm = 0, bn = 0, bk = 0, tm = 0, tn = 0;
+    int threads = 0, stages = 0, smem = 0, minb = 1;
+    bool vec = true;  // 16-byte staging (needs aligned operands)
+    bool tc = false;  // tensor-core (DMMA) variant
+    const char* name = "";
+    const void* func = nullptr;
+    LaunchFn launch = nullptr;
+};
+
+// Per (body, dtype) helpers that are not tile variants.
+struct BodyAux {
+    int body = 0;
+    int dtype = 0;
+    LaunchFn assign = nullptr;  // "=" statements: last k wins
+    LaunchFn reduce = nullptr;  // split-K ordered reduction into R
+    const void* assign_func = nullptr;
+    const void* reduce_func = nullptr;
+};
+
+struct Registry {
+    std::vector<VariantDesc> variants;
+    std::vector<BodyAux> aux;
+};
+
+// Defined once per (body, dtype) translation unit (kernels_inst.cu) and by
+// the DMMA GEMM unit; collected by registry() in amlt_gpu.cu.
+void register_all(Registry& reg);
+
+template <class Cfg, class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES,
+          bool VEC, int MINB>
+cudaError_t launch_tile(const KParams& p, dim3 grid, cudaStream_t s) {
+    mmlt_tile_kernel<Body, T, TM, TN, WR, WC, BK, STAGES, VEC, MINB>
+        <<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(p);
+    return cudaGetLastError();
+}
+
+template <class Body, typename T>
+cudaError_t launch_assign(const KParams& p, dim3 grid, cudaStream_t s) {
+    mmlt_assign_kernel<Body, T><<<grid, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_reduce(const KParams& p, dim3 grid, cudaStream_t s) {
+    mmlt_splitk_reduce<T><<<grid, 256, 0, s>>>(p);
+    return cudaGetLastError();
+}
+
+template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, bool VEC,
+          int MINB>
+void add_variant(Registry& reg, int body, int dtype, const char* name) {
+    using Cfg = MmltTile<Body, T, TM, TN, WR, WC, BK, STAGES, VEC, MINB>;
+    // Register budget guard: accumulators (two-level bodies keep a second
+    // set) must leave room for operands; larger tiles are not instantiated.
+    constexpr int acc_regs =
+        TM * TN * Body::NACC * (Body::TWO_LEVEL ? 2 : 1) * (int)(sizeof(typename Body::Acc) / 4);
+    if constexpr (acc_regs <= 136) {
+        VariantDesc v;
+        v.body = body;
+        v.dtype = dtype;
+        v.bm = Cfg::BM;
+        v.bn = Cfg::BN;
+        v.bk = BK;
+        v.tm = TM;
+        v.tn = TN;
+        v.threads = Cfg::THREADS;
+        v.stages = STAGES;
+        v.smem = Cfg::SMEM_BYTES;
+        v.minb = MINB;
+        v.vec = VEC;
+        v.name = name;
+        v.func = reinterpret_cast<const void*>(
+            &mmlt_tile_kernel<Body, T, TM, TN, WR, WC, BK, STAGES, VEC, MINB>);
+        v.launch = &launch_tile<Cfg, Body, T, TM, TN, WR, WC, BK, STAGES, VEC, MINB>;
+        reg.variants.push_back(v);
+    }
+}
+
+}  // namespace amltk

@@ -1,0 +1,318 @@
+"""Task front-end: DSL text -> which GPU body implements it.
+
+The reference compiles a task through parse_task -> recognize -> build_dag ->
+schedule (src/engine.cpp:86-102). The GPU backend needs only the outcome:
+whether the statement is one of the bodies it has a fused kernel for, the
+operands' roles (A, B, threshold, discount vector) and their orientations.
+This module restates just enough of that pipeline:
+
+* a recursive-descent parser for the task grammar (README.md:37-60;
+  parser.cpp:142-365): ``where(v in [a..b] and ...) { T[x][y] (+)= expr; }``
+  with ``//`` and ``#`` comments;
+* the structural recognition conditions 2-4 (recognize.cpp:84-166): three loop
+  variables, a 2-D target on two distinct loop variables, exactly one
+  ``[i][k]``/``[k][i]`` array (A), one ``[k][j]``/``[j][k]`` array (B), and aux
+  leaves that are scalars, ``[i]``, ``[j]`` or ``[i][j]``;
+* a match of the statement tree against the five bodies' canonical trees
+  (presets.cpp:52-94 plus the sqdiff / eqcount statements), allowing operand
+  swaps of commutative nodes (a swap never changes an IEEE result).
+
+Anything else raises UnsupportedExpression, as the reference does for forms
+its vector backend cannot lower.
+"""
+from __future__ import annotations
+
+import re
+from dataclasses import dataclass
+from typing import List, Optional, Tuple
+
+from . import _native as N
+
+
+class TaskError(ValueError):
+    pass
+
+
+# ---------------------------------------------------------------------------
+# lexer / parser
+
+_TOK = re.compile(r"\s*(?:(//[^\n]*|#[^\n]*)|(\d+(?:\.\d+)?(?:[eE][-+]?\d+)?)|([A-Za-z_]\w*)|"
+                  r"(\+=|==|>=|<=|\.\.|[-+*/<>=()\[\]{};]))")
+
+
+def _lex(src: str) -> List[str]:
+    out, pos = [], 0
+    while pos < len(src):
+        m = _TOK.match(src, pos)
+        if not m or m.end() == pos:
+            if src[pos:].strip() == "":
+                break
+            raise TaskError(f"parse error near {src[pos:pos + 12]!r}")
+        pos = m.end()
+        if m.group(1):
+            continue
+        out.append(m.group(2) or m.group(3) or m.group(4))
+    return out
+
+
+# expression trees: ("num", v) | ("ref", name, (idx names...)) | (op, lhs, rhs)
+class _Parser:
+    def __init__(self, toks):
+        self.t = toks
+        self.p = 0
+
+    def peek(self):
+        return self.t[self.p] if self.p < len(self.t) else None
+
+    def take(self, want=None):
+        tok = self.peek()
+        if tok is None or (want is not None and tok != want):
+            raise TaskError(f"parse error: expected {want!r}, got {tok!r}")
+        self.p += 1
+        return tok
+
+    def ident(self):
+        tok = self.take()
+        if not re.match(r"[A-Za-z_]\w*$", tok):
+            raise TaskError(f"parse error: expected identifier, got {tok!r}")
+        return tok
+
+    def task(self):
+        self.take("where")
+        self.take("(")
+        loops = [self.clause()]
+        while self.peek() == "and":
+            self.take("and")
+            loops.append(self.clause())
+        self.take(")")
+        self.take("{")
+        target = self.ident()
+        subs = []
+        while self.peek() == "[":
+            self.take("[")
+            subs.append(self.ident())
+            self.take("]")
+        op = self.take()
+        if op not in ("=", "+="):
+            raise TaskError("statement must be `=` or `+=`")
+        rhs = self.expr()
+        self.take(";")
+        self.take("}")
+        if self.peek() is not None:
+            raise TaskError("trailing input after the task")
+        return loops, target, subs, op == "+=", rhs
+
+    def clause(self):
+        v = self.ident()
+        self.take("in")
+        self.take("[")
+        lo = self.bound()
+        self.take("..")
+        hi = self.bound()
+        self.take("]")
+        return v, lo, hi
+
+    def bound(self):
+        tok = self.take()
+        return int(tok) if tok.isdigit() else tok
+
+    def expr(self):
+        lhs = self.sum()
+        if self.peek() in (">", ">=", "<", "<=", "=="):
+            op = self.take()
+            return (op, lhs, self.sum())
+        return lhs
+
+    def sum(self):
+        node = self.term()
+        while self.peek() in ("+", "-"):
+            op = self.take()
+            node = (op, node, self.term())
+        return node
+
+    def term(self):
+        node = self.factor()
+        while self.peek() in ("*", "/"):
+            op = self.take()
+            node = (op, node, self.factor())
+        return node
+
+    def factor(self):
+        tok = self.peek()
+        if tok == "(":
+            self.take("(")
+            e = self.expr()
+            self.take(")")
+            return e
+        if tok is not None and re.match(r"\d", tok):
+            self.take()
+            return ("num", float(tok))
+        name = self.ident()
+        idx = []
+        while self.peek() == "[":
+            self.take("[")
+            idx.append(self.ident())
+            self.take("]")
+        return ("ref", name, tuple(idx))
+
+
+# ---------------------------------------------------------------------------
+# recognition + body match
+
+
+@dataclass(frozen=True)
+class TaskPlan:
+    """What the GPU backend needs from a compiled task."""
+    body: int
+    body_name: str
+    accumulate: bool
+    layout_a: int
+    layout_b: int
+    thres_class: int
+    thres_value: float
+    a_name: str
+    b_name: str
+    result_name: str
+    thres_name: Optional[str]
+    dis_name: Optional[str]
+    var_i: str
+    var_j: str
+    var_k: str
+    dims: Tuple[str, str, str]  # range-end identifiers bound to (M, K, N)
+
+
+_TEMPLATES = [
+    ("gemm", N.BODY_GEMM, "A*B"),
+    ("discount", N.BODY_DISCOUNT, "A*B - (A*B > T)*A*B*D"),
+    ("boost", N.BODY_BOOST, "A*B + (A*B > T)*(A*B - T)"),
+    ("sqdiff", N.BODY_SQDIFF, "(A - B)*(A - B)"),
+    ("eqcount", N.BODY_EQCOUNT, "A == B"),
+    ("thrcount", N.BODY_THRCOUNT, "A*B > T"),
+]
+_COMMUTATIVE = {"+", "*", "=="}
+
+
+def _template_tree(text):
+    p = _Parser(_lex(text))
+    e = p.expr()
+    return e
+
+
+def _match(tpl, node, env) -> bool:
+    kind = tpl[0]
+    if kind == "ref":  # template placeholder A, B, T or D
+        ph = tpl[1]
+        if ph in ("A", "B"):
+            return node == ("role", ph)
+        if ph == "T":
+            if node[0] not in ("aux", "num"):
+                return False
+            if node[0] == "aux" and node[2] not in ("c", "i", "j", "ij"):
+                return False
+        if ph == "D" and not (node[0] == "aux" and node[2] == "j"):
+            return False
+        if ph in env:
+            return env[ph] == node
+        env[ph] = node
+        return True
+    if kind == "num":
+        return node == tpl
+    if node[0] != kind:
+        return False
+    saved = dict(env)
+    if _match(tpl[1], node[1], env) and _match(tpl[2], node[2], env):
+        return True
+    env.clear()
+    env.update(saved)
+    if kind in _COMMUTATIVE and _match(tpl[1], node[2], env) and _match(tpl[2], node[1], env):
+        return True
+    env.clear()
+    env.update(saved)
+    return False
+
+
+def compile_task(source: str) -> TaskPlan:
+    """Parses and recognises a task; raises UnsupportedExpression (from
+    engine) when it is not one of the GPU bodies."""
+    from .engine import UnsupportedExpression
+
+    loops, target, subs, accumulate, rhs = _Parser(_lex(source)).task()
+    var_names = [v for v, _, _ in loops]
+    if len(loops) != 3:
+        raise UnsupportedExpression("not an MMLT: needs exactly three loop variables")
+    if len(subs) != 2 or subs[0] == subs[1] or any(s not in var_names for s in subs):
+        raise UnsupportedExpression("not an MMLT: target must be 2-D over two distinct loop variables")
+    vi, vj = subs
+    vk = next(v for v in var_names if v not in subs)
+    ends = {v: hi for v, _, hi in loops}
+    starts = {v: lo for v, lo, _ in loops}
+    if any(starts[v] != 0 for v in var_names):
+        raise UnsupportedExpression("loop ranges must start at 0 for the GPU backend")
+
+    roles = {}  # name -> ("A"|"B", layout) or ("aux", cls)
+
+    def classify(node):
+        k = node[0]
+        if k == "num":
+            return node
+        if k == "ref":
+            name, idx = node[1], node[2]
+            if name == target:
+                raise UnsupportedExpression("target appears on the right-hand side")
+            if not idx:
+                if name in var_names:
+                    raise UnsupportedExpression("loop variable used as a value")
+                return ("aux", name, "c")
+            if any(x not in var_names for x in idx):
+                raise UnsupportedExpression("subscripts must be loop variables")
+            if idx == (vi, vk) or idx == (vk, vi):
+                role = ("A", N.LAYOUT_NORMAL if idx == (vi, vk) else N.LAYOUT_TRANSPOSED)
+            elif idx == (vk, vj) or idx == (vj, vk):
+                role = ("B", N.LAYOUT_NORMAL if idx == (vk, vj) else N.LAYOUT_TRANSPOSED)
+            elif idx == (vi,):
+                role = ("aux", "i")
+            elif idx == (vj,):
+                role = ("aux", "j")
+            elif idx == (vi, vj):
+                role = ("aux", "ij")
+            else:
+                raise UnsupportedExpression(f"operand {name}{list(idx)} does not fit the MMLT pattern")
+            prev = roles.get(name)
+            if prev is not None and prev != role:
+                raise UnsupportedExpression(f"array {name} used with two index patterns")
+            roles[name] = role
+            if role[0] in ("A", "B"):
+                return ("role", role[0])
+            return ("aux", name, role[1])
+        return (k, classify(node[1]), classify(node[2]))
+
+    tree = classify(rhs)
+    a_names = [n for n, r in roles.items() if r[0] == "A"]
+    b_names = [n for n, r in roles.items() if r[0] == "B"]
+    if len(a_names) != 1 or len(b_names) != 1:
+        raise UnsupportedExpression("not an MMLT: needs exactly one A[i][k] and one B[k][j] array")
+
+    for name, bid, text in _TEMPLATES:
+        env = {}
+        if _match(_template_tree(text), tree, env):
+            t = env.get("T")
+            d = env.get("D")
+            if t is None:
+                tcls, tval, tname = N.LEAF_CONSTANT, 0.0, None
+            elif t[0] == "num":
+                tcls, tval, tname = N.LEAF_CONSTANT, t[1], None
+            elif t[2] == "c":
+                # named scalar: bound at run time as a 1 x 1 buffer
+                tcls, tval, tname = N.LEAF_CONSTANT, 0.0, t[1]
+            else:
+                tcls = {"i": N.LEAF_VEC_I, "j": N.LEAF_VEC_J, "ij": N.LEAF_MAT_IJ}[t[2]]
+                tval, tname = 0.0, t[1]
+            return TaskPlan(
+                body=bid, body_name=name, accumulate=accumulate,
+                layout_a=roles[a_names[0]][1], layout_b=roles[b_names[0]][1],
+                thres_class=tcls, thres_value=tval, a_name=a_names[0], b_name=b_names[0],
+                result_name=target, thres_name=tname, dis_name=d[1] if d else None,
+                var_i=vi, var_j=vj, var_k=vk,
+                dims=(str(ends[vi]), str(ends[vk]), str(ends[vj])))
+    raise UnsupportedExpression("statement is an MMLT but not one of the GPU bodies "
+                                "(gemm, discount, boost, sqdiff, eqcount, thrcount)")

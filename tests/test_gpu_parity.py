@@ -1,0 +1,236 @@
+"""GPU parity: the sm_100a kernels through the C-ABI vs the CPU oracle.
+
+Integer-valued data (the reference's own determinism convention,
+test_support / acceptance.cpp:109-132): bit-exact for every body, dtype and
+tile variant, on the acceptance dims including ragged ones. BASELINE
+distributions: within BASELINE's tolerances (fp64 1e-12, fp32 1e-5 relative
+vs the fp64 oracle; normwise for GEMM), int32 bit-exact.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from tests.helpers import ACCEPT_DIMS, NP_DT, cast, check, make_inputs, oracle
+
+pytestmark = pytest.mark.gpu
+
+BODY_DTYPES = [("gemm", "f64"), ("gemm", "f32"), ("discount", "f64"), ("discount", "f32"),
+               ("boost", "f64"), ("boost", "f32"), ("sqdiff", "f64"), ("sqdiff", "f32"),
+               ("eqcount", "f64"), ("eqcount", "f32"), ("eqcount", "i32"),
+               ("thrcount", "f64"), ("thrcount", "f32"), ("thrcount", "i32")]
+
+
+def dev(x, dtype):
+    import torch
+
+    if x is None:
+        return None
+    return torch.from_numpy(np.ascontiguousarray(x.astype(NP_DT[dtype]))).cuda()
+
+
+def run_gpu(ctx, body, dtype, A, B, thres=None, dis=None, R0=None, bounds=None, tile=None,
+            adaptive=False, thres_class="j", thres_value=0.0):
+    import paper_2305_08872_b200 as P
+
+    M, N, K = A.shape[0], B.shape[1], A.shape[1]
+    plan = ctx.plan(body, dtype, thres_class=thres_class, thres_value=thres_value)
+    R = dev(np.zeros((M, N)) if R0 is None else R0, dtype)
+    ops = P.Operands(dev(A, dtype), dev(B, dtype), R, dev(thres, dtype), dev(dis, dtype))
+    b = P.Bounds(*bounds) if bounds else P.Bounds(0, M, 0, N, 0, K)
+    if adaptive:
+        rep = P.adaptive_execute(plan, ops, b)
+        return R.cpu().numpy(), rep
+    P.run_subtask(plan, ops, tile or P.TileParams(), b)
+    return R.cpu().numpy(), None
+
+
+@pytest.mark.parametrize("body,dtype", BODY_DTYPES)
+def test_int_valued_all_variants_bit_exact(gpu_ctx, body, dtype):
+    import paper_2305_08872_b200 as P
+
+    plan = gpu_ctx.plan(body, dtype)
+    for vi, v in enumerate(plan.variants()):
+        for (M, K, N) in ACCEPT_DIMS:
+            A, B, t, d = make_inputs(body, M, K, N, "int", seed=M * 7 + K)
+            want = oracle(body, A, B, t, d)
+            tile = P.TileParams(variant=vi)  # the unaligned variant runs on aligned data too
+            got, _ = run_gpu(gpu_ctx, body, dtype, A, B, t, d, tile=tile)
+            check(body, dtype, got, want, exact=True, what=f"{v.name} {M}x{K}x{N}")
+
+
+@pytest.mark.parametrize("body,dtype", BODY_DTYPES)
+def test_reference_goldens(gpu_ctx, body, dtype):
+    """Against outputs of the UNMODIFIED reference (run_naive on its own
+    seeded IntValued data), committed under tests/golden/."""
+    from tests.golden.load import load_golden
+
+    for case in load_golden(body):
+        A, B, t, d, want = case["A"], case["B"], case.get("thres"), case.get("dis"), case["R"]
+        tcls, tval = ("c", case["thres_const"]) if "thres_const" in case else ("j", 0.0)
+        got, _ = run_gpu(gpu_ctx, body, dtype, A, B, t, d, adaptive=True, thres_class=tcls,
+                         thres_value=tval)
+        check(body, dtype, got, want, exact=True, what=f"golden {case['name']}")
+
+
+@pytest.mark.parametrize("body,dtype", [("discount", "f64"), ("boost", "f64"), ("boost", "f32"),
+                                        ("gemm", "f64"), ("gemm", "f32"), ("sqdiff", "f32"),
+                                        ("eqcount", "i32"), ("discount", "f32"),
+                                        ("thrcount", "f64")])
+def test_baseline_distributions_tolerance(gpu_ctx, body, dtype):
+    M, K, N = 384, 1000, 320
+    A, B, t, d = make_inputs(body, M, K, N, "baseline", seed=11)
+    A, B, t, d = (cast(x, dtype) for x in (A, B, t, d))
+    want = oracle(body, A, B, t, d)
+    got, _ = run_gpu(gpu_ctx, body, dtype, A, B, t, d, adaptive=True)
+    check(body, dtype, got, want, A=A, B=B, what=f"{body}/{dtype} baseline dist")
+
+
+def test_config0_discount_full(gpu_ctx):
+    """Config 0 in full: discount fp64 1024^3, BASELINE distributions."""
+    A, B, t, d = make_inputs("discount", 1024, 1024, 1024, "baseline", seed=1)
+    want = oracle("discount", A, B, t, d)
+    got, rep = run_gpu(gpu_ctx, "discount", "f64", A, B, t, d, adaptive=True)
+    check("discount", "f64", got, want, what="config 0")
+
+
+@pytest.mark.parametrize("body,dtype,M,K,N", [
+    ("boost", "f32", 4096, 4096, 4096), ("boost", "f64", 4096, 4096, 4096),
+    ("gemm", "f64", 2048, 8192, 2048), ("gemm", "f32", 2048, 8192, 2048),
+    ("sqdiff", "f32", 65536, 1024, 256), ("eqcount", "i32", 65536, 1024, 256)])
+def test_large_configs_sampled_rows(gpu_ctx, body, dtype, M, K, N):
+    """BASELINE-size shapes; the oracle checks sampled rows (rows of R are
+    independent, so the oracle on those rows of A is exact for them)."""
+    A, B, t, d = make_inputs(body, M, K, N, "baseline", seed=5)
+    A, B, t, d = (cast(x, dtype) for x in (A, B, t, d))
+    got, rep = run_gpu(gpu_ctx, body, dtype, A, B, t, d, adaptive=True)
+    rows = np.unique(np.r_[0, M - 1, np.random.default_rng(2).integers(0, M, 14)])
+    want = oracle(body, A[rows], B, t, d)
+    check(body, dtype, got[rows], want, A=A[rows], B=B, what=f"{body}/{dtype} {M}x{K}x{N}")
+
+
+@pytest.mark.parametrize("body,dtype", [("discount", "f64"), ("boost", "f32"), ("eqcount", "i32"),
+                                        ("gemm", "f64")])
+def test_split_k_and_nc(gpu_ctx, body, dtype):
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 300, 777, 200
+    A, B, t, d = make_inputs(body, M, K, N, "int", seed=3)
+    want = oracle(body, A, B, t, d)
+    for kc in (64, 100, 256, 777, 5000):
+        for nc in (0, 64, 128, 1000):
+            got, _ = run_gpu(gpu_ctx, body, dtype, A, B, t, d, tile=P.TileParams(kc=kc, nc=nc))
+            check(body, dtype, got, want, exact=True, what=f"kc={kc} nc={nc}")
+
+
+@pytest.mark.parametrize("body,dtype", [("discount", "f64"), ("sqdiff", "f32"), ("eqcount", "i32")])
+def test_subrectangle_isolation(gpu_ctx, body, dtype):
+    """Only R inside the bounds changes (test_tiled.cpp:172-188); the rest of
+    R keeps its prior values; k outside [k0,k1) never contributes."""
+    M, K, N = 90, 70, 110
+    A, B, t, d = make_inputs(body, M, K, N, "int", seed=9)
+    R0 = np.random.default_rng(4).integers(-50, 50, (M, N)).astype(np.float64)
+    for bounds in [(3, 77, 5, 101, 2, 61), (0, 1, 0, 1, 0, 1), (10, 10, 0, N, 0, K),
+                   (0, M, 0, N, 30, 30), (5, 9, 7, 8, 0, K)]:
+        want = oracle(body, A, B, t, d, R0=R0, bounds=bounds)
+        got, _ = run_gpu(gpu_ctx, body, dtype, A, B, t, d, R0=R0, bounds=bounds)
+        check(body, dtype, got, want, exact=True, what=f"bounds {bounds}")
+
+
+@pytest.mark.parametrize("body,dtype", [("discount", "f64"), ("boost", "f32"), ("eqcount", "i32")])
+def test_unaligned_operands(gpu_ctx, body, dtype):
+    """Odd leading dimensions and odd offsets force the element-wise staging
+    variant; results unchanged."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 77, 51, 93
+    A, B, t, d = make_inputs(body, M, K, N, "int", seed=21)
+    want = oracle(body, A, B, t, d)
+    dt = NP_DT[dtype]
+    Ab = dev(np.zeros((M, K + 3)), dtype)
+    Ab[:, 1:K + 1] = dev(A, dtype)
+    Bb = dev(np.zeros((K, N + 1)), dtype)
+    Bb[:, :N] = dev(B, dtype)
+    R = torch.zeros((M, N), dtype=Ab.dtype, device="cuda")
+    plan = gpu_ctx.plan(body, dtype)
+    ops = P.Operands(Ab[:, 1:K + 1], Bb[:, :N], R, dev(t, dtype), dev(d, dtype))
+    P.run_subtask(plan, ops, P.TileParams(), P.Bounds(0, M, 0, N, 0, K))
+    check(body, dtype, R.cpu().numpy(), want, exact=True, what="unaligned")
+    del dt
+
+
+@pytest.mark.parametrize("body,dtype", [("discount", "f64"), ("gemm", "f32"), ("eqcount", "i32")])
+def test_assignment_last_k_wins(gpu_ctx, body, dtype):
+    """`R[i][j] = ...` keeps only the k = k1-1 term (test_exec.cpp:159-171)."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 40, 6, 33
+    A, B, t, d = make_inputs(body, M, K, N, "int", seed=13)
+    want = oracle(body, A, B, t, d, accumulate=False)
+    plan = gpu_ctx.plan(body, dtype, accumulate=False)
+    R = torch.zeros((M, N), dtype=dev(A, dtype).dtype, device="cuda")
+    P.run_subtask(plan, P.Operands(dev(A, dtype), dev(B, dtype), R, dev(t, dtype), dev(d, dtype)),
+                  P.TileParams(), P.Bounds(0, M, 0, N, 0, K))
+    check(body, dtype, R.cpu().numpy(), want, exact=True, what="assign")
+
+
+def test_adaptive_coverage_exactly_once(gpu_ctx):
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 8192, 256, 1024
+    A, B, t, d = make_inputs("discount", M, K, N, "int", seed=17)
+    want = oracle("discount", A[:64], B, t, d)
+    log = P.ExecLog()
+    plan = gpu_ctx.plan("discount", "f64")
+    R = dev(np.zeros((M, N)), "f64")
+    rep = P.adaptive_execute(plan, P.Operands(dev(A, "f64"), dev(B, "f64"), R, dev(t, "f64"),
+                                              dev(d, "f64")), P.Bounds(0, M, 0, N, 0, K), log=log)
+    assert rep.tuned and len(rep.trials) >= 2
+    covered = np.zeros(M, dtype=np.int32)
+    for c in rep.coverage:
+        assert (c.j0, c.j1, c.k0, c.k1) == (0, N, 0, K)
+        covered[c.i0:c.i1] += 1
+    assert (covered == 1).all()
+    assert len(log.records) == len(rep.coverage)
+    best = min(rep.trials, key=lambda tr: tr.score)
+    assert rep.best_variant == best.value
+    got = R.cpu().numpy()
+    check("discount", "f64", got[:64], want, exact=True, what="adaptive rows")
+    full = oracle("discount", A[-64:], B, t, d)
+    check("discount", "f64", got[-64:], full, exact=True, what="adaptive tail rows")
+
+
+def test_run_host_e2e(gpu_ctx):
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 513, 300, 257
+    A, B, t, d = make_inputs("discount", M, K, N, "baseline", seed=23)
+    want = oracle("discount", A, B, t, d)
+    R = np.zeros((M, N))
+    plan = gpu_ctx.plan("discount", "f64")
+    el = P.run_host(plan, P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K))
+    assert el > 0
+    check("discount", "f64", R, want, what="run_host")
+
+
+def test_edge_empty_and_tiny(gpu_ctx):
+    for (M, K, N) in [(1, 1, 1), (1, 1000, 1), (2, 3, 1), (1, 2, 300)]:
+        for body, dtype in [("discount", "f64"), ("eqcount", "i32"), ("boost", "f32")]:
+            A, B, t, d = make_inputs(body, M, K, N, "int", seed=M + N + K)
+            want = oracle(body, A, B, t, d)
+            got, _ = run_gpu(gpu_ctx, body, dtype, A, B, t, d, adaptive=True)
+            check(body, dtype, got, want, exact=True, what=f"tiny {M}x{K}x{N}")
+
+
+def test_missing_binding_raises(gpu_ctx):
+    import paper_2305_08872_b200 as P
+
+    A, B, t, d = make_inputs("discount", 8, 8, 8, "int")
+    plan = gpu_ctx.plan("discount", "f64")
+    with pytest.raises(P.MissingBinding):
+        P.run_subtask(plan, P.Operands(dev(A, "f64"), dev(B, "f64"), dev(np.zeros((8, 8)), "f64"),
+                                       dev(t, "f64"), None), P.TileParams(), P.Bounds(0, 8, 0, 8, 0, 8))
