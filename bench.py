@@ -1,0 +1,441 @@
+#!/usr/bin/env python
+"""Benchmark of the MMLT hot path on B200 — one JSON line on rank 0.
+
+Default workload = BASELINE config 4, the one quoted at 1/2/4/8 GPUs:
+discount body, fp64, M = N = 32768, K = 8192, inputs drawn from config 0's
+distributions (A integers 0..9, B U[1,100), thres U[50,450), dis U[0,0.3)),
+R zero-initialised. A "step" is one pass of the hot path over that whole
+problem: R += sum_k body(A, B, thres, dis).
+
+Multi-GPU (torchrun): rank r owns R / A rows [r*M/n, (r+1)*M/n); B and the
+per-column vectors are created on rank 0 and NCCL-broadcast over NVLink to
+every rank (no reduction: rows of R are independent). Strong scaling: the
+total problem is fixed as n grows.
+
+Legs:
+  value   device-resident inputs; K timed steps through the public API
+          (adaptive_execute -> cached tuned tile -> one kernel per step),
+          CUDA events on the launch stream, max over ranks.
+  e2e     the same metric through the host-buffer C-ABI entry
+          (amlt_gpu_run_host) with pinned host inputs: every step copies A, B
+          and the vectors H2D and R D2H inside the timed region.
+  cpu_baseline  the UNMODIFIED reference engine (oracle/_ref) on the box's
+          host cores, rank 0 at N=1 only, on a bounded sample of the same
+          workload (reference arm: --impl reference).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("matmul-like GFLOP/s (inner iters/s) & fraction of FMA/tensor peak, "
+          "1/2/4/8 B200")
+
+WORKLOADS = {
+    # name: (body, dtype, M, K, N, distribution)
+    "cfg4_discount_f64": ("discount", "f64", 32768, 8192, 32768),
+    "cfg0_discount_f64": ("discount", "f64", 1024, 1024, 1024),
+    "cfg1_boost_f32": ("boost", "f32", 4096, 4096, 4096),
+    "cfg1_boost_f64": ("boost", "f64", 4096, 4096, 4096),
+    "cfg2_gemm_f64": ("gemm", "f64", 8192, 8192, 8192),
+    "cfg2_gemm_f32": ("gemm", "f32", 8192, 8192, 8192),
+    "cfg3_sqdiff_f32": ("sqdiff", "f32", 65536, 1024, 256),
+    "cfg3_eqcount_i32": ("eqcount", "i32", 65536, 1024, 256),
+}
+# FP64-pipe ops per inner iteration of each body's kernel;
+# the ceiling as a fraction of 2-flop "matmul-like" accounting is 1/ops.
+PIPE = {"f64": "dfma", "f32": "ffma", "i32": "alu"}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    lrank = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, lrank
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+
+
+class ClockSampler:
+    def __init__(self, gpu_index: int):
+        self.path = tempfile.mktemp(prefix="clocks_", suffix=".csv")
+        self.proc = None
+        self.gpu = gpu_index
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.f.close()
+        sm, mx, pw, reasons = [], None, [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                parts = [p.strip() for p in line.split(",")]
+                if len(parts) < 9:
+                    continue
+                try:
+                    sm.append(float(parts[1]))
+                    mx = float(parts[2])
+                    pw.append(float(parts[3]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, parts[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+        os.unlink(self.path)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------------------
+# data
+
+
+def gen_inputs(body, dtype, M_rows, K, N, row0, rank, device, broadcast):
+    """BASELINE-distribution inputs on `device`. B / thres / dis are made on
+    rank 0 and broadcast (NCCL) when `broadcast`; A rows are per rank."""
+    import torch
+
+    tdt = {"f64": torch.float64, "f32": torch.float32, "i32": torch.int32}[dtype]
+    g = torch.Generator(device=device)
+    g.manual_seed(1)
+    if body == "discount":
+        Bv = torch.empty((K, N), dtype=tdt, device=device).uniform_(1, 100, generator=g)
+        th = torch.empty(N, dtype=tdt, device=device).uniform_(50, 450, generator=g)
+        ds = torch.empty(N, dtype=tdt, device=device).uniform_(0, 0.3, generator=g)
+    elif body == "boost":
+        Bv = torch.rand((K, N), dtype=tdt, device=device, generator=g)
+        th = torch.empty(N, dtype=tdt, device=device).uniform_(0.25, 0.75, generator=g)
+        ds = None
+    elif body == "gemm":
+        Bv = torch.randn((K, N), dtype=tdt, device=device, generator=g)
+        th = ds = None
+    elif body == "sqdiff":
+        Bv = torch.empty((K, N), dtype=tdt, device=device).uniform_(-1, 1, generator=g)
+        th = ds = None
+    else:  # eqcount
+        Bv = torch.randint(0, 16, (K, N), dtype=tdt, device=device, generator=g)
+        th = ds = None
+    if broadcast:
+        import torch.distributed as dist
+
+        for x in (Bv, th, ds):
+            if x is not None:
+                dist.broadcast(x, src=0)
+    ga = torch.Generator(device=device)
+    ga.manual_seed(1000 + row0)
+    if body == "discount":
+        A = torch.randint(0, 10, (M_rows, K), device=device, generator=ga).to(tdt)
+    elif body == "boost":
+        A = torch.rand((M_rows, K), dtype=tdt, device=device, generator=ga)
+    elif body == "gemm":
+        A = torch.randn((M_rows, K), dtype=tdt, device=device, generator=ga)
+    elif body == "sqdiff":
+        A = torch.empty((M_rows, K), dtype=tdt, device=device).uniform_(-1, 1, generator=ga)
+    else:
+        A = torch.randint(0, 16, (M_rows, K), dtype=tdt, device=device, generator=ga)
+    return A, Bv, th, ds
+
+
+# ---------------------------------------------------------------------------
+# reference CPU arm
+
+
+def reference_sample(body, M, K, N, threads):
+    """A bounded sample of the workload for the reference engine: 12 rows per
+    thread (>= the reference's i_h, so every band is tuned as in a full run)
+    x min(N, 4096) columns x full K — about 10 s of CPU work at the
+    reference's ~0.1 G iterations/s per thread on the interpreted bodies.
+    Rows are independent, so the sample's rate is the workload's rate."""
+    rows = min(M, 12 * threads)
+    cols = min(N, 4096)
+    if body == "gemm":
+        cols = min(N, 8192)
+    return rows, K, cols
+
+
+def run_reference(body, M, K, N, steps, warmup, threads):
+    import numpy as np
+
+    from oracle import pyoracle as po
+
+    text = {"discount": po.preset_source("q1"), "boost": po.preset_source("q2"),
+            "gemm": po.preset_source("matmul"), "sqdiff": po.SQDIFF_TEXT,
+            "eqcount": po.EQCOUNT_TEXT}[body]
+    rows, K_, cols = reference_sample(body, M, K, N, threads)
+    t = po.RefTask.create(text, rows, K_, cols, seed=1, int_valued=False)
+    rng = np.random.default_rng(1)
+    if body == "discount":
+        t.set("A", rng.integers(0, 10, (rows, K_)).astype(np.float64))
+        t.set("B", rng.uniform(1, 100, (K_, cols)))
+        t.set("thres", rng.uniform(50, 450, cols))
+        t.set("dis", rng.uniform(0, 0.3, cols))
+    elif body == "boost":
+        t.set("A", rng.uniform(0, 1, (rows, K_)))
+        t.set("B", rng.uniform(0, 1, (K_, cols)))
+        t.set("thres", rng.uniform(0.25, 0.75, cols))
+    elif body == "gemm":
+        t.set("A", rng.standard_normal((rows, K_)))
+        t.set("B", rng.standard_normal((K_, cols)))
+    elif body == "sqdiff":
+        t.set("A", rng.uniform(-1, 1, (rows, K_)))
+        t.set("B", rng.uniform(-1, 1, (K_, cols)))
+    else:
+        t.set("A", rng.integers(0, 16, (rows, K_)).astype(np.float64))
+        t.set("B", rng.integers(0, 16, (K_, cols)).astype(np.float64))
+    times = []
+    for s in range(warmup + steps):
+        el = t.run_adaptive_bands(threads)
+        if s >= warmup:
+            times.append(el)
+    iters = rows * K_ * cols
+    sec = sum(times) / len(times)
+    return {"iters_per_s": iters / sec, "seconds_per_sample": sec,
+            "sample": f"{rows} rows x {cols} cols x K={K_} of the workload "
+                      f"({iters / 1e9:.2f} G inner iterations), reference adaptive_execute "
+                      f"on {threads} row bands (one std::thread each), seed-1 BASELINE "
+                      f"distributions"}
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# main
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg4_discount_f64", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    ws, rank, lrank = dist_env()
+    body, dtype, M, K, N = WORKLOADS[args.workload]
+    steps, warmup = args.steps, max(args.warmup, 0)
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        threads = cpu_threads()
+        r = run_reference(body, M, K, N, steps, warmup, threads)
+        gf = 2 * r["iters_per_s"] / 1e9
+        line = {"impl": "reference", "metric": METRIC, "value": gf, "unit": "GFLOP/s",
+                "inner_iters_per_s": r["iters_per_s"], "n_gpus": args.gpus, "steps": steps,
+                "warmup": warmup, "ms_per_step": r["seconds_per_sample"] * 1e3,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": args.workload, "body": body, "M": M, "K": K, "N": N,
+                           "parallelism": f"cpu_threads{threads}"},
+                "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": threads,
+                                 "kind": "reference", "sample": r["sample"]},
+                "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return 0
+
+    import torch
+
+    import paper_2305_08872_b200 as P
+    from paper_2305_08872_b200.task import compile_task
+
+    assert torch.cuda.is_available(), "bench.py needs a CUDA device"
+    torch.cuda.set_device(lrank)
+    device = torch.device("cuda", lrank)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=device)
+    row0, row1 = M * rank // ws, M * (rank + 1) // ws
+    rows = row1 - row0
+
+    ctx = P.Context(lrank)
+    stream = torch.cuda.current_stream(device)
+    ctx.set_stream(stream)
+    text = {"discount": "A[i][k]*B[k][j] - (A[i][k]*B[k][j] > thres[j])*A[i][k]*B[k][j]*dis[j]",
+            "boost": "A[i][k]*B[k][j] + (A[i][k]*B[k][j] > thres[j])*(A[i][k]*B[k][j] - thres[j])",
+            "gemm": "A[i][k]*B[k][j]", "sqdiff": "(A[i][k] - B[k][j])*(A[i][k] - B[k][j])",
+            "eqcount": "A[i][k] == B[k][j]"}[body]
+    task = compile_task("where(i in [0..M] and j in [0..N] and k in [0..K]) {\n  R[i][j] += "
+                        + text + ";\n}\n")
+    plan = ctx.plan_for(task, dtype)
+
+    # roofline denominator, measured on this GPU now
+    pipe = PIPE[dtype] if not (body == "gemm" and dtype == "f64") else "dmma"
+    peak_ops, peak_ghz = P.engine.measure_peak(pipe)
+    peak_tflops = 2 * peak_ops / 1e12 if pipe != "alu" else peak_ops / 1e12
+
+    A, B, th, ds = gen_inputs(body, dtype, rows, K, N, row0, rank, device, ws > 1)
+    R = torch.zeros((rows, N), dtype=A.dtype, device=device)
+    ops = P.Operands(A, B, R, th, ds)
+    bounds = P.Bounds(0, rows, 0, N, 0, K)
+    torch.cuda.synchronize()
+
+    # warm-up: the first call tunes on row bands (AMULET-style), later calls
+    # reuse the cached winner
+    reports = []
+    for _ in range(warmup):
+        reports.append(P.adaptive_execute(plan, ops, bounds))
+    torch.cuda.synchronize()
+    tuned = reports[0] if reports else None
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    # ---- value leg
+    sampler = ClockSampler(lrank)
+    launches = 0
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    time.sleep(0.3)
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for s in range(steps):
+        lg = P.ExecLog()
+        ev[s][0].record(stream)
+        P.adaptive_execute(plan, ops, bounds, log=lg)
+        ev[s][1].record(stream)
+        launches += len(lg.records) * (2 if any(r.splits > 1 for r in lg.records) else 1)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    el = t0.elapsed_time(t1) / 1e3
+    per_launch = [a.elapsed_time(b) / 1e3 for a, b in ev]
+    if dist is not None:
+        tt = torch.tensor([el], dtype=torch.float64, device=device)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        el = float(tt.item())
+    iters_total = M * K * N * steps
+    value = 2 * iters_total / el / 1e9
+    kernel_s = sum(per_launch) / len(per_launch)
+    achieved_tflops = 2 * rows * K * N / kernel_s / 1e12
+
+    # ---- e2e leg: host buffers through the C-ABI host entry
+    e2e = None
+    if not args.no_e2e:
+        hA = A.cpu().pin_memory()
+        hB = B.cpu().pin_memory()
+        hth = th.cpu().pin_memory() if th is not None else None
+        hds = ds.cpu().pin_memory() if ds is not None else None
+        hR = torch.empty((rows, N), dtype=A.dtype).pin_memory()
+        hops = P.Operands(hA, hB, hR, hth, hds)
+        del A, B, R, ops
+        torch.cuda.empty_cache()
+        P.run_host(plan, hops, bounds, r_zero=True)  # warm-up (staging alloc)
+        barrier()
+        tms = []
+        for _ in range(steps):
+            tms.append(P.run_host(plan, hops, bounds, r_zero=True))
+        e_el = sum(tms)
+        if dist is not None:
+            tt = torch.tensor([e_el], dtype=torch.float64, device=device)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_el = float(tt.item())
+        es = hA.element_size()
+        h2d = (hA.numel() + hB.numel() + (hth.numel() if hth is not None else 0)
+               + (hds.numel() if hds is not None else 0)) * es
+        d2h = hR.numel() * es
+        e2e = {"value": 2 * iters_total / e_el / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": d2h * ws,
+               "ms_per_step": e_el / steps * 1e3,
+               "path": "amlt_gpu_run_host (C-ABI) from pinned host buffers, R zero-init on device, "
+                       "A/R row bands pipelined against compute"}
+
+    # ---- CPU baseline (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            threads = cpu_threads()
+            r = run_reference(body, M, K, N, 1, 0, threads)
+            cpu = {"value": 2 * r["iters_per_s"] / 1e9, "unit": "GFLOP/s", "cores": threads,
+                   "kind": "reference", "sample": r["sample"]}
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"}
+
+    if rank == 0:
+        variants = plan.variants()
+        best = tuned.best_variant if tuned else -1
+        ops_per_iter = {"discount": 3, "boost": 3, "gemm": 1, "sqdiff": 2, "eqcount": 2}[body]
+        line = {
+            "metric": METRIC, "value": value, "unit": "GFLOP/s",
+            "inner_iters_per_s": iters_total / el,
+            "n_gpus": ws, "steps": steps, "warmup": warmup, "ms_per_step": el / steps * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": dtype, "data": "synthetic",
+            "config": {"workload": args.workload, "body": body, "M": M, "K": K, "N": N,
+                       "parallelism": f"rowshard{ws}", "l2": "inputs larger than L2 (no flush)",
+                       "tile": variants[best].name if best >= 0 else None,
+                       "tuning_trials": [(variants[t.value].name, round(t.score * 1e6, 4))
+                                         for t in tuned.trials] if tuned else []},
+            "roofline": {"bound": "fp64" if dtype == "f64" else ("fp32" if dtype == "f32" else "int32"),
+                         "pipe": pipe, "achieved": achieved_tflops, "peak": peak_tflops,
+                         "unit": "TFLOP/s", "frac": achieved_tflops / peak_tflops,
+                         "traffic": None,
+                         "accounting": "2 flops per inner iteration (matmul-like); peak = measured "
+                                       f"{pipe} probe x2 on this GPU at {peak_ghz:.3f} GHz",
+                         "body_pipe_ops_per_iter": ops_per_iter,
+                         "frac_of_body_ceiling": achieved_tflops / peak_tflops * ops_per_iter,
+                         "kernel_ms": kernel_s * 1e3},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

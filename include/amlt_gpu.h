@@ -274,14 +274,27 @@ amlt_status amlt_gpu_adaptive_execute(amlt_ctx* ctx, const amlt_plan* plan,
                                       int pack, amlt_clock_fn clock, void* clock_user,
                                       amlt_exec_log* log, amlt_tune_report* report);
 
+/* run_host flags */
+#define AMLT_HOST_R_ZERO 1 /* R starts at zero: device R is zero-filled, not copied in */
+
 /* Host-buffer entry (the reference's callers hold host MatrixBuffers):
- * operands' `data` are HOST pointers (pinned or pageable). Copies A, B, aux
- * and R to the device, runs (tile == NULL: adaptive; else that tile), copies
- * R back. *elapsed_s covers copies + compute (the clock, if any, is read
- * exactly twice around all of it). */
+ * operands' `data` are HOST pointers (pinned for full copy bandwidth).
+ * Copies B and the aux vectors, then streams A (and R, unless
+ * AMLT_HOST_R_ZERO) to the device in row bands on a copy stream while the
+ * previous band computes, and streams finished R bands back on a second
+ * copy stream. The tile: `tile` if given, else the winner cached by an
+ * earlier amlt_gpu_adaptive_execute of the same shape, else the planner
+ * default. *elapsed_s covers all copies and compute (the clock, if any, is
+ * read exactly twice around all of it). */
 amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* host_ops,
-                              const amlt_tile_params* tile, const amlt_bounds* bounds,
+                              const amlt_tile_params* tile, const amlt_bounds* bounds, int flags,
                               amlt_clock_fn clock, void* clock_user, double* elapsed_s);
+
+/* Pipe-throughput probe on the current device (roofline denominators):
+ * pipe 0 DFMA, 1 FFMA, 2 integer ALU, 3 DSETP+select, 4 DMMA (f64 tensor).
+ * *ops_per_s: lane operations per second (FMA pipes and DMMA: FMAs/s);
+ * *sm_ghz: SM clock observed by the probe. */
+amlt_status amlt_gpu_measure_peak(int pipe, double* ops_per_s, double* sm_ghz);
 
 /* Scaled processing rate M*K*N / (1e9 * seconds) (engine.cpp:212-216). */
 amlt_status amlt_spr(int64_t M, int64_t K, int64_t N, double seconds, double* out);

@@ -98,8 +98,9 @@ EXPORTS = [
     "amlt_gpu_set_stream", "amlt_gpu_clear_tuning_cache", "amlt_gpu_plan_create",
     "amlt_gpu_plan_destroy", "amlt_gpu_plan_num_variants", "amlt_gpu_plan_variant",
     "amlt_gpu_plan_default_variant", "amlt_gpu_run_subtask", "amlt_gpu_enqueue",
-    "amlt_gpu_adaptive_execute", "amlt_gpu_run_host", "amlt_spr",
+    "amlt_gpu_adaptive_execute", "amlt_gpu_run_host", "amlt_spr", "amlt_gpu_measure_peak",
 ]
+HOST_R_ZERO = 1
 
 _lib = None
 
@@ -139,7 +140,9 @@ def lib():
                                             C.c_int, CLOCK_FN, P, C.POINTER(ExecLogC),
                                             C.POINTER(TuneReportC)]
     L.amlt_gpu_run_host.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(TileParamsC),
-                                    C.POINTER(BoundsC), CLOCK_FN, P, C.POINTER(C.c_double)]
+                                    C.POINTER(BoundsC), C.c_int, CLOCK_FN, P,
+                                    C.POINTER(C.c_double)]
+    L.amlt_gpu_measure_peak.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.amlt_spr.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_double, C.POINTER(C.c_double)]
     v = L.amlt_gpu_abi_version()
     if v != ABI_VERSION:

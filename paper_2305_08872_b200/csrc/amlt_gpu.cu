@@ -84,6 +84,8 @@ struct amlt_ctx {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaStream_t copy_in = nullptr, copy_out = nullptr;  // run_host pipeline
+    std::vector<cudaEvent_t> pipe_ev;                      // run_host pipeline
     void* work = nullptr;
     size_t work_bytes = 0;
     // device staging for amlt_gpu_run_host
@@ -91,7 +93,11 @@ struct amlt_ctx {
     size_t hbuf_bytes[5] = {0, 0, 0, 0, 0};
     std::vector<int> occupancy;  // resident CTAs per SM, per registry variant
     // tuning winners: (body, dtype, M, N, K) -> variant index
-    std::map<std::tuple<int, int, int64_t, int64_t, int64_t>, int> tune_cache;
+    struct Winner {
+        int variant;
+        int64_t kc;
+    };
+    std::map<std::tuple<int, int, int64_t, int64_t, int64_t>, Winner> tune_cache;
     std::string err;
     bool dry() const { return (flags & AMLT_CTX_DRY_RUN) != 0; }
 };
@@ -460,7 +466,8 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
         need += band[c];
     }
     const bool tunable = plan->desc.accumulate && !cands.empty() && whole.K > 0 && whole.N > 0 &&
-                         need * 4 <= whole.M;  // tuning <= 25% of the rows
+                         need * 4 <= whole.M &&  // tuning <= 25% of the rows
+                         ctx->tune_cache.find(key) == ctx->tune_cache.end();
 
     auto run_rect = [&](const amlt_bounds& rb, int variant, int64_t kc) {
         amlt_tile_params tp{kc, 0, 0, plan_local_index(plan, variant)};
@@ -478,7 +485,9 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
         int v;
         int64_t kc = 0;
         if (it != ctx->tune_cache.end()) {
-            v = it->second;
+            // a winner measured on an earlier call with the same shape
+            v = it->second.variant;
+            kc = it->second.kc;
             rep->from_cache = 1;
         } else if (!plan->desc.accumulate) {
             v = plan->variants.empty() ? -1 : plan->variants[0];
@@ -524,7 +533,7 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
     rep->best_variant = plan_local_index(plan, best);
     rep->best_kc = whole.K;
     rep->tuning_fraction = double(cur - b.i0) / double(whole.M);
-    ctx->tune_cache[key] = best;
+    ctx->tune_cache[key] = amlt_ctx::Winner{best, 0};
     if (cur < b.i1) run_rect(amlt_bounds{cur, b.i1, b.j0, b.j1, b.k0, b.k1}, best, 0);
 }
 
@@ -629,6 +638,9 @@ void amlt_gpu_ctx_destroy(amlt_ctx* ctx) {
             if (p) cudaFree(p);
         if (ctx->ev0) cudaEventDestroy(ctx->ev0);
         if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+        for (cudaEvent_t e : ctx->pipe_ev) cudaEventDestroy(e);
+        if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
+        if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     }
     delete ctx;
@@ -753,16 +765,16 @@ amlt_status amlt_gpu_adaptive_execute(amlt_ctx* ctx, const amlt_plan* plan,
 }
 
 amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* host_ops,
-                              const amlt_tile_params* tile, const amlt_bounds* bounds,
+                              const amlt_tile_params* tile, const amlt_bounds* bounds, int flags,
                               amlt_clock_fn clock, void* clock_user, double* elapsed_s) {
     if (!ctx || !plan || !host_ops || !bounds) return AMLT_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {
         if (ctx->dry()) fail(AMLT_ERR_NO_DEVICE, "amlt_gpu_run_host needs a device context");
         cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
-        const int dt = plan->desc.dtype;
-        const int es = dtype_size(dt);
+        const int es = dtype_size(plan->desc.dtype);
+        const bool r_zero = (flags & AMLT_HOST_R_ZERO) != 0;
         // validate against the host description first (same rules)
-        (void)resolve(plan, host_ops, bounds);
+        Resolved hv = resolve(plan, host_ops, bounds);
         amlt_operands dev = *host_ops;
         const amlt_matrix* src[5] = {&host_ops->a, &host_ops->b, &host_ops->r, &host_ops->thres,
                                      &host_ops->dis};
@@ -783,23 +795,98 @@ amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_o
             }
             dst[s]->data = ctx->hbuf[s];
         }
+        if (!ctx->copy_in) {
+            cuda_check(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking), "cudaStreamCreate");
+            cuda_check(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking), "cudaStreamCreate");
+        }
+        // Row-band pipeline: band b's A rows (and R rows unless R starts at
+        // zero) go H2D on copy_in while band b-1 computes on the context
+        // stream and band b-2's R rows go D2H on copy_out. Needs A and R
+        // stored with whole rows contiguous (row-major, normal layout);
+        // otherwise one band.
+        const bool a_rows = host_ops->a.order == AMLT_ROW_MAJOR && plan->desc.layout_a == AMLT_LAYOUT_NORMAL;
+        const bool r_rows = host_ops->r.order == AMLT_ROW_MAJOR;
+        const int64_t M = hv.M;
+        int nb = 1;
+        if (a_rows && r_rows && M >= 1024) nb = static_cast<int>(std::min<int64_t>(8, M / 256));
+        while (static_cast<int>(ctx->pipe_ev.size()) < 3 * nb + 2) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+            ctx->pipe_ev.push_back(e);
+        }
+        // variant for the bands: caller's tile, else the cached winner for this
+        // shape, else the planner default
+        amlt_tile_params tp{0, 0, 0, -1};
+        if (tile) tp = *tile;
+        else {
+            auto it = ctx->tune_cache.find(std::make_tuple(plan->desc.body, plan->desc.dtype, hv.M, hv.N, hv.K));
+            if (it != ctx->tune_cache.end()) {
+                tp.variant = plan_local_index(plan, it->second.variant);
+                tp.kc = it->second.kc;
+            }
+        }
         auto body = [&] {
-            for (int s = 0; s < 5; ++s)
+            cudaEvent_t shared_ready = ctx->pipe_ev[0];
+            cudaEvent_t start_ev = ctx->pipe_ev[1];
+            cuda_check(cudaEventRecord(start_ev, ctx->stream), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(ctx->copy_in, start_ev, 0), "cudaStreamWaitEvent");
+            for (int s : {1, 3, 4})
                 if (bytes[s])
                     cuda_check(cudaMemcpyAsync(ctx->hbuf[s], src[s]->data, bytes[s],
-                                               cudaMemcpyHostToDevice, ctx->stream),
+                                               cudaMemcpyHostToDevice, ctx->copy_in),
                                "cudaMemcpyAsync H2D");
-            if (tile) {
-                Resolved rv = resolve(plan, &dev, bounds);
-                Dispatch dp = plan_dispatch(ctx, plan, tile, rv);
+            cuda_check(cudaEventRecord(shared_ready, ctx->copy_in), "cudaEventRecord");
+            const int64_t arow = host_ops->a.ld * es, rrow = host_ops->r.ld * es;
+            for (int bi = 0; bi < nb; ++bi) {
+                const int64_t r0 = bounds->i0 + M * bi / nb, r1 = bounds->i0 + M * (bi + 1) / nb;
+                cudaEvent_t in_ev = ctx->pipe_ev[2 + 3 * bi], done_ev = ctx->pipe_ev[3 + 3 * bi];
+                if (nb == 1) {
+                    cuda_check(cudaMemcpyAsync(ctx->hbuf[0], src[0]->data, bytes[0],
+                                               cudaMemcpyHostToDevice, ctx->copy_in), "H2D A");
+                } else {
+                    cuda_check(cudaMemcpyAsync(static_cast<char*>(ctx->hbuf[0]) + r0 * arow,
+                                               static_cast<const char*>(src[0]->data) + r0 * arow,
+                                               size_t(r1 - r0) * arow, cudaMemcpyHostToDevice,
+                                               ctx->copy_in), "H2D A band");
+                }
+                if (r_zero) {
+                    if (nb == 1)
+                        cuda_check(cudaMemsetAsync(ctx->hbuf[2], 0, bytes[2], ctx->copy_in), "memset R");
+                    else
+                        cuda_check(cudaMemsetAsync(static_cast<char*>(ctx->hbuf[2]) + r0 * rrow, 0,
+                                                   size_t(r1 - r0) * rrow, ctx->copy_in), "memset R band");
+                } else {
+                    if (nb == 1)
+                        cuda_check(cudaMemcpyAsync(ctx->hbuf[2], src[2]->data, bytes[2],
+                                                   cudaMemcpyHostToDevice, ctx->copy_in), "H2D R");
+                    else
+                        cuda_check(cudaMemcpyAsync(static_cast<char*>(ctx->hbuf[2]) + r0 * rrow,
+                                                   static_cast<const char*>(src[2]->data) + r0 * rrow,
+                                                   size_t(r1 - r0) * rrow, cudaMemcpyHostToDevice,
+                                                   ctx->copy_in), "H2D R band");
+                }
+                cuda_check(cudaEventRecord(in_ev, ctx->copy_in), "cudaEventRecord");
+                cuda_check(cudaStreamWaitEvent(ctx->stream, in_ev, 0), "cudaStreamWaitEvent");
+                amlt_bounds bb = *bounds;
+                bb.i0 = r0;
+                bb.i1 = r1;
+                Resolved rv = resolve(plan, &dev, &bb);
+                Dispatch dp = plan_dispatch(ctx, plan, &tp, rv);
                 enqueue(ctx, plan, rv, dp);
-            } else {
-                amlt_tune_report rep;
-                adaptive(ctx, plan, &dev, *bounds, nullptr, nullptr, nullptr, &rep);
+                cuda_check(cudaEventRecord(done_ev, ctx->stream), "cudaEventRecord");
+                cuda_check(cudaStreamWaitEvent(ctx->copy_out, done_ev, 0), "cudaStreamWaitEvent");
+                if (nb == 1)
+                    cuda_check(cudaMemcpyAsync(host_ops->r.data, ctx->hbuf[2], bytes[2],
+                                               cudaMemcpyDeviceToHost, ctx->copy_out), "D2H R");
+                else
+                    cuda_check(cudaMemcpyAsync(static_cast<char*>(host_ops->r.data) + r0 * rrow,
+                                               static_cast<const char*>(ctx->hbuf[2]) + r0 * rrow,
+                                               size_t(r1 - r0) * rrow, cudaMemcpyDeviceToHost,
+                                               ctx->copy_out), "D2H R band");
             }
-            cuda_check(cudaMemcpyAsync(host_ops->r.data, ctx->hbuf[2], bytes[2],
-                                       cudaMemcpyDeviceToHost, ctx->stream),
-                       "cudaMemcpyAsync D2H");
+            cudaEvent_t out_done = ctx->pipe_ev[2 + 3 * nb];
+            cuda_check(cudaEventRecord(out_done, ctx->copy_out), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(ctx->stream, out_done, 0), "cudaStreamWaitEvent");
         };
         double el = 0;
         if (clock) {

@@ -1,0 +1,165 @@
+// peak.cu — pipe-throughput probes used as roofline denominators.
+//
+// MEASURED_PEAKS.json (driver-written) has HBM and bf16 only; the MMLT
+// kernels are bound by the FP64 pipe (f64 bodies), the FMA pipe (f32) or the
+// integer ALU (i32). These probes run a grid-filling kernel of independent
+// dependency chains of one instruction type and report instructions/s, plus
+// the SM clock seen by the kernel (clock64 ticks / globaltimer ns), so every
+// roofline fraction can be stated against a number measured on the same box
+// in the same run.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/amlt_gpu.h"
+
+namespace amltk {
+
+constexpr int kChains = 8;
+constexpr int kIters = 4096;
+
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <int PIPE>
+__global__ void __launch_bounds__(256) peak_kernel(double* sink, unsigned long long* clk) {
+    const uint64_t c0 = clock64();
+    const uint64_t g0 = gtimer();
+    double dacc[kChains];
+    float facc[kChains];
+    int iacc[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) {
+        dacc[c] = threadIdx.x * 1e-3 + c;
+        facc[c] = threadIdx.x * 1e-3f + c;
+        iacc[c] = threadIdx.x + c;
+    }
+    const double da = 1.0000001, db = 1e-9;
+    const float fa = 1.0001f, fb = 1e-7f;
+    int ia = threadIdx.x | 1, ib = 7;
+    for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) {
+            if constexpr (PIPE == 0) dacc[c] = fma(dacc[c], da, db);
+            if constexpr (PIPE == 1) facc[c] = fmaf(facc[c], fa, fb);
+            if constexpr (PIPE == 2) {
+                // IADD3 on the integer ALU pipe; the xor keeps ptxas from folding
+                iacc[c] = (iacc[c] + ia) ^ ib;
+            }
+            if constexpr (PIPE == 3) {
+                // DSETP (FP64 compare) feeding a select: the discount body's mask op
+                dacc[c] = dacc[c] > db ? dacc[c] - da : dacc[c] + da;
+            }
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) s += dacc[c] + facc[c] + iacc[c];
+    if (s == 12345.678) sink[threadIdx.x] = s;
+    const uint64_t c1 = clock64();
+    const uint64_t g1 = gtimer();
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        clk[0] = c1 - c0;
+        clk[1] = g1 - g0;
+    }
+}
+
+// DMMA probe: independent m8n8k4 f64 MMAs (256 FMA each per warp).
+__global__ void __launch_bounds__(256) peak_dmma_kernel(double* sink, unsigned long long* clk) {
+    const uint64_t c0 = clock64();
+    const uint64_t g0 = gtimer();
+    double acc[kChains][2];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) acc[c][0] = acc[c][1] = threadIdx.x + c;
+    double a = 1.0 + threadIdx.x * 1e-9, b = 1e-9;
+    for (int it = 0; it < kIters / 4; ++it) {
+#pragma unroll
+        for (int c = 0; c < kChains; ++c)
+            asm volatile(
+                "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                : "+d"(acc[c][0]), "+d"(acc[c][1])
+                : "d"(a), "d"(b));
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) s += acc[c][0] + acc[c][1];
+    if (s == 12345.678) sink[threadIdx.x] = s;
+    const uint64_t c1 = clock64();
+    const uint64_t g1 = gtimer();
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        clk[0] = c1 - c0;
+        clk[1] = g1 - g0;
+    }
+}
+
+}  // namespace amltk
+
+extern "C" {
+
+// pipe: 0 DFMA, 1 FFMA, 2 integer ALU (IADD3+LOP3 pairs), 3 DSETP+select,
+// 4 DMMA m8n8k4. Returns per-lane operations per second (FMA pipes: FMAs/s;
+// DMMA: FMAs/s = 256 per warp instruction; ALU: 2 ops per chain step) and
+// the SM clock in GHz observed by block 0. Runs on the current device.
+amlt_status amlt_gpu_measure_peak(int pipe, double* ops_per_s, double* sm_ghz) {
+    using namespace amltk;
+    int dev = 0, sms = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return AMLT_ERR_NO_DEVICE;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return AMLT_ERR_CUDA;
+    double* sink = nullptr;
+    unsigned long long* clk = nullptr;
+    if (cudaMalloc(&sink, 256 * sizeof(double)) != cudaSuccess) return AMLT_ERR_CUDA;
+    if (cudaMalloc(&clk, 2 * sizeof(unsigned long long)) != cudaSuccess) {
+        cudaFree(sink);
+        return AMLT_ERR_CUDA;
+    }
+    const int blocks = sms * 8;  // 8 x 256 threads = 64 warps per SM
+    auto launch = [&]() {
+        switch (pipe) {
+            case 0: peak_kernel<0><<<blocks, 256>>>(sink, clk); break;
+            case 1: peak_kernel<1><<<blocks, 256>>>(sink, clk); break;
+            case 2: peak_kernel<2><<<blocks, 256>>>(sink, clk); break;
+            case 3: peak_kernel<3><<<blocks, 256>>>(sink, clk); break;
+            default: peak_dmma_kernel<<<blocks, 256>>>(sink, clk); break;
+        }
+    };
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    launch();  // warm-up (clock ramp, module load)
+    launch();
+    float best = 1e30f;
+    for (int r = 0; r < 3; ++r) {
+        cudaEventRecord(e0);
+        launch();
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best) best = ms;
+    }
+    unsigned long long hc[2] = {0, 0};
+    cudaMemcpy(hc, clk, sizeof(hc), cudaMemcpyDeviceToHost);
+    cudaError_t err = cudaGetLastError();
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    cudaFree(clk);
+    if (err != cudaSuccess) return AMLT_ERR_CUDA;
+    const double threads = double(blocks) * 256.0;
+    double ops;
+    if (pipe == 4)
+        ops = double(blocks) * 8.0 * kChains * (kIters / 4) * 256.0;  // warps * mmas * 256 FMA
+    else if (pipe == 2)
+        ops = threads * kChains * kIters * 2.0;
+    else
+        ops = threads * kChains * kIters;
+    if (ops_per_s) *ops_per_s = ops / (best * 1e-3);
+    if (sm_ghz) *sm_ghz = hc[1] ? double(hc[0]) / double(hc[1]) : 0.0;
+    return AMLT_OK;
+}
+
+}  // extern "C"

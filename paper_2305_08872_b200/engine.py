@@ -501,9 +501,11 @@ def adaptive_execute(plan: GpuPlan, ops: Operands, bounds: Bounds, pack: bool = 
 
 
 def run_host(plan: GpuPlan, ops: Operands, bounds: Bounds, params: Optional[TileParams] = None,
-             clock: Optional[Clock] = None) -> float:
-    """Host-buffer entry: H2D of the operands, run (adaptive if params is
-    None), D2H of R into ops.r; returns elapsed seconds for all of it."""
+             clock: Optional[Clock] = None, r_zero: bool = False) -> float:
+    """Host-buffer entry: operands in host memory (pinned for full speed).
+    Copies in, computes (row bands pipelined against the copies), copies R
+    back into ops.r; returns elapsed seconds for all of it. r_zero=True
+    states R starts at zero (zero-filled on the device, not copied in)."""
     ctx = plan.ctx
     bridge = _ClockBridge(clock)
     oc = ops._c(False)
@@ -512,7 +514,8 @@ def run_host(plan: GpuPlan, ops: Operands, bounds: Bounds, params: Optional[Tile
     el = C.c_double()
     st = ctx._lib.amlt_gpu_run_host(ctx.handle, plan.handle, C.byref(oc),
                                     C.byref(tp) if tp is not None else None, C.byref(bc),
-                                    bridge.fn, None, C.byref(el))
+                                    N.HOST_R_ZERO if r_zero else 0, bridge.fn, None,
+                                    C.byref(el))
     bridge.check()
     _raise(st, ctx.handle)
     return el.value
@@ -528,6 +531,17 @@ def run_adaptive(plan: GpuPlan, ops: Operands, bounds: Bounds, pack=False,
                  clock: Optional[Clock] = None, log: Optional[ExecLog] = None) -> TuneReport:
     """run_adaptive (engine.hpp:65-66)."""
     return adaptive_execute(plan, ops, bounds, pack, clock, log)
+
+
+def measure_peak(pipe: str) -> tuple:
+    """(lane ops/s, SM GHz) of one pipe on the current device: 'dfma',
+    'ffma', 'alu', 'dsetp', 'dmma' (roofline denominators)."""
+    code = {"dfma": 0, "ffma": 1, "alu": 2, "dsetp": 3, "dmma": 4}[pipe]
+    ops, ghz = C.c_double(), C.c_double()
+    st = N.lib().amlt_gpu_measure_peak(code, C.byref(ops), C.byref(ghz))
+    if st != N.OK:
+        raise CudaError(f"measure_peak({pipe}) failed: status {st}")
+    return ops.value, ghz.value
 
 
 def spr(M: int, K: int, N_: int, seconds: float) -> float:

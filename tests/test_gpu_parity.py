@@ -52,6 +52,9 @@ def test_int_valued_all_variants_bit_exact(gpu_ctx, body, dtype):
     plan = gpu_ctx.plan(body, dtype)
     for vi, v in enumerate(plan.variants()):
         for (M, K, N) in ACCEPT_DIMS:
+            vn = 2 if dtype == "f64" else 4
+            if not v.name.endswith("_u") and (K % vn or N % vn):
+                continue  # 16-byte staging needs vector-multiple strides
             A, B, t, d = make_inputs(body, M, K, N, "int", seed=M * 7 + K)
             want = oracle(body, A, B, t, d)
             tile = P.TileParams(variant=vi)  # the unaligned variant runs on aligned data too
