@@ -337,8 +337,11 @@ Dispatch plan_dispatch(const amlt_ctx* ctx, const amlt_plan* plan, const amlt_ti
     dp.variant = choose_variant(ctx, plan, tile, rv);
     dp.kslice = rv.K;
     if (tile && tile->kc > 0 && tile->kc < rv.K) {
-        dp.splits = static_cast<int>((rv.K + tile->kc - 1) / tile->kc);
-        dp.kslice = tile->kc;
+        // Segment starts stay multiples of 32 elements so every segment's
+        // operand rows keep the 16-byte alignment the staged copies need.
+        const int64_t kc = (tile->kc + 31) / 32 * 32;
+        dp.splits = static_cast<int>((rv.K + kc - 1) / kc);
+        dp.kslice = kc;
         if (dp.splits > 65535) fail(AMLT_ERR_INVALID_ARGUMENT, "kc too small: more than 65535 K segments");
     }
     return dp;
@@ -425,7 +428,7 @@ Resolved resolve_sub(const amlt_plan* plan, const amlt_operands* ops, const amlt
 //
 // Candidates are the plan's tile variants (+ split-K forms when the output is
 // too small to fill the GPU). Each candidate runs ONE row band of the real
-// task (full N, full K), large enough to keep every SM busy for >= 2 waves,
+// task (full N, full K), large enough to keep every SM busy for one wave,
 // and is scored by elapsed / rows. The rest of the rows run with the winner.
 // Every band writes its rows of R, so no work is repeated, and the coverage
 // ledger proves every output is produced exactly once. A problem too small to
@@ -453,14 +456,14 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
         const VariantDesc& v = vdesc(idx);
         if (v.vec == whole.aligned && (!v.tc || whole.aligned)) cands.push_back(idx);
     }
-    // band height per candidate: >= 2 full waves of CTAs across all SMs
+    // band height per candidate: one full wave of CTAs across all SMs
     std::vector<int64_t> band(cands.size());
     int64_t need = 0;
     for (size_t c = 0; c < cands.size(); ++c) {
         const VariantDesc& v = vdesc(cands[c]);
         const int occ = ctx->occupancy.empty() ? v.minb : std::max(1, ctx->occupancy[cands[c]]);
         const int64_t tiles_n = (whole.N + v.bn - 1) / v.bn;
-        const int64_t want_ctas = int64_t(2) * ctx->num_sms * occ;
+        const int64_t want_ctas = int64_t(ctx->num_sms) * occ;  // one full wave
         const int64_t tiles_m = std::max<int64_t>(1, (want_ctas + tiles_n - 1) / tiles_n);
         band[c] = tiles_m * v.bm;
         need += band[c];
