@@ -812,7 +812,9 @@ amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_o
         const int64_t M = hv.M;
         int nb = 1;
         if (a_rows && r_rows && M >= 1024) nb = static_cast<int>(std::min<int64_t>(8, M / 256));
-        while (static_cast<int>(ctx->pipe_ev.size()) < 3 * nb + 2) {
+        // events: [0] shared inputs ready, [1] start, per band [2+3b] inputs
+        // in, [3+3b] computed, and [2+3nb] all outputs out
+        while (static_cast<int>(ctx->pipe_ev.size()) < 3 * nb + 3) {
             cudaEvent_t e;
             cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
             ctx->pipe_ev.push_back(e);
