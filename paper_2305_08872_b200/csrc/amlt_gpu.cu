@@ -23,6 +23,8 @@
 #include "../../include/amlt_gpu.h"
 #include "variants.h"
 
+#include <cudaTypedefs.h>
+
 using namespace amltk;
 
 namespace {
@@ -232,8 +234,8 @@ Resolved resolve(const amlt_plan* plan, const amlt_operands* ops, const amlt_bou
     const int es = dtype_size(d.dtype);
     const int vn = 16 / es;
     auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    rv.aligned = al16(kp.A) && al16(kp.B) && (kp.lda % vn == 0 || rv.M <= 1) &&
-                 (kp.ldb % vn == 0 || rv.K <= 1);
+    // TMA staging: 16-byte aligned bases and row pitches
+    rv.aligned = al16(kp.A) && al16(kp.B) && kp.lda % vn == 0 && kp.ldb % vn == 0;
     kp.r_vec_ok = al16(kp.R) && (kp.ldr % vn == 0 || rv.M <= 1);
     return rv;
 }
@@ -316,6 +318,40 @@ int plan_local_index(const amlt_plan* plan, int reg_idx) {
 // ---------------------------------------------------------------------------
 // launch
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no
+// libcuda link dependency).
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) fail(AMLT_ERR_CUDA, "cuTensorMapEncodeTiled is unavailable");
+    return fn;
+}
+
+void make_tensor_map(CUtensorMap* m, int dtype, const void* base, uint64_t inner, uint64_t outer,
+                     uint64_t row_bytes, int box_inner, int box_outer) {
+    const CUtensorMapDataType dt = dtype == AMLT_F64   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                   : dtype == AMLT_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                                       : CU_TENSOR_MAP_DATA_TYPE_INT32;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = tensor_map_encoder()(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fail(AMLT_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+}
+
 void ensure_work(amlt_ctx* ctx, size_t bytes) {
     if (bytes <= ctx->work_bytes) return;
     if (ctx->work) cudaFree(ctx->work);
@@ -371,7 +407,20 @@ void enqueue(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch&
         ensure_work(ctx, size_t(dp.splits) * size_t(rv.M) * size_t(rv.N) * dtype_size(plan->desc.dtype));
         kp.work = ctx->work;
     }
-    cuda_check(v.launch(kp, dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(dp.splits)),
+    CUtensorMap ma, mb;
+    std::memset(&ma, 0, sizeof(ma));
+    std::memset(&mb, 0, sizeof(mb));
+    if (v.vec && !v.tc) {
+        const int es = dtype_size(plan->desc.dtype);
+        // A: inner dim k (K), outer dim i (M), box BK x BM; B: inner j (N),
+        // outer k (K), box BN x BK. Zero fill outside the bounds rectangle.
+        make_tensor_map(&ma, plan->desc.dtype, kp.A, uint64_t(rv.K), uint64_t(rv.M),
+                        uint64_t(kp.lda) * es, v.bk, v.bm);
+        make_tensor_map(&mb, plan->desc.dtype, kp.B, uint64_t(rv.N), uint64_t(rv.K),
+                        uint64_t(kp.ldb) * es, v.bn, v.bk);
+    }
+    cuda_check(v.launch(kp, ma, mb,
+                        dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(dp.splits)),
                         ctx->stream),
                "tile kernel launch");
     if (dp.splits > 1) {

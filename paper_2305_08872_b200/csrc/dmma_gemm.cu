@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB) dmma_gemm_kernel
 }
 
 template <int WTM, int WTN, int WARPS_M, int WARPS_N, int BK, int STAGES, int MINB>
-cudaError_t launch_dmma(const KParams& p, dim3 grid, cudaStream_t s) {
+cudaError_t launch_dmma(const KParams& p, const CUtensorMap&, const CUtensorMap&, dim3 grid,
+                        cudaStream_t s) {
     using Cfg = DmmaCfg<WTM, WTN, WARPS_M, WARPS_N, BK, STAGES>;
     dmma_gemm_kernel<WTM, WTN, WARPS_M, WARPS_N, BK, STAGES, MINB>
         <<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(p);

@@ -17,20 +17,20 @@ void AMLT_CAT4(register_, AMLT_BODY, _, AMLT_DT)(Registry& reg) {
     using Body = AMLT_CAT(Body, AMLT_BODY)<T>;
     constexpr int ID = AMLT_BODY_ID;
     constexpr int DT = AMLT_DT;
-    //                    TM TN WR WC BK ST  VEC  MINB
+    //                    TM TN WR WC BK ST  LOAD       MINB
     if constexpr (sizeof(T) == 8) {
-        add_variant<Body, T, 8, 4, 8, 1, 16, 3, true, 1>(reg, ID, DT, "t8x4_w8x1");
-        add_variant<Body, T, 8, 2, 8, 1, 16, 3, true, 2>(reg, ID, DT, "t8x2_w8x1");
-        add_variant<Body, T, 4, 4, 8, 1, 16, 3, true, 2>(reg, ID, DT, "t4x4_w8x1");
-        add_variant<Body, T, 4, 4, 4, 1, 16, 4, true, 3>(reg, ID, DT, "t4x4_w4x1");
-        add_variant<Body, T, 4, 2, 4, 1, 16, 4, true, 4>(reg, ID, DT, "t4x2_w4x1");
-        add_variant<Body, T, 4, 4, 8, 1, 16, 3, false, 2>(reg, ID, DT, "t4x4_w8x1_u");
+        add_variant<Body, T, 8, 4, 8, 1, 16, 3, LOAD_TMA, 1>(reg, ID, DT, "t8x4_w8x1");
+        add_variant<Body, T, 8, 2, 8, 1, 16, 3, LOAD_TMA, 2>(reg, ID, DT, "t8x2_w8x1");
+        add_variant<Body, T, 4, 4, 8, 1, 16, 3, LOAD_TMA, 2>(reg, ID, DT, "t4x4_w8x1");
+        add_variant<Body, T, 4, 4, 4, 1, 16, 4, LOAD_TMA, 3>(reg, ID, DT, "t4x4_w4x1");
+        add_variant<Body, T, 4, 2, 4, 1, 16, 4, LOAD_TMA, 4>(reg, ID, DT, "t4x2_w4x1");
+        add_variant<Body, T, 4, 4, 8, 1, 16, 3, LOAD_ELEM, 2>(reg, ID, DT, "t4x4_w8x1_u");
     } else {
-        add_variant<Body, T, 8, 8, 4, 1, 32, 3, true, 1>(reg, ID, DT, "t8x8_w4x1");
-        add_variant<Body, T, 8, 4, 8, 1, 32, 3, true, 1>(reg, ID, DT, "t8x4_w8x1");
-        add_variant<Body, T, 4, 4, 8, 1, 32, 3, true, 2>(reg, ID, DT, "t4x4_w8x1");
-        add_variant<Body, T, 4, 4, 4, 1, 32, 4, true, 3>(reg, ID, DT, "t4x4_w4x1");
-        add_variant<Body, T, 4, 4, 8, 1, 32, 3, false, 2>(reg, ID, DT, "t4x4_w8x1_u");
+        add_variant<Body, T, 8, 8, 4, 1, 32, 3, LOAD_TMA, 1>(reg, ID, DT, "t8x8_w4x1");
+        add_variant<Body, T, 8, 4, 8, 1, 32, 3, LOAD_TMA, 1>(reg, ID, DT, "t8x4_w8x1");
+        add_variant<Body, T, 4, 4, 8, 1, 32, 3, LOAD_TMA, 2>(reg, ID, DT, "t4x4_w8x1");
+        add_variant<Body, T, 4, 4, 4, 1, 32, 4, LOAD_TMA, 3>(reg, ID, DT, "t4x4_w4x1");
+        add_variant<Body, T, 4, 4, 8, 1, 32, 3, LOAD_ELEM, 2>(reg, ID, DT, "t4x4_w8x1_u");
     }
     BodyAux a;
     a.body = ID;

@@ -9,7 +9,8 @@
 //
 // Structure (one CTA = BM x BN output tile, one thread = TM x TN micro-tile):
 //  * A (BM x BK) and B (BK x BN) tiles are staged into shared memory with a
-//    STAGES-deep cp.async (LDGSTS) ring: the reference's packing
+//    STAGES-deep TMA ring (cp.async.bulk.tensor + mbarrier; per-element
+//    cp.async for unaligned operands): the reference's packing
 //    (src/packing.cpp:5-45) becomes the SMEM copy.
 //  * Every lane of a warp owns the SAME TM rows, so each A read is a 16-byte
 //    shared-memory broadcast (one wavefront, no bank conflicts); B reads are
@@ -24,6 +25,7 @@
 //    reduced in segment order by mmlt_splitk_reduce: deterministic.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -250,9 +252,54 @@ __device__ __forceinline__ void BodyThrcount<int>::step(int* acc, int a, int b, 
 }
 
 // --------------------------------------------------------------------------
-// The tiled kernel
+// TMA + mbarrier helpers (sm_90+ PTX; on sm_100a the copies are UTMALDG)
 
-template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, bool VEC,
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// --------------------------------------------------------------------------
+// The tiled kernel
+//
+// LOAD selects the staging path:
+//   LOAD_TMA   one thread issues two cp.async.bulk.tensor copies per stage (A
+//              box BK x BM, B box BN x BK) that complete on the stage's
+//              mbarrier; out-of-range rows/columns arrive zero-filled. No
+//              per-thread address arithmetic in the main loop.
+//   LOAD_ELEM  per-element cp.async (4/8-byte LDGSTS) for operands whose base
+//              or leading dimension is not 16-byte aligned.
+
+constexpr int LOAD_ELEM = 0;
+constexpr int LOAD_TMA = 1;
+
+template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, int LOAD,
           int MINB>
 struct MmltTile {
     static constexpr int VN = V16<T>::n;
@@ -261,16 +308,21 @@ struct MmltTile {
     static constexpr int BN = 32 * TN * WC;
     static constexpr int SMEM_A = BM * BK;  // elements per stage
     static constexpr int SMEM_B = BK * BN;
-    static constexpr int SMEM_BYTES = STAGES * (SMEM_A + SMEM_B) * (int)sizeof(T);
+    static constexpr int BAR_BYTES = 8 * STAGES;
+    static constexpr int SMEM_BYTES = STAGES * (SMEM_A + SMEM_B) * (int)sizeof(T) + 128;
     static_assert(TN % VN == 0, "TN must be a multiple of the 16B vector width");
     static_assert(BK % VN == 0, "BK must be a multiple of the 16B vector width");
     static_assert(STAGES >= 2, "need at least double buffering");
+    static_assert((SMEM_A * sizeof(T)) % 128 == 0, "TMA stage buffers must stay 128B aligned");
+    static_assert(BN <= 256 && BM <= 256 && BK <= 256, "TMA box dims are at most 256");
 };
 
-template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, bool VEC,
+template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, int LOAD,
           int MINB>
-__global__ void __launch_bounds__(32 * WR * WC, MINB) mmlt_tile_kernel(const KParams p) {
-    using Cfg = MmltTile<Body, T, TM, TN, WR, WC, BK, STAGES, VEC, MINB>;
+__global__ void __launch_bounds__(32 * WR * WC, MINB)
+    mmlt_tile_kernel(const __grid_constant__ KParams p, const __grid_constant__ CUtensorMap tmA,
+                     const __grid_constant__ CUtensorMap tmB) {
+    using Cfg = MmltTile<Body, T, TM, TN, WR, WC, BK, STAGES, LOAD, MINB>;
     constexpr int VN = Cfg::VN;
     constexpr int THREADS = Cfg::THREADS;
     constexpr int BM = Cfg::BM;
@@ -282,6 +334,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB) mmlt_tile_kernel(const KPa
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* As = reinterpret_cast<T*>(smem_raw);
     T* Bs = As + STAGES * Cfg::SMEM_A;
+    uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * Cfg::SMEM_B);
 
     // ---- tile coordinates: grouped raster (8 row-tiles per group) so the B
     // column panels of concurrently resident CTAs are shared through L2.
@@ -309,56 +362,62 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB) mmlt_tile_kernel(const KPa
 
     const T* __restrict__ Ag = static_cast<const T*>(p.A);
     const T* __restrict__ Bg = static_cast<const T*>(p.B);
+    const int nkt = static_cast<int>((kspan + BK - 1) / BK);
 
-    // ---- stage loader
-    auto load_tile = [&](int stage, int64_t k0) {
+    // ---- stage loaders
+    constexpr uint32_t STAGE_TX = (Cfg::SMEM_A + Cfg::SMEM_B) * sizeof(T);
+    auto tma_stage = [&](int stage, int kt) {  // called by one thread
+        mbar_expect_tx(&full[stage], STAGE_TX);
+        const int32_t k = static_cast<int32_t>(kbeg + static_cast<int64_t>(kt) * BK);
+        tma_load_2d(As + stage * Cfg::SMEM_A, &tmA, k, static_cast<int32_t>(m0), &full[stage]);
+        tma_load_2d(Bs + stage * Cfg::SMEM_B, &tmB, static_cast<int32_t>(n0), k, &full[stage]);
+    };
+    auto elem_stage = [&](int stage, int kt) {  // called by all threads
         T* as = As + stage * Cfg::SMEM_A;
         T* bs = Bs + stage * Cfg::SMEM_B;
+        const int64_t k0 = kbeg + static_cast<int64_t>(kt) * BK;
         const int64_t kend = kbeg + kspan;
-        if constexpr (VEC) {
-            constexpr int ACH = BK / VN;  // 16B chunks per A tile row
-            for (int c = tid; c < BM * ACH; c += THREADS) {
-                const int row = c / ACH;
-                const int kc = (c - row * ACH) * VN;
-                const int64_t gi = m0 + row;
-                const int64_t gk = k0 + kc;
-                int64_t rem = (gi < p.M) ? (kend - gk) : 0;
-                rem = rem < 0 ? 0 : (rem > VN ? VN : rem);
-                const T* src = rem > 0 ? Ag + gi * p.lda + gk : Ag;
-                cp_async16(as + row * BK + kc, src, static_cast<int>(rem * sizeof(T)));
-            }
-            constexpr int BCH = BN / VN;
-            for (int c = tid; c < BK * BCH; c += THREADS) {
-                const int kr = c / BCH;
-                const int cc = (c - kr * BCH) * VN;
-                const int64_t gk = k0 + kr;
-                const int64_t gj = n0 + cc;
-                int64_t rem = (gk < kend) ? (p.N - gj) : 0;
-                rem = rem < 0 ? 0 : (rem > VN ? VN : rem);
-                const T* src = rem > 0 ? Bg + gk * p.ldb + gj : Bg;
-                cp_async16(bs + kr * BN + cc, src, static_cast<int>(rem * sizeof(T)));
-            }
-        } else {
-            for (int c = tid; c < BM * BK; c += THREADS) {
-                const int row = c / BK;
-                const int kc = c - row * BK;
-                const int64_t gi = m0 + row;
-                const int64_t gk = k0 + kc;
-                const bool ok = gi < p.M && gk < kend;
-                cp_async_elem<sizeof(T)>(as + row * BK + kc, ok ? Ag + gi * p.lda + gk : Ag,
-                                         ok ? (int)sizeof(T) : 0);
-            }
-            for (int c = tid; c < BK * BN; c += THREADS) {
-                const int kr = c / BN;
-                const int cc = c - kr * BN;
-                const int64_t gk = k0 + kr;
-                const int64_t gj = n0 + cc;
-                const bool ok = gk < kend && gj < p.N;
-                cp_async_elem<sizeof(T)>(bs + kr * BN + cc, ok ? Bg + gk * p.ldb + gj : Bg,
-                                         ok ? (int)sizeof(T) : 0);
-            }
+        for (int c = tid; c < BM * BK; c += THREADS) {
+            const int row = c / BK;
+            const int kc = c - row * BK;
+            const int64_t gi = m0 + row;
+            const int64_t gk = k0 + kc;
+            const bool ok = gi < p.M && gk < kend;
+            cp_async_elem<sizeof(T)>(as + row * BK + kc, ok ? Ag + gi * p.lda + gk : Ag,
+                                     ok ? (int)sizeof(T) : 0);
+        }
+        for (int c = tid; c < BK * BN; c += THREADS) {
+            const int kr = c / BN;
+            const int cc = c - kr * BN;
+            const int64_t gk = k0 + kr;
+            const int64_t gj = n0 + cc;
+            const bool ok = gk < kend && gj < p.N;
+            cp_async_elem<sizeof(T)>(bs + kr * BN + cc, ok ? Bg + gk * p.ldb + gj : Bg,
+                                     ok ? (int)sizeof(T) : 0);
         }
     };
+
+    if constexpr (LOAD == LOAD_TMA) {
+        if (tid == 0) {
+#pragma unroll
+            for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+        }
+        __syncthreads();
+        if (tid == 0) {
+#pragma unroll
+            for (int s = 0; s < STAGES; ++s)
+                if (s < nkt) tma_stage(s, s);
+        }
+    } else {
+#pragma unroll
+        for (int s = 0; s < STAGES - 1; ++s) {
+            if (s < nkt) elem_stage(s, s);
+            cp_async_commit();
+        }
+    }
 
     // ---- per-thread columns: local col of element (q, e) is
     //      wc*32*TN + q*32*VN + lane*VN + e
@@ -388,28 +447,22 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB) mmlt_tile_kernel(const KPa
                 for (int n = 0; n < NACC; ++n) part[r][c][n] = Acc(0);
     }
 
-    const int nkt = static_cast<int>((kspan + BK - 1) / BK);
-#pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < nkt) load_tile(s, kbeg + static_cast<int64_t>(s) * BK);
-        cp_async_commit();
-    }
-
     for (int kt = 0; kt < nkt; ++kt) {
-        cp_async_wait<STAGES - 2>();
-        __syncthreads();
-        {
+        const int stage = kt % STAGES;
+        if constexpr (LOAD == LOAD_TMA) {
+            mbar_wait(&full[stage], static_cast<uint32_t>((kt / STAGES) & 1));
+        } else {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();
             const int nxt = kt + STAGES - 1;
-            if (nxt < nkt) load_tile(nxt % STAGES, kbeg + static_cast<int64_t>(nxt) * BK);
+            if (nxt < nkt) elem_stage(nxt % STAGES, nxt);
             cp_async_commit();
         }
-        const int stage = kt % STAGES;
         const T* as = As + stage * Cfg::SMEM_A + (wr * TM) * BK;
         const T* bs = Bs + stage * Cfg::SMEM_B + wc * 32 * TN + lane * VN;
-        const int kcount = static_cast<int>(min(static_cast<int64_t>(BK), kspan - static_cast<int64_t>(kt) * BK));
+        const int kcount =
+            static_cast<int>(min(static_cast<int64_t>(BK), kspan - static_cast<int64_t>(kt) * BK));
 
-        auto* work = Body::TWO_LEVEL ? &part[0][0][0] : &acc[0][0][0];
-        (void)work;
         if (kcount == BK) {
 #pragma unroll
             for (int kk = 0; kk < BK; kk += VN) {
@@ -471,8 +524,13 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB) mmlt_tile_kernel(const KPa
                         part[r][c][n] = Acc(0);
                     }
         }
+        if constexpr (LOAD == LOAD_TMA) {
+            // every warp is done reading this stage: refill it with tile kt+STAGES
+            __syncthreads();
+            if (tid == 0 && kt + STAGES < nkt) tma_stage(stage, kt + STAGES);
+        }
     }
-    cp_async_wait<0>();
+    if constexpr (LOAD != LOAD_TMA) cp_async_wait<0>();
 
     // ---- epilogue: R (+)= value, or the split-K workspace
     T* Rg = static_cast<T*>(p.R);

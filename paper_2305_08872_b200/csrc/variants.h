@@ -16,17 +16,21 @@
 namespace amltk {
 
 using LaunchFn = cudaError_t (*)(const KParams&, dim3 grid, cudaStream_t);
+// Tile kernels also take the two TMA descriptors (A box BK x BM, B box
+// BN x BK); element-staged variants receive zeroed descriptors.
+using TileLaunchFn = cudaError_t (*)(const KParams&, const CUtensorMap& a, const CUtensorMap& b,
+                                     dim3 grid, cudaStream_t);
 
 struct VariantDesc {
     int body = 0;
     int dtype = 0;
     int bm = 0, bn = 0, bk = 0, tm = 0, tn = 0;
     int threads = 0, stages = 0, smem = 0, minb = 1;
-    bool vec = true;  // 16-byte staging (needs aligned operands)
+    bool vec = true;  // TMA staging (needs 16-byte aligned operands and strides)
     bool tc = false;  // tensor-core (DMMA) variant
     const char* name = "";
     const void* func = nullptr;
-    LaunchFn launch = nullptr;
+    TileLaunchFn launch = nullptr;
 };
 
 // Per (body, dtype) helpers that are not tile variants.
@@ -49,10 +53,11 @@ struct Registry {
 void register_all(Registry& reg);
 
 template <class Cfg, class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES,
-          bool VEC, int MINB>
-cudaError_t launch_tile(const KParams& p, dim3 grid, cudaStream_t s) {
-    mmlt_tile_kernel<Body, T, TM, TN, WR, WC, BK, STAGES, VEC, MINB>
-        <<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(p);
+          int LOAD, int MINB>
+cudaError_t launch_tile(const KParams& p, const CUtensorMap& a, const CUtensorMap& b, dim3 grid,
+                        cudaStream_t s) {
+    mmlt_tile_kernel<Body, T, TM, TN, WR, WC, BK, STAGES, LOAD, MINB>
+        <<<grid, Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(p, a, b);
     return cudaGetLastError();
 }
 
@@ -68,10 +73,10 @@ cudaError_t launch_reduce(const KParams& p, dim3 grid, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, bool VEC,
+template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, int LOAD,
           int MINB>
 void add_variant(Registry& reg, int body, int dtype, const char* name) {
-    using Cfg = MmltTile<Body, T, TM, TN, WR, WC, BK, STAGES, VEC, MINB>;
+    using Cfg = MmltTile<Body, T, TM, TN, WR, WC, BK, STAGES, LOAD, MINB>;
     // Register budget guard: accumulators (two-level bodies keep a second
     // set) must leave room for operands; larger tiles are not instantiated.
     constexpr int acc_regs =
@@ -89,11 +94,11 @@ void add_variant(Registry& reg, int body, int dtype, const char* name) {
         v.stages = STAGES;
         v.smem = Cfg::SMEM_BYTES;
         v.minb = MINB;
-        v.vec = VEC;
+        v.vec = LOAD == LOAD_TMA;
         v.name = name;
         v.func = reinterpret_cast<const void*>(
-            &mmlt_tile_kernel<Body, T, TM, TN, WR, WC, BK, STAGES, VEC, MINB>);
-        v.launch = &launch_tile<Cfg, Body, T, TM, TN, WR, WC, BK, STAGES, VEC, MINB>;
+            &mmlt_tile_kernel<Body, T, TM, TN, WR, WC, BK, STAGES, LOAD, MINB>);
+        v.launch = &launch_tile<Cfg, Body, T, TM, TN, WR, WC, BK, STAGES, LOAD, MINB>;
         reg.variants.push_back(v);
     }
 }

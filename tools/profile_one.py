@@ -1,0 +1,33 @@
+"""Runs one MMLT configuration a few times through the C-ABI (for ncu).
+
+    python tools/profile_one.py <body> <dtype> M K N [variant] [reps]
+
+Device-resident BASELINE-distribution inputs; prints per-launch ms.
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2305_08872_b200 as P  # noqa: E402
+from bench import gen_inputs  # noqa: E402
+
+body, dtype = sys.argv[1], sys.argv[2]
+M, K, N = (int(x) for x in sys.argv[3:6])
+variant = int(sys.argv[6]) if len(sys.argv) > 6 else -1
+reps = int(sys.argv[7]) if len(sys.argv) > 7 else 2
+dev = torch.device("cuda", 0)
+ctx = P.Context(0)
+plan = ctx.plan(body, dtype)
+A, B, th, ds = gen_inputs(body, dtype, M, K, N, 0, 0, dev, False)
+R = torch.zeros((M, N), dtype=A.dtype, device=dev)
+ops = P.Operands(A, B, R, th, ds)
+vs = plan.variants()
+if variant < 0:
+    variant = plan.default_variant(M, N, K)
+print("variant", vs[variant].name, flush=True)
+for _ in range(reps):
+    el = P.run_subtask(plan, ops, P.TileParams(variant=variant), P.Bounds(0, M, 0, N, 0, K))
+    print(f"{el * 1e3:.3f} ms  {2 * M * N * K / el / 1e12:.3f} TFLOP/s", flush=True)
