@@ -10,8 +10,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 
 #include "../../include/amlt_gpu.h"
+#include "mmlt_kernel.cuh"
 
 namespace amltk {
 
@@ -95,6 +97,54 @@ __global__ void __launch_bounds__(256) peak_dmma_kernel(double* sink, unsigned l
     }
 }
 
+
+// Body probe: the fused body of one MMLT kernel on register operands only
+// (no shared memory, no barriers): 4 a-values x 8 b-values per round, each
+// of the 32 products updating its own accumulator chain. Its iteration rate
+// is the ceiling the tiled kernel's instruction mix can reach on this chip.
+template <class Body, typename T>
+__global__ void __launch_bounds__(256) body_probe_kernel(const KParams p, double* sink,
+                                                         unsigned long long* clk) {
+    const uint64_t c0 = clock64();
+    const uint64_t g0 = gtimer();
+    T a[8], b[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        a[c] = static_cast<T>((threadIdx.x + c) % 10);
+        b[c] = static_cast<T>(1 + (threadIdx.x * 7 + c) % 97);
+    }
+    typename Body::Col col[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) col[c] = Body::col(p, c);
+    typename Body::Acc acc[4][8][Body::NACC];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+#pragma unroll
+            for (int n = 0; n < Body::NACC; ++n) acc[r][c][n] = 0;
+    for (int it = 0; it < kIters / 8; ++it) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c) asm volatile("" : "+r"(*reinterpret_cast<int*>(&b[c])));
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) Body::step(acc[r][c], a[r], b[c], col[c]);
+    }
+    double s = 0;
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) s += static_cast<double>(Body::finish(acc[r][c], col[c], kIters));
+    if (s == 12345.678) sink[threadIdx.x] = s;
+    const uint64_t c1 = clock64();
+    const uint64_t g1 = gtimer();
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        clk[0] = c1 - c0;
+        clk[1] = g1 - g0;
+    }
+}
+
 }  // namespace amltk
 
 extern "C" {
@@ -116,14 +166,28 @@ amlt_status amlt_gpu_measure_peak(int pipe, double* ops_per_s, double* sm_ghz) {
         cudaFree(sink);
         return AMLT_ERR_CUDA;
     }
-    const int blocks = sms * 8;  // 8 x 256 threads = 64 warps per SM
+    const int blocks = sms * (pipe >= 5 ? 2 : 8);  // probes: 64 / 16 warps per SM
+    // body probes read thres (constant) and dis (a small device vector)
+    KParams bp;
+    std::memset(&bp, 0, sizeof(bp));
+    bp.tconst = 50.0;
+    bp.dis = sink;  // zeroed below: dis = 0 -> c1 = 1
+    bp.d_sj = 0;
+    cudaMemset(sink, 0, 256 * sizeof(double));
     auto launch = [&]() {
         switch (pipe) {
             case 0: peak_kernel<0><<<blocks, 256>>>(sink, clk); break;
             case 1: peak_kernel<1><<<blocks, 256>>>(sink, clk); break;
             case 2: peak_kernel<2><<<blocks, 256>>>(sink, clk); break;
             case 3: peak_kernel<3><<<blocks, 256>>>(sink, clk); break;
-            default: peak_dmma_kernel<<<blocks, 256>>>(sink, clk); break;
+            case 4: peak_dmma_kernel<<<blocks, 256>>>(sink, clk); break;
+            case 5: body_probe_kernel<BodyDiscount<double>, double><<<blocks, 256>>>(bp, sink, clk); break;
+            case 6: body_probe_kernel<BodyBoost<double>, double><<<blocks, 256>>>(bp, sink, clk); break;
+            case 7: body_probe_kernel<BodyBoost<float>, float><<<blocks, 256>>>(bp, sink, clk); break;
+            case 8: body_probe_kernel<BodySqdiff<float>, float><<<blocks, 256>>>(bp, sink, clk); break;
+            case 9: body_probe_kernel<BodyEqcount<int>, int><<<blocks, 256>>>(bp, sink, clk); break;
+            case 10: body_probe_kernel<BodyGemm<float>, float><<<blocks, 256>>>(bp, sink, clk); break;
+            default: body_probe_kernel<BodyGemm<double>, double><<<blocks, 256>>>(bp, sink, clk); break;
         }
     };
     cudaEvent_t e0, e1;
@@ -151,7 +215,9 @@ amlt_status amlt_gpu_measure_peak(int pipe, double* ops_per_s, double* sm_ghz) {
     if (err != cudaSuccess) return AMLT_ERR_CUDA;
     const double threads = double(blocks) * 256.0;
     double ops;
-    if (pipe == 4)
+    if (pipe >= 5)
+        ops = threads * 32.0 * (kIters / 8);  // inner iterations (4 x 8 per round)
+    else if (pipe == 4)
         ops = double(blocks) * 8.0 * kChains * (kIters / 4) * 256.0;  // warps * mmas * 256 FMA
     else if (pipe == 2)
         ops = threads * kChains * kIters * 2.0;
