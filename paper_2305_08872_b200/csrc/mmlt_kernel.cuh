@@ -29,8 +29,6 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include <type_traits>
-
 namespace amltk {
 
 // --------------------------------------------------------------------------
@@ -157,54 +155,8 @@ struct BodyDiscount {
         T f = pr > c.t ? c.c1 : T(1);
         acc[0] = fma_rn(pr, f, acc[0]);
     }
-    // Pipe-balanced form (fp64, every threshold of the CTA >= +0): for
-    // t >= +0, `p > t` equals the signed 64-bit integer compare of the bit
-    // patterns for every non-NaN p, so odd columns test the mask with two
-    // ISETPs on the integer ALU instead of a DSETP on the FP64 pipe. Per
-    // iteration the FP64 pipe then carries DMUL + DFMA + half a DSETP and
-    // the ALU two FSELs + one ISETP: both near 6 cycles per warp instead of
-    // FP64 alone at 7 (DFMA's three 64-bit sources cost 3 register-read
-    // cycles). Identical results: the mask is the same boolean.
-    static constexpr bool HAS_ALT = sizeof(T) == 8;
-    __device__ static bool alt_ok(const Col& c) {
-        if constexpr (sizeof(T) == 8) return __double_as_longlong(c.t) >= 0;
-        return false;
-    }
-    __device__ static __forceinline__ void step_alt(Acc* acc, T a, T b, const Col& c, int cidx) {
-        T pr = mul_rn(a, b);
-        bool m;
-        if constexpr (sizeof(T) == 8) {
-            if (cidx & 1)
-                m = __double_as_longlong(pr) > __double_as_longlong(c.t);
-            else
-                m = pr > c.t;
-        } else {
-            m = pr > c.t;
-        }
-        T f = m ? c.c1 : T(1);
-        acc[0] = fma_rn(pr, f, acc[0]);
-    }
     __device__ static __forceinline__ T finish(const Acc* acc, const Col&, int64_t) { return acc[0]; }
 };
-
-// Bodies without a pipe-balanced alternative.
-template <class Body, class = void>
-struct HasAlt {
-    static constexpr bool value = false;
-};
-template <class Body>
-struct HasAlt<Body, decltype(void(Body::HAS_ALT))> {
-    static constexpr bool value = Body::HAS_ALT;
-};
-
-template <class Body, bool ALT, typename T>
-__device__ __forceinline__ void body_step(typename Body::Acc* acc, T a, T b,
-                                          const typename Body::Col& c, int cidx) {
-    if constexpr (ALT)
-        Body::step_alt(acc, a, b, c, cidx);
-    else
-        Body::step(acc, a, b, c);
-}
 
 // BOOST — preset q2: `R += A*B + (A*B > thres[j])*(A*B - thres[j])`
 // (presets.cpp:68-69; ref program `mul; gtcmp; sub; maskadd; add`).
@@ -495,18 +447,6 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
                 for (int n = 0; n < NACC; ++n) part[r][c][n] = Acc(0);
     }
 
-    // CTA-uniform choice of the body's pipe-balanced form (discount fp64 with
-    // non-negative thresholds); the main loop is compiled once per form.
-    bool alt = false;
-    if constexpr (HasAlt<Body>::value) {
-        bool mine = true;
-#pragma unroll
-        for (int c = 0; c < TN; ++c) mine = mine && Body::alt_ok(colst[c]);
-        alt = __syncthreads_and(mine) != 0;
-    }
-
-    auto main_loop = [&](auto alt_tag) {
-    constexpr bool ALT = decltype(alt_tag)::value;
     for (int kt = 0; kt < nkt; ++kt) {
         const int stage = kt % STAGES;
         if constexpr (LOAD == LOAD_TMA) {
@@ -544,9 +484,9 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
 #pragma unroll
                         for (int c = 0; c < TN; ++c) {
                             if constexpr (Body::TWO_LEVEL)
-                                body_step<Body, ALT>(part[r][c], a, b[c], colst[c], c);
+                                Body::step(part[r][c], a, b[c], colst[c]);
                             else
-                                body_step<Body, ALT>(acc[r][c], a, b[c], colst[c], c);
+                                Body::step(acc[r][c], a, b[c], colst[c]);
                         }
                     }
                 }
@@ -589,15 +529,6 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
             __syncthreads();
             if (tid == 0 && kt + STAGES < nkt) tma_stage(stage, kt + STAGES);
         }
-    }
-    };
-    if constexpr (HasAlt<Body>::value) {
-        if (alt)
-            main_loop(std::true_type{});
-        else
-            main_loop(std::false_type{});
-    } else {
-        main_loop(std::false_type{});
     }
     if constexpr (LOAD != LOAD_TMA) cp_async_wait<0>();
 
