@@ -553,7 +553,7 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
             const int64_t slots = int64_t(ctx->num_sms) * occ;
             if (ctas > 0 && ctas < slots && whole.K >= 512) {
                 int64_t splits = std::min<int64_t>((slots + ctas - 1) / ctas, whole.K / 256);
-                if (splits > 1) kc = (whole.K + splits - 1) / splits;
+                if (splits > 1) kc = ((whole.K + splits - 1) / splits + 31) / 32 * 32;
             }
         }
         rep->best_variant = v >= 0 ? plan_local_index(plan, v) : -1;

@@ -69,6 +69,30 @@ __global__ void __launch_bounds__(256) peak_kernel(double* sink, unsigned long l
     }
 }
 
+// FFMA2 probe: packed two-wide fp32 FMAs (sm_100 FFMA2), 8 float2 chains.
+__global__ void __launch_bounds__(256) peak_ffma2_kernel(double* sink, unsigned long long* clk) {
+    const uint64_t c0 = clock64();
+    const uint64_t g0 = gtimer();
+    float2 acc[kChains];
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) acc[c] = make_float2(threadIdx.x * 1e-3f + c, c * 0.5f);
+    const float2 fa = make_float2(1.0001f, 0.9999f), fb = make_float2(1e-7f, 2e-7f);
+    for (int it = 0; it < kIters; ++it) {
+#pragma unroll
+        for (int c = 0; c < kChains; ++c) acc[c] = __ffma2_rn(acc[c], fa, fb);
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < kChains; ++c) s += acc[c].x + acc[c].y;
+    if (s == 12345.678) sink[threadIdx.x] = s;
+    const uint64_t c1 = clock64();
+    const uint64_t g1 = gtimer();
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        clk[0] = c1 - c0;
+        clk[1] = g1 - g0;
+    }
+}
+
 // DMMA probe: independent m8n8k4 f64 MMAs (256 FMA each per warp).
 __global__ void __launch_bounds__(256) peak_dmma_kernel(double* sink, unsigned long long* clk) {
     const uint64_t c0 = clock64();
@@ -166,7 +190,8 @@ amlt_status amlt_gpu_measure_peak(int pipe, double* ops_per_s, double* sm_ghz) {
         cudaFree(sink);
         return AMLT_ERR_CUDA;
     }
-    const int blocks = sms * (pipe >= 5 ? 2 : 8);  // probes: 64 / 16 warps per SM
+    const bool body = pipe >= 5 && pipe <= 11;
+    const int blocks = sms * (body ? 2 : 8);  // 64 warps per SM; body probes 16
     // body probes read thres (constant) and dis (a small device vector)
     KParams bp;
     std::memset(&bp, 0, sizeof(bp));
@@ -187,7 +212,8 @@ amlt_status amlt_gpu_measure_peak(int pipe, double* ops_per_s, double* sm_ghz) {
             case 8: body_probe_kernel<BodySqdiff<float>, float><<<blocks, 256>>>(bp, sink, clk); break;
             case 9: body_probe_kernel<BodyEqcount<int>, int><<<blocks, 256>>>(bp, sink, clk); break;
             case 10: body_probe_kernel<BodyGemm<float>, float><<<blocks, 256>>>(bp, sink, clk); break;
-            default: body_probe_kernel<BodyGemm<double>, double><<<blocks, 256>>>(bp, sink, clk); break;
+            case 11: body_probe_kernel<BodyGemm<double>, double><<<blocks, 256>>>(bp, sink, clk); break;
+            default: peak_ffma2_kernel<<<blocks, 256>>>(sink, clk); break;
         }
     };
     cudaEvent_t e0, e1;
@@ -215,8 +241,10 @@ amlt_status amlt_gpu_measure_peak(int pipe, double* ops_per_s, double* sm_ghz) {
     if (err != cudaSuccess) return AMLT_ERR_CUDA;
     const double threads = double(blocks) * 256.0;
     double ops;
-    if (pipe >= 5)
-        ops = threads * 32.0 * (kIters / 8);  // inner iterations (4 x 8 per round)
+    if (body)
+        ops = threads * 32.0 * (kIters / 8);
+    else if (pipe == 12)
+        ops = threads * kChains * kIters * 2.0;  // two FMAs per FFMA2  // inner iterations (4 x 8 per round)
     else if (pipe == 4)
         ops = double(blocks) * 8.0 * kChains * (kIters / 4) * 256.0;  // warps * mmas * 256 FMA
     else if (pipe == 2)

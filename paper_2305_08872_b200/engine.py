@@ -538,7 +538,7 @@ def measure_peak(pipe: str) -> tuple:
     'ffma', 'alu', 'dsetp', 'dmma' (roofline denominators)."""
     code = {"dfma": 0, "ffma": 1, "alu": 2, "dsetp": 3, "dmma": 4, "discount_f64": 5,
             "boost_f64": 6, "boost_f32": 7, "sqdiff_f32": 8, "eqcount_i32": 9, "gemm_f32": 10,
-            "gemm_f64": 11}[pipe]
+            "gemm_f64": 11, "ffma2": 12}[pipe]
     ops, ghz = C.c_double(), C.c_double()
     st = N.lib().amlt_gpu_measure_peak(code, C.byref(ops), C.byref(ghz))
     if st != N.OK:

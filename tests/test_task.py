@@ -1,0 +1,104 @@
+"""CPU: the task front-end recognises exactly the GPU bodies.
+
+Restates the reference's recognition conditions (recognize.cpp:84-166) and
+checks the body match against the reference's own preset texts
+(presets.cpp:52-94) and recognition verdicts (oracle/_ref).
+"""
+from __future__ import annotations
+
+import pytest
+
+import paper_2305_08872_b200 as P
+from paper_2305_08872_b200 import _native as N
+from paper_2305_08872_b200.task import TaskError, compile_task
+from oracle import pyoracle as po
+
+WRAP = "where(i in [0..M] and j in [0..N] and k in [0..K]) {{\n  R[i][j] {op} {rhs};\n}}\n"
+
+
+def wrap(rhs, op="+="):
+    return WRAP.format(op=op, rhs=rhs)
+
+
+@pytest.mark.parametrize("rhs,body", [
+    ("A[i][k]*B[k][j]", "gemm"),
+    ("B[k][j]*A[i][k]", "gemm"),
+    ("A[i][k]*B[k][j] - (A[i][k]*B[k][j] > thres[j])*A[i][k]*B[k][j]*dis[j]", "discount"),
+    ("A[i][k]*B[k][j] + (A[i][k]*B[k][j] > thres[j])*(A[i][k]*B[k][j] - thres[j])", "boost"),
+    ("(A[i][k] - B[k][j])*(A[i][k] - B[k][j])", "sqdiff"),
+    ("A[i][k] == B[k][j]", "eqcount"),
+    ("B[k][j] == A[i][k]", "eqcount"),
+    ("(A[i][k]*B[k][j] > 100)", "thrcount"),
+])
+def test_bodies_recognised(rhs, body):
+    t = compile_task(wrap(rhs))
+    assert t.body_name == body
+    assert t.a_name == "A" and t.b_name == "B" and t.result_name == "R"
+    assert t.accumulate
+
+
+def test_roles_and_forms():
+    t = compile_task(wrap("A[i][k]*B[k][j] - (A[i][k]*B[k][j] > thres[j])*A[i][k]*B[k][j]*dis[j]"))
+    assert (t.thres_name, t.dis_name, t.thres_class) == ("thres", "dis", N.LEAF_VEC_J)
+    t = compile_task(wrap("(A[i][k]*B[k][j] > 100)"))
+    assert t.thres_class == N.LEAF_CONSTANT and t.thres_value == 100.0
+    t = compile_task(wrap("A[k][i]*B[j][k]"))
+    assert (t.layout_a, t.layout_b) == (N.LAYOUT_TRANSPOSED, N.LAYOUT_TRANSPOSED)
+    t = compile_task(wrap("A[i][k]*B[k][j]", "="))
+    assert not t.accumulate
+    # roles follow the target's subscripts, not loop declaration order
+    t = compile_task("where(k in [0..K] and j in [0..N] and i in [0..M]) {\n"
+                     "  R[i][j] += X[i][k]*Y[k][j];\n}\n")
+    assert (t.a_name, t.b_name, t.var_k) == ("X", "Y", "k")
+    # comments
+    t = compile_task("// a comment\n" + wrap("A[i][k]*B[k][j]"))
+    assert t.body_name == "gemm"
+
+
+@pytest.mark.parametrize("rhs", [
+    "A[i][k]*B[k][j] + u[i]*v[j]",          # a recognised MMLT, but not one of the bodies
+    "A[i][k]*B[k][j]*s + u[i] - v[j]*W[i][j]",
+    "(A[i][k] + 1)*(B[k][j] - 1)/2 + W[i][j]",
+    "A[i][k]*B[k][j] - (A[i][k]*B[k][j] < thres[j])*A[i][k]*B[k][j]",
+    "A[i][k]*C[k][j]*B[k][j]",               # two k-indexed B-role arrays
+    "A[i][k]*u[k]",                          # u[k] does not fit the pattern
+])
+def test_non_bodies_are_unsupported(rhs):
+    with pytest.raises(P.UnsupportedExpression):
+        compile_task(wrap(rhs))
+
+
+def test_not_mmlt():
+    with pytest.raises(P.UnsupportedExpression):
+        compile_task("where(i in [0..M] and j in [0..N]) {\n  R[i][j] += A[i][j];\n}\n")
+    with pytest.raises(P.UnsupportedExpression):
+        compile_task(wrap("R[i][j]*A[i][k]*B[k][j]"))
+    with pytest.raises(TaskError):
+        compile_task("where(i in [0..M] {")
+
+
+@pytest.mark.skipif(not po.ref_available(), reason="reference engine not built")
+def test_reference_presets():
+    """Every reference preset the reference recognises as an MMLT: q1/q2
+    (any threshold form, any orientation), matmul and q3 map to their body;
+    the reference and we agree on the operand roles."""
+    names = (["matmul-" + o for o in ("ab", "atb", "abt", "atbt")]
+             + [f"{q}-{f}-{o}" for q in ("q1", "q2", "q3") for f in ("tc", "ti", "tj", "tij")
+                for o in ("ab", "atb", "abt", "atbt")])
+    assert len(names) == 52
+    want_body = {"matmul": "gemm", "q1": "discount", "q2": "boost", "q3": "thrcount"}
+    for name in names:
+        src = po.preset_source(name)
+        t = compile_task(src)
+        assert t.body_name == want_body[name.split("-")[0]], name
+        ref = po.RefTask.create(src, 4, 4, 4)
+        assert ref.is_mmlt()
+        a, b, aux = ref.roles()
+        assert (t.a_name, t.b_name) == (a, b)
+        form = name.split("-")[1] if not name.startswith("matmul") else None
+        if form:
+            want_cls = {"tc": N.LEAF_CONSTANT, "ti": N.LEAF_VEC_I, "tj": N.LEAF_VEC_J,
+                        "tij": N.LEAF_MAT_IJ}[form]
+            assert t.thres_class == want_cls, name
+        assert t.layout_a == (N.LAYOUT_TRANSPOSED if "-at" in name else N.LAYOUT_NORMAL)
+        assert t.layout_b == (N.LAYOUT_TRANSPOSED if name.endswith("bt") else N.LAYOUT_NORMAL)
