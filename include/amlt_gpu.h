@@ -247,7 +247,28 @@ amlt_status amlt_gpu_set_stream(amlt_ctx* ctx, void* stream);
 /* Forget tuning winners cached by amlt_gpu_adaptive_execute. */
 void amlt_gpu_clear_tuning_cache(amlt_ctx* ctx);
 
+/* The compile_task boundary (src/engine.cpp:86-102): which GPU body a task
+ * text is, and which arrays play A, B, R, the threshold and the discount
+ * vector. Names are "" for absent roles. */
+typedef struct {
+    amlt_body_desc desc; /* dtype left 0; the caller chooses it          */
+    char a[64];
+    char b[64];
+    char r[64];
+    char thres[64];
+    char dis[64];
+} amlt_task_info;
+
+/* Parses and recognises a task in the reference DSL. UNSUPPORTED for a task
+ * that is not one of the GPU bodies (the reference then runs it on its CPU
+ * path); ENGINE for a parse error. Message: amlt_gpu_last_error(NULL). */
+amlt_status amlt_gpu_recognize(const char* task_source, amlt_task_info* info);
+
 amlt_status amlt_gpu_plan_create(amlt_ctx* ctx, const amlt_body_desc* desc, amlt_plan** out);
+/* amlt_gpu_recognize + amlt_gpu_plan_create in the given dtype; `info`
+ * (optional) receives the roles. */
+amlt_status amlt_gpu_plan_from_source(amlt_ctx* ctx, const char* task_source, int dtype,
+                                      amlt_plan** out, amlt_task_info* info);
 void amlt_gpu_plan_destroy(amlt_plan* plan);
 int amlt_gpu_plan_num_variants(const amlt_plan* plan);
 amlt_status amlt_gpu_plan_variant(const amlt_plan* plan, int idx, amlt_variant_info* info);

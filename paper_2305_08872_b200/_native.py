@@ -91,6 +91,11 @@ class TuneReportC(C.Structure):
                 ("total_seconds", C.c_double)]
 
 
+class TaskInfoC(C.Structure):
+    _fields_ = [("desc", BodyDesc), ("a", C.c_char * 64), ("b", C.c_char * 64),
+                ("r", C.c_char * 64), ("thres", C.c_char * 64), ("dis", C.c_char * 64)]
+
+
 CLOCK_FN = C.CFUNCTYPE(C.c_double, C.c_void_p)
 
 EXPORTS = [
@@ -99,6 +104,7 @@ EXPORTS = [
     "amlt_gpu_plan_destroy", "amlt_gpu_plan_num_variants", "amlt_gpu_plan_variant",
     "amlt_gpu_plan_default_variant", "amlt_gpu_run_subtask", "amlt_gpu_enqueue",
     "amlt_gpu_adaptive_execute", "amlt_gpu_run_host", "amlt_spr", "amlt_gpu_measure_peak",
+    "amlt_gpu_recognize", "amlt_gpu_plan_from_source",
 ]
 HOST_R_ZERO = 1
 
@@ -143,6 +149,9 @@ def lib():
                                     C.POINTER(BoundsC), C.c_int, CLOCK_FN, P,
                                     C.POINTER(C.c_double)]
     L.amlt_gpu_measure_peak.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.amlt_gpu_recognize.argtypes = [C.c_char_p, C.POINTER(TaskInfoC)]
+    L.amlt_gpu_plan_from_source.argtypes = [P, C.c_char_p, C.c_int, C.POINTER(P),
+                                            C.POINTER(TaskInfoC)]
     L.amlt_spr.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_double, C.POINTER(C.c_double)]
     v = L.amlt_gpu_abi_version()
     if v != ABI_VERSION:

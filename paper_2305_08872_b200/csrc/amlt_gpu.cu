@@ -27,6 +27,8 @@
 
 using namespace amltk;
 
+#include "task.h"
+
 namespace {
 
 // ---------------------------------------------------------------------------
@@ -721,6 +723,11 @@ amlt_status amlt_gpu_plan_create(amlt_ctx* ctx, const amlt_body_desc* desc, amlt
         if ((d.layout_a != AMLT_LAYOUT_NORMAL && d.layout_a != AMLT_LAYOUT_TRANSPOSED) ||
             (d.layout_b != AMLT_LAYOUT_NORMAL && d.layout_b != AMLT_LAYOUT_TRANSPOSED))
             fail(AMLT_ERR_INVALID_ARGUMENT, "unknown operand layout");
+        const bool needs_t = d.body == AMLT_BODY_DISCOUNT || d.body == AMLT_BODY_BOOST ||
+                             d.body == AMLT_BODY_THRCOUNT;
+        if (needs_t && (d.thres_class == AMLT_LEAF_VEC_I || d.thres_class == AMLT_LEAF_MAT_IJ))
+            fail(AMLT_ERR_UNSUPPORTED,
+                 "threshold operands indexed [i] or [i][j] are not supported by the GPU kernels yet");
         plan->desc = d;
         plan->ctx = ctx;
         plan->aux = find_aux(d.body, d.dtype);
@@ -740,6 +747,45 @@ amlt_status amlt_gpu_plan_create(amlt_ctx* ctx, const amlt_body_desc* desc, amlt
     }
     *out = plan;
     return AMLT_OK;
+}
+
+amlt_status amlt_gpu_recognize(const char* task_source, amlt_task_info* info) {
+    if (!task_source || !info) return AMLT_ERR_INVALID_ARGUMENT;
+    try {
+        amltk::RecognizedTask rt = amltk::recognize_task(task_source);
+        std::memset(info, 0, sizeof(*info));
+        info->desc = rt.desc;
+        auto put = [](char* dst, const std::string& s) {
+            std::snprintf(dst, 64, "%s", s.c_str());
+        };
+        put(info->a, rt.a);
+        put(info->b, rt.b);
+        put(info->r, rt.r);
+        put(info->thres, rt.thres);
+        put(info->dis, rt.dis);
+        g_create_error.clear();
+        return AMLT_OK;
+    } catch (const amltk::TaskError& e) {
+        g_create_error = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_create_error = e.what();
+        return AMLT_ERR_ENGINE;
+    }
+}
+
+amlt_status amlt_gpu_plan_from_source(amlt_ctx* ctx, const char* task_source, int dtype,
+                                      amlt_plan** out, amlt_task_info* info) {
+    if (!ctx || !out) return AMLT_ERR_INVALID_ARGUMENT;
+    amlt_task_info local;
+    amlt_task_info* ti = info ? info : &local;
+    amlt_status st = amlt_gpu_recognize(task_source, ti);
+    if (st != AMLT_OK) {
+        ctx->err = g_create_error;
+        return st;
+    }
+    ti->desc.dtype = dtype;
+    return amlt_gpu_plan_create(ctx, &ti->desc, out);
 }
 
 void amlt_gpu_plan_destroy(amlt_plan* plan) { delete plan; }

@@ -1,0 +1,24 @@
+// task.h — the task-text recogniser shared by task.cpp and the C-ABI.
+#pragma once
+
+#include <stdexcept>
+#include <string>
+
+#include "../../include/amlt_gpu.h"
+
+namespace amltk {
+
+struct TaskError : std::runtime_error {
+    amlt_status code;
+    TaskError(amlt_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+struct RecognizedTask {
+    amlt_body_desc desc{};
+    std::string a, b, r, thres, dis;  // array names per role ("" when absent)
+};
+
+// Parse + recognise; throws TaskError (UNSUPPORTED / ENGINE).
+RecognizedTask recognize_task(const std::string& source);
+
+}  // namespace amltk

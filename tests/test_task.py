@@ -102,3 +102,47 @@ def test_reference_presets():
             assert t.thres_class == want_cls, name
         assert t.layout_a == (N.LAYOUT_TRANSPOSED if "-at" in name else N.LAYOUT_NORMAL)
         assert t.layout_b == (N.LAYOUT_TRANSPOSED if name.endswith("bt") else N.LAYOUT_NORMAL)
+
+
+def native_recognize(src):
+    import ctypes as C
+
+    info = N.TaskInfoC()
+    st = N.lib().amlt_gpu_recognize(src.encode(), C.byref(info))
+    return st, info
+
+
+CASES = [
+    "A[i][k]*B[k][j]", "B[k][j]*A[i][k]", "A[k][i]*B[j][k]",
+    "A[i][k]*B[k][j] - (A[i][k]*B[k][j] > thres[j])*A[i][k]*B[k][j]*dis[j]",
+    "A[i][k]*B[k][j] + (A[i][k]*B[k][j] > thres[j])*(A[i][k]*B[k][j] - thres[j])",
+    "A[i][k]*B[k][j] + (A[i][k]*B[k][j] > s)*(A[i][k]*B[k][j] - s)",
+    "(A[i][k] - B[k][j])*(A[i][k] - B[k][j])", "A[i][k] == B[k][j]", "(A[i][k]*B[k][j] > 100)",
+    "A[i][k]*B[k][j] + u[i]*v[j]", "A[i][k]*u[k]", "A[i][k]*C[k][j]*B[k][j]",
+    "A[i][k]*B[k][j] - (A[i][k]*B[k][j] < thres[j])*A[i][k]*B[k][j]",
+]
+
+
+@pytest.mark.parametrize("rhs", CASES)
+@pytest.mark.parametrize("op", ["+=", "="])
+def test_native_recognizer_agrees_with_python(rhs, op):
+    src = wrap(rhs, op)
+    st, info = native_recognize(src)
+    try:
+        t = compile_task(src)
+    except P.UnsupportedExpression:
+        assert st == N.ERR_UNSUPPORTED
+        return
+    assert st == N.OK, N.lib().amlt_gpu_last_error(None)
+    d = info.desc
+    assert (d.body, d.accumulate, d.layout_a, d.layout_b, d.thres_class) == \
+        (t.body, int(t.accumulate), t.layout_a, t.layout_b, t.thres_class)
+    assert d.thres_value == t.thres_value
+    assert (info.a.decode(), info.b.decode(), info.r.decode()) == (t.a_name, t.b_name, t.result_name)
+    assert info.thres.decode() == (t.thres_name or "") and info.dis.decode() == (t.dis_name or "")
+
+
+def test_native_recognizer_parse_error():
+    st, _ = native_recognize("where(i in [0..M] {")
+    assert st == N.ERR_ENGINE
+    assert b"parse error" in N.lib().amlt_gpu_last_error(None)
