@@ -400,6 +400,7 @@ void enqueue(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch&
     const VariantDesc& v = vdesc(dp.variant);
     kp.tiles_m = static_cast<int32_t>((rv.M + v.bm - 1) / v.bm);
     kp.tiles_n = static_cast<int32_t>((rv.N + v.bn - 1) / v.bn);
+    kp.group_m = std::min(64, std::max(8, 512 / v.bm));
     const int64_t tiles = int64_t(kp.tiles_m) * kp.tiles_n;
     if (tiles > 0x7fffffffLL) fail(AMLT_ERR_INVALID_ARGUMENT, "problem too large for one launch");
     kp.splits = dp.splits;
@@ -507,17 +508,23 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
         const VariantDesc& v = vdesc(idx);
         if (v.vec == whole.aligned && (!v.tc || whole.aligned)) cands.push_back(idx);
     }
-    // band height per candidate: one full wave of CTAs across all SMs
+    // Band height per candidate: `waves` full waves of CTAs across all SMs
+    // (4 when the rows allow it, so partial-wave tails weigh little in the
+    // score; otherwise 1).
     std::vector<int64_t> band(cands.size());
     int64_t need = 0;
-    for (size_t c = 0; c < cands.size(); ++c) {
-        const VariantDesc& v = vdesc(cands[c]);
-        const int occ = ctx->occupancy.empty() ? v.minb : std::max(1, ctx->occupancy[cands[c]]);
-        const int64_t tiles_n = (whole.N + v.bn - 1) / v.bn;
-        const int64_t want_ctas = int64_t(ctx->num_sms) * occ;  // one full wave
-        const int64_t tiles_m = std::max<int64_t>(1, (want_ctas + tiles_n - 1) / tiles_n);
-        band[c] = tiles_m * v.bm;
-        need += band[c];
+    for (int waves : {4, 1}) {
+        need = 0;
+        for (size_t c = 0; c < cands.size(); ++c) {
+            const VariantDesc& v = vdesc(cands[c]);
+            const int occ = ctx->occupancy.empty() ? v.minb : std::max(1, ctx->occupancy[cands[c]]);
+            const int64_t tiles_n = (whole.N + v.bn - 1) / v.bn;
+            const int64_t want_ctas = int64_t(waves) * ctx->num_sms * occ;
+            const int64_t tiles_m = std::max<int64_t>(1, (want_ctas + tiles_n - 1) / tiles_n);
+            band[c] = tiles_m * v.bm;
+            need += band[c];
+        }
+        if (need * 4 <= whole.M) break;
     }
     const bool tunable = plan->desc.accumulate && !cands.empty() && whole.K > 0 && whole.N > 0 &&
                          need * 4 <= whole.M &&  // tuning <= 25% of the rows

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB) dmma_gemm_kernel
     double* As = reinterpret_cast<double*>(smem_raw);
     double* Bs = As + STAGES * Cfg::SMEM_A;
 
-    constexpr int G = 8;
+    const int G = p.group_m;
     const int bid = blockIdx.x;
     const int per_group = G * p.tiles_n;
     const int group = bid / per_group;

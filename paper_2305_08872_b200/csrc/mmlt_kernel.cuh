@@ -47,6 +47,7 @@ struct KParams {
     int64_t kslice;    // K depth per split (== K when splits == 1)
     int32_t splits;
     int32_t tiles_m, tiles_n;
+    int32_t group_m;   // row tiles per raster group (L2 reuse of B panels)
     int32_t r_vec_ok;  // R base 16B aligned and ldr a multiple of the vector width
     double tconst;     // threshold when thres == nullptr
 };
@@ -336,9 +337,10 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
     T* Bs = As + STAGES * Cfg::SMEM_A;
     uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * Cfg::SMEM_B);
 
-    // ---- tile coordinates: grouped raster (8 row-tiles per group) so the B
-    // column panels of concurrently resident CTAs are shared through L2.
-    constexpr int G = 8;
+    // ---- tile coordinates: grouped raster (group_m row-tiles per group, about
+    // 512 rows) so the B column panels of concurrently resident CTAs are
+    // shared through L2 while the group's A rows also stay resident.
+    const int G = p.group_m;
     const int bid = blockIdx.x;
     const int per_group = G * p.tiles_n;
     const int group = bid / per_group;
