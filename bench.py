@@ -230,6 +230,29 @@ def run_reference(body, M, K, N, steps, warmup, threads):
                       f"distributions"}
 
 
+def traffic_for(workload, tile):
+    """DRAM bytes per launch of this workload's kernel from the newest
+    committed ncu capture (profiles/r*/traffic.json), or None."""
+    import glob
+
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")),
+                       reverse=True):
+        try:
+            d = json.load(open(path)).get(workload, {})
+        except (OSError, ValueError):
+            continue
+        if tile in d:
+            return d[tile]["dram_read"] + d[tile]["dram_write"]
+    return None
+
+
+def algorithmic_bytes(body, dtype, M, K, N):
+    """Compulsory HBM bytes per launch: A, B, R read + R write, vectors."""
+    es = 8 if dtype == "f64" else 4
+    vec = {"discount": 2, "boost": 1}.get(body, 0) * N
+    return es * (M * K + K * N + 2 * M * N + vec)
+
+
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -419,7 +442,11 @@ def main():
             "roofline": {"bound": "fp64" if dtype == "f64" else ("fp32" if dtype == "f32" else "int32"),
                          "pipe": pipe, "achieved": achieved_tflops, "peak": peak_tflops,
                          "unit": "TFLOP/s", "frac": achieved_tflops / peak_tflops,
-                         "traffic": None,
+                         "traffic": traffic_for(args.workload,
+                                                variants[best].name if best >= 0 else None),
+                         "traffic_unit": "bytes per launch (ncu dram read+write, committed "
+                                         "capture profiles/*/traffic.json)",
+                         "algorithmic_bytes": algorithmic_bytes(body, dtype, M, K, N),
                          "accounting": "2 flops per inner iteration (matmul-like); peak = measured "
                                        f"{pipe} probe x2 on this GPU at {peak_ghz:.3f} GHz",
                          "body_pipe_ops_per_iter": ops_per_iter,
