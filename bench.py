@@ -149,12 +149,10 @@ def gen_inputs(body, dtype, M_rows, K, N, row0, rank, device, broadcast):
     else:  # eqcount
         Bv = torch.randint(0, 16, (K, N), dtype=tdt, device=device, generator=g)
         th = ds = None
-    if broadcast:
-        import torch.distributed as dist
+    if broadcast:  # B and the per-column vectors: NCCL broadcast from rank 0
+        from paper_2305_08872_b200.sharded import broadcast_replicated
 
-        for x in (Bv, th, ds):
-            if x is not None:
-                dist.broadcast(x, src=0)
+        broadcast_replicated([Bv, th, ds], src=0)
     ga = torch.Generator(device=device)
     ga.manual_seed(1000 + row0)
     if body == "discount":
@@ -307,11 +305,13 @@ def main():
     torch.cuda.set_device(lrank)
     device = torch.device("cuda", lrank)
     dist = None
-    if ws > 1:
+    if ws > 1 or "TORCHELASTIC_RUN_ID" in os.environ:  # launched by torchrun
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=device)
-    row0, row1 = M * rank // ws, M * (rank + 1) // ws
+    from paper_2305_08872_b200.sharded import row_band
+
+    row0, row1 = row_band(M, ws, rank, align=64)
     rows = row1 - row0
 
     ctx = P.Context(lrank)
@@ -330,7 +330,7 @@ def main():
     peak_ops, peak_ghz = P.engine.measure_peak(pipe)
     peak_tflops = 2 * peak_ops / 1e12 if pipe != "alu" else peak_ops / 1e12
 
-    A, B, th, ds = gen_inputs(body, dtype, rows, K, N, row0, rank, device, ws > 1)
+    A, B, th, ds = gen_inputs(body, dtype, rows, K, N, row0, rank, device, dist is not None)
     R = torch.zeros((rows, N), dtype=A.dtype, device=device)
     ops = P.Operands(A, B, R, th, ds)
     bounds = P.Bounds(0, rows, 0, N, 0, K)
