@@ -8,7 +8,7 @@
 // tests/acceptance.cpp:109-110, plus a larger one): compile_task,
 // make_task_data (the reference's own seeded generator), run on the GPU via
 // the adapter (run_adaptive and run_fixed), verify. A task the GPU has no
-// body for (q1-ti: threshold indexed [i]) must raise UnsupportedExpression so
+// body for (`A[i][k]*B[k][j] + u[i]*v[j]`) must raise UnsupportedExpression so
 // the caller keeps the CPU path.
 //
 // Built by oracle/Makefile into oracle/_ref/ (it links the reference's
@@ -35,6 +35,9 @@ int main(int argc, char** argv) {
         {"matmul", *preset_source("matmul")},
         {"q3", *preset_source("q3")},
         {"q1-tc", *preset_source("q1-tc")},
+        {"q1-ti", *preset_source("q1-ti")},
+        {"q2-tij", *preset_source("q2-tij")},
+        {"q3-ti", *preset_source("q3-ti")},
         {"sqdiff", wrap_head + "(A[i][k] - B[k][j])*(A[i][k] - B[k][j]);\n}\n"},
         {"eqcount", wrap_head + "A[i][k] == B[k][j];\n}\n"},
     };
@@ -76,7 +79,7 @@ int main(int argc, char** argv) {
     // a recognised MMLT the GPU has no body for: the adapter must refuse it
     bool refused = false;
     try {
-        CompiledTask ct = compile_task(*preset_source("q1-ti"), MachineModel{});
+        CompiledTask ct = compile_task(wrap_head + "A[i][k]*B[k][j] + u[i]*v[j];\n}\n", MachineModel{});
         DimBinding bind = bind_dims(ct, 8, 8, 8);
         TaskData data = make_task_data(ct, bind, 1, StorageOrder::RowMajor, StorageOrder::RowMajor,
                                        DataMode::IntValued);
@@ -92,7 +95,7 @@ int main(int argc, char** argv) {
     }
     if (!refused) {
         ++failures;
-        std::printf("FAIL q1-ti was not refused\n");
+        std::printf("FAIL a non-body MMLT was not refused\n");
     }
     std::printf("%s: %d checks, %d failures%s\n", failures ? "FAIL" : "PASS", checks, failures,
                 dry ? " (dry run: plumbing only)" : "");

@@ -204,23 +204,38 @@ Resolved resolve(const amlt_plan* plan, const amlt_operands* ops, const amlt_bou
     const bool needs_d = d.body == AMLT_BODY_DISCOUNT;
     kp.thres = nullptr;
     kp.tconst = d.thres_value;
+    kp.t_si = 0;
+    kp.t_sj = 0;
+    const int64_t tes = dtype_size(d.dtype);
+    // element step of a len x 1 (or 1 x len) vector buffer (kernel_exec.hpp:13-16)
+    auto vec_step = [](const amlt_matrix& t) {
+        return (t.cols == 1) ? (t.order == AMLT_ROW_MAJOR ? t.ld : 1)
+                             : (t.order == AMLT_ROW_MAJOR ? 1 : t.ld);
+    };
     if (needs_t && d.thres_class == AMLT_LEAF_CONSTANT && ops->thres.data) {
         // named scalar threshold (a 1 x 1 buffer): broadcast from device memory
         check_matrix(ops->thres, d.dtype, "thres");
         kp.thres = ops->thres.data;
-        kp.t_sj = 0;
-    } else if (needs_t && d.thres_class != AMLT_LEAF_CONSTANT) {
-        if (d.thres_class != AMLT_LEAF_VEC_J)
-            fail(AMLT_ERR_UNSUPPORTED,
-                 "threshold operands indexed [i] or [i][j] are not supported by the GPU kernels yet");
+    } else if (needs_t && d.thres_class == AMLT_LEAF_VEC_J) {
         check_matrix(ops->thres, d.dtype, "thres");
         const amlt_matrix& t = ops->thres;
-        // VecJ leaves are N x 1 buffers (kernel_exec.hpp:13-16)
         if (t.rows * t.cols < b->j1) fail(AMLT_ERR_INVALID_ARGUMENT, "thres shorter than j1");
-        const int64_t step = (t.cols == 1) ? (t.order == AMLT_ROW_MAJOR ? t.ld : 1)
-                                           : (t.order == AMLT_ROW_MAJOR ? 1 : t.ld);
-        kp.thres = static_cast<const char*>(t.data) + b->j0 * step * dtype_size(d.dtype);
-        kp.t_sj = step;
+        kp.t_sj = vec_step(t);
+        kp.thres = static_cast<const char*>(t.data) + b->j0 * kp.t_sj * tes;
+    } else if (needs_t && d.thres_class == AMLT_LEAF_VEC_I) {
+        check_matrix(ops->thres, d.dtype, "thres");
+        const amlt_matrix& t = ops->thres;
+        if (t.rows * t.cols < b->i1) fail(AMLT_ERR_INVALID_ARGUMENT, "thres shorter than i1");
+        kp.t_si = vec_step(t);
+        kp.thres = static_cast<const char*>(t.data) + b->i0 * kp.t_si * tes;
+    } else if (needs_t && d.thres_class == AMLT_LEAF_MAT_IJ) {
+        check_matrix(ops->thres, d.dtype, "thres");
+        const amlt_matrix& t = ops->thres;  // M x N, element (i, j)
+        if (t.rows < b->i1 || t.cols < b->j1)
+            fail(AMLT_ERR_INVALID_ARGUMENT, "thres[i][j] smaller than the bounds");
+        kp.t_si = t.order == AMLT_ROW_MAJOR ? t.ld : 1;
+        kp.t_sj = t.order == AMLT_ROW_MAJOR ? 1 : t.ld;
+        kp.thres = static_cast<const char*>(t.data) + (b->i0 * kp.t_si + b->j0 * kp.t_sj) * tes;
     }
     kp.dis = nullptr;
     if (needs_d) {
@@ -732,9 +747,11 @@ amlt_status amlt_gpu_plan_create(amlt_ctx* ctx, const amlt_body_desc* desc, amlt
             fail(AMLT_ERR_INVALID_ARGUMENT, "unknown operand layout");
         const bool needs_t = d.body == AMLT_BODY_DISCOUNT || d.body == AMLT_BODY_BOOST ||
                              d.body == AMLT_BODY_THRCOUNT;
-        if (needs_t && (d.thres_class == AMLT_LEAF_VEC_I || d.thres_class == AMLT_LEAF_MAT_IJ))
-            fail(AMLT_ERR_UNSUPPORTED,
-                 "threshold operands indexed [i] or [i][j] are not supported by the GPU kernels yet");
+        if (d.thres_class < AMLT_LEAF_CONSTANT || d.thres_class > AMLT_LEAF_MAT_IJ)
+            fail(AMLT_ERR_INVALID_ARGUMENT, "unknown threshold leaf class");
+        // thresholds indexed by i or (i, j) run the per-output-threshold variants
+        const bool tout =
+            needs_t && (d.thres_class == AMLT_LEAF_VEC_I || d.thres_class == AMLT_LEAF_MAT_IJ);
         plan->desc = d;
         plan->ctx = ctx;
         plan->aux = find_aux(d.body, d.dtype);
@@ -743,7 +760,8 @@ amlt_status amlt_gpu_plan_create(amlt_ctx* ctx, const amlt_body_desc* desc, amlt
                                            " in " + dtype_name(d.dtype));
         const auto& reg = registry();
         for (size_t i = 0; i < reg.variants.size(); ++i)
-            if (reg.variants[i].body == d.body && reg.variants[i].dtype == d.dtype)
+            if (reg.variants[i].body == d.body && reg.variants[i].dtype == d.dtype &&
+                reg.variants[i].tout == tout)
                 plan->variants.push_back(static_cast<int>(i));
         if (plan->variants.empty())
             fail(AMLT_ERR_NO_FEASIBLE_KERNEL, "no tile variant compiled for this body/dtype");

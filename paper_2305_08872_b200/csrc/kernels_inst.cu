@@ -32,6 +32,20 @@ void AMLT_CAT4(register_, AMLT_BODY, _, AMLT_DT)(Registry& reg) {
         add_variant<Body, T, 4, 4, 4, 1, 32, 4, LOAD_TMA, 3>(reg, ID, DT, "t4x4_w4x1");
         add_variant<Body, T, 4, 4, 8, 1, 32, 3, LOAD_ELEM, 2>(reg, ID, DT, "t4x4_w8x1_u");
     }
+    // Thresholds indexed by i or by (i, j) (presets -ti / -tij): per-output
+    // threshold state, smaller micro-tiles for the extra registers.
+    if constexpr (UsesThreshold<Body>::value) {
+        constexpr int TT = LOAD_TMA | LOAD_TOUT, TE = LOAD_ELEM | LOAD_TOUT;
+        if constexpr (sizeof(T) == 8) {
+            add_variant<Body, T, 4, 4, 8, 1, 16, 3, TT, 1>(reg, ID, DT, "t4x4_w8x1_ti");
+            add_variant<Body, T, 4, 2, 4, 1, 16, 4, TT, 4>(reg, ID, DT, "t4x2_w4x1_ti");
+            add_variant<Body, T, 4, 4, 8, 1, 16, 3, TE, 1>(reg, ID, DT, "t4x4_w8x1_ti_u");
+        } else {
+            add_variant<Body, T, 4, 4, 8, 1, 32, 3, TT, 2>(reg, ID, DT, "t4x4_w8x1_ti");
+            add_variant<Body, T, 4, 4, 4, 1, 32, 4, TT, 3>(reg, ID, DT, "t4x4_w4x1_ti");
+            add_variant<Body, T, 4, 4, 8, 1, 32, 3, TE, 2>(reg, ID, DT, "t4x4_w8x1_ti_u");
+        }
+    }
     BodyAux a;
     a.body = ID;
     a.dtype = DT;

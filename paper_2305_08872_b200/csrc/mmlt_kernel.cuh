@@ -43,6 +43,7 @@ struct KParams {
     void* work;         // split-K workspace: [splits][M][N] of T
     int64_t lda, ldb, ldr;
     int64_t t_sj, d_sj;
+    int64_t t_si;      // threshold row stride (T indexed by i or by (i, j)); 0 otherwise
     int64_t M, N, K;   // extents of the bounds rectangle
     int64_t kslice;    // K depth per split (== K when splits == 1)
     int32_t splits;
@@ -151,6 +152,11 @@ struct BodyDiscount {
         c.c1 = T(1) - ldg_elem<T>(p.dis, j * p.d_sj);
         return c;
     }
+    static constexpr bool USES_T = true;
+    __device__ static __forceinline__ Col with_t(Col c, T t) {
+        c.t = t;
+        return c;
+    }
     __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col& c) {
         T pr = mul_rn(a, b);
         T f = pr > c.t ? c.c1 : T(1);
@@ -180,6 +186,12 @@ struct BodyBoost {
         Col c;
         c.t = p.thres ? ldg_elem<T>(p.thres, j * p.t_sj) : static_cast<T>(p.tconst);
         c.nt = -c.t;
+        return c;
+    }
+    static constexpr bool USES_T = true;
+    __device__ static __forceinline__ Col with_t(Col c, T t) {
+        c.t = t;
+        c.nt = -t;
         return c;
     }
     __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col& c) {
@@ -240,6 +252,11 @@ struct BodyThrcount {
         c.t = p.thres ? ldg_elem<T>(p.thres, j * p.t_sj) : static_cast<T>(p.tconst);
         return c;
     }
+    static constexpr bool USES_T = true;
+    __device__ static __forceinline__ Col with_t(Col c, T t) {
+        c.t = t;
+        return c;
+    }
     __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col& c) {
         acc[0] += (mul_rn(a, b) > c.t) ? 1 : 0;
     }
@@ -250,6 +267,27 @@ struct BodyThrcount {
 template <>
 __device__ __forceinline__ void BodyThrcount<int>::step(int* acc, int a, int b, const Col& c) {
     acc[0] += (a * b > c.t) ? 1 : 0;
+}
+
+// Bodies with a threshold operand T (discount, boost, thrcount).
+template <class Body, class = void>
+struct UsesThreshold {
+    static constexpr bool value = false;
+};
+template <class Body>
+struct UsesThreshold<Body, decltype(void(Body::USES_T))> {
+    static constexpr bool value = Body::USES_T;
+};
+
+// Column state with the threshold of output (i, j) when T is indexed by i or
+// by (i, j): T(i, j) = thres[i * t_si + j * t_sj] (TCLS == 1 kernels).
+template <class Body, typename T>
+__device__ __forceinline__ typename Body::Col col_at(const typename Body::Col& c, const KParams& p,
+                                                     int64_t i, int64_t j) {
+    if constexpr (UsesThreshold<Body>::value)
+        return Body::with_t(c, ldg_elem<T>(p.thres, i * p.t_si + j * p.t_sj));
+    else
+        return c;
 }
 
 // --------------------------------------------------------------------------
@@ -299,6 +337,8 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
 
 constexpr int LOAD_ELEM = 0;
 constexpr int LOAD_TMA = 1;
+// flag: per-output threshold state (T indexed by i or by (i, j))
+constexpr int LOAD_TOUT = 2;
 
 template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, int LOAD,
           int MINB>
@@ -324,6 +364,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
     mmlt_tile_kernel(const __grid_constant__ KParams p, const __grid_constant__ CUtensorMap tmA,
                      const __grid_constant__ CUtensorMap tmB) {
     using Cfg = MmltTile<Body, T, TM, TN, WR, WC, BK, STAGES, LOAD, MINB>;
+    constexpr bool TOUT = (LOAD & LOAD_TOUT) != 0;
     constexpr int VN = Cfg::VN;
     constexpr int THREADS = Cfg::THREADS;
     constexpr int BM = Cfg::BM;
@@ -399,7 +440,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
         }
     };
 
-    if constexpr (LOAD == LOAD_TMA) {
+    if constexpr ((LOAD & LOAD_TMA) != 0) {
         if (tid == 0) {
 #pragma unroll
             for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
@@ -431,6 +472,23 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
             const int64_t gj = n0 + wc * 32 * TN + q * 32 * VN + lane * VN + e;
             colst[q * VN + e] = Body::col(p, gj < p.N ? gj : 0);
         }
+    // Thresholds indexed by i or (i, j) (LOAD_TOUT variants): one state per
+    // output element, loaded once.
+    typename Body::Col colrc[TOUT ? TM : 1][TOUT ? TN : 1];
+    if constexpr (TOUT) {
+#pragma unroll
+        for (int r = 0; r < TM; ++r)
+#pragma unroll
+            for (int q = 0; q < TN / VN; ++q)
+#pragma unroll
+                for (int e = 0; e < VN; ++e) {
+                    const int64_t gi = m0 + wr * TM + r;
+                    const int64_t gj = n0 + wc * 32 * TN + q * 32 * VN + lane * VN + e;
+                    colrc[r][q * VN + e] = col_at<Body, T>(colst[q * VN + e], p, gi < p.M ? gi : 0,
+                                                           gj < p.N ? gj : 0);
+                }
+    }
+#define COL(r, c) (TOUT ? colrc[TOUT ? (r) : 0][TOUT ? (c) : 0] : colst[c])
 
     Acc acc[TM][TN][NACC];
     Acc part[Body::TWO_LEVEL ? TM : 1][Body::TWO_LEVEL ? TN : 1][NACC];
@@ -451,7 +509,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
 
     for (int kt = 0; kt < nkt; ++kt) {
         const int stage = kt % STAGES;
-        if constexpr (LOAD == LOAD_TMA) {
+        if constexpr ((LOAD & LOAD_TMA) != 0) {
             mbar_wait(&full[stage], static_cast<uint32_t>((kt / STAGES) & 1));
         } else {
             cp_async_wait<STAGES - 2>();
@@ -486,9 +544,9 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
 #pragma unroll
                         for (int c = 0; c < TN; ++c) {
                             if constexpr (Body::TWO_LEVEL)
-                                Body::step(part[r][c], a, b[c], colst[c]);
+                                Body::step(part[r][c], a, b[c], COL(r, c));
                             else
-                                Body::step(acc[r][c], a, b[c], colst[c]);
+                                Body::step(acc[r][c], a, b[c], COL(r, c));
                         }
                     }
                 }
@@ -508,9 +566,9 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
 #pragma unroll
                     for (int c = 0; c < TN; ++c) {
                         if constexpr (Body::TWO_LEVEL)
-                            Body::step(part[r][c], a, b[c], colst[c]);
+                            Body::step(part[r][c], a, b[c], COL(r, c));
                         else
-                            Body::step(acc[r][c], a, b[c], colst[c]);
+                            Body::step(acc[r][c], a, b[c], COL(r, c));
                     }
                 }
             }
@@ -526,13 +584,13 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
                         part[r][c][n] = Acc(0);
                     }
         }
-        if constexpr (LOAD == LOAD_TMA) {
+        if constexpr ((LOAD & LOAD_TMA) != 0) {
             // every warp is done reading this stage: refill it with tile kt+STAGES
             __syncthreads();
             if (tid == 0 && kt + STAGES < nkt) tma_stage(stage, kt + STAGES);
         }
     }
-    if constexpr (LOAD != LOAD_TMA) cp_async_wait<0>();
+    if constexpr ((LOAD & LOAD_TMA) == 0) cp_async_wait<0>();
 
     // ---- epilogue: R (+)= value, or the split-K workspace
     T* Rg = static_cast<T*>(p.R);
@@ -546,7 +604,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
             const int64_t gj0 = n0 + wc * 32 * TN + q * 32 * VN + lane * VN;
             T val[VN];
 #pragma unroll
-            for (int e = 0; e < VN; ++e) val[e] = Body::finish(acc[r][q * VN + e], colst[q * VN + e], kspan);
+            for (int e = 0; e < VN; ++e) val[e] = Body::finish(acc[r][q * VN + e], COL(r, q * VN + e), kspan);
             if (p.splits > 1) {
                 T* dst = Wg + (static_cast<int64_t>(split) * p.M + gi) * p.N + gj0;
 #pragma unroll
@@ -569,6 +627,8 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
         }
     }
 }
+
+#undef COL
 
 // R[i][j] (+)= sum over splits s = 0..S-1 (ascending) of work[s][i][j].
 template <typename T>
@@ -607,7 +667,8 @@ __global__ void mmlt_assign_kernel(const KParams p) {
         typename Body::Acc acc[Body::NACC];
 #pragma unroll
         for (int n = 0; n < Body::NACC; ++n) acc[n] = typename Body::Acc(0);
-        const typename Body::Col c = Body::col(p, j);
+        const typename Body::Col c =
+            p.t_si ? col_at<Body, T>(Body::col(p, j), p, i, j) : Body::col(p, j);
         Body::step(acc, A[i * p.lda + k], B[k * p.ldb + j], c);
         R[i * p.ldr + j] = Body::finish(acc, c, 1);
     }

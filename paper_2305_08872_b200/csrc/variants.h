@@ -28,6 +28,7 @@ struct VariantDesc {
     int threads = 0, stages = 0, smem = 0, minb = 1;
     bool vec = true;  // TMA staging (needs 16-byte aligned operands and strides)
     bool tc = false;  // tensor-core (DMMA) variant
+    bool tout = false;  // per-output threshold state (T indexed by i or (i, j))
     const char* name = "";
     const void* func = nullptr;
     TileLaunchFn launch = nullptr;
@@ -94,7 +95,8 @@ void add_variant(Registry& reg, int body, int dtype, const char* name) {
         v.stages = STAGES;
         v.smem = Cfg::SMEM_BYTES;
         v.minb = MINB;
-        v.vec = LOAD == LOAD_TMA;
+        v.vec = (LOAD & LOAD_TMA) != 0;
+        v.tout = (LOAD & LOAD_TOUT) != 0;
         v.name = name;
         v.func = reinterpret_cast<const void*>(
             &mmlt_tile_kernel<Body, T, TM, TN, WR, WC, BK, STAGES, LOAD, MINB>);

@@ -237,3 +237,58 @@ def test_missing_binding_raises(gpu_ctx):
     with pytest.raises(P.MissingBinding):
         P.run_subtask(plan, P.Operands(dev(A, "f64"), dev(B, "f64"), dev(np.zeros((8, 8)), "f64"),
                                        dev(t, "f64"), None), P.TileParams(), P.Bounds(0, 8, 0, 8, 0, 8))
+
+
+@pytest.mark.parametrize("body,dtype", [("discount", "f64"), ("discount", "f32"), ("boost", "f64"),
+                                        ("boost", "f32"), ("thrcount", "f64"),
+                                        ("thrcount", "i32")])
+@pytest.mark.parametrize("form", ["i", "ij", "c"])
+def test_threshold_forms_all_variants(gpu_ctx, body, dtype, form):
+    """Presets -ti / -tij / -tc (presets.cpp:52-61): thresholds indexed [i],
+    [i][j] or a constant, every variant of the plan, ragged dims, bit-exact on
+    int-valued data; the constant also as a named 1 x 1 scalar buffer."""
+    import paper_2305_08872_b200 as P
+
+    rng = np.random.default_rng(31)
+    for (M, K, N) in [(96, 128, 160), (257, 129, 65), (13, 17, 5)]:
+        A, B = (rng.integers(-8, 9, s).astype(np.float64) for s in ((M, K), (K, N)))
+        dis = rng.integers(-8, 9, N).astype(np.float64) if body == "discount" else None
+        if form == "i":
+            thres = rng.integers(-8, 9, M).astype(np.float64)
+        elif form == "ij":
+            thres = rng.integers(-8, 9, (M, N)).astype(np.float64)
+        else:
+            thres = 3.0
+        want = np.zeros((M, N))
+        from oracle import pyoracle as po
+        po.oracle_run({"discount": po.DISCOUNT, "boost": po.BOOST, "thrcount": po.THRCOUNT}[body],
+                      A, B, want, thres=thres, dis=dis, thres_form=form)
+        if form == "c":
+            for named in (False, True):
+                plan = gpu_ctx.plan(body, dtype, thres_class="c", thres_value=0.0 if named else 3.0)
+                R = dev(np.zeros((M, N)), dtype)
+                tb = dev(np.array([[3.0]]), dtype) if named else None
+                P.adaptive_execute(plan, P.Operands(dev(A, dtype), dev(B, dtype), R, tb,
+                                                    dev(dis, dtype)), P.Bounds(0, M, 0, N, 0, K))
+                check(body, dtype, R.cpu().numpy(), want, exact=True, what=f"tc named={named}")
+            continue
+        plan = gpu_ctx.plan(body, dtype, thres_class=form)
+        vn = 2 if dtype == "f64" else 4
+        for vi, v in enumerate(plan.variants()):
+            if not v.name.endswith("_u") and (K % vn or N % vn):
+                continue
+            R = dev(np.zeros((M, N)), dtype)
+            P.run_subtask(plan, P.Operands(dev(A, dtype), dev(B, dtype), R, dev(thres, dtype),
+                                           dev(dis, dtype)), P.TileParams(variant=vi),
+                          P.Bounds(0, M, 0, N, 0, K))
+            check(body, dtype, R.cpu().numpy(), want, exact=True, what=f"t{form} {v.name} {M}x{K}x{N}")
+        # sub-rectangle: the threshold offsets follow the bounds
+        R0 = rng.integers(-5, 5, (M, N)).astype(np.float64)
+        bnd = (2, M - 1, 1, N, 3, K)
+        want2 = R0.copy()
+        po.oracle_run({"discount": po.DISCOUNT, "boost": po.BOOST, "thrcount": po.THRCOUNT}[body],
+                      A, B, want2, thres=thres, dis=dis, thres_form=form, bounds=bnd)
+        R = dev(R0, dtype)
+        P.run_subtask(plan, P.Operands(dev(A, dtype), dev(B, dtype), R, dev(thres, dtype),
+                                       dev(dis, dtype)), P.TileParams(), P.Bounds(*bnd))
+        check(body, dtype, R.cpu().numpy(), want2, exact=True, what=f"t{form} bounds")

@@ -214,10 +214,19 @@ def test_errors_map_to_reference_hierarchy(dry_ctx):
     with pytest.raises(P.UnsupportedExpression):  # A[k][i] over a row-major buffer
         P.run_subtask(tplan, big_ops(16, 16, 16, "gemm"), P.TileParams(),
                       P.Bounds(0, 16, 0, 16, 0, 16))
-    with pytest.raises(P.UnsupportedExpression):
-        dry_ctx.plan("eqcount", "i32", thres_class="i")
-        P.run_subtask(dry_ctx.plan("discount", "f64", thres_class="i"), big_ops(16, 16, 16),
-                      P.TileParams(), P.Bounds(0, 16, 0, 16, 0, 16))
+    bplan = dry_ctx.plan("gemm", "f64", layout_b=N.LAYOUT_TRANSPOSED)
+    with pytest.raises(P.UnsupportedExpression):  # B[j][k] over a row-major buffer
+        P.run_subtask(bplan, big_ops(16, 16, 16, "gemm"), P.TileParams(),
+                      P.Bounds(0, 16, 0, 16, 0, 16))
+    # thresholds indexed [i]: accepted, and the vector must cover i1
+    iplan = dry_ctx.plan("discount", "f64", thres_class="i")
+    assert all(v.name.endswith(("_ti", "_ti_u")) for v in iplan.variants())
+    ops_i = big_ops(16, 16, 16)
+    P.run_subtask(iplan, ops_i, P.TileParams(), P.Bounds(0, 16, 0, 16, 0, 16),
+                  clock=P.FakeClock([1.0]))
+    ops_i.thres = np.empty(8)
+    with pytest.raises(P.EngineError):
+        P.run_subtask(iplan, ops_i, P.TileParams(), P.Bounds(0, 16, 0, 16, 0, 16))
     with pytest.raises(P.UnsupportedExpression):
         dry_ctx.plan("gemm", "i32")  # no int32 GEMM kernel
     with pytest.raises(P.EngineError):  # dtype mismatch
