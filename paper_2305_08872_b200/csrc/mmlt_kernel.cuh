@@ -29,6 +29,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace amltk {
 
 // --------------------------------------------------------------------------
@@ -231,7 +233,15 @@ struct BodyEqcount {
     struct Col {};
     __device__ static Col col(const KParams&, int64_t) { return {}; }
     __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col&) {
-        acc[0] += (a == b) ? 1 : 0;
+        if constexpr (sizeof(T) == 4 && std::is_integral<T>::value) {
+            // ISETP + predicated IADD: two issue slots (nvcc's own lowering is a
+            // speculative add plus a predicated move, three)
+            asm("{\n .reg .pred p;\n setp.eq.s32 p, %1, %2;\n @p add.s32 %0, %0, 1;\n}\n"
+                : "+r"(acc[0])
+                : "r"(a), "r"(b));
+        } else {
+            acc[0] += (a == b) ? 1 : 0;
+        }
     }
     __device__ static __forceinline__ T finish(const Acc* acc, const Col&, int64_t) {
         return static_cast<T>(acc[0]);
@@ -489,6 +499,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
                 }
     }
 #define COL(r, c) (TOUT ? colrc[TOUT ? (r) : 0][TOUT ? (c) : 0] : colst[c])
+#define STEP(accv, a_, c_, col_) Body::step(accv, a_, b[c_], col_)
 
     Acc acc[TM][TN][NACC];
     Acc part[Body::TWO_LEVEL ? TM : 1][Body::TWO_LEVEL ? TN : 1][NACC];
@@ -544,9 +555,9 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
 #pragma unroll
                         for (int c = 0; c < TN; ++c) {
                             if constexpr (Body::TWO_LEVEL)
-                                Body::step(part[r][c], a, b[c], COL(r, c));
+                                STEP(part[r][c], a, c, COL(r, c));
                             else
-                                Body::step(acc[r][c], a, b[c], COL(r, c));
+                                STEP(acc[r][c], a, c, COL(r, c));
                         }
                     }
                 }
@@ -566,9 +577,9 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
 #pragma unroll
                     for (int c = 0; c < TN; ++c) {
                         if constexpr (Body::TWO_LEVEL)
-                            Body::step(part[r][c], a, b[c], COL(r, c));
+                            STEP(part[r][c], a, c, COL(r, c));
                         else
-                            Body::step(acc[r][c], a, b[c], COL(r, c));
+                            STEP(acc[r][c], a, c, COL(r, c));
                     }
                 }
             }
@@ -629,6 +640,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
 }
 
 #undef COL
+#undef STEP
 
 // R[i][j] (+)= sum over splits s = 0..S-1 (ascending) of work[s][i][j].
 template <typename T>
