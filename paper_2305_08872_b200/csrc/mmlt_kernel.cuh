@@ -113,6 +113,39 @@ __device__ __forceinline__ T ldg_elem(const void* base, int64_t idx) {
     return __ldg(static_cast<const T*>(base) + idx);
 }
 
+// Counting bodies: acc += (x CMP y), as SETP + predicated add — two issue
+// slots (nvcc's own lowering of `acc += cond ? 1 : 0` is a speculative add
+// plus a predicated move, three).
+constexpr int CMP_EQ = 0;
+constexpr int CMP_GT = 1;
+template <int CMP>
+__device__ __forceinline__ void inc_if(int& acc, int x, int y) {
+    if constexpr (CMP == CMP_EQ)
+        asm("{\n .reg .pred p;\n setp.eq.s32 p, %1, %2;\n @p add.s32 %0, %0, 1;\n}\n"
+            : "+r"(acc) : "r"(x), "r"(y));
+    else
+        asm("{\n .reg .pred p;\n setp.gt.s32 p, %1, %2;\n @p add.s32 %0, %0, 1;\n}\n"
+            : "+r"(acc) : "r"(x), "r"(y));
+}
+template <int CMP>
+__device__ __forceinline__ void inc_if(int& acc, float x, float y) {
+    if constexpr (CMP == CMP_EQ)
+        asm("{\n .reg .pred p;\n setp.eq.f32 p, %1, %2;\n @p add.s32 %0, %0, 1;\n}\n"
+            : "+r"(acc) : "f"(x), "f"(y));
+    else
+        asm("{\n .reg .pred p;\n setp.gt.f32 p, %1, %2;\n @p add.s32 %0, %0, 1;\n}\n"
+            : "+r"(acc) : "f"(x), "f"(y));
+}
+template <int CMP>
+__device__ __forceinline__ void inc_if(int& acc, double x, double y) {
+    if constexpr (CMP == CMP_EQ)
+        asm("{\n .reg .pred p;\n setp.eq.f64 p, %1, %2;\n @p add.s32 %0, %0, 1;\n}\n"
+            : "+r"(acc) : "d"(x), "d"(y));
+    else
+        asm("{\n .reg .pred p;\n setp.gt.f64 p, %1, %2;\n @p add.s32 %0, %0, 1;\n}\n"
+            : "+r"(acc) : "d"(x), "d"(y));
+}
+
 // --------------------------------------------------------------------------
 // Bodies. Each gives the per-(i,j,k) update on the accumulators of one
 // output element, the per-column state it needs, and the final value added
@@ -233,15 +266,7 @@ struct BodyEqcount {
     struct Col {};
     __device__ static Col col(const KParams&, int64_t) { return {}; }
     __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col&) {
-        if constexpr (sizeof(T) == 4 && std::is_integral<T>::value) {
-            // ISETP + predicated IADD: two issue slots (nvcc's own lowering is a
-            // speculative add plus a predicated move, three)
-            asm("{\n .reg .pred p;\n setp.eq.s32 p, %1, %2;\n @p add.s32 %0, %0, 1;\n}\n"
-                : "+r"(acc[0])
-                : "r"(a), "r"(b));
-        } else {
-            acc[0] += (a == b) ? 1 : 0;
-        }
+        inc_if<CMP_EQ>(acc[0], a, b);
     }
     __device__ static __forceinline__ T finish(const Acc* acc, const Col&, int64_t) {
         return static_cast<T>(acc[0]);
@@ -268,7 +293,7 @@ struct BodyThrcount {
         return c;
     }
     __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col& c) {
-        acc[0] += (mul_rn(a, b) > c.t) ? 1 : 0;
+        inc_if<CMP_GT>(acc[0], mul_rn(a, b), c.t);
     }
     __device__ static __forceinline__ T finish(const Acc* acc, const Col&, int64_t) {
         return static_cast<T>(acc[0]);
@@ -276,7 +301,7 @@ struct BodyThrcount {
 };
 template <>
 __device__ __forceinline__ void BodyThrcount<int>::step(int* acc, int a, int b, const Col& c) {
-    acc[0] += (a * b > c.t) ? 1 : 0;
+    inc_if<CMP_GT>(acc[0], a * b, c.t);
 }
 
 // Bodies with a threshold operand T (discount, boost, thrcount).

@@ -1,0 +1,91 @@
+// mixbench.cu — throughput of fp64 instruction mixes on one SM (scratch
+// experiment, not product code). Each thread runs NCH independent chains;
+// grid = SMs x BLK blocks of 256 threads. Prints cycles per warp-iteration per
+// SMSP for each mix.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mixbench tools/mixbench.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int NCH = 16;
+constexpr int ITERS = 2048;
+
+template <int MIX>
+__global__ void __launch_bounds__(256) mix(double* out, const double* in, int n) {
+    double a[NCH], b[NCH], acc[NCH];
+    const double t = in[0], c1 = in[1];
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+        a[c] = in[2 + (threadIdx.x + c) % 8];
+        b[c] = in[10 + (threadIdx.x * 3 + c) % 8];
+        acc[c] = 0;
+    }
+    for (int it = 0; it < n; ++it) {
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) {
+            if constexpr (MIX == 0) {  // DFMA, three distinct fresh sources
+                acc[c] = __fma_rn(a[c], b[c], acc[c]);
+            } else if constexpr (MIX == 1) {  // discount: DMUL DSETP 2xFSEL DFMA
+                double p = __dmul_rn(a[c], b[c]);
+                double f = p > t ? c1 : 1.0;
+                acc[c] = __fma_rn(p, f, acc[c]);
+            } else if constexpr (MIX == 2) {  // DMUL + DFMA(p, c1, acc)
+                double p = __dmul_rn(a[c], b[c]);
+                acc[c] = __fma_rn(p, c1, acc[c]);
+            } else if constexpr (MIX == 3) {  // DMUL + DSETP + DADD predicated-select
+                double p = __dmul_rn(a[c], b[c]);
+                acc[c] = p > t ? acc[c] + p : acc[c];
+            } else if constexpr (MIX == 4) {  // DFMA sharing a (reuse slot)
+                acc[c] = __fma_rn(a[0], b[c], acc[c]);
+            } else if constexpr (MIX == 5) {  // discount, select p instead: 2 accs
+                double p = __dmul_rn(a[c], b[c]);
+                acc[c] = __dadd_rn(acc[c], p > t ? p * c1 : p);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NCH; ++c) asm volatile("" : "+d"(b[c]));
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) s += acc[c];
+    if (s == 1234.5) out[threadIdx.x] = s;
+}
+
+template <int MIX>
+void run(int sms, int blk, const char* name, double* out, const double* in) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    mix<MIX><<<sms * blk, 256>>>(out, in, ITERS);
+    cudaEventRecord(e0);
+    mix<MIX><<<sms * blk, 256>>>(out, in, ITERS);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    int clk;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    double warp_iters_per_smsp = double(blk) * 8 * NCH * ITERS / 4.0;
+    double cycles = ms * 1e-3 * clk * 1e3;  // at max clock
+    printf("%-44s blk=%d  %.3f ms  %.2f cycles/warp-iter/SMSP (at max clock)\n", name, blk, ms,
+           cycles / warp_iters_per_smsp);
+}
+
+int main() {
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    double *out, *in;
+    cudaMalloc(&out, 1024 * 8);
+    cudaMalloc(&in, 32 * 8);
+    double h[32];
+    for (int i = 0; i < 32; ++i) h[i] = 1.0 + i * 0.25;
+    cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
+    for (int blk : {1, 2, 4}) {
+        run<0>(sms, blk, "DFMA a,b,acc (3 fresh)", out, in);
+        run<4>(sms, blk, "DFMA a0(shared),b,acc", out, in);
+        run<1>(sms, blk, "discount DMUL DSETP 2FSEL DFMA", out, in);
+        run<2>(sms, blk, "DMUL + DFMA(p,c1,acc)", out, in);
+        run<3>(sms, blk, "DMUL DSETP DADD-select", out, in);
+        run<5>(sms, blk, "DMUL DSETP DMUL-select DADD", out, in);
+    }
+    return 0;
+}
