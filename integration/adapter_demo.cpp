@@ -38,6 +38,9 @@ int main(int argc, char** argv) {
         {"q1-ti", *preset_source("q1-ti")},
         {"q2-tij", *preset_source("q2-tij")},
         {"q3-ti", *preset_source("q3-ti")},
+        {"matmul-atb", *preset_source("matmul-atb")},
+        {"q1-tj-abt", *preset_source("q1-tj-abt")},
+        {"q2-tij-atbt", *preset_source("q2-tij-atbt")},
         {"sqdiff", wrap_head + "(A[i][k] - B[k][j])*(A[i][k] - B[k][j]);\n}\n"},
         {"eqcount", wrap_head + "A[i][k] == B[k][j];\n}\n"},
     };

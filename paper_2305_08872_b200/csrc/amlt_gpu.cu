@@ -92,6 +92,8 @@ struct amlt_ctx {
     std::vector<cudaEvent_t> pipe_ev;                      // run_host pipeline
     void* work = nullptr;
     size_t work_bytes = 0;
+    void* pack_ws = nullptr;  // dense copies of operands in other layouts
+    size_t pack_bytes = 0;
     // device staging for amlt_gpu_run_host
     void* hbuf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     size_t hbuf_bytes[5] = {0, 0, 0, 0, 0};
@@ -119,10 +121,19 @@ namespace {
 // operand validation (the GPU analogue of make_operands / find_aux,
 // src/engine.cpp:153-163, src/kernel_exec.cpp:48-52)
 
+// An operand region that must be packed into a dense row-major workspace.
+struct Strided {
+    const void* p = nullptr;
+    int64_t rows = 0, cols = 0, s0 = 0, s1 = 0;
+    bool need = false;
+};
+
 struct Resolved {
     KParams kp{};
     int64_t M = 0, N = 0, K = 0;
     bool aligned = true;  // 16-byte staging possible
+    Strided pack_a, pack_b, pack_r;
+    bool packed() const { return pack_a.need || pack_b.need || pack_r.need; }
 };
 
 // Element (r, c) of a statement operand with the given layout: returns the
@@ -179,21 +190,30 @@ Resolved resolve(const amlt_plan* plan, const amlt_operands* ops, const amlt_bou
     stmt_addr(ops->a, d.layout_a, b->i0, b->k0, "A", &pa, &sai, &sak);
     stmt_addr(ops->b, d.layout_b, b->k0, b->j0, "B", &pb, &sbk, &sbj);
     stmt_addr(ops->r, AMLT_LAYOUT_NORMAL, b->i0, b->j0, "R", &pr, &sri, &srj);
-    // The staged kernels read A along k and B/R along j contiguously.
-    if (sak != 1 && rv.K > 1)
-        fail(AMLT_ERR_UNSUPPORTED, "A operand with non-contiguous k (A[k][i] row-major or "
-                                   "A[i][k] col-major) is not supported by the GPU kernels yet");
-    if (sbj != 1 && rv.N > 1)
-        fail(AMLT_ERR_UNSUPPORTED, "B operand with non-contiguous j (B[j][k] row-major or "
-                                   "B[k][j] col-major) is not supported by the GPU kernels yet");
-    if (srj != 1 && rv.N > 1)
-        fail(AMLT_ERR_UNSUPPORTED, "column-major R is not supported by the GPU kernels yet");
+    // The staged kernels read A along k and B / R along j contiguously. Any
+    // other layout (transposed statements, col-major storage) is packed into
+    // a dense row-major workspace first (packing.hpp:11-18), R also unpacked
+    // after; the dense pitch is a multiple of 16 bytes (TMA).
+    const int64_t vn16 = 16 / dtype_size(d.dtype);
+    auto dense_ld = [&](int64_t cols) { return (std::max<int64_t>(cols, 1) + vn16 - 1) / vn16 * vn16; };
     kp.A = pa;
     kp.B = pb;
     kp.R = pr;
     kp.lda = sai;
     kp.ldb = sbk;
     kp.ldr = sri;
+    if (sak != 1 && rv.K > 1) {
+        rv.pack_a = {pa, rv.M, rv.K, sai, sak, true};
+        kp.lda = dense_ld(rv.K);
+    }
+    if (sbj != 1 && rv.N > 1) {
+        rv.pack_b = {pb, rv.K, rv.N, sbk, sbj, true};
+        kp.ldb = dense_ld(rv.N);
+    }
+    if (srj != 1 && rv.N > 1) {
+        rv.pack_r = {pr, rv.M, rv.N, sri, srj, true};
+        kp.ldr = dense_ld(rv.N);
+    }
     kp.M = rv.M;
     kp.N = rv.N;
     kp.K = rv.K;
@@ -252,8 +272,10 @@ Resolved resolve(const amlt_plan* plan, const amlt_operands* ops, const amlt_bou
     const int vn = 16 / es;
     auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
     // TMA staging: 16-byte aligned bases and row pitches
-    rv.aligned = al16(kp.A) && al16(kp.B) && kp.lda % vn == 0 && kp.ldb % vn == 0;
-    kp.r_vec_ok = al16(kp.R) && (kp.ldr % vn == 0 || rv.M <= 1);
+    // (packed operands land in a 256-byte aligned workspace)
+    rv.aligned = (rv.pack_a.need || al16(kp.A)) && (rv.pack_b.need || al16(kp.B)) &&
+                 kp.lda % vn == 0 && kp.ldb % vn == 0;
+    kp.r_vec_ok = (rv.pack_r.need || al16(kp.R)) && (kp.ldr % vn == 0 || rv.M <= 1);
     return rv;
 }
 
@@ -400,11 +422,57 @@ Dispatch plan_dispatch(const amlt_ctx* ctx, const amlt_plan* plan, const amlt_ti
     return dp;
 }
 
+void enqueue_compute(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch& dp,
+                     KParams kp);
+
 void enqueue(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch& dp) {
     if (rv.M == 0 || rv.N == 0) return;
     if (rv.K == 0) return;  // empty k range: R untouched
     if (ctx->dry()) return;
     KParams kp = rv.kp;
+    if (!rv.packed()) {
+        enqueue_compute(ctx, plan, rv, dp, kp);
+        return;
+    }
+    // Pack the operands the kernels cannot stage directly into one dense
+    // row-major workspace (A, then B, then R), compute, unpack R.
+    const size_t es = dtype_size(plan->desc.dtype);
+    auto bytes_of = [&](const Strided& s, int64_t ld) {
+        return s.need ? (size_t(s.rows) * size_t(ld) * es + 255) / 256 * 256 : size_t(0);
+    };
+    const size_t ba = bytes_of(rv.pack_a, kp.lda), bb = bytes_of(rv.pack_b, kp.ldb),
+                 br = bytes_of(rv.pack_r, kp.ldr);
+    if (ba + bb + br > ctx->pack_bytes) {
+        if (ctx->pack_ws) cudaFree(ctx->pack_ws);
+        ctx->pack_ws = nullptr;
+        ctx->pack_bytes = 0;
+        cuda_check(cudaMalloc(&ctx->pack_ws, ba + bb + br), "cudaMalloc(pack workspace)");
+        ctx->pack_bytes = ba + bb + br;
+    }
+    char* w = static_cast<char*>(ctx->pack_ws);
+    auto pack = [&](const Strided& s, void* dst, int64_t ld, int unpack) {
+        PackParams pp{unpack ? dst : s.p, unpack ? const_cast<void*>(s.p) : dst, s.rows, s.cols,
+                      s.s0, s.s1, ld, unpack};
+        cuda_check(plan->aux->pack(pp, ctx->stream), "pack kernel launch");
+    };
+    if (rv.pack_a.need) {
+        pack(rv.pack_a, w, kp.lda, 0);
+        kp.A = w;
+    }
+    if (rv.pack_b.need) {
+        pack(rv.pack_b, w + ba, kp.ldb, 0);
+        kp.B = w + ba;
+    }
+    if (rv.pack_r.need) {
+        pack(rv.pack_r, w + ba + bb, kp.ldr, 0);
+        kp.R = w + ba + bb;
+    }
+    enqueue_compute(ctx, plan, rv, dp, kp);
+    if (rv.pack_r.need) pack(rv.pack_r, w + ba + bb, kp.ldr, 1);
+}
+
+void enqueue_compute(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch& dp,
+                     KParams kp) {
     if (!plan->desc.accumulate) {
         // "=": only the last k term reaches R.
         const int64_t total = rv.M * rv.N;
@@ -693,6 +761,7 @@ amlt_status amlt_gpu_ctx_create(int device, int flags, amlt_ctx** out) {
             cudaFuncAttributes fa;
             cuda_check(cudaFuncGetAttributes(&fa, a.assign_func), "cudaFuncGetAttributes");
             cuda_check(cudaFuncGetAttributes(&fa, a.reduce_func), "cudaFuncGetAttributes");
+            cuda_check(cudaFuncGetAttributes(&fa, a.pack_func), "cudaFuncGetAttributes");
         }
     });
     if (st != AMLT_OK) {
@@ -710,6 +779,7 @@ void amlt_gpu_ctx_destroy(amlt_ctx* ctx) {
         cudaSetDevice(ctx->device);
         if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
         if (ctx->work) cudaFree(ctx->work);
+        if (ctx->pack_ws) cudaFree(ctx->pack_ws);
         for (void* p : ctx->hbuf)
             if (p) cudaFree(p);
         if (ctx->ev0) cudaEventDestroy(ctx->ev0);

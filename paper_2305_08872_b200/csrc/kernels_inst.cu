@@ -53,6 +53,8 @@ void AMLT_CAT4(register_, AMLT_BODY, _, AMLT_DT)(Registry& reg) {
     a.reduce = &launch_reduce<T>;
     a.assign_func = reinterpret_cast<const void*>(&mmlt_assign_kernel<Body, T>);
     a.reduce_func = reinterpret_cast<const void*>(&mmlt_splitk_reduce<T>);
+    a.pack = &launch_pack<T>;
+    a.pack_func = reinterpret_cast<const void*>(&mmlt_pack_kernel<T>);
     reg.aux.push_back(a);
 }
 

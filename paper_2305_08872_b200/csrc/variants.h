@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "mmlt_kernel.cuh"
+#include "pack.cuh"
 
 namespace amltk {
 
@@ -40,6 +41,8 @@ struct BodyAux {
     int dtype = 0;
     LaunchFn assign = nullptr;  // "=" statements: last k wins
     LaunchFn reduce = nullptr;  // split-K ordered reduction into R
+    cudaError_t (*pack)(const PackParams&, cudaStream_t) = nullptr;  // layout packing
+    const void* pack_func = nullptr;
     const void* assign_func = nullptr;
     const void* reduce_func = nullptr;
 };

@@ -292,3 +292,50 @@ def test_threshold_forms_all_variants(gpu_ctx, body, dtype, form):
         P.run_subtask(plan, P.Operands(dev(A, dtype), dev(B, dtype), R, dev(thres, dtype),
                                        dev(dis, dtype)), P.TileParams(), P.Bounds(*bnd))
         check(body, dtype, R.cpu().numpy(), want2, exact=True, what=f"t{form} bounds")
+
+
+@pytest.mark.parametrize("body,dtype", [("discount", "f64"), ("boost", "f32"), ("gemm", "f64"),
+                                        ("eqcount", "i32"), ("sqdiff", "f32")])
+def test_orientations_and_storage_orders(gpu_ctx, body, dtype):
+    """All four statement orientations (presets -ab/-atb/-abt/-atbt) over
+    row- and col-major buffers (test_exec.cpp:109-130), and col-major R: the
+    layouts the kernels do not stage directly are packed first, like the
+    reference's packing (packing.hpp:11-18)."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+    from oracle import pyoracle as po
+
+    M, K, N = 97, 61, 83
+    A, B, t, d = make_inputs(body, M, K, N, "int", seed=41)
+    R0 = np.random.default_rng(8).integers(-9, 9, (M, N)).astype(np.float64)
+    bounds = (3, M - 2, 1, N, 2, K - 1)
+    want = oracle(body, A, B, t, d, R0=R0, bounds=bounds)
+
+    def buf(x, transposed, colmajor):
+        """Buffer whose statement view is x: (x.T if transposed) stored row/col-major."""
+        y = x.T if transposed else x
+        tt = dev(np.ascontiguousarray(y), dtype)
+        if colmajor:
+            tt = tt.t().contiguous().t()  # same logical matrix, col-major strides
+        return tt
+
+    for at in (0, 1):
+        for bt in (0, 1):
+            plan = gpu_ctx.plan(body, dtype, layout_a=at, layout_b=bt)
+            for acm in (False, True):
+                for bcm in (False, True):
+                    for rcm in (False, True):
+                        Rb = dev(R0, dtype)
+                        if rcm:
+                            Rb = Rb.t().contiguous().t()
+                        ops = P.Operands(buf(A, at, acm), buf(B, bt, bcm), Rb, dev(t, dtype),
+                                         dev(d, dtype))
+                        P.run_subtask(plan, ops, P.TileParams(), P.Bounds(*bounds))
+                        check(body, dtype, Rb.cpu().numpy(), want, exact=True,
+                              what=f"at={at} bt={bt} acm={acm} bcm={bcm} rcm={rcm}")
+            # adaptive path too (one layout combination per orientation)
+            Rb = dev(R0, dtype)
+            ops = P.Operands(buf(A, at, True), buf(B, bt, False), Rb, dev(t, dtype), dev(d, dtype))
+            P.adaptive_execute(plan, ops, P.Bounds(*bounds))
+            check(body, dtype, Rb.cpu().numpy(), want, exact=True, what=f"adaptive at={at} bt={bt}")

@@ -210,14 +210,14 @@ def test_errors_map_to_reference_hierarchy(dry_ctx):
         P.run_subtask(plan, ops, P.TileParams(), P.Bounds(0, 16, 0, 16, 0, 16))
     with pytest.raises(P.EngineError):
         P.run_subtask(plan, big_ops(16, 16, 16), P.TileParams(), P.Bounds(0, 17, 0, 16, 0, 16))
-    tplan = dry_ctx.plan("gemm", "f64", layout_a=N.LAYOUT_TRANSPOSED)
-    with pytest.raises(P.UnsupportedExpression):  # A[k][i] over a row-major buffer
-        P.run_subtask(tplan, big_ops(16, 16, 16, "gemm"), P.TileParams(),
-                      P.Bounds(0, 16, 0, 16, 0, 16))
-    bplan = dry_ctx.plan("gemm", "f64", layout_b=N.LAYOUT_TRANSPOSED)
-    with pytest.raises(P.UnsupportedExpression):  # B[j][k] over a row-major buffer
-        P.run_subtask(bplan, big_ops(16, 16, 16, "gemm"), P.TileParams(),
-                      P.Bounds(0, 16, 0, 16, 0, 16))
+    # A[k][i] / B[j][k] over row-major buffers are packed (packing.hpp:11-18)
+    for lay in ({"layout_a": N.LAYOUT_TRANSPOSED}, {"layout_b": N.LAYOUT_TRANSPOSED}):
+        tplan = dry_ctx.plan("gemm", "f64", **lay)
+        assert P.run_subtask(tplan, big_ops(16, 16, 16, "gemm"), P.TileParams(),
+                             P.Bounds(0, 16, 0, 16, 0, 16), clock=P.FakeClock([0.5])) == 0.5
+    with pytest.raises(P.UnsupportedExpression):  # not one of the bodies
+        P.compile_task("where(i in [0..M] and j in [0..N] and k in [0..K]) {\n"
+                       "  R[i][j] += A[i][k]*B[k][j] + u[i]*v[j];\n}\n")
     # thresholds indexed [i]: accepted, and the vector must cover i1
     iplan = dry_ctx.plan("discount", "f64", thres_class="i")
     assert all(v.name.endswith(("_ti", "_ti_u")) for v in iplan.variants())
