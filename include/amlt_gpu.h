@@ -298,6 +298,51 @@ amlt_status amlt_gpu_adaptive_execute(amlt_ctx* ctx, const amlt_plan* plan,
 /* run_host flags */
 #define AMLT_HOST_R_ZERO 1 /* R starts at zero: device R is zero-filled, not copied in */
 
+/* AMULET's own tuner contract, restated on the GPU executor
+ * (src/autotuner.cpp:8-151): find_kc lays kc candidates (K, then repeated
+ * ceil-halving down to 16) along K on two i_w-wide column strips and scores
+ * elapsed / kc; find_nc scores column strips of width i_w, 2 i_w, ... by
+ * elapsed / nc until the first increase or the column budget; the remainder
+ * runs with the winners; tasks with N < 4 i_w or fewer than i_h rows run
+ * untuned (kc = min(K, 256), nc = N). Every subtask writes R and the (k, j)
+ * coverage ledger tiles K x N exactly once. On the GPU, a subtask's kc is its
+ * K-segment depth (split-K, ordered reduction) and nc picks the tile width.
+ * Pass the reference plan's kernel shape (i_h, i_w) to reproduce its
+ * decisions exactly under the same clock script. */
+#define AMLT_MAX_REF_TRIALS 64
+#define AMLT_MAX_REF_COVER 128
+
+typedef struct {
+    int64_t value;  /* kc or nc tried */
+    double elapsed;
+    double score;   /* elapsed / value */
+} amlt_ref_trial;
+
+typedef struct {
+    int64_t k0, k1;
+    int64_t j0, j1;
+} amlt_ref_cover; /* CoverRect: full M rows */
+
+typedef struct {
+    int32_t n_kc_trials;
+    amlt_ref_trial kc_trials[AMLT_MAX_REF_TRIALS];
+    int32_t n_nc_trials;
+    amlt_ref_trial nc_trials[AMLT_MAX_REF_TRIALS];
+    int64_t best_kc;
+    int64_t best_nc;
+    int32_t tuned;
+    int32_t n_cover;
+    amlt_ref_cover coverage[AMLT_MAX_REF_COVER];
+    double tuning_fraction;
+    double total_seconds;
+} amlt_amulet_report;
+
+amlt_status amlt_gpu_adaptive_execute_amulet(amlt_ctx* ctx, const amlt_plan* plan,
+                                             const amlt_operands* ops, const amlt_bounds* bounds,
+                                             int i_h, int i_w, amlt_clock_fn clock,
+                                             void* clock_user, amlt_exec_log* log,
+                                             amlt_amulet_report* report);
+
 /* Host-buffer entry (the reference's callers hold host MatrixBuffers):
  * operands' `data` are HOST pointers (pinned for full copy bandwidth).
  * Copies B and the aux vectors, then streams A (and R, unless

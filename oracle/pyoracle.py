@@ -277,6 +277,18 @@ class RefTask:
                                                     C.byref(nc)))
         return s.value, kc.value, nc.value
 
+    def run_adaptive_scripted(self, deltas):
+        """run_adaptive under the reference's FakeClock with `deltas`:
+        (best_kc, best_nc, tuned, intervals consumed, [(k0, k1, j0, j1)])."""
+        arr = (C.c_double * len(deltas))(*deltas)
+        kc, nc, tuned, used, ncov = C.c_int64(), C.c_int64(), C.c_int(), C.c_int(), C.c_int(256)
+        cov = (C.c_int64 * (4 * 256))()
+        self._check(ref_lib().ref_task_run_adaptive_scripted(
+            self._h, arr, C.c_int(len(deltas)), C.byref(kc), C.byref(nc), C.byref(tuned),
+            C.byref(used), C.byref(ncov), cov))
+        rects = [tuple(cov[4 * i:4 * i + 4]) for i in range(ncov.value)]
+        return kc.value, nc.value, bool(tuned.value), used.value, rects
+
     def run_fixed(self, kc, nc, pack=False) -> float:
         s = C.c_double()
         self._check(ref_lib().ref_task_run_fixed(self._h, C.c_int64(kc), C.c_int64(nc), int(pack),

@@ -188,6 +188,33 @@ int ref_task_run_adaptive(void* h, int pack, double* seconds, std::int64_t* best
     });
 }
 
+// run_adaptive driven by the reference's FakeClock (clock.hpp:29-55) with the
+// given interval script: the tuner's decisions and the number of intervals it
+// consumed, for comparing tuner logic decision-for-decision.
+int ref_task_run_adaptive_scripted(void* h, const double* deltas, int n, std::int64_t* best_kc,
+                                   std::int64_t* best_nc, int* tuned, int* consumed,
+                                   int* n_cover, std::int64_t* cover4) {
+    auto* t = static_cast<RefTask*>(h);
+    return guarded([&] {
+        FakeClock clock(std::vector<double>(deltas, deltas + n));
+        TuneReport rep = run_adaptive(t->ct, t->data, t->bind, false, clock);
+        *best_kc = rep.best_kc;
+        *best_nc = rep.best_nc;
+        *tuned = rep.tuned ? 1 : 0;
+        *consumed = static_cast<int>(clock.consumed());
+        int m = 0;
+        for (const auto& c : rep.coverage) {
+            if (m >= *n_cover) break;
+            cover4[4 * m + 0] = c.k0;
+            cover4[4 * m + 1] = c.k1;
+            cover4[4 * m + 2] = c.j0;
+            cover4[4 * m + 3] = c.j1;
+            ++m;
+        }
+        *n_cover = m;
+    });
+}
+
 int ref_task_run_fixed(void* h, std::int64_t kc, std::int64_t nc, int pack, double* seconds) {
     auto* t = static_cast<RefTask*>(h);
     return guarded([&] {

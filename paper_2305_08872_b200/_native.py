@@ -91,6 +91,26 @@ class TuneReportC(C.Structure):
                 ("total_seconds", C.c_double)]
 
 
+MAX_REF_TRIALS = 64
+MAX_REF_COVER = 128
+
+
+class RefTrialC(C.Structure):
+    _fields_ = [("value", C.c_int64), ("elapsed", C.c_double), ("score", C.c_double)]
+
+
+class RefCoverC(C.Structure):
+    _fields_ = [("k0", C.c_int64), ("k1", C.c_int64), ("j0", C.c_int64), ("j1", C.c_int64)]
+
+
+class AmuletReportC(C.Structure):
+    _fields_ = [("n_kc_trials", C.c_int32), ("kc_trials", RefTrialC * MAX_REF_TRIALS),
+                ("n_nc_trials", C.c_int32), ("nc_trials", RefTrialC * MAX_REF_TRIALS),
+                ("best_kc", C.c_int64), ("best_nc", C.c_int64), ("tuned", C.c_int32),
+                ("n_cover", C.c_int32), ("coverage", RefCoverC * MAX_REF_COVER),
+                ("tuning_fraction", C.c_double), ("total_seconds", C.c_double)]
+
+
 class TaskInfoC(C.Structure):
     _fields_ = [("desc", BodyDesc), ("a", C.c_char * 64), ("b", C.c_char * 64),
                 ("r", C.c_char * 64), ("thres", C.c_char * 64), ("dis", C.c_char * 64)]
@@ -104,7 +124,7 @@ EXPORTS = [
     "amlt_gpu_plan_destroy", "amlt_gpu_plan_num_variants", "amlt_gpu_plan_variant",
     "amlt_gpu_plan_default_variant", "amlt_gpu_run_subtask", "amlt_gpu_enqueue",
     "amlt_gpu_adaptive_execute", "amlt_gpu_run_host", "amlt_spr", "amlt_gpu_measure_peak",
-    "amlt_gpu_recognize", "amlt_gpu_plan_from_source",
+    "amlt_gpu_recognize", "amlt_gpu_plan_from_source", "amlt_gpu_adaptive_execute_amulet",
 ]
 HOST_R_ZERO = 1
 
@@ -149,6 +169,9 @@ def lib():
                                     C.POINTER(BoundsC), C.c_int, CLOCK_FN, P,
                                     C.POINTER(C.c_double)]
     L.amlt_gpu_measure_peak.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.amlt_gpu_adaptive_execute_amulet.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(BoundsC),
+                                                   C.c_int, C.c_int, CLOCK_FN, P,
+                                                   C.POINTER(ExecLogC), C.POINTER(AmuletReportC)]
     L.amlt_gpu_recognize.argtypes = [C.c_char_p, C.POINTER(TaskInfoC)]
     L.amlt_gpu_plan_from_source.argtypes = [P, C.c_char_p, C.c_int, C.POINTER(P),
                                             C.POINTER(TaskInfoC)]

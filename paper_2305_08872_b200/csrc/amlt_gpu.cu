@@ -682,6 +682,134 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
 }
 
 // ---------------------------------------------------------------------------
+// AMULET's tuner contract (src/autotuner.cpp:8-151), restated over the GPU
+// executor. Decisions depend only on the clock readings, so a scripted clock
+// reproduces the reference's kc / nc choices exactly.
+
+struct AmuletTuner {
+    amlt_ctx* ctx;
+    const amlt_plan* plan;
+    const amlt_operands* ops;
+    amlt_clock_fn clock;
+    void* user;
+    amlt_exec_log* log;
+    amlt_amulet_report* rep;
+
+    // run_subtask with TileParams{kc, nc}
+    double sub(const amlt_bounds& b, int64_t kc, int64_t nc) {
+        amlt_tile_params tp{kc, nc, 0, -1};
+        Resolved rv = resolve(plan, ops, &b);
+        Dispatch dp = plan_dispatch(ctx, plan, &tp, rv);
+        double el = timed_subtask(ctx, plan, rv, dp, b, clock, user, log);
+        rep->total_seconds += el;
+        return el;
+    }
+    void cover(int64_t k0, int64_t k1, int64_t j0, int64_t j1) {
+        if (rep->n_cover < AMLT_MAX_REF_COVER) rep->coverage[rep->n_cover++] = {k0, k1, j0, j1};
+    }
+    static void trial(amlt_ref_trial* arr, int32_t* n, int64_t v, double el) {
+        if (*n < AMLT_MAX_REF_TRIALS) arr[(*n)++] = {v, el, el / double(v)};
+    }
+    // kc_candidates (autotuner.cpp:8-16)
+    static std::vector<int64_t> kc_candidates(int64_t K) {
+        std::vector<int64_t> out;
+        if (K < 16) {
+            out.push_back(K);
+            return out;
+        }
+        for (int64_t c = K; c >= 16; c = (c + 1) / 2) out.push_back(c);
+        return out;
+    }
+    int64_t best_kc_so_far(const std::vector<int64_t>& cands) const {
+        int64_t best = cands[0];
+        double best_score = rep->n_kc_trials ? rep->kc_trials[0].score : 0.0;
+        for (int t = 0; t < rep->n_kc_trials; ++t)
+            if (rep->kc_trials[t].score < best_score) {
+                best_score = rep->kc_trials[t].score;
+                best = rep->kc_trials[t].value;
+            }
+        return best;
+    }
+    // find_kc (autotuner.cpp:18-68)
+    int64_t find_kc(const amlt_bounds& b, int64_t iw) {
+        const auto cands = kc_candidates(b.k1 - b.k0);
+        {
+            amlt_bounds s1{b.i0, b.i1, b.j0, b.j0 + 2 * iw, b.k0, b.k1};
+            double el = sub(s1, cands[0], iw);
+            trial(rep->kc_trials, &rep->n_kc_trials, cands[0], el);
+            cover(b.k0, b.k1, s1.j0, s1.j1);
+        }
+        const int64_t sj0 = b.j0 + 2 * iw, sj1 = b.j0 + 4 * iw;
+        int64_t kcur = b.k0;
+        for (size_t ci = 1; ci < cands.size(); ++ci) {
+            const int64_t len = cands[ci];
+            if (kcur + len > b.k1) continue;
+            double el = sub(amlt_bounds{b.i0, b.i1, sj0, sj1, kcur, kcur + len}, len, iw);
+            trial(rep->kc_trials, &rep->n_kc_trials, len, el);
+            cover(kcur, kcur + len, sj0, sj1);
+            kcur += len;
+        }
+        if (kcur < b.k1) {
+            sub(amlt_bounds{b.i0, b.i1, sj0, sj1, kcur, b.k1}, best_kc_so_far(cands), iw);
+            cover(kcur, b.k1, sj0, sj1);
+        }
+        return best_kc_so_far(cands);
+    }
+    // find_nc (autotuner.cpp:70-101)
+    int64_t find_nc(const amlt_bounds& b, int64_t best_kc, int64_t iw) {
+        int64_t jcur = b.j0 + 4 * iw;
+        const int64_t kb1 = std::min(b.k0 + best_kc, b.k1);
+        int64_t best = 0, prev = 0;
+        double best_score = 0.0, prev_score = 0.0;
+        for (int64_t w = iw;; w *= 2) {
+            if (jcur + w > b.j1) break;
+            double el = sub(amlt_bounds{b.i0, b.i1, jcur, jcur + w, b.k0, kb1}, best_kc, w);
+            const double score = el / double(w);
+            trial(rep->nc_trials, &rep->n_nc_trials, w, el);
+            cover(b.k0, kb1, jcur, jcur + w);
+            jcur += w;
+            if (prev != 0 && score > prev_score) return prev;
+            prev = w;
+            prev_score = score;
+            if (best == 0 || score < best_score) {
+                best = w;
+                best_score = score;
+            }
+        }
+        return best != 0 ? best : b.j1 - b.j0;
+    }
+    // adaptive_execute (autotuner.cpp:103-151)
+    void run(const amlt_bounds& b, int64_t ih, int64_t iw) {
+        const int64_t N = b.j1 - b.j0, K = b.k1 - b.k0;
+        if (N < 4 * iw || b.i1 - b.i0 < ih) {
+            rep->tuned = 0;
+            rep->best_kc = std::min<int64_t>(K, 256);
+            rep->best_nc = N;
+            sub(b, rep->best_kc, rep->best_nc);
+            cover(b.k0, b.k1, b.j0, b.j1);
+            rep->tuning_fraction = 0.0;
+            return;
+        }
+        rep->tuned = 1;
+        rep->best_kc = find_kc(b, iw);
+        rep->best_nc = find_nc(b, rep->best_kc, iw);
+        int64_t tested_w = 0;
+        for (int t = 0; t < rep->n_nc_trials; ++t) tested_w += rep->nc_trials[t].value;
+        rep->tuning_fraction = double(4 * iw + tested_w) / double(N);
+        const int64_t nc_j0 = b.j0 + 4 * iw, nc_j1 = nc_j0 + tested_w;
+        const int64_t kb1 = std::min(b.k0 + rep->best_kc, b.k1);
+        if (tested_w > 0 && kb1 < b.k1) {
+            sub(amlt_bounds{b.i0, b.i1, nc_j0, nc_j1, kb1, b.k1}, rep->best_kc, rep->best_nc);
+            cover(kb1, b.k1, nc_j0, nc_j1);
+        }
+        if (nc_j1 < b.j1) {
+            sub(amlt_bounds{b.i0, b.i1, nc_j1, b.j1, b.k0, b.k1}, rep->best_kc, rep->best_nc);
+            cover(b.k0, b.k1, nc_j1, b.j1);
+        }
+    }
+};
+
+// ---------------------------------------------------------------------------
 // boundary helpers
 
 template <class F>
@@ -954,6 +1082,21 @@ amlt_status amlt_gpu_adaptive_execute(amlt_ctx* ctx, const amlt_plan* plan,
         if (!ctx->dry()) cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
         amlt_tune_report local;
         adaptive(ctx, plan, ops, *bounds, clock, clock_user, log, report ? report : &local);
+    });
+}
+
+amlt_status amlt_gpu_adaptive_execute_amulet(amlt_ctx* ctx, const amlt_plan* plan,
+                                             const amlt_operands* ops, const amlt_bounds* bounds,
+                                             int i_h, int i_w, amlt_clock_fn clock,
+                                             void* clock_user, amlt_exec_log* log,
+                                             amlt_amulet_report* report) {
+    if (!ctx || !plan || !bounds || !report || i_h < 1 || i_w < 1) return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (!ctx->dry()) cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        std::memset(report, 0, sizeof(*report));
+        (void)resolve(plan, ops, bounds);  // validate once up front
+        AmuletTuner t{ctx, plan, ops, clock, clock_user, log, report};
+        t.run(*bounds, i_h, i_w);
     });
 }
 

@@ -500,6 +500,62 @@ def adaptive_execute(plan: GpuPlan, ops: Operands, bounds: Bounds, pack: bool = 
     return _report(rc)
 
 
+@dataclass
+class RefTrial:
+    value: int
+    elapsed: float
+    score: float
+
+
+@dataclass
+class RefCoverRect:
+    k0: int
+    k1: int
+    j0: int
+    j1: int
+
+
+@dataclass
+class AmuletTuneReport:
+    """The reference's TuneReport (autotuner.hpp:26-34)."""
+    kc_trials: List[RefTrial] = field(default_factory=list)
+    nc_trials: List[RefTrial] = field(default_factory=list)
+    best_kc: int = 0
+    best_nc: int = 0
+    tuned: bool = False
+    coverage: List[RefCoverRect] = field(default_factory=list)
+    tuning_fraction: float = 0.0
+    total_seconds: float = 0.0
+
+
+def adaptive_execute_amulet(plan: GpuPlan, ops: Operands, bounds: Bounds, i_h: int = 12,
+                            i_w: int = 16, clock: Optional[Clock] = None,
+                            log: Optional[ExecLog] = None) -> AmuletTuneReport:
+    """AMULET's own tuner contract over the GPU executor (find_kc / find_nc /
+    remainder rectangles, autotuner.cpp:8-151). With the reference plan's
+    (i_h, i_w) and the same clock script it makes the reference's choices."""
+    ctx = plan.ctx
+    bridge = _ClockBridge(clock)
+    oc = ops._c(None if ctx.dry_run else True)
+    bc = bounds._c()
+    lc, recs = _log_c(log)
+    rc = N.AmuletReportC()
+    st = ctx._lib.amlt_gpu_adaptive_execute_amulet(ctx.handle, plan.handle, C.byref(oc),
+                                                   C.byref(bc), i_h, i_w, bridge.fn, None,
+                                                   C.byref(lc) if lc is not None else None,
+                                                   C.byref(rc))
+    bridge.check()
+    _raise(st, ctx.handle)
+    _log_back(log, lc, recs)
+    rep = AmuletTuneReport()
+    rep.kc_trials = [RefTrial(t.value, t.elapsed, t.score) for t in rc.kc_trials[:rc.n_kc_trials]]
+    rep.nc_trials = [RefTrial(t.value, t.elapsed, t.score) for t in rc.nc_trials[:rc.n_nc_trials]]
+    rep.best_kc, rep.best_nc, rep.tuned = rc.best_kc, rc.best_nc, bool(rc.tuned)
+    rep.coverage = [RefCoverRect(c.k0, c.k1, c.j0, c.j1) for c in rc.coverage[:rc.n_cover]]
+    rep.tuning_fraction, rep.total_seconds = rc.tuning_fraction, rc.total_seconds
+    return rep
+
+
 def run_host(plan: GpuPlan, ops: Operands, bounds: Bounds, params: Optional[TileParams] = None,
              clock: Optional[Clock] = None, r_zero: bool = False) -> float:
     """Host-buffer entry: operands in host memory (pinned for full speed).

@@ -339,3 +339,22 @@ def test_orientations_and_storage_orders(gpu_ctx, body, dtype):
             ops = P.Operands(buf(A, at, True), buf(B, bt, False), Rb, dev(t, dtype), dev(d, dtype))
             P.adaptive_execute(plan, ops, P.Bounds(*bounds))
             check(body, dtype, Rb.cpu().numpy(), want, exact=True, what=f"adaptive at={at} bt={bt}")
+
+
+@pytest.mark.parametrize("body,dtype", [("discount", "f64"), ("gemm", "f32"), ("eqcount", "i32")])
+def test_amulet_tuner_contract_on_gpu(gpu_ctx, body, dtype):
+    """AMULET's own tuner (find_kc / find_nc / remainder, autotuner.cpp)
+    driving the GPU executor with real timing: the result is exact."""
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 150, 700, 900
+    A, B, t, d = make_inputs(body, M, K, N, "int", seed=51)
+    want = oracle(body, A, B, t, d)
+    plan = gpu_ctx.plan(body, dtype)
+    R = dev(np.zeros((M, N)), dtype)
+    log = P.ExecLog()
+    rep = P.engine.adaptive_execute_amulet(
+        plan, P.Operands(dev(A, dtype), dev(B, dtype), R, dev(t, dtype), dev(d, dtype)),
+        P.Bounds(0, M, 0, N, 0, K), i_h=12, i_w=16, log=log)
+    assert rep.tuned and rep.kc_trials and rep.nc_trials
+    check(body, dtype, R.cpu().numpy(), want, exact=True, what="amulet tuner")
