@@ -575,10 +575,10 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
                         for (int e = 0; e < VN; ++e) b[q * VN + e] = V16<T>::get(bv, e);
                     }
 #pragma unroll
-                    for (int r = 0; r < TM; ++r) {
-                        const T a = V16<T>::get(av[r], v);
+                    for (int c = 0; c < TN; ++c) {
 #pragma unroll
-                        for (int c = 0; c < TN; ++c) {
+                        for (int r = 0; r < TM; ++r) {
+                            const T a = V16<T>::get(av[r], v);
                             if constexpr (Body::TWO_LEVEL)
                                 STEP(part[r][c], a, c, COL(r, c));
                             else

@@ -13,15 +13,44 @@ template <int MIX>
 __global__ void __launch_bounds__(256) mix(double* out, const double* in, int n) {
     double a[NCH], b[NCH], acc[NCH];
     const double t = in[0], c1 = in[1];
+    double tt[4], cc[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        tt[c] = in[18 + (threadIdx.x + c) % 8];
+        cc[c] = in[26 + c % 4];
+    }
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
         a[c] = in[2 + (threadIdx.x + c) % 8];
         b[c] = in[10 + (threadIdx.x * 3 + c) % 8];
         acc[c] = 0;
     }
+    __shared__ __align__(16) double sA[16 * 8 * 4];
+    __shared__ __align__(16) double sB[16 * 128];
+    if constexpr (MIX == 8) {
+        for (int i = threadIdx.x; i < 16 * 8 * 4; i += blockDim.x) sA[i] = in[i % 16];
+        for (int i = threadIdx.x; i < 16 * 128; i += blockDim.x) sB[i] = in[(i * 7) % 16];
+        __syncthreads();
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int it = 0; it < n; ++it) {
+        if constexpr (MIX == 8) {
+            // the tiled kernel's operand traffic: per k, B = 4 lane-interleaved
+            // columns (2 x LDS.128), A = 4 rows broadcast (LDS.64 each)
+            const int k = it & 15;
+            const double2 b01 = *reinterpret_cast<const double2*>(sB + k * 128 + lane * 2);
+            const double2 b23 = *reinterpret_cast<const double2*>(sB + k * 128 + 64 + lane * 2);
+            b[0] = b01.x; b[1] = b01.y; b[2] = b23.x; b[3] = b23.y;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) a[r] = sA[(warp * 4 + r) * 16 + k];
+        }
 #pragma unroll
         for (int c = 0; c < NCH; ++c) {
+            if constexpr (MIX == 8) {
+                double p = __dmul_rn(a[c / 4], b[c % 4]);
+                double f = p > tt[c % 4] ? cc[c % 4] : 1.0;
+                acc[c] = __fma_rn(p, f, acc[c]);
+            }
             if constexpr (MIX == 0) {  // DFMA, three distinct fresh sources
                 acc[c] = __fma_rn(a[c], b[c], acc[c]);
             } else if constexpr (MIX == 1) {  // discount: DMUL DSETP 2xFSEL DFMA
@@ -39,6 +68,14 @@ __global__ void __launch_bounds__(256) mix(double* out, const double* in, int n)
             } else if constexpr (MIX == 5) {  // discount, select p instead: 2 accs
                 double p = __dmul_rn(a[c], b[c]);
                 acc[c] = __dadd_rn(acc[c], p > t ? p * c1 : p);
+            } else if constexpr (MIX == 6) {  // discount with per-column t, c1 (4 columns)
+                double p = __dmul_rn(a[c], b[c]);
+                double f = p > tt[c % 4] ? cc[c % 4] : 1.0;
+                acc[c] = __fma_rn(p, f, acc[c]);
+            } else if constexpr (MIX == 7) {  // discount, 4x4 tile: a per row, b/t/c1 per col
+                double p = __dmul_rn(a[c / 4], b[c % 4]);
+                double f = p > tt[c % 4] ? cc[c % 4] : 1.0;
+                acc[c] = __fma_rn(p, f, acc[c]);
             }
         }
 #pragma unroll
@@ -75,9 +112,9 @@ int main() {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     double *out, *in;
     cudaMalloc(&out, 1024 * 8);
-    cudaMalloc(&in, 32 * 8);
-    double h[32];
-    for (int i = 0; i < 32; ++i) h[i] = 1.0 + i * 0.25;
+    cudaMalloc(&in, 64 * 8);
+    double h[64];
+    for (int i = 0; i < 64; ++i) h[i] = 1.0 + i * 0.25;
     cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
     for (int blk : {1, 2, 4}) {
         run<0>(sms, blk, "DFMA a,b,acc (3 fresh)", out, in);
@@ -86,6 +123,9 @@ int main() {
         run<2>(sms, blk, "DMUL + DFMA(p,c1,acc)", out, in);
         run<3>(sms, blk, "DMUL DSETP DADD-select", out, in);
         run<5>(sms, blk, "DMUL DSETP DMUL-select DADD", out, in);
+        run<6>(sms, blk, "discount, per-column t/c1 (4 cols)", out, in);
+        run<7>(sms, blk, "discount 4x4 tile (a per row, b/t/c1 per col)", out, in);
+        run<8>(sms, blk, "discount 4x4 tile, operands from smem", out, in);
     }
     return 0;
 }
