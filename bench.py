@@ -239,8 +239,9 @@ def traffic_for(workload, tile):
             d = json.load(open(path)).get(workload, {})
         except (OSError, ValueError):
             continue
-        if tile in d:
-            return d[tile]["dram_read"] + d[tile]["dram_write"]
+        entry = d.get(tile) or d.get("*")  # "*": tile-independent (same raster groups)
+        if entry:
+            return entry["dram_read"] + entry["dram_write"]
     return None
 
 
