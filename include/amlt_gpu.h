@@ -220,6 +220,9 @@ typedef struct {
     int64_t best_kc;
     int32_t tuned;      /* 0: too small to tune, ran whole with the default */
     int32_t from_cache; /* 1: winner reused from an earlier tuning          */
+    int32_t scratch_tuned; /* 1: too small for row-band trials: candidates
+                              timed on the whole task against a scratch R
+                              (trials rows == M), then the task ran once    */
     int32_t n_cover;
     amlt_cover_rect coverage[AMLT_MAX_COVER]; /* disjoint, union = bounds   */
     double tuning_fraction;                   /* tuned rows / M             */

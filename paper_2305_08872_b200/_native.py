@@ -86,7 +86,7 @@ class CoverRectC(C.Structure):
 class TuneReportC(C.Structure):
     _fields_ = [("n_trials", C.c_int32), ("trials", TrialC * MAX_TRIALS),
                 ("best_variant", C.c_int32), ("best_kc", C.c_int64), ("tuned", C.c_int32),
-                ("from_cache", C.c_int32), ("n_cover", C.c_int32),
+                ("from_cache", C.c_int32), ("scratch_tuned", C.c_int32), ("n_cover", C.c_int32),
                 ("coverage", CoverRectC * MAX_COVER), ("tuning_fraction", C.c_double),
                 ("total_seconds", C.c_double)]
 

@@ -94,6 +94,8 @@ struct amlt_ctx {
     size_t work_bytes = 0;
     void* pack_ws = nullptr;  // dense copies of operands in other layouts
     size_t pack_bytes = 0;
+    void* scratch = nullptr;  // scratch R for whole-task tuning trials
+    size_t scratch_bytes = 0;
     // device staging for amlt_gpu_run_host
     void* hbuf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     size_t hbuf_bytes[5] = {0, 0, 0, 0, 0};
@@ -578,6 +580,73 @@ void add_cover(amlt_tune_report* rep, const amlt_bounds& b) {
     }
 }
 
+// Whole-task trials against a scratch R (see adaptive()). Records one trial
+// per candidate (rows = M; score = elapsed / M) and caches the winner.
+void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops,
+                  const amlt_bounds& b, const Resolved& whole, const std::vector<int>& cands,
+                  amlt_tune_report* rep) {
+    const size_t bytes = size_t(whole.M) * size_t(whole.N) * dtype_size(plan->desc.dtype);
+    if (bytes > ctx->scratch_bytes) {
+        if (ctx->scratch) cudaFree(ctx->scratch);
+        ctx->scratch = nullptr;
+        ctx->scratch_bytes = 0;
+        cuda_check(cudaMalloc(&ctx->scratch, bytes), "cudaMalloc(tuning scratch)");
+        ctx->scratch_bytes = bytes;
+    }
+    struct Cand {
+        int variant;
+        int64_t kc;
+    };
+    std::vector<Cand> trials;
+    for (int v : cands) {
+        trials.push_back({v, 0});
+        const VariantDesc& vd = vdesc(v);
+        const int occ = ctx->occupancy.empty() ? vd.minb : std::max(1, ctx->occupancy[v]);
+        const int64_t ctas = ctas_for(vd, whole.M, whole.N);
+        const int64_t slots = int64_t(ctx->num_sms) * occ;
+        if (ctas < 2 * slots && whole.K >= 512) {  // split-K forms for small outputs
+            for (int64_t splits : {int64_t(2), (2 * slots + ctas - 1) / ctas}) {
+                splits = std::min<int64_t>(splits, whole.K / 128);
+                if (splits < 2) continue;
+                const int64_t kc = ((whole.K + splits - 1) / splits + 31) / 32 * 32;
+                if (trials.back().kc != kc) trials.push_back({v, kc});
+            }
+        }
+    }
+    Resolved rs = resolve(plan, ops, &b);
+    rs.kp.R = ctx->scratch;  // scratch R: dense row-major M x N
+    rs.kp.ldr = whole.N;
+    rs.kp.r_vec_ok = (whole.N * dtype_size(plan->desc.dtype)) % 16 == 0;
+    rs.pack_r = Strided{};
+    double best_t = 0;
+    Cand best{-1, 0};
+    for (const Cand& c : trials) {
+        amlt_tile_params tp{c.kc, 0, 0, plan_local_index(plan, c.variant)};
+        Dispatch dp = plan_dispatch(ctx, plan, &tp, rs);
+        cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
+        enqueue(ctx, plan, rs, dp);
+        cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
+        cuda_check(cudaEventSynchronize(ctx->ev1), "cudaEventSynchronize");
+        float ms = 0;
+        cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "cudaEventElapsedTime");
+        const double el = ms * 1e-3;
+        if (rep->n_trials < AMLT_MAX_TRIALS) {
+            amlt_trial& t = rep->trials[rep->n_trials++];
+            t.value = plan_local_index(plan, c.variant);
+            t.rows = whole.M;
+            t.elapsed = el;
+            t.score = el / double(whole.M);
+        }
+        if (best.variant < 0 || el < best_t) {
+            best_t = el;
+            best = c;
+        }
+    }
+    rep->scratch_tuned = 1;
+    ctx->tune_cache[std::make_tuple(plan->desc.body, plan->desc.dtype, whole.M, whole.N, whole.K)] =
+        amlt_ctx::Winner{best.variant, best.kc};
+}
+
 void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, const amlt_bounds& b,
               amlt_clock_fn clock, void* user, amlt_exec_log* log, amlt_tune_report* rep) {
     std::memset(rep, 0, sizeof(*rep));
@@ -623,6 +692,18 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
         return el;
     };
 
+    // Too small for row-band trials (each candidate would need more than a
+    // quarter of the rows to fill the GPU): measure every candidate — tile
+    // variants, plus split-K forms when the output cannot fill the SMs — on
+    // the whole task against a scratch R, once per shape; the winner is
+    // cached and the real task runs once with it. Skipped in dry-run
+    // contexts and for tasks too large to repeat cheaply.
+    if (!tunable && plan->desc.accumulate && !ctx->dry() && !cands.empty() && whole.M > 0 &&
+        whole.N > 0 && whole.K > 0 && ctx->tune_cache.find(key) == ctx->tune_cache.end() &&
+        double(whole.M) * double(whole.N) * double(whole.K) <= 1.5e11 &&
+        whole.M * whole.N * dtype_size(plan->desc.dtype) <= (int64_t(1) << 30)) {
+        scratch_tune(ctx, plan, ops, b, whole, cands, rep);
+    }
     if (!tunable) {
         rep->tuned = 0;
         auto it = ctx->tune_cache.find(key);
@@ -908,6 +989,7 @@ void amlt_gpu_ctx_destroy(amlt_ctx* ctx) {
         if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
         if (ctx->work) cudaFree(ctx->work);
         if (ctx->pack_ws) cudaFree(ctx->pack_ws);
+        if (ctx->scratch) cudaFree(ctx->scratch);
         for (void* p : ctx->hbuf)
             if (p) cudaFree(p);
         if (ctx->ev0) cudaEventDestroy(ctx->ev0);

@@ -220,6 +220,7 @@ class TuneReport:
     best_kc: int = 0
     tuned: bool = False
     from_cache: bool = False
+    scratch_tuned: bool = False
     coverage: List[CoverRect] = field(default_factory=list)
     tuning_fraction: float = 0.0
     total_seconds: float = 0.0
@@ -472,6 +473,7 @@ def _report(rc: N.TuneReportC) -> TuneReport:
     rep.best_kc = rc.best_kc
     rep.tuned = bool(rc.tuned)
     rep.from_cache = bool(rc.from_cache)
+    rep.scratch_tuned = bool(rc.scratch_tuned)
     rep.coverage = [CoverRect(c.i0, c.i1, c.k0, c.k1, c.j0, c.j1)
                     for c in rc.coverage[:rc.n_cover]]
     rep.tuning_fraction = rc.tuning_fraction
