@@ -316,7 +316,10 @@ def main():
     rows = row1 - row0
 
     ctx = P.Context(lrank)
-    stream = torch.cuda.current_stream(device)
+    # one explicit (non-default) stream for torch and the kernels alike, so the
+    # CUDA events below bracket exactly the launches
+    stream = torch.cuda.Stream(device)
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream)
     text = {"discount": "A[i][k]*B[k][j] - (A[i][k]*B[k][j] > thres[j])*A[i][k]*B[k][j]*dis[j]",
             "boost": "A[i][k]*B[k][j] + (A[i][k]*B[k][j] > thres[j])*(A[i][k]*B[k][j] - thres[j])",
@@ -329,7 +332,14 @@ def main():
     # roofline denominator, measured on this GPU now
     pipe = PIPE[dtype] if not (body == "gemm" and dtype == "f64") else "dmma"
     peak_ops, peak_ghz = P.engine.measure_peak(pipe)
-    peak_tflops = 2 * peak_ops / 1e12 if pipe != "alu" else peak_ops / 1e12
+    if pipe == "alu":
+        # integer bodies are issue-bound (ISETP + predicated add per
+        # iteration, both integer-pipe instructions): the ceiling is the
+        # SM's issue rate, 4 schedulers x 32 lanes per clock
+        props = torch.cuda.get_device_properties(device)
+        peak_tflops = 128 * props.multi_processor_count * peak_ghz * 1e9 / 1e12
+    else:
+        peak_tflops = 2 * peak_ops / 1e12
 
     A, B, th, ds = gen_inputs(body, dtype, rows, K, N, row0, rank, device, dist is not None)
     R = torch.zeros((rows, N), dtype=A.dtype, device=device)
@@ -442,7 +452,9 @@ def main():
     if rank == 0:
         variants = plan.variants()
         best = last.best_variant if last else -1
-        ops_per_iter = {"discount": 3, "boost": 3, "gemm": 1, "sqdiff": 2, "eqcount": 2}[body]
+        # pipe instructions per inner iteration of the body's kernel; the
+        # ceiling under 2-op accounting is 1/ops of the pipe peak
+        ops_per_iter = {"discount": 3, "boost": 3, "gemm": 1, "sqdiff": 2, "eqcount": 1}[body]
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s",
             "inner_iters_per_s": iters_total / el,
@@ -469,8 +481,13 @@ def main():
                          "traffic_unit": "bytes per launch (ncu dram read+write, committed "
                                          "capture profiles/*/traffic.json)",
                          "algorithmic_bytes": algorithmic_bytes(body, dtype, M, K, N),
-                         "accounting": "2 flops per inner iteration (matmul-like); peak = measured "
-                                       f"{pipe} probe x2 on this GPU at {peak_ghz:.3f} GHz",
+                         "accounting": (
+                             "2 ops per inner iteration (matmul-like); peak = the SM issue rate "
+                             f"(128 lane-instructions/clk/SM) at the probe's {peak_ghz:.3f} GHz; the "
+                             "body issues exactly 2 instructions per iteration"
+                             if pipe == "alu" else
+                             "2 flops per inner iteration (matmul-like); peak = measured "
+                             f"{pipe} probe x2 on this GPU at {peak_ghz:.3f} GHz"),
                          "body_pipe_ops_per_iter": ops_per_iter,
                          "frac_of_body_ceiling": achieved_tflops / peak_tflops * ops_per_iter,
                          "kernel_ms": kernel_s * 1e3},
