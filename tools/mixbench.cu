@@ -33,6 +33,68 @@ __global__ void __launch_bounds__(256) mix(double* out, const double* in, int n)
         __syncthreads();
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if constexpr (MIX == 11 || MIX == 12) {
+        // B only from smem, A in registers. MIX 11: 4 x LDS.64 per k (one per
+        // column); MIX 12: column-major B tile, one LDS.128 = 2 k values of a
+        // column, 4 per 2 k.
+        for (int i = threadIdx.x; i < 16 * 128; i += blockDim.x) sB[i] = in[(i * 7) % 16];
+        __syncthreads();
+        for (int it = 0; it < n; it += 4) {
+#pragma unroll
+            for (int kk = 0; kk < 4; kk += 2) {
+                const int k = (it + kk) & 15;
+                double bb[2][4];
+                if constexpr (MIX == 11) {
+#pragma unroll
+                    for (int v = 0; v < 2; ++v)
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) bb[v][c] = sB[(k + v) * 128 + c * 32 + lane];
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const double2 t2 = *reinterpret_cast<const double2*>(
+                            sB + ((c * 32 + lane) * 16 + k) % (16 * 128));
+                        bb[0][c] = t2.x;
+                        bb[1][c] = t2.y;
+                    }
+                }
+#pragma unroll
+                for (int v = 0; v < 2; ++v)
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) {
+                        double p = __dmul_rn(a[c / 4], bb[v][c % 4]);
+                        double f = p > tt[c % 4] ? cc[c % 4] : 1.0;
+                        acc[c] = __fma_rn(p, f, acc[c]);
+                    }
+            }
+        }
+    } else
+    if constexpr (MIX == 9 || MIX == 10) {
+        // MIX 9: 4x4 tile fed from smem, 4 k per loop trip (loads hoistable);
+        // MIX 10: same with only the B loads (A from registers)
+        for (int i = threadIdx.x; i < 16 * 8 * 4; i += blockDim.x) sA[i] = in[i % 16];
+        for (int i = threadIdx.x; i < 16 * 128; i += blockDim.x) sB[i] = in[(i * 7) % 16];
+        __syncthreads();
+        for (int it = 0; it < n; it += 4) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                const int k = (it + kk) & 15;
+                const double2 b01 = *reinterpret_cast<const double2*>(sB + k * 128 + lane * 2);
+                const double2 b23 = *reinterpret_cast<const double2*>(sB + k * 128 + 64 + lane * 2);
+                double bb[4] = {b01.x, b01.y, b23.x, b23.y};
+                double aa[4];
+#pragma unroll
+                for (int r = 0; r < 4; ++r)
+                    aa[r] = MIX == 9 ? sA[(warp * 4 + r) * 16 + k] : a[r];
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    double p = __dmul_rn(aa[c / 4], bb[c % 4]);
+                    double f = p > tt[c % 4] ? cc[c % 4] : 1.0;
+                    acc[c] = __fma_rn(p, f, acc[c]);
+                }
+            }
+        }
+    } else
     for (int it = 0; it < n; ++it) {
         if constexpr (MIX == 8) {
             // the tiled kernel's operand traffic: per k, B = 4 lane-interleaved
@@ -126,6 +188,10 @@ int main() {
         run<6>(sms, blk, "discount, per-column t/c1 (4 cols)", out, in);
         run<7>(sms, blk, "discount 4x4 tile (a per row, b/t/c1 per col)", out, in);
         run<8>(sms, blk, "discount 4x4 tile, operands from smem", out, in);
+        run<9>(sms, blk, "discount 4x4, smem, 4 k unrolled", out, in);
+        run<10>(sms, blk, "discount 4x4, smem B only, 4 k unrolled", out, in);
+        run<11>(sms, blk, "discount 4x4, smem B only, LDS.64 per column", out, in);
+        run<12>(sms, blk, "discount 4x4, smem B only, col-major LDS.128 (2 k)", out, in);
     }
     return 0;
 }
