@@ -79,6 +79,31 @@ int main(int argc, char** argv) {
             }
         }
     }
+    // every one of the reference's 52 presets at the dims of test_engine.cpp:145-167,
+    // int-valued data, adaptive: bit-exact against run_naive
+    const std::int64_t pdims[][3] = {{32, 24, 40}, {13, 17, 5}};
+    for (const std::string& name : all_preset_names()) {
+        CompiledTask ct = compile_task(*preset_source(name), MachineModel{});
+        for (const auto& d : pdims) {
+            DimBinding bind = bind_dims(ct, d[0], d[1], d[2]);
+            TaskData data = make_task_data(ct, bind, 1, StorageOrder::RowMajor,
+                                           StorageOrder::RowMajor, DataMode::IntValued);
+            if (dry) {
+                std::unique_ptr<amlt_gpu::Plan> plan(gpu::plan_for(gpu, ct));
+                (void)gpu::operands(*plan, data);
+                continue;
+            }
+            SteadyClock clock;
+            gpu::run_adaptive(gpu, ct, data, bind, false, clock);
+            VerifyResult v = verify_against_naive(ct, data, bind, DataMode::IntValued);
+            ++checks;
+            if (!v.exact) {
+                ++failures;
+                std::printf("FAIL preset %s %lldx%lldx%lld: max_abs=%.3e\n", name.c_str(),
+                            (long long)d[0], (long long)d[1], (long long)d[2], v.max_abs_err);
+            }
+        }
+    }
     // a recognised MMLT the GPU has no body for: the adapter must refuse it
     bool refused = false;
     try {
