@@ -359,6 +359,23 @@ amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_o
                               const amlt_tile_params* tile, const amlt_bounds* bounds, int flags,
                               amlt_clock_fn clock, void* clock_user, double* elapsed_s);
 
+/* Row-band multi-GPU execution of one task from a single process (the
+ * reference engine's process model). Device d of n owns rows
+ * [i0 + M d/n, i0 + M (d+1)/n) of A and R; B and the per-column vectors are
+ * copied to devices[0] once and replicated with one NCCL broadcast each over
+ * NVLink / NVSwitch; there is no reduction (rows of R are independent). Each
+ * device then runs amlt_gpu_adaptive_execute on its band (one host thread
+ * per device) and its R rows are copied back. Operands are HOST buffers, as
+ * for amlt_gpu_run_host; A must keep each row's k values contiguous
+ * (A[i][k] row-major or A[k][i] col-major) and R must be row-major, so bands
+ * are contiguous blocks (else UNSUPPORTED). NCCL (libnccl.so.2) is loaded at
+ * run time. *elapsed_s covers copies, broadcast and compute. */
+amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const amlt_operands* host_ops,
+                                 const amlt_bounds* bounds, int n_devices, const int* devices,
+                                 int flags, double* elapsed_s);
+/* Message of the calling thread's last failing amlt_gpu_run_sharded. */
+const char* amlt_gpu_sharded_last_error(void);
+
 /* Pipe-throughput probe on the current device (roofline denominators):
  * pipe 0 DFMA, 1 FFMA, 2 integer ALU, 3 DSETP+select, 4 DMMA (f64 tensor).
  * *ops_per_s: lane operations per second (FMA pipes and DMMA: FMAs/s);

@@ -125,6 +125,7 @@ EXPORTS = [
     "amlt_gpu_plan_default_variant", "amlt_gpu_run_subtask", "amlt_gpu_enqueue",
     "amlt_gpu_adaptive_execute", "amlt_gpu_run_host", "amlt_spr", "amlt_gpu_measure_peak",
     "amlt_gpu_recognize", "amlt_gpu_plan_from_source", "amlt_gpu_adaptive_execute_amulet",
+    "amlt_gpu_run_sharded", "amlt_gpu_sharded_last_error",
 ]
 HOST_R_ZERO = 1
 
@@ -172,6 +173,10 @@ def lib():
     L.amlt_gpu_adaptive_execute_amulet.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(BoundsC),
                                                    C.c_int, C.c_int, CLOCK_FN, P,
                                                    C.POINTER(ExecLogC), C.POINTER(AmuletReportC)]
+    L.amlt_gpu_run_sharded.argtypes = [C.POINTER(BodyDesc), C.POINTER(OperandsC),
+                                       C.POINTER(BoundsC), C.c_int, C.POINTER(C.c_int), C.c_int,
+                                       C.POINTER(C.c_double)]
+    L.amlt_gpu_sharded_last_error.restype = C.c_char_p
     L.amlt_gpu_recognize.argtypes = [C.c_char_p, C.POINTER(TaskInfoC)]
     L.amlt_gpu_plan_from_source.argtypes = [P, C.c_char_p, C.c_int, C.POINTER(P),
                                             C.POINTER(TaskInfoC)]

@@ -58,7 +58,8 @@ def _jobs():
         out = os.path.join(OBJ, f"k_{body}_{dt}.o")
         defs = [f"-DAMLT_BODY={body}", f"-DAMLT_BODY_ID={bid}", f"-DAMLT_T={ctype}", f"-DAMLT_DT={dt}"]
         jobs.append((inst, out, defs))
-    for src in ("dmma_gemm.cu", "register_all.cu", "amlt_gpu.cu", "peak.cu", "task.cpp"):
+    for src in ("dmma_gemm.cu", "register_all.cu", "amlt_gpu.cu", "peak.cu", "task.cpp",
+                "sharded.cu"):
         obj = os.path.splitext(src)[0] + ".o"
         jobs.append((os.path.join(CSRC, src), os.path.join(OBJ, obj), []))
     return jobs
@@ -93,7 +94,7 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
                 f.write(f"==== {os.path.basename(k)}\n{v}\n")
     objs = [out for _, out, _ in _jobs()]
     if todo or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [exe, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]
+        cmd = [exe, *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs, "-ldl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed:\n" + r.stderr[-4000:])

@@ -579,6 +579,23 @@ def run_host(plan: GpuPlan, ops: Operands, bounds: Bounds, params: Optional[Tile
     return el.value
 
 
+def run_sharded_host(desc_plan: GpuPlan, ops: Operands, bounds: Bounds, devices,
+                     r_zero: bool = False) -> float:
+    """Single-process row-band multi-GPU run (amlt_gpu_run_sharded): host
+    operands, B and vectors NCCL-broadcast from devices[0], one band per
+    device, R rows copied back. Returns elapsed seconds."""
+    devs = (C.c_int * len(devices))(*devices)
+    oc = ops._c(False)
+    bc = bounds._c()
+    el = C.c_double()
+    st = N.lib().amlt_gpu_run_sharded(C.byref(desc_plan.desc), C.byref(oc), C.byref(bc),
+                                      len(devices), devs, N.HOST_R_ZERO if r_zero else 0,
+                                      C.byref(el))
+    if st != N.OK:
+        raise _ERRS.get(st, EngineError)(N.lib().amlt_gpu_sharded_last_error().decode())
+    return el.value
+
+
 def run_fixed(plan: GpuPlan, ops: Operands, bounds: Bounds, kc: int, nc: int, pack=False,
               clock: Optional[Clock] = None, log: Optional[ExecLog] = None) -> float:
     """run_fixed (engine.hpp:67-68): one subtask over the whole bounds."""

@@ -358,3 +358,28 @@ def test_amulet_tuner_contract_on_gpu(gpu_ctx, body, dtype):
         P.Bounds(0, M, 0, N, 0, K), i_h=12, i_w=16, log=log)
     assert rep.tuned and rep.kc_trials and rep.nc_trials
     check(body, dtype, R.cpu().numpy(), want, exact=True, what="amulet tuner")
+
+
+def test_run_sharded_single_process(gpu_ctx):
+    """amlt_gpu_run_sharded: single-process row-band execution from host
+    buffers (one band per device; here the box's one device), for A[i][k]
+    row-major and A[k][i] col-major; other A layouts are refused."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    ndev = torch.cuda.device_count()
+    M, K, N = 700, 300, 260
+    A, B, t, d = make_inputs("discount", M, K, N, "baseline", seed=61)
+    want = oracle("discount", A, B, t, d)
+    for at, Abuf in ((0, np.ascontiguousarray(A)), (1, np.asfortranarray(A.T))):
+        plan = gpu_ctx.plan("discount", "f64", layout_a=at)
+        R = np.zeros((M, N))
+        el = P.engine.run_sharded_host(plan, P.Operands(Abuf, B, R, t, d),
+                                       P.Bounds(0, M, 0, N, 0, K), list(range(ndev)), r_zero=True)
+        assert el > 0
+        check("discount", "f64", R, want, what=f"sharded layout_a={at}")
+    plan = gpu_ctx.plan("discount", "f64", layout_a=1)
+    with pytest.raises(P.UnsupportedExpression):
+        P.engine.run_sharded_host(plan, P.Operands(np.ascontiguousarray(A.T), B, np.zeros((M, N)),
+                                                   t, d), P.Bounds(0, M, 0, N, 0, K), [0])
