@@ -285,6 +285,17 @@ amlt_status amlt_gpu_run_subtask(amlt_ctx* ctx, const amlt_plan* plan, const aml
                                  amlt_clock_fn clock, void* clock_user, amlt_exec_log* log,
                                  double* elapsed_s);
 
+/* The per-element device executor (GPU counterpart of run_naive,
+ * src/naive.cpp:65-117,157-166, and execute_scalar_region,
+ * src/kernel_exec.cpp:408-457): one thread per R element walks k ascending,
+ * evaluating the statement term node by node (no contraction) and
+ * accumulating `R += v` (or `R = v` for assignments). The untiled reference
+ * path behind "naive" runs and --verify; synchronous; timed like
+ * run_subtask (two clock reads, or CUDA events when clock is NULL). */
+amlt_status amlt_gpu_run_naive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops,
+                               const amlt_bounds* bounds, amlt_clock_fn clock, void* clock_user,
+                               double* elapsed_s);
+
 /* Asynchronous form of run_subtask: enqueues on the context stream and
  * returns; no clock reads, no synchronisation. */
 amlt_status amlt_gpu_enqueue(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops,
@@ -375,6 +386,29 @@ amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const amlt_operands
                                  int flags, double* elapsed_s);
 /* Message of the calling thread's last failing amlt_gpu_run_sharded. */
 const char* amlt_gpu_sharded_last_error(void);
+
+/* The reference's AMLT binary matrix files (README.md:146-157,
+ * src/matrix.cpp:64-114; the CLI's --a-file / --b-file): 24-byte header
+ * ("AMLT", u32 rows, u32 cols, u8 order, zero padding) then rows*cols f64
+ * values in storage order. Reads convert to the requested dtype and can land
+ * directly in device memory (chunked through a pinned buffer); writes
+ * accept f64 / f32 / i32 host or device buffers in storage order. Errors:
+ * ENGINE (bad magic, unknown order, truncated, unopenable), with the message
+ * in amlt_matrix_file_last_error(). */
+amlt_status amlt_matrix_file_info(const char* path, int64_t* rows, int64_t* cols, int* order);
+amlt_status amlt_matrix_file_read(const char* path, void* dst, int dtype, int dst_on_device);
+amlt_status amlt_matrix_file_write(const char* path, const void* src, int64_t rows, int64_t cols,
+                                   int order, int dtype, int src_on_device);
+const char* amlt_matrix_file_last_error(void);
+
+/* The reference's seeded inputs (src/matrix.cpp:20-37, src/engine.cpp:147):
+ * amlt_gen_matrix fills rows*cols values in storage order from mt19937_64
+ * over seed_seq{seed, rows, cols, order, mode}; mode 0 = IntValued ([-8, 8]),
+ * 1 = Real ([0, 1)). amlt_operand_seed(seed, name) = seed ^ fnv1a(name), the
+ * per-array seed make_task_data uses. */
+uint64_t amlt_operand_seed(uint64_t seed, const char* name);
+amlt_status amlt_gen_matrix(uint64_t seed, int64_t rows, int64_t cols, int order, int mode,
+                            void* dst, int dtype, int dst_on_device);
 
 /* Pipe-throughput probe on the current device (roofline denominators):
  * pipe 0 DFMA, 1 FFMA, 2 integer ALU, 3 DSETP+select, 4 DMMA (f64 tensor).

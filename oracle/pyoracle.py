@@ -156,8 +156,50 @@ def ref_lib():
         lib.ref_task_array_name.restype = C.c_char_p
         lib.ref_task_result_name.restype = C.c_char_p
         lib.ref_last_error.restype = C.c_char_p
+        lib.ref_gen_matrix.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int,
+                                       C.c_void_p]
+        lib.ref_write_matrix_file.argtypes = [C.c_char_p, C.c_int64, C.c_int64, C.c_int,
+                                              C.c_void_p]
+        lib.ref_read_matrix_file.argtypes = [C.c_char_p, C.POINTER(C.c_int64),
+                                             C.POINTER(C.c_int64), C.POINTER(C.c_int),
+                                             C.c_void_p, C.c_int64]
         _ref = lib
     return _ref
+
+
+def ref_gen_matrix(seed: int, rows: int, cols: int, order: int, mode: int):
+    """The reference's gen_matrix (src/matrix.cpp:20-37): the storage-order
+    buffer as a flat float64 array."""
+    import numpy as np
+    out = np.empty(rows * cols, dtype=np.float64)
+    if ref_lib().ref_gen_matrix(seed & 0xFFFFFFFFFFFFFFFF, rows, cols, order, mode,
+                                out.ctypes.data) != 0:
+        raise RuntimeError(ref_lib().ref_last_error().decode())
+    return out
+
+
+def ref_write_matrix_file(path: str, rows: int, cols: int, order: int, storage) -> None:
+    """The reference's write_matrix_file (src/matrix.cpp:64-88)."""
+    import numpy as np
+    s = np.ascontiguousarray(storage, dtype=np.float64).ravel()
+    if ref_lib().ref_write_matrix_file(str(path).encode(), rows, cols, order, s.ctypes.data) != 0:
+        raise RuntimeError(ref_lib().ref_last_error().decode())
+
+
+def ref_read_matrix_file(path: str):
+    """The reference's read_matrix_file (src/matrix.cpp:90-114) ->
+    (rows, cols, order, flat storage-order float64 array); raises
+    RuntimeError carrying the reference's EngineError message."""
+    import numpy as np
+    r, c, o = C.c_int64(), C.c_int64(), C.c_int()
+    lib = ref_lib()
+    if lib.ref_read_matrix_file(str(path).encode(), C.byref(r), C.byref(c), C.byref(o), None, 0):
+        raise RuntimeError(lib.ref_last_error().decode())
+    out = np.empty(r.value * c.value, dtype=np.float64)
+    if lib.ref_read_matrix_file(str(path).encode(), C.byref(r), C.byref(c), C.byref(o),
+                                out.ctypes.data, out.size):
+        raise RuntimeError(lib.ref_last_error().decode())
+    return r.value, c.value, o.value, out
 
 
 def ref_available() -> bool:

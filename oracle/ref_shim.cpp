@@ -11,6 +11,7 @@
 //   run_adaptive      (src/engine.cpp:165-169 -> src/autotuner.cpp:103-151)
 //   run_fixed         (src/engine.cpp:171-175 -> src/tiled_executor.cpp:9-77)
 //   execute_scalar_region (src/kernel_exec.cpp:408-457)
+//   gen_matrix / write_matrix_file / read_matrix_file (src/matrix.cpp:20-114)
 //   adaptive_execute on row bands from N threads (the "all cores" CPU
 //   baseline of SURVEY.md §8(d); each thread owns disjoint rows of R).
 // Only tests/, __graft_entry__.smoke() and bench.py (cpu baseline / reference
@@ -27,6 +28,7 @@
 #include "amlt/clock.hpp"
 #include "amlt/engine.hpp"
 #include "amlt/errors.hpp"
+#include "amlt/matrix.hpp"
 #include "amlt/presets.hpp"
 
 using namespace amlt;
@@ -264,6 +266,43 @@ int ref_task_run_adaptive_bands(void* h, int nthreads, std::int64_t i0, std::int
         for (auto& e : errs)
             if (!e.empty()) throw EngineError(e);
         *seconds = std::chrono::duration<double>(t1 - t0).count();
+    });
+}
+
+// gen_matrix (src/matrix.cpp:20-37): values in storage order into out.
+int ref_gen_matrix(std::uint64_t seed, std::int64_t rows, std::int64_t cols, int order, int mode,
+                   double* out) {
+    return guarded([&] {
+        MatrixBuffer m = gen_matrix(seed, rows, cols, static_cast<StorageOrder>(order),
+                                    mode == 0 ? DataMode::IntValued : DataMode::Real);
+        std::memcpy(out, m.data(), static_cast<size_t>(rows * cols) * sizeof(double));
+    });
+}
+
+// write_matrix_file (src/matrix.cpp:64-88) of a storage-order buffer.
+int ref_write_matrix_file(const char* path, std::int64_t rows, std::int64_t cols, int order,
+                          const double* data) {
+    return guarded([&] {
+        MatrixBuffer m(rows, cols, static_cast<StorageOrder>(order));
+        std::memcpy(m.data(), data, static_cast<size_t>(rows * cols) * sizeof(double));
+        write_matrix_file(path, m);
+    });
+}
+
+// read_matrix_file (src/matrix.cpp:90-114). out may be null (header only);
+// otherwise it must hold cap doubles.
+int ref_read_matrix_file(const char* path, std::int64_t* rows, std::int64_t* cols, int* order,
+                         double* out, std::int64_t cap) {
+    return guarded([&] {
+        MatrixBuffer m = read_matrix_file(path);
+        *rows = m.rows();
+        *cols = m.cols();
+        *order = static_cast<int>(m.order());
+        const std::int64_t n = m.rows() * m.cols();
+        if (out) {
+            if (n > cap) throw EngineError("buffer too small");
+            std::memcpy(out, m.data(), static_cast<size_t>(n) * sizeof(double));
+        }
     });
 }
 

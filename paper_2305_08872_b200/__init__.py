@@ -11,7 +11,8 @@ from .engine import (Bounds, Clock, Context, CoverRect, EngineError, ExecLog, Ex
                      FakeClock, GpuPlan, MissingBinding, NoDevice, NoFeasibleKernel,
                      NonPositiveTime, Operands, SteadyClock, TileParams, Trial, TuneReport,
                      UnsupportedExpression, adaptive_execute, bounds_of, enqueue, operands_of,
-                     run_adaptive, run_fixed, run_host, run_subtask, spr)
+                     run_adaptive, run_fixed, run_host, run_naive, run_subtask,
+                     spr)
 from .task import TaskPlan, compile_task  # noqa: F401
 
 __all__ = [n for n in dir() if not n.startswith("_")]

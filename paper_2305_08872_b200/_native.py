@@ -125,7 +125,9 @@ EXPORTS = [
     "amlt_gpu_plan_default_variant", "amlt_gpu_run_subtask", "amlt_gpu_enqueue",
     "amlt_gpu_adaptive_execute", "amlt_gpu_run_host", "amlt_spr", "amlt_gpu_measure_peak",
     "amlt_gpu_recognize", "amlt_gpu_plan_from_source", "amlt_gpu_adaptive_execute_amulet",
-    "amlt_gpu_run_sharded", "amlt_gpu_sharded_last_error",
+    "amlt_gpu_run_sharded", "amlt_gpu_sharded_last_error", "amlt_matrix_file_info",
+    "amlt_matrix_file_read", "amlt_matrix_file_write", "amlt_matrix_file_last_error",
+    "amlt_operand_seed", "amlt_gen_matrix", "amlt_gpu_run_naive",
 ]
 HOST_R_ZERO = 1
 
@@ -161,6 +163,8 @@ def lib():
     L.amlt_gpu_run_subtask.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(TileParamsC),
                                        C.POINTER(BoundsC), CLOCK_FN, P, C.POINTER(ExecLogC),
                                        C.POINTER(C.c_double)]
+    L.amlt_gpu_run_naive.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(BoundsC), CLOCK_FN, P,
+                                      C.POINTER(C.c_double)]
     L.amlt_gpu_enqueue.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(TileParamsC),
                                    C.POINTER(BoundsC)]
     L.amlt_gpu_adaptive_execute.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(BoundsC),
@@ -177,6 +181,16 @@ def lib():
                                        C.POINTER(BoundsC), C.c_int, C.POINTER(C.c_int), C.c_int,
                                        C.POINTER(C.c_double)]
     L.amlt_gpu_sharded_last_error.restype = C.c_char_p
+    L.amlt_matrix_file_info.argtypes = [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                        C.POINTER(C.c_int)]
+    L.amlt_matrix_file_read.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int]
+    L.amlt_matrix_file_write.argtypes = [C.c_char_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int,
+                                         C.c_int, C.c_int]
+    L.amlt_matrix_file_last_error.restype = C.c_char_p
+    L.amlt_operand_seed.argtypes = [C.c_uint64, C.c_char_p]
+    L.amlt_operand_seed.restype = C.c_uint64
+    L.amlt_gen_matrix.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_void_p,
+                                  C.c_int, C.c_int]
     L.amlt_gpu_recognize.argtypes = [C.c_char_p, C.POINTER(TaskInfoC)]
     L.amlt_gpu_plan_from_source.argtypes = [P, C.c_char_p, C.c_int, C.POINTER(P),
                                             C.POINTER(TaskInfoC)]

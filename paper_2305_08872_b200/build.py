@@ -59,7 +59,7 @@ def _jobs():
         defs = [f"-DAMLT_BODY={body}", f"-DAMLT_BODY_ID={bid}", f"-DAMLT_T={ctype}", f"-DAMLT_DT={dt}"]
         jobs.append((inst, out, defs))
     for src in ("dmma_gemm.cu", "register_all.cu", "amlt_gpu.cu", "peak.cu", "task.cpp",
-                "sharded.cu"):
+                "sharded.cu", "matrix_file.cpp", "naive.cu"):
         obj = os.path.splitext(src)[0] + ".o"
         jobs.append((os.path.join(CSRC, src), os.path.join(OBJ, obj), []))
     return jobs

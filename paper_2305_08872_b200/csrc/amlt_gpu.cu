@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/amlt_gpu.h"
+#include "naive.h"
 #include "variants.h"
 
 #include <cudaTypedefs.h>
@@ -1140,6 +1141,54 @@ amlt_status amlt_gpu_run_subtask(amlt_ctx* ctx, const amlt_plan* plan, const aml
         Resolved rv = resolve(plan, ops, bounds);
         Dispatch dp = plan_dispatch(ctx, plan, tile, rv);
         double el = timed_subtask(ctx, plan, rv, dp, *bounds, clock, clock_user, log);
+        if (elapsed_s) *elapsed_s = el;
+    });
+}
+
+amlt_status amlt_gpu_run_naive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops,
+                               const amlt_bounds* bounds, amlt_clock_fn clock, void* clock_user,
+                               double* elapsed_s) {
+    if (!ctx || !plan) return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        // same operand rules as the tiled path; the per-element kernel then
+        // addresses every operand through its own strides (no packing)
+        Resolved rv = resolve(plan, ops, bounds);
+        const amlt_body_desc& d = plan->desc;
+        NaiveParams np{};
+        char *pa, *pb, *pr;
+        stmt_addr(ops->a, d.layout_a, bounds->i0, bounds->k0, "A", &pa, &np.sai, &np.sak);
+        stmt_addr(ops->b, d.layout_b, bounds->k0, bounds->j0, "B", &pb, &np.sbk, &np.sbj);
+        stmt_addr(ops->r, AMLT_LAYOUT_NORMAL, bounds->i0, bounds->j0, "R", &pr, &np.sri, &np.srj);
+        np.A = pa;
+        np.B = pb;
+        np.R = pr;
+        np.thres = rv.kp.thres;
+        np.t_si = rv.kp.t_si;
+        np.t_sj = rv.kp.t_sj;
+        np.tconst = rv.kp.tconst;
+        np.dis = rv.kp.dis;
+        np.d_sj = rv.kp.d_sj;
+        np.M = rv.M;
+        np.N = rv.N;
+        np.K = rv.K;
+        np.accumulate = d.accumulate;
+        double el = 0.0;
+        if (!ctx->dry()) {
+            cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+            const double t0 = clock ? clock(clock_user) : 0.0;
+            if (!clock) cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
+            cuda_check(launch_naive(np, d.body, d.dtype, ctx->num_sms, ctx->stream), "naive kernel");
+            if (clock) {
+                cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+                el = clock(clock_user) - t0;
+            } else {
+                cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
+                cuda_check(cudaEventSynchronize(ctx->ev1), "cudaEventSynchronize");
+                float ms = 0.f;
+                cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "cudaEventElapsedTime");
+                el = ms * 1e-3;
+            }
+        }
         if (elapsed_s) *elapsed_s = el;
     });
 }

@@ -289,7 +289,7 @@ def matrix_of(x, expect_device: Optional[bool] = None) -> N.Matrix:
         raise EngineError("operands must be 1-D or 2-D")
     r, c = shape
     s0, s1 = strides
-    if s1 == 1 or c == 1:
+    if s1 == 1 or c == 1 or r == 0 or c == 0:
         return N.Matrix(ptr, r, c, max(s0, c, 1), N.ROW_MAJOR, dt)
     if s0 == 1 or r == 1:
         return N.Matrix(ptr, r, c, max(s1, r, 1), N.COL_MAJOR, dt)
@@ -452,6 +452,24 @@ def run_subtask(plan: GpuPlan, ops: Operands, params: TileParams, bounds: Bounds
     bridge.check()
     _raise(st, ctx.handle)
     _log_back(log, lc, recs)
+    return el.value
+
+
+def run_naive(plan: GpuPlan, ops: Operands, bounds: Bounds,
+              clock: Optional[Clock] = None) -> float:
+    """The per-element device executor (amlt_gpu_run_naive): the GPU
+    counterpart of run_naive / execute_scalar_region (src/naive.cpp:157-166,
+    src/kernel_exec.cpp:408-457) — untiled, k ascending, one IEEE operation
+    per syntax-tree node. Synchronous; returns elapsed seconds."""
+    ctx = plan.ctx
+    bridge = _ClockBridge(clock)
+    oc = ops._c(None if ctx.dry_run else True)
+    bc = bounds._c()
+    el = C.c_double()
+    st = ctx._lib.amlt_gpu_run_naive(ctx.handle, plan.handle, C.byref(oc), C.byref(bc), bridge.fn,
+                                     None, C.byref(el))
+    bridge.check()
+    _raise(st, ctx.handle)
     return el.value
 
 

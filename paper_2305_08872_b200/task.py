@@ -316,3 +316,51 @@ def compile_task(source: str) -> TaskPlan:
                 dims=(str(ends[vi]), str(ends[vk]), str(ends[vj])))
     raise UnsupportedExpression("statement is an MMLT but not one of the GPU bodies "
                                 "(gemm, discount, boost, sqdiff, eqcount, thrcount)")
+
+
+# ---------------------------------------------------------------------------
+# built-in task names (presets.hpp / src/presets.cpp:8-94): matmul, q1, q2, q3
+# with an optional threshold suffix (-tc | -ti | -tj | -tij; q1/q2 default
+# -tj, q3 default -tc, none for matmul) and an optional orientation suffix
+# (-ab | -atb | -abt | -atbt), in any order, each at most once.
+
+_PRESET_BASES = ("matmul", "q1", "q2", "q3")
+_THRES_FORMS = {"tc": "100", "ti": "thres[i]", "tj": "thres[j]", "tij": "thres[i][j]"}
+_ORIENTS = ("ab", "atb", "abt", "atbt")
+
+
+def preset_names() -> List[str]:
+    """Every accepted built-in name with explicit suffixes (the 52 of
+    presets.cpp: 4 matmul orientations + 3 bases x 4 thresholds x 4)."""
+    out = [f"matmul-{o}" for o in _ORIENTS]
+    for base in ("q1", "q2", "q3"):
+        out += [f"{base}-{t}-{o}" for t in _THRES_FORMS for o in _ORIENTS]
+    return out
+
+
+def preset_source(name: str) -> Optional[str]:
+    """DSL text of a built-in task, or None for an unknown name."""
+    parts = name.split("-")
+    base = parts[0]
+    if base not in _PRESET_BASES:
+        return None
+    thres = "tc" if base == "q3" else "tj"
+    orient = "ab"
+    seen_t = seen_o = False
+    for s in parts[1:]:
+        if s in _THRES_FORMS and not seen_t and base != "matmul":
+            thres, seen_t = s, True
+        elif s in _ORIENTS and not seen_o:
+            orient, seen_o = s, True
+        else:
+            return None
+    a = "A[k][i]" if orient in ("atb", "atbt") else "A[i][k]"
+    b = "B[j][k]" if orient in ("abt", "atbt") else "B[k][j]"
+    ab = f"{a}*{b}"
+    t = _THRES_FORMS[thres]
+    rhs = {"matmul": ab,
+           "q1": f"{ab} - ({ab} > {t})*{ab}*dis[j]",
+           "q2": f"{ab} + ({ab} > {t})*({ab} - {t})",
+           "q3": f"({ab} > {t})"}[base]
+    return ("where(i in [0..M] and j in [0..N] and k in [0..K]) {\n"
+            f"  R[i][j] += {rhs};\n}}\n")

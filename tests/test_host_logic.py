@@ -270,3 +270,16 @@ def test_no_device_context_fails_loudly():
         pytest.skip("a GPU is present")
     with pytest.raises(P.NoDevice):
         P.Context(0)
+
+
+def test_run_naive_validates_like_run_subtask(dry_ctx):
+    """amlt_gpu_run_naive shares the operand rules (missing aux, bounds
+    beyond an operand) and never reads the clock in a dry-run context."""
+    plan = dry_ctx.plan("discount", "f64")
+    ops = big_ops(16, 16, 16)
+    assert P.run_naive(plan, ops, P.Bounds(0, 16, 0, 16, 0, 16)) == 0.0
+    ops.dis = None
+    with pytest.raises(P.MissingBinding):
+        P.run_naive(plan, ops, P.Bounds(0, 16, 0, 16, 0, 16))
+    with pytest.raises(P.EngineError):
+        P.run_naive(plan, big_ops(16, 16, 16), P.Bounds(0, 16, 0, 17, 0, 16))
