@@ -211,5 +211,6 @@ def test_read_and_generate_straight_into_device_memory(tmp_path, order, dtype):
     p2 = str(tmp_path / "d2.amlt")
     io.write_matrix_file(p2, g)  # device source
     if dtype != "f64":
-        io.write_matrix_file(p, torch.from_numpy(np.ascontiguousarray(m)).to(d.dtype))
+        io.write_matrix_file(p, torch.from_numpy(np.ascontiguousarray(m)).to(d.dtype),
+                             order=order)
     assert open(p2, "rb").read() == open(p, "rb").read()
