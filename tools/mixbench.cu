@@ -134,6 +134,43 @@ __global__ void __launch_bounds__(256) mix(double* out, const double* in, int n)
                 double p = __dmul_rn(a[c], b[c]);
                 double f = p > tt[c % 4] ? cc[c % 4] : 1.0;
                 acc[c] = __fma_rn(p, f, acc[c]);
+            } else if constexpr (MIX == 13) {  // DMUL chains only
+                acc[c] = __dmul_rn(acc[c], b[c]);
+            } else if constexpr (MIX == 14) {  // DADD chains only
+                acc[c] = __dadd_rn(acc[c], b[c]);
+            } else if constexpr (MIX == 15) {  // DSETP + 2 FSEL only (acc = select)
+                acc[c] = b[c] > acc[c] ? c1 : 1.0;
+            } else if constexpr (MIX == 16) {  // DMUL, DSETP, 1 SEL (hi word) -> m, DFMA c, DFMA acc
+                double p = __dmul_rn(a[c], b[c]);
+                unsigned hi;
+                asm("{ .reg .pred P; setp.gt.f64 P, %1, %2; selp.b32 %0, 0x3ff00000, 0, P; }"
+                    : "=r"(hi) : "d"(p), "d"(t));
+                double m = __hiloint2double(int(hi), 0);
+                double cf = __fma_rn(-m, c1, 1.0);
+                acc[c] = __fma_rn(p, cf, acc[c]);
+            } else if constexpr (MIX == 17) {  // predicated DFMA / DADD
+                double p = __dmul_rn(a[c], b[c]);
+                asm("{ .reg .pred P; setp.gt.f64 P, %1, %2; @P fma.rn.f64 %0, %1, %3, %0; "
+                    "@!P add.rn.f64 %0, %0, %1; }" : "+d"(acc[c]) : "d"(p), "d"(t), "d"(c1));
+            } else if constexpr (MIX == 18) {  // two accumulators: DFMA all, @P DADD masked
+                double p = __dmul_rn(a[c], b[c]);
+                asm("{ .reg .pred P; setp.gt.f64 P, %1, %2; @P add.rn.f64 %0, %0, %1; }"
+                    : "+d"(a[(c + 1) % NCH]) : "d"(p), "d"(t));
+                acc[c] = __dadd_rn(acc[c], p);
+            } else if constexpr (MIX == 19) {  // DSETP + DADD (pred add)
+                asm("{ .reg .pred P; setp.gt.f64 P, %1, %2; @P add.rn.f64 %0, %0, %1; }"
+                    : "+d"(acc[c]) : "d"(b[c]), "d"(t));
+            } else if constexpr (MIX == 20) {  // DMUL + DSETP + 1 SEL only
+                double p = __dmul_rn(a[c], b[c]);
+                unsigned hi;
+                asm("{ .reg .pred P; setp.gt.f64 P, %1, %2; selp.b32 %0, 0x3ff00000, 0, P; }"
+                    : "=r"(hi) : "d"(p), "d"(t));
+                acc[c] = __hiloint2double(int(hi) ^ __double2hiint(acc[c]), 0);
+            } else if constexpr (MIX == 21) {  // DSETP alone (predicate feeds an int add)
+                unsigned hi;
+                asm("{ .reg .pred P; setp.gt.f64 P, %1, %2; selp.b32 %0, 1, 0, P; }"
+                    : "=r"(hi) : "d"(b[c]), "d"(acc[c]));
+                acc[c] = __hiloint2double(__double2hiint(acc[c]) + int(hi), __double2loint(acc[c]));
             } else if constexpr (MIX == 7) {  // discount, 4x4 tile: a per row, b/t/c1 per col
                 double p = __dmul_rn(a[c / 4], b[c % 4]);
                 double f = p > tt[c % 4] ? cc[c % 4] : 1.0;
@@ -178,6 +215,17 @@ int main() {
     double h[64];
     for (int i = 0; i < 64; ++i) h[i] = 1.0 + i * 0.25;
     cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
+    for (int blk : {2, 4}) {
+        run<13>(sms, blk, "DMUL only", out, in);
+        run<14>(sms, blk, "DADD only", out, in);
+        run<15>(sms, blk, "DSETP + 2 FSEL only", out, in);
+        run<16>(sms, blk, "discount via m: DMUL DSETP SEL DFMA DFMA", out, in);
+        run<17>(sms, blk, "discount predicated @P DFMA / @!P DADD", out, in);
+        run<18>(sms, blk, "two accs: DMUL DSETP @P DADD DADD", out, in);
+        run<19>(sms, blk, "DSETP + @P DADD", out, in);
+        run<20>(sms, blk, "DMUL DSETP SEL (+int ops)", out, in);
+        run<21>(sms, blk, "DSETP SEL IADD", out, in);
+    }
     for (int blk : {1, 2, 4}) {
         run<0>(sms, blk, "DFMA a,b,acc (3 fresh)", out, in);
         run<4>(sms, blk, "DFMA a0(shared),b,acc", out, in);
