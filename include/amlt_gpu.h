@@ -50,7 +50,10 @@
 extern "C" {
 #endif
 
-#define AMLT_GPU_ABI_VERSION 1
+#define AMLT_GPU_ABI_VERSION 2
+
+/* Aux arrays one generated (AMLT_BODY_GENERIC) statement may name. */
+#define AMLT_MAX_AUX 8
 
 /* Error codes; the C++ shim (amlt_gpu.hpp) rethrows the matching
  * EngineError subclass (errors.hpp:10-60). */
@@ -72,14 +75,21 @@ typedef enum {
  *   BOOST     R += A*B + (A*B > T)*(A*B - T)            preset q2
  *   SQDIFF    R += (A - B)*(A - B)
  *   EQCOUNT   R += A == B
- *   THRCOUNT  R += A*B > T                              preset q3           */
+ *   THRCOUNT  R += A*B > T                              preset q3
+ * and GENERIC: any other recognised multiply-accumulate-like statement
+ * (recognize.cpp:84-166: one A[i][k]/A[k][i], one B[k][j]/B[j][k], aux
+ * leaves that are scalars, [i], [j] or [i][j]; + - * / and comparisons).
+ * Its body is generated from the statement and compiled at plan time
+ * (NVRTC) into the same tile kernels; such plans come only from
+ * amlt_gpu_plan_from_source.                                               */
 typedef enum {
     AMLT_BODY_GEMM = 0,
     AMLT_BODY_DISCOUNT = 1,
     AMLT_BODY_BOOST = 2,
     AMLT_BODY_SQDIFF = 3,
     AMLT_BODY_EQCOUNT = 4,
-    AMLT_BODY_THRCOUNT = 5
+    AMLT_BODY_THRCOUNT = 5,
+    AMLT_BODY_GENERIC = 6
 } amlt_body;
 
 typedef enum { AMLT_F64 = 0, AMLT_F32 = 1, AMLT_I32 = 2 } amlt_dtype;
@@ -122,13 +132,18 @@ typedef struct {
 } amlt_matrix;
 
 /* Operands (kernel_exec.hpp:17-24). `thres` and `dis` are the aux leaves the
- * body names; a body that needs one which is absent -> MISSING_BINDING. */
+ * fixed bodies name; a GENERIC plan binds its aux leaves by position in
+ * `aux`, in the order amlt_task_info.aux_names lists them (scalars as 1 x 1,
+ * [i] / [j] vectors as len x 1, [i][j] as M x N buffers). A body that needs
+ * an absent leaf -> MISSING_BINDING. */
 typedef struct {
     amlt_matrix a;
     amlt_matrix b;
     amlt_matrix r;
     amlt_matrix thres; /* data == NULL when unbound */
     amlt_matrix dis;   /* data == NULL when unbound */
+    int32_t n_aux;     /* GENERIC plans: bound entries of aux */
+    amlt_matrix aux[AMLT_MAX_AUX];
 } amlt_operands;
 
 /* Half-open index rectangle (tiled_executor.hpp:17-21). */
@@ -252,7 +267,8 @@ void amlt_gpu_clear_tuning_cache(amlt_ctx* ctx);
 
 /* The compile_task boundary (src/engine.cpp:86-102): which GPU body a task
  * text is, and which arrays play A, B, R, the threshold and the discount
- * vector. Names are "" for absent roles. */
+ * vector. Names are "" for absent roles. GENERIC statements list their aux
+ * leaves (first-use order) with their index classes. */
 typedef struct {
     amlt_body_desc desc; /* dtype left 0; the caller chooses it          */
     char a[64];
@@ -260,11 +276,15 @@ typedef struct {
     char r[64];
     char thres[64];
     char dis[64];
+    int32_t n_aux;
+    char aux_names[AMLT_MAX_AUX][64];
+    int32_t aux_class[AMLT_MAX_AUX]; /* amlt_leaf_class */
 } amlt_task_info;
 
 /* Parses and recognises a task in the reference DSL. UNSUPPORTED for a task
- * that is not one of the GPU bodies (the reference then runs it on its CPU
- * path); ENGINE for a parse error. Message: amlt_gpu_last_error(NULL). */
+ * that is not multiply-accumulate-like (the reference then runs it on its
+ * CPU interpreter); ENGINE for a parse error. Message:
+ * amlt_gpu_last_error(NULL). */
 amlt_status amlt_gpu_recognize(const char* task_source, amlt_task_info* info);
 
 amlt_status amlt_gpu_plan_create(amlt_ctx* ctx, const amlt_body_desc* desc, amlt_plan** out);
@@ -272,6 +292,12 @@ amlt_status amlt_gpu_plan_create(amlt_ctx* ctx, const amlt_body_desc* desc, amlt
  * (optional) receives the roles. */
 amlt_status amlt_gpu_plan_from_source(amlt_ctx* ctx, const char* task_source, int dtype,
                                       amlt_plan** out, amlt_task_info* info);
+/* The CUDA source amlt_gpu_plan_from_source compiles (NVRTC, sm_100a) for a
+ * GENERIC statement: the tile-kernel header plus the generated Body. Writes
+ * at most buflen bytes (NUL-terminated) and returns the full length, or -1
+ * (message in amlt_gpu_last_error(NULL)) for a fixed-body or unrecognised
+ * statement. */
+int64_t amlt_gpu_generated_source(const char* task_source, int dtype, char* buf, int64_t buflen);
 void amlt_gpu_plan_destroy(amlt_plan* plan);
 int amlt_gpu_plan_num_variants(const amlt_plan* plan);
 amlt_status amlt_gpu_plan_variant(const amlt_plan* plan, int idx, amlt_variant_info* info);

@@ -150,7 +150,19 @@ struct Matrix {
 
 struct Operands {
     Matrix a, b, r, thres, dis;
-    amlt_operands c() const { return amlt_operands{a.c(), b.c(), r.c(), thres.c(), dis.c()}; }
+    int n_aux = 0;              // generated bodies: aux leaves by position
+    Matrix aux[AMLT_MAX_AUX];   // (Plan::roles().aux_names)
+    amlt_operands c() const {
+        amlt_operands o{};
+        o.a = a.c();
+        o.b = b.c();
+        o.r = r.c();
+        o.thres = thres.c();
+        o.dis = dis.c();
+        o.n_aux = n_aux;
+        for (int q = 0; q < n_aux && q < AMLT_MAX_AUX; ++q) o.aux[q] = aux[q].c();
+        return o;
+    }
 };
 
 // ---------------------------------------------------------------------------

@@ -7,9 +7,11 @@
 // eqcount statements) and each dims triple (the acceptance suite's dims,
 // tests/acceptance.cpp:109-110, plus a larger one): compile_task,
 // make_task_data (the reference's own seeded generator), run on the GPU via
-// the adapter (run_adaptive and run_fixed), verify. A task the GPU has no
-// body for (`A[i][k]*B[k][j] + u[i]*v[j]`) must raise UnsupportedExpression so
-// the caller keeps the CPU path.
+// the adapter (run_adaptive and run_fixed), verify. Then random recognised
+// statements outside the six bodies (aux leaves u[i], v[j], W[i][j], s,
+// constants, + - * / and comparisons), which run through generated bodies.
+// A statement that is not multiply-accumulate-like (`... * u[k]`) must
+// raise UnsupportedExpression so the caller keeps the CPU path.
 //
 // Built by oracle/Makefile into oracle/_ref/ (it links the reference's
 // objects); run by tests/test_gpu_integration.py on the GPU box.
@@ -17,6 +19,9 @@
 //   adapter_demo --dry-run  plumbing only (no device; nothing verified)
 #include <cstdio>
 #include <cstring>
+#include <functional>
+#include <memory>
+#include <random>
 #include <string>
 #include <vector>
 
@@ -104,18 +109,70 @@ int main(int argc, char** argv) {
             }
         }
     }
-    // a recognised MMLT the GPU has no body for: the adapter must refuse it
+    // random recognised statements outside the six bodies: generated bodies
+    // (compiled at plan time) must agree with run_naive bit for bit on
+    // int-valued data, both orientations, row/col-major storage, "=" and "+="
+    {
+        std::mt19937_64 rng(20261020);
+        auto pick = [&](int n) { return static_cast<int>(rng() % static_cast<unsigned>(n)); };
+        const int n_stmt = dry ? 3 : 40;
+        for (int n = 0; n < n_stmt; ++n) {
+            const bool at = pick(3) == 0, bt = pick(3) == 0;
+            const std::string A = at ? "A[k][i]" : "A[i][k]", B = bt ? "B[j][k]" : "B[k][j]";
+            std::function<std::string(int)> expr = [&](int depth) -> std::string {
+                if (depth >= 3 || pick(3) == 0) {
+                    switch (pick(8)) {
+                        case 0: return A;
+                        case 1: return B;
+                        case 2: return "u[i]";
+                        case 3: return "v[j]";
+                        case 4: return "W[i][j]";
+                        case 5: return "s";
+                        default: return std::to_string(pick(7));
+                    }
+                }
+                const std::string l = expr(depth + 1);
+                if (pick(10) == 0) return "(" + l + ")/" + std::to_string(2 << pick(3));
+                static const char* ops[] = {" + ", " - ", "*", " > ", " >= ", " < ", " <= ", " == "};
+                return "(" + l + ")" + ops[pick(pick(4) == 0 ? 8 : 3)] + "(" + expr(depth + 1) + ")";
+            };
+            const std::string rhs = A + "*" + B + (pick(2) ? " + " : " - ") + "(" + expr(0) + ")";
+            const bool acc = pick(8) != 0;
+            const std::string src = "where(i in [0..M] and j in [0..N] and k in [0..K]) {\n  R[i][j] " +
+                                    std::string(acc ? "+=" : "=") + " " + rhs + ";\n}\n";
+            CompiledTask ct = compile_task(src, MachineModel{});
+            if (!ct.mmlt) continue;
+            const std::int64_t M = 5 + pick(70), K = 1 + pick(60), N = 5 + pick(90);
+            const StorageOrder oa = n % 2 ? StorageOrder::ColMajor : StorageOrder::RowMajor;
+            const StorageOrder ob = n % 3 ? StorageOrder::ColMajor : StorageOrder::RowMajor;
+            for (int fixed = 0; fixed < 2; ++fixed) {
+                DimBinding bind = bind_dims(ct, M, K, N);
+                TaskData data = make_task_data(ct, bind, 7 + n, oa, ob, DataMode::IntValued);
+                if (dry) {
+                    std::unique_ptr<amlt_gpu::Plan> plan(gpu::plan_for(gpu, ct));
+                    (void)gpu::operands(*plan, data);
+                    continue;
+                }
+                SteadyClock clock;
+                if (fixed)
+                    gpu::run_fixed(gpu, ct, data, bind, 32, 64, false, clock);
+                else
+                    gpu::run_adaptive(gpu, ct, data, bind, false, clock);
+                VerifyResult v = verify_against_naive(ct, data, bind, DataMode::IntValued);
+                ++checks;
+                if (!v.exact) {
+                    ++failures;
+                    std::printf("FAIL generated %s %lldx%lldx%lld: max_abs=%.3e\n%s", fixed ? "fixed" : "adaptive",
+                                (long long)M, (long long)K, (long long)N, v.max_abs_err, src.c_str());
+                }
+            }
+        }
+    }
+    // a statement that is not multiply-accumulate-like: the adapter must refuse it
     bool refused = false;
     try {
-        CompiledTask ct = compile_task(wrap_head + "A[i][k]*B[k][j] + u[i]*v[j];\n}\n", MachineModel{});
-        DimBinding bind = bind_dims(ct, 8, 8, 8);
-        TaskData data = make_task_data(ct, bind, 1, StorageOrder::RowMajor, StorageOrder::RowMajor,
-                                       DataMode::IntValued);
-        SteadyClock clock;
-        if (dry)
-            std::unique_ptr<amlt_gpu::Plan>(gpu::plan_for(gpu, ct));
-        else
-            gpu::run_adaptive(gpu, ct, data, bind, false, clock);
+        CompiledTask ct = compile_task(wrap_head + "A[i][k]*B[k][j]*u[k];\n}\n", MachineModel{});
+        std::unique_ptr<amlt_gpu::Plan>(gpu::plan_for(gpu, ct));
     } catch (const UnsupportedExpression&) {
         refused = true;
     } catch (const amlt_gpu::UnsupportedExpression&) {
@@ -123,7 +180,7 @@ int main(int argc, char** argv) {
     }
     if (!refused) {
         ++failures;
-        std::printf("FAIL a non-body MMLT was not refused\n");
+        std::printf("FAIL a non-MMLT statement was not refused\n");
     }
     std::printf("%s: %d checks, %d failures%s\n", failures ? "FAIL" : "PASS", checks, failures,
                 dry ? " (dry run: plumbing only)" : "");

@@ -13,8 +13,10 @@
 //
 // with the same arguments, the same Clock (the reference's FakeClock drives
 // the GPU executor's timing too), the same result in data.result(), and the
-// same errors (UnsupportedExpression for a task the GPU has no body for, so
-// the caller keeps its CPU path for it). Operands stay the reference's
+// same errors (UnsupportedExpression for a task that is not
+// multiply-accumulate-like, so the caller keeps its CPU path for it; every
+// recognised statement runs on the GPU, the six fixed bodies through their
+// hand-written kernels and the rest through bodies generated at plan time). Operands stay the reference's
 // f64 MatrixBuffers in host memory; the backend copies them in and R out.
 #pragma once
 
@@ -66,6 +68,9 @@ inline amlt_gpu::Operands operands(const amlt_gpu::Plan& plan, TaskData& data) {
     ops.r = view(data.result());
     if (r.thres[0]) ops.thres = view(need(r.thres));
     if (r.dis[0]) ops.dis = view(need(r.dis));
+    // generated bodies (any other recognised statement): aux leaves by position
+    ops.n_aux = r.n_aux;
+    for (int q = 0; q < r.n_aux; ++q) ops.aux[q] = view(need(r.aux_names[q]));
     return ops;
 }
 

@@ -12,14 +12,16 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "lib", "libamlt_gpu.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
+MAX_AUX = 8
 
 # amlt_status
 OK, ERR_ENGINE, ERR_UNSUPPORTED, ERR_MISSING_BINDING, ERR_NO_FEASIBLE_KERNEL, \
     ERR_NON_POSITIVE_TIME, ERR_INVALID_ARGUMENT, ERR_CUDA, ERR_NO_DEVICE = range(9)
 
 # amlt_body
-BODY_GEMM, BODY_DISCOUNT, BODY_BOOST, BODY_SQDIFF, BODY_EQCOUNT, BODY_THRCOUNT = range(6)
+BODY_GEMM, BODY_DISCOUNT, BODY_BOOST, BODY_SQDIFF, BODY_EQCOUNT, BODY_THRCOUNT, \
+    BODY_GENERIC = range(7)
 # amlt_dtype
 F64, F32, I32 = range(3)
 ROW_MAJOR, COL_MAJOR = 0, 1
@@ -42,7 +44,8 @@ class Matrix(C.Structure):
 
 
 class OperandsC(C.Structure):
-    _fields_ = [("a", Matrix), ("b", Matrix), ("r", Matrix), ("thres", Matrix), ("dis", Matrix)]
+    _fields_ = [("a", Matrix), ("b", Matrix), ("r", Matrix), ("thres", Matrix), ("dis", Matrix),
+                ("n_aux", C.c_int32), ("aux", Matrix * MAX_AUX)]
 
 
 class BoundsC(C.Structure):
@@ -113,7 +116,9 @@ class AmuletReportC(C.Structure):
 
 class TaskInfoC(C.Structure):
     _fields_ = [("desc", BodyDesc), ("a", C.c_char * 64), ("b", C.c_char * 64),
-                ("r", C.c_char * 64), ("thres", C.c_char * 64), ("dis", C.c_char * 64)]
+                ("r", C.c_char * 64), ("thres", C.c_char * 64), ("dis", C.c_char * 64),
+                ("n_aux", C.c_int32), ("aux_names", (C.c_char * 64) * MAX_AUX),
+                ("aux_class", C.c_int32 * MAX_AUX)]
 
 
 CLOCK_FN = C.CFUNCTYPE(C.c_double, C.c_void_p)
@@ -127,7 +132,7 @@ EXPORTS = [
     "amlt_gpu_recognize", "amlt_gpu_plan_from_source", "amlt_gpu_adaptive_execute_amulet",
     "amlt_gpu_run_sharded", "amlt_gpu_sharded_last_error", "amlt_matrix_file_info",
     "amlt_matrix_file_read", "amlt_matrix_file_write", "amlt_matrix_file_last_error",
-    "amlt_operand_seed", "amlt_gen_matrix", "amlt_gpu_run_naive",
+    "amlt_operand_seed", "amlt_gen_matrix", "amlt_gpu_run_naive", "amlt_gpu_generated_source",
 ]
 HOST_R_ZERO = 1
 
@@ -191,6 +196,8 @@ def lib():
     L.amlt_operand_seed.restype = C.c_uint64
     L.amlt_gen_matrix.argtypes = [C.c_uint64, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_void_p,
                                   C.c_int, C.c_int]
+    L.amlt_gpu_generated_source.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_int64]
+    L.amlt_gpu_generated_source.restype = C.c_int64
     L.amlt_gpu_recognize.argtypes = [C.c_char_p, C.POINTER(TaskInfoC)]
     L.amlt_gpu_plan_from_source.argtypes = [P, C.c_char_p, C.c_int, C.POINTER(P),
                                             C.POINTER(TaskInfoC)]

@@ -22,8 +22,9 @@ OBJ = os.path.join(PKG, "build", "obj")
 LIB = os.path.join(PKG, "lib", "libamlt_gpu.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+GEN = os.path.join(PKG, "build", "gen")
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
-              "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")]
+              "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I" + GEN]
 
 # (body template name, amlt_body id, C type, amlt_dtype id)
 PAIRS = [
@@ -59,14 +60,29 @@ def _jobs():
         defs = [f"-DAMLT_BODY={body}", f"-DAMLT_BODY_ID={bid}", f"-DAMLT_T={ctype}", f"-DAMLT_DT={dt}"]
         jobs.append((inst, out, defs))
     for src in ("dmma_gemm.cu", "register_all.cu", "amlt_gpu.cu", "peak.cu", "task.cpp",
-                "sharded.cu", "matrix_file.cpp", "naive.cu"):
+                "sharded.cu", "matrix_file.cpp", "naive.cu", "jit.cu"):
         obj = os.path.splitext(src)[0] + ".o"
         jobs.append((os.path.join(CSRC, src), os.path.join(OBJ, obj), []))
     return jobs
 
 
+def _embed_kernel_header() -> None:
+    """build/gen/mmlt_kernel_src.inc: the tile-kernel header as a C++ raw
+    string, compiled again at run time (NVRTC) around generated bodies."""
+    os.makedirs(GEN, exist_ok=True)
+    src = os.path.join(CSRC, "mmlt_kernel.cuh")
+    out = os.path.join(GEN, "mmlt_kernel_src.inc")
+    text = open(src).read()
+    assert ")AMLT_SRC" not in text
+    body = 'R"AMLT_SRC(' + text + ')AMLT_SRC"\n'
+    if not os.path.exists(out) or open(out).read() != body:
+        with open(out, "w") as f:
+            f.write(body)
+
+
 def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -> str:
     os.makedirs(OBJ, exist_ok=True)
+    _embed_kernel_header()
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     hdr_mtime = max(os.path.getmtime(h) for h in _headers())
     todo = []

@@ -152,6 +152,10 @@ class TaskData:
             self.thres = gen(tp.thres_name, tshape, io.ROW_MAJOR)
         if tp.dis_name:
             self.dis = gen(tp.dis_name, (N_, 1), io.ROW_MAJOR)
+        shapes = {N.LEAF_CONSTANT: (1, 1), N.LEAF_VEC_I: (M, 1), N.LEAF_VEC_J: (N_, 1),
+                  N.LEAF_MAT_IJ: (M, N_)}
+        self.aux = tuple(gen(nm, shapes[cls], io.ROW_MAJOR)
+                         for nm, cls in zip(tp.aux_names, tp.aux_classes))
         tdt = {"f64": torch.float64, "f32": torch.float32, "i32": torch.int32}[a.dtype]
         self.R = torch.zeros((M, N_), dtype=tdt, device=device)
 
@@ -164,7 +168,8 @@ class TaskData:
         return io.read_matrix_file(path, dtype, device)
 
     def operands(self, R=None) -> E.Operands:
-        return E.Operands(self.A, self.B, self.R if R is None else R, self.thres, self.dis)
+        return E.Operands(self.A, self.B, self.R if R is None else R, self.thres, self.dis,
+                          self.aux)
 
 
 def _verify(plan, data: TaskData, bounds: E.Bounds, dtype: str, mode: str) -> str:
@@ -213,6 +218,21 @@ def _setup(a):
     plan = ctx.plan_for(tp, a.dtype)
     data = TaskData(tp, M, K, N_, a, device)
     return tp, ctx, plan, data, E.Bounds(0, M, 0, N_, 0, K), (M, K, N_)
+
+
+def _generated_term(source: str, dtype: str) -> str:
+    """The generated body's term expression (amlt_gpu_generated_source)."""
+    import ctypes as C
+    dt = {"f64": N.F64, "f32": N.F32, "i32": N.I32}[dtype]
+    n = N.lib().amlt_gpu_generated_source(source.encode(), dt, None, 0)
+    if n < 0:
+        raise E.EngineError(N.lib().amlt_gpu_last_error(None).decode())
+    buf = C.create_string_buffer(int(n) + 1)
+    N.lib().amlt_gpu_generated_source(source.encode(), dt, buf, n + 1)
+    text = buf.value.decode()
+    body = text[text.index("T term("):]
+    body = body[body.index("return ") + 7:]
+    return body[:body.index(";")]
 
 
 def _block(tp: TaskPlan) -> Tuple[int, int, int]:
@@ -360,13 +380,22 @@ def cmd_explain(a) -> int:
     out.append(f"recognition: MMLT  A={tp.a_name} ({lay[tp.layout_a]})  "
                f"B={tp.b_name} ({lay[tp.layout_b]})  R={tp.result_name}  "
                f"aux={{{', '.join(aux)}}}  {'+=' if tp.accumulate else '='}")
-    out.append(f"body: {tp.body_name}")
-    tname = tp.thres_name or f"${tp.thres_value:g}"
-    prog = [s.format(t=tname, d=tp.dis_name or "dis") for s in _PROGRAMS[tp.body]]
-    out.append(f"\npseudo program ({len(prog)} instructions):")
-    out += ["  " + s for s in prog]
-    i_h, i_w, regs = _block(tp)
-    out.append(f"\nreference kernel shape: {i_h} x {i_w} ({regs} registers)")
+    if tp.body == N.BODY_GENERIC:
+        for nm, cls in zip(tp.aux_names, tp.aux_classes):
+            aux.append(f"{nm} {_CLASS[cls]}")
+        out[-1] = (f"recognition: MMLT  A={tp.a_name} ({lay[tp.layout_a]})  "
+                   f"B={tp.b_name} ({lay[tp.layout_b]})  R={tp.result_name}  "
+                   f"aux={{{', '.join(aux)}}}  {'+=' if tp.accumulate else '='}")
+        out.append("body: generated (NVRTC-compiled into the tile kernels at plan time)")
+        out.append(f"term: {_generated_term(tp.source, a.dtype)}")
+    else:
+        out.append(f"body: {tp.body_name}")
+        tname = tp.thres_name or f"${tp.thres_value:g}"
+        prog = [s.format(t=tname, d=tp.dis_name or "dis") for s in _PROGRAMS[tp.body]]
+        out.append(f"\npseudo program ({len(prog)} instructions):")
+        out += ["  " + s for s in prog]
+        i_h, i_w, regs = _block(tp)
+        out.append(f"\nreference kernel shape: {i_h} x {i_w} ({regs} registers)")
     ctx = E.Context(a.device, dry_run=True)
     plan = ctx.plan_for(tp, a.dtype)
     out.append(f"\nB200 variants ({a.dtype}):")

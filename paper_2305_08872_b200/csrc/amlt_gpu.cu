@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/amlt_gpu.h"
+#include "jit.h"
 #include "naive.h"
 #include "variants.h"
 
@@ -55,6 +56,7 @@ const char* body_name(int b) {
         case AMLT_BODY_SQDIFF: return "sqdiff";
         case AMLT_BODY_EQCOUNT: return "eqcount";
         case AMLT_BODY_THRCOUNT: return "thrcount";
+        case AMLT_BODY_GENERIC: return "generic";
     }
     return "?";
 }
@@ -64,12 +66,13 @@ int dtype_size(int d) { return d == AMLT_F64 ? 8 : 4; }
 // ---------------------------------------------------------------------------
 // registry of compiled variants (variants.h)
 
-const Registry& registry() {
+Registry& registry_storage() {
     static Registry reg;
     static std::once_flag once;
     std::call_once(once, [] { register_all(reg); });
     return reg;
 }
+const Registry& registry() { return registry_storage(); }
 
 const BodyAux* find_aux(int body, int dtype) {
     for (const auto& a : registry().aux)
@@ -78,6 +81,14 @@ const BodyAux* find_aux(int body, int dtype) {
 }
 
 }  // namespace
+
+namespace amltk {
+Registry& registry_mut() { return registry_storage(); }
+std::mutex& registry_mutex() {
+    static std::mutex m;
+    return m;
+}
+}  // namespace amltk
 
 // ---------------------------------------------------------------------------
 // context and plan
@@ -98,9 +109,10 @@ struct amlt_ctx {
     void* scratch = nullptr;  // scratch R for whole-task tuning trials
     size_t scratch_bytes = 0;
     // device staging for amlt_gpu_run_host
-    void* hbuf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-    size_t hbuf_bytes[5] = {0, 0, 0, 0, 0};
-    std::vector<int> occupancy;  // resident CTAs per SM, per registry variant
+    // slots: A, B, R, thres, dis, then the aux leaves of generated bodies
+    void* hbuf[5 + AMLT_MAX_AUX] = {};
+    size_t hbuf_bytes[5 + AMLT_MAX_AUX] = {};
+    mutable std::vector<int> occupancy;  // resident CTAs per SM, per registry variant (lazy for JIT)
     // tuning winners: (body, dtype, M, N, K) -> variant index
     struct Winner {
         int variant;
@@ -116,6 +128,9 @@ struct amlt_plan {
     std::vector<int> variants;  // registry indices usable for this body/dtype
     const BodyAux* aux = nullptr;
     const amlt_ctx* ctx = nullptr;
+    // AMLT_BODY_GENERIC: the generated body's aux leaves, bound by position
+    std::vector<std::string> aux_names;
+    std::vector<int> aux_class;
 };
 
 namespace {
@@ -271,6 +286,45 @@ Resolved resolve(const amlt_plan* plan, const amlt_operands* ops, const amlt_bou
         kp.d_sj = step;
     }
 
+    // generated bodies: aux leaf q bound to ops->aux[q] by its index class
+    for (int q = 0; q < AMLT_KP_MAX_AUX; ++q) {
+        kp.gaux[q] = nullptr;
+        kp.gaux_si[q] = 0;
+        kp.gaux_sj[q] = 0;
+    }
+    if (d.body == AMLT_BODY_GENERIC) {
+        const int nq = static_cast<int>(plan->aux_names.size());
+        for (int q = 0; q < nq; ++q) {
+            const std::string& nm = plan->aux_names[static_cast<size_t>(q)];
+            if (q >= ops->n_aux || !ops->aux[q].data)
+                fail(AMLT_ERR_MISSING_BINDING, "missing binding for '" + nm + "'");
+            const amlt_matrix& t = ops->aux[q];
+            check_matrix(t, d.dtype, nm.c_str());
+            const int cls = plan->aux_class[static_cast<size_t>(q)];
+            int64_t si = 0, sj = 0, off = 0;
+            if (cls == AMLT_LEAF_CONSTANT) {
+                if (t.rows * t.cols < 1) fail(AMLT_ERR_INVALID_ARGUMENT, nm + " is empty");
+            } else if (cls == AMLT_LEAF_VEC_I) {
+                if (t.rows * t.cols < b->i1) fail(AMLT_ERR_INVALID_ARGUMENT, nm + " shorter than i1");
+                si = vec_step(t);
+                off = b->i0 * si;
+            } else if (cls == AMLT_LEAF_VEC_J) {
+                if (t.rows * t.cols < b->j1) fail(AMLT_ERR_INVALID_ARGUMENT, nm + " shorter than j1");
+                sj = vec_step(t);
+                off = b->j0 * sj;
+            } else {
+                if (t.rows < b->i1 || t.cols < b->j1)
+                    fail(AMLT_ERR_INVALID_ARGUMENT, nm + "[i][j] smaller than the bounds");
+                si = t.order == AMLT_ROW_MAJOR ? t.ld : 1;
+                sj = t.order == AMLT_ROW_MAJOR ? 1 : t.ld;
+                off = b->i0 * si + b->j0 * sj;
+            }
+            kp.gaux[q] = static_cast<const char*>(t.data) + off * tes;
+            kp.gaux_si[q] = si;
+            kp.gaux_sj[q] = sj;
+        }
+    }
+
     const int es = dtype_size(d.dtype);
     const int vn = 16 / es;
     auto al16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
@@ -286,6 +340,28 @@ Resolved resolve(const amlt_plan* plan, const amlt_operands* ops, const amlt_bou
 // variant choice
 
 const VariantDesc& vdesc(int idx) { return registry().variants.at(static_cast<size_t>(idx)); }
+
+// Resident CTAs per SM of a registry variant on this context; computed on
+// first use for variants added after the context was created (run-time
+// compiled bodies).
+int occ_of(const amlt_ctx* ctx, int idx) {
+    const VariantDesc& v = vdesc(idx);
+    if (!ctx) return v.minb;
+    if (idx < static_cast<int>(ctx->occupancy.size()) && ctx->occupancy[static_cast<size_t>(idx)] > 0)
+        return ctx->occupancy[static_cast<size_t>(idx)];
+    int occ = v.minb;
+    if (!ctx->dry() && v.func) {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, v.func, v.threads, v.smem) == cudaSuccess &&
+            o > 0)
+            occ = o;
+        else
+            (void)cudaGetLastError();
+    }
+    if (static_cast<int>(ctx->occupancy.size()) <= idx) ctx->occupancy.resize(static_cast<size_t>(idx) + 1, 0);
+    ctx->occupancy[static_cast<size_t>(idx)] = occ;
+    return occ;
+}
 
 int64_t ctas_for(const VariantDesc& v, int64_t M, int64_t N) {
     return ((M + v.bm - 1) / v.bm) * ((N + v.bn - 1) / v.bn);
@@ -303,7 +379,7 @@ int default_variant(const amlt_ctx* ctx, const amlt_plan* plan, int64_t M, int64
         const VariantDesc& v = vdesc(idx);
         if (v.vec != aligned) continue;
         if (v.tc) continue;
-        const int occ = ctx && !ctx->occupancy.empty() ? std::max(1, ctx->occupancy[idx]) : v.minb;
+        const int occ = occ_of(ctx, idx);
         const int sms = ctx ? ctx->num_sms : 148;
         const double waves = double(ctas_for(v, M, N)) / double(sms * occ);
         const double area = double(v.bm) * v.bn;
@@ -480,7 +556,9 @@ void enqueue_compute(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const D
         // "=": only the last k term reaches R.
         const int64_t total = rv.M * rv.N;
         const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 32));
-        cuda_check(plan->aux->assign(kp, dim3(blocks), ctx->stream), "assign kernel launch");
+        cuda_check(launch_helper_any(plan->aux->assign, plan->aux->assign_func, kp, dim3(blocks),
+                                     ctx->stream),
+                   "assign kernel launch");
         return;
     }
     const VariantDesc& v = vdesc(dp.variant);
@@ -508,14 +586,16 @@ void enqueue_compute(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const D
         make_tensor_map(&mb, plan->desc.dtype, kp.B, uint64_t(rv.N), uint64_t(rv.K),
                         uint64_t(kp.ldb) * es, v.bn, v.bk);
     }
-    cuda_check(v.launch(kp, ma, mb,
-                        dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(dp.splits)),
-                        ctx->stream),
+    cuda_check(launch_tile_any(v, kp, ma, mb,
+                               dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(dp.splits)),
+                               ctx->stream),
                "tile kernel launch");
     if (dp.splits > 1) {
         const int64_t total = rv.M * rv.N;
         const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-        cuda_check(plan->aux->reduce(kp, dim3(blocks), ctx->stream), "split-K reduce launch");
+        cuda_check(launch_helper_any(plan->aux->reduce, plan->aux->reduce_func, kp, dim3(blocks),
+                                     ctx->stream),
+                   "split-K reduce launch");
     }
 }
 
@@ -602,7 +682,7 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
     for (int v : cands) {
         trials.push_back({v, 0});
         const VariantDesc& vd = vdesc(v);
-        const int occ = ctx->occupancy.empty() ? vd.minb : std::max(1, ctx->occupancy[v]);
+        const int occ = occ_of(ctx, v);
         const int64_t ctas = ctas_for(vd, whole.M, whole.N);
         const int64_t slots = int64_t(ctx->num_sms) * occ;
         if (ctas < 2 * slots && whole.K >= 512) {  // split-K forms for small outputs
@@ -670,7 +750,7 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
         need = 0;
         for (size_t c = 0; c < cands.size(); ++c) {
             const VariantDesc& v = vdesc(cands[c]);
-            const int occ = ctx->occupancy.empty() ? v.minb : std::max(1, ctx->occupancy[cands[c]]);
+            const int occ = occ_of(ctx, cands[c]);
             const int64_t tiles_n = (whole.N + v.bn - 1) / v.bn;
             const int64_t want_ctas = int64_t(waves) * ctx->num_sms * occ;
             const int64_t tiles_m = std::max<int64_t>(1, (want_ctas + tiles_n - 1) / tiles_n);
@@ -722,7 +802,7 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
             // Output too small to fill the GPU: split K so every SM has work
             // (per-segment partials are reduced in order: deterministic).
             const VariantDesc& vd = vdesc(v);
-            const int occ = ctx->occupancy.empty() ? vd.minb : std::max(1, ctx->occupancy[v]);
+            const int occ = occ_of(ctx, v);
             const int64_t ctas = ctas_for(vd, whole.M, whole.N);
             const int64_t slots = int64_t(ctx->num_sms) * occ;
             if (ctas > 0 && ctas < slots && whole.K >= 512) {
@@ -959,6 +1039,10 @@ amlt_status amlt_gpu_ctx_create(int device, int flags, amlt_ctx** out) {
         ctx->occupancy.assign(reg.variants.size(), 1);
         for (size_t i = 0; i < reg.variants.size(); ++i) {
             const VariantDesc& v = reg.variants[i];
+            if (!v.launch) {  // run-time compiled: loaded and sized on demand
+                ctx->occupancy[i] = 0;
+                continue;
+            }
             cuda_check(cudaFuncSetAttribute(v.func, cudaFuncAttributeMaxDynamicSharedMemorySize, v.smem),
                        "cudaFuncSetAttribute");
             int occ = 0;
@@ -968,6 +1052,7 @@ amlt_status amlt_gpu_ctx_create(int device, int flags, amlt_ctx** out) {
             ctx->occupancy[i] = occ;
         }
         for (const auto& a : reg.aux) {
+            if (!a.assign) continue;  // run-time compiled body
             cudaFuncAttributes fa;
             cuda_check(cudaFuncGetAttributes(&fa, a.assign_func), "cudaFuncGetAttributes");
             cuda_check(cudaFuncGetAttributes(&fa, a.reduce_func), "cudaFuncGetAttributes");
@@ -1019,6 +1104,9 @@ amlt_status amlt_gpu_plan_create(amlt_ctx* ctx, const amlt_body_desc* desc, amlt
     amlt_plan* plan = new amlt_plan();
     amlt_status st = guarded(ctx, [&] {
         const amlt_body_desc& d = *desc;
+        if (d.body == AMLT_BODY_GENERIC)
+            fail(AMLT_ERR_UNSUPPORTED,
+                 "generated bodies are planned from the task text (amlt_gpu_plan_from_source)");
         if (d.body < AMLT_BODY_GEMM || d.body > AMLT_BODY_THRCOUNT)
             fail(AMLT_ERR_UNSUPPORTED, "unknown body " + std::to_string(d.body));
         if (d.dtype < AMLT_F64 || d.dtype > AMLT_I32)
@@ -1069,6 +1157,11 @@ amlt_status amlt_gpu_recognize(const char* task_source, amlt_task_info* info) {
         put(info->r, rt.r);
         put(info->thres, rt.thres);
         put(info->dis, rt.dis);
+        info->n_aux = static_cast<int32_t>(rt.aux_names.size());
+        for (size_t q = 0; q < rt.aux_names.size(); ++q) {
+            put(info->aux_names[q], rt.aux_names[q]);
+            info->aux_class[q] = rt.aux_class[q];
+        }
         g_create_error.clear();
         return AMLT_OK;
     } catch (const amltk::TaskError& e) {
@@ -1091,7 +1184,49 @@ amlt_status amlt_gpu_plan_from_source(amlt_ctx* ctx, const char* task_source, in
         return st;
     }
     ti->desc.dtype = dtype;
-    return amlt_gpu_plan_create(ctx, &ti->desc, out);
+    if (ti->desc.body != AMLT_BODY_GENERIC) return amlt_gpu_plan_create(ctx, &ti->desc, out);
+    *out = nullptr;
+    amlt_plan* plan = new amlt_plan();
+    st = guarded(ctx, [&] {
+        if (dtype != AMLT_F64 && dtype != AMLT_F32)
+            fail(AMLT_ERR_UNSUPPORTED, "generated bodies compute in f64 or f32");
+        amltk::RecognizedTask rt;
+        try {
+            rt = amltk::recognize_task(task_source);
+            const amltk::JitBody& jb = amltk::jit_body(rt, dtype, !ctx->dry());
+            plan->variants = jb.variants;
+            plan->aux = jb.aux;
+        } catch (const amltk::TaskError& e) {
+            fail(e.code, e.what());
+        }
+        plan->desc = ti->desc;
+        plan->ctx = ctx;
+        plan->aux_names = rt.aux_names;
+        plan->aux_class = rt.aux_class;
+    });
+    if (st != AMLT_OK) {
+        delete plan;
+        return st;
+    }
+    *out = plan;
+    return AMLT_OK;
+}
+
+int64_t amlt_gpu_generated_source(const char* task_source, int dtype, char* buf, int64_t buflen) {
+    if (!task_source) return -1;
+    try {
+        amltk::RecognizedTask rt = amltk::recognize_task(task_source);
+        if (rt.desc.body != AMLT_BODY_GENERIC) {
+            g_create_error = "statement has a fixed body; no generated source";
+            return -1;
+        }
+        const std::string src = amltk::jit_source(rt, dtype);
+        if (buf && buflen > 0) std::snprintf(buf, static_cast<size_t>(buflen), "%s", src.c_str());
+        return static_cast<int64_t>(src.size());
+    } catch (const std::exception& e) {
+        g_create_error = e.what();
+        return -1;
+    }
 }
 
 void amlt_gpu_plan_destroy(amlt_plan* plan) { delete plan; }
@@ -1177,7 +1312,23 @@ amlt_status amlt_gpu_run_naive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_
             cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
             const double t0 = clock ? clock(clock_user) : 0.0;
             if (!clock) cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
-            cuda_check(launch_naive(np, d.body, d.dtype, ctx->num_sms, ctx->stream), "naive kernel");
+            if (d.body == AMLT_BODY_GENERIC) {
+                KParams kp = rv.kp;
+                kp.A = np.A;
+                kp.B = np.B;
+                kp.R = np.R;
+                NaiveStrides ns{np.sai, np.sak, np.sbk, np.sbj, np.sri, np.srj, d.accumulate};
+                const int64_t total = rv.M * rv.N;
+                if (total > 0) {
+                    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, int64_t(ctx->num_sms) * 16));
+                    void* args[2] = {&kp, &ns};
+                    cuda_check(cudaLaunchKernel(plan->aux->naive_func, dim3(blocks), dim3(256), args, 0,
+                                                ctx->stream),
+                               "naive kernel");
+                }
+            } else {
+                cuda_check(launch_naive(np, d.body, d.dtype, ctx->num_sms, ctx->stream), "naive kernel");
+            }
             if (clock) {
                 cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
                 el = clock(clock_user) - t0;
@@ -1243,11 +1394,16 @@ amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_o
         // validate against the host description first (same rules)
         Resolved hv = resolve(plan, host_ops, bounds);
         amlt_operands dev = *host_ops;
-        const amlt_matrix* src[5] = {&host_ops->a, &host_ops->b, &host_ops->r, &host_ops->thres,
-                                     &host_ops->dis};
-        amlt_matrix* dst[5] = {&dev.a, &dev.b, &dev.r, &dev.thres, &dev.dis};
-        size_t bytes[5];
-        for (int s = 0; s < 5; ++s) {
+        const int nslot = 5 + std::max(0, std::min<int>(host_ops->n_aux, AMLT_MAX_AUX));
+        const amlt_matrix* src[5 + AMLT_MAX_AUX] = {&host_ops->a, &host_ops->b, &host_ops->r,
+                                                    &host_ops->thres, &host_ops->dis};
+        amlt_matrix* dst[5 + AMLT_MAX_AUX] = {&dev.a, &dev.b, &dev.r, &dev.thres, &dev.dis};
+        for (int q = 0; q + 5 < nslot; ++q) {
+            src[5 + q] = &host_ops->aux[q];
+            dst[5 + q] = &dev.aux[q];
+        }
+        size_t bytes[5 + AMLT_MAX_AUX] = {};
+        for (int s = 0; s < nslot; ++s) {
             const amlt_matrix& m = *src[s];
             bytes[s] = 0;
             if (!m.data) continue;
@@ -1299,8 +1455,8 @@ amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_o
             cudaEvent_t start_ev = ctx->pipe_ev[1];
             cuda_check(cudaEventRecord(start_ev, ctx->stream), "cudaEventRecord");
             cuda_check(cudaStreamWaitEvent(ctx->copy_in, start_ev, 0), "cudaStreamWaitEvent");
-            for (int s : {1, 3, 4})
-                if (bytes[s])
+            for (int s = 1; s < nslot; ++s)
+                if (s != 2 && bytes[s])
                     cuda_check(cudaMemcpyAsync(ctx->hbuf[s], src[s]->data, bytes[s],
                                                cudaMemcpyHostToDevice, ctx->copy_in),
                                "cudaMemcpyAsync H2D");

@@ -25,11 +25,26 @@
 //    reduced in segment order by mmlt_splitk_reduce: deterministic.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#else
+// Compiled at run time by NVRTC for generated bodies (csrc/jit.cu): no host
+// headers, so the few types the kernels use are declared here.
+typedef long long int64_t;
+typedef unsigned long long uint64_t;
+typedef int int32_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uintptr_t;
+struct alignas(64) CUtensorMap_st {
+    unsigned long long opaque[16];
+};
+typedef CUtensorMap_st CUtensorMap;
+#endif
 
-#include <type_traits>
+// Aux leaves of a generated (generic) body: at most this many arrays.
+#define AMLT_KP_MAX_AUX 8
 
 namespace amltk {
 
@@ -53,6 +68,11 @@ struct KParams {
     int32_t group_m;   // row tiles per raster group (L2 reuse of B panels)
     int32_t r_vec_ok;  // R base 16B aligned and ldr a multiple of the vector width
     double tconst;     // threshold when thres == nullptr
+    // Generated bodies (AMLT_BODY_GENERIC): aux leaf q of output (i, j) is
+    // gaux[q][i * gaux_si[q] + j * gaux_sj[q]], offset to (i0, j0).
+    const void* gaux[AMLT_KP_MAX_AUX];
+    int64_t gaux_si[AMLT_KP_MAX_AUX];
+    int64_t gaux_sj[AMLT_KP_MAX_AUX];
 };
 
 // --------------------------------------------------------------------------
@@ -107,6 +127,10 @@ __device__ __forceinline__ double fma_rn(double a, double b, double c) { return 
 __device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
 
 template <typename T>
 __device__ __forceinline__ T ldg_elem(const void* base, int64_t idx) {
@@ -317,12 +341,25 @@ struct UsesThreshold<Body, decltype(void(Body::USES_T))> {
     static constexpr bool value = Body::USES_T;
 };
 
+// Generated bodies with aux leaves indexed by i or (i, j) complete their
+// column state per output element (Body::at).
+template <class Body, class = void>
+struct HasAt {
+    static constexpr bool value = false;
+};
+template <class Body>
+struct HasAt<Body, decltype(void(Body::HAS_AT))> {
+    static constexpr bool value = Body::HAS_AT;
+};
+
 // Column state with the threshold of output (i, j) when T is indexed by i or
 // by (i, j): T(i, j) = thres[i * t_si + j * t_sj] (TCLS == 1 kernels).
 template <class Body, typename T>
 __device__ __forceinline__ typename Body::Col col_at(const typename Body::Col& c, const KParams& p,
                                                      int64_t i, int64_t j) {
-    if constexpr (UsesThreshold<Body>::value)
+    if constexpr (HasAt<Body>::value)
+        return Body::at(c, p, i, j);
+    else if constexpr (UsesThreshold<Body>::value)
         return Body::with_t(c, ldg_elem<T>(p.thres, i * p.t_si + j * p.t_sj));
     else
         return c;
@@ -707,10 +744,39 @@ __global__ void mmlt_assign_kernel(const KParams p) {
         typename Body::Acc acc[Body::NACC];
 #pragma unroll
         for (int n = 0; n < Body::NACC; ++n) acc[n] = typename Body::Acc(0);
-        const typename Body::Col c =
-            p.t_si ? col_at<Body, T>(Body::col(p, j), p, i, j) : Body::col(p, j);
+        const typename Body::Col c = (p.t_si || HasAt<Body>::value)
+                                         ? col_at<Body, T>(Body::col(p, j), p, i, j)
+                                         : Body::col(p, j);
         Body::step(acc, A[i * p.lda + k], B[k * p.ldb + j], c);
         R[i * p.ldr + j] = Body::finish(acc, c, 1);
+    }
+}
+
+// Per-element executor for generated bodies (the naive run mode; the fixed
+// bodies have theirs in naive.cu): one thread per R element, k ascending,
+// `R += term` per k (or `R = term`), operands addressed through full strides.
+struct NaiveStrides {
+    int64_t sai, sak, sbk, sbj, sri, srj;
+    int32_t accumulate;
+};
+template <class Body, typename T>
+__global__ void mmlt_naive_body_kernel(const KParams p, const NaiveStrides s) {
+    const int64_t total = p.M * p.N;
+    const T* A = static_cast<const T*>(p.A);
+    const T* B = static_cast<const T*>(p.B);
+    T* R = static_cast<T*>(p.R);
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / p.N;
+        const int64_t j = idx - i * p.N;
+        const typename Body::Col c = col_at<Body, T>(Body::col(p, j), p, i, j);
+        T* r = R + i * s.sri + j * s.srj;
+        T acc = s.accumulate ? *r : T(0);
+        for (int64_t k = 0; k < p.K; ++k) {
+            const T v = Body::term(A[i * s.sai + k * s.sak], B[k * s.sbk + j * s.sbj], c);
+            acc = s.accumulate ? add_rn(acc, v) : v;
+        }
+        if (p.K > 0 || s.accumulate) *r = acc;
     }
 }
 

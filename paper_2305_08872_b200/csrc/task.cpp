@@ -11,6 +11,7 @@
 // operand swaps at commutative nodes (a swap never changes an IEEE result).
 // Python twin: paper_2305_08872_b200/task.py (same rules, tested together).
 #include <cctype>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -357,8 +358,61 @@ RecognizedTask recognize_task(const std::string& source) {
         if (d != env.end()) rt.dis = d->second->name;
         return rt;
     }
-    throw unsup("statement is an MMLT but not one of the GPU bodies "
-                "(gemm, discount, boost, sqdiff, eqcount, thrcount)");
+    // Any other recognised statement: a generated body (csrc/jit.cu compiles
+    // it into the same tile kernels at plan time).
+    rt.desc.body = AMLT_BODY_GENERIC;
+    rt.desc.accumulate = op == "+=" ? 1 : 0;
+    rt.desc.thres_class = AMLT_LEAF_CONSTANT;
+    rt.desc.thres_value = 0.0;
+    std::function<std::string(const P&)> gen = [&](const P& n) -> std::string {
+        switch (n->kind) {
+            case Node::Num: {
+                char buf[64];
+                std::snprintf(buf, sizeof(buf), "T(%a)", n->num);
+                return buf;
+            }
+            case Node::Role:
+                return n->cls == "A" ? "a" : "b";
+            case Node::Aux: {
+                size_t q = 0;
+                while (q < rt.aux_names.size() && rt.aux_names[q] != n->name) ++q;
+                if (q == rt.aux_names.size()) {
+                    if (q >= AMLT_MAX_AUX)
+                        throw unsup("more than " + std::to_string(AMLT_MAX_AUX) +
+                                    " auxiliary arrays in one statement");
+                    rt.aux_names.push_back(n->name);
+                    rt.aux_class.push_back(n->cls == "c"   ? AMLT_LEAF_CONSTANT
+                                           : n->cls == "i" ? AMLT_LEAF_VEC_I
+                                           : n->cls == "j" ? AMLT_LEAF_VEC_J
+                                                           : AMLT_LEAF_MAT_IJ);
+                }
+                return "c.v[" + std::to_string(q) + "]";
+            }
+            case Node::Bin: {
+                const std::string l = gen(n->l), r = gen(n->r);
+                if (n->op == "+") return "add_rn(" + l + ", " + r + ")";
+                if (n->op == "-") return "sub_rn(" + l + ", " + r + ")";
+                if (n->op == "*") return "mul_rn(" + l + ", " + r + ")";
+                if (n->op == "/") {
+                    // x / 2^e == x * 2^-e exactly (both are the correctly
+                    // rounded x * 2^-e): a multiply instead of a division
+                    int e2 = 0;
+                    if (n->r->kind == Node::Num && n->r->num > 0 &&
+                        std::frexp(n->r->num, &e2) == 0.5 && e2 - 1 < 120 && e2 - 1 > -120) {
+                        char buf[64];
+                        std::snprintf(buf, sizeof(buf), "T(%a)", std::ldexp(1.0, -(e2 - 1)));
+                        return "mul_rn(" + l + ", " + buf + ")";
+                    }
+                    return "div_rn(" + l + ", " + r + ")";
+                }
+                return "((" + l + ") " + n->op + " (" + r + ") ? T(1) : T(0))";
+            }
+            default:
+                throw unsup("unexpected node in the statement");
+        }
+    };
+    rt.expr = gen(tree);
+    return rt;
 }
 
 }  // namespace amltk

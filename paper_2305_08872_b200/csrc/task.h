@@ -3,6 +3,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "../../include/amlt_gpu.h"
 
@@ -16,6 +17,12 @@ struct TaskError : std::runtime_error {
 struct RecognizedTask {
     amlt_body_desc desc{};
     std::string a, b, r, thres, dis;  // array names per role ("" when absent)
+    // AMLT_BODY_GENERIC: the statement term as a CUDA expression over
+    // `a`, `b` and the aux leaves `c.v[q]` (one IEEE operation per syntax
+    // tree node, in the tree's order), and the aux leaves in first-use order.
+    std::string expr;
+    std::vector<std::string> aux_names;
+    std::vector<int> aux_class;  // amlt_leaf_class
 };
 
 // Parse + recognise; throws TaskError (UNSUPPORTED / ENGINE).

@@ -9,6 +9,8 @@
 
 #include <cuda_runtime.h>
 
+#include <deque>
+#include <mutex>
 #include <vector>
 
 #include "mmlt_kernel.cuh"
@@ -39,6 +41,9 @@ struct VariantDesc {
 struct BodyAux {
     int body = 0;
     int dtype = 0;
+    // Generated bodies: launched through the kernel handles below
+    // (assign == nullptr); naive_func is their per-element executor.
+    const void* naive_func = nullptr;
     LaunchFn assign = nullptr;  // "=" statements: last k wins
     LaunchFn reduce = nullptr;  // split-K ordered reduction into R
     cudaError_t (*pack)(const PackParams&, cudaStream_t) = nullptr;  // layout packing
@@ -47,10 +52,34 @@ struct BodyAux {
     const void* reduce_func = nullptr;
 };
 
+// Append-only (run-time compiled bodies add entries): deques keep the
+// addresses of existing entries stable.
 struct Registry {
-    std::vector<VariantDesc> variants;
-    std::vector<BodyAux> aux;
+    std::deque<VariantDesc> variants;
+    std::deque<BodyAux> aux;
 };
+
+// The process-wide registry (amlt_gpu.cu); appends take registry_mutex().
+Registry& registry_mut();
+std::mutex& registry_mutex();
+
+// Launch a tile variant / helper kernel whether it is a compiled-in template
+// (launch function) or a run-time compiled kernel handle (func only).
+inline cudaError_t launch_tile_any(const VariantDesc& v, const KParams& p, const CUtensorMap& a,
+                                   const CUtensorMap& b, dim3 grid, cudaStream_t s) {
+    if (v.launch) return v.launch(p, a, b, grid, s);
+    if (!v.func) return cudaErrorInvalidDeviceFunction;
+    void* args[3] = {const_cast<KParams*>(&p), const_cast<CUtensorMap*>(&a),
+                     const_cast<CUtensorMap*>(&b)};
+    return cudaLaunchKernel(v.func, grid, dim3(v.threads), args, static_cast<size_t>(v.smem), s);
+}
+inline cudaError_t launch_helper_any(LaunchFn fn, const void* func, const KParams& p, dim3 grid,
+                                     cudaStream_t s) {
+    if (fn) return fn(p, grid, s);
+    if (!func) return cudaErrorInvalidDeviceFunction;
+    void* args[1] = {const_cast<KParams*>(&p)};
+    return cudaLaunchKernel(func, grid, dim3(256), args, 0, s);
+}
 
 // Defined once per (body, dtype) translation unit (kernels_inst.cu) and by
 // the DMMA GEMM unit; collected by registry() in amlt_gpu.cu.

@@ -307,11 +307,15 @@ class Operands:
     r: object
     thres: object = None
     dis: object = None
+    aux: tuple = ()  # generated bodies: aux leaves by position (TaskPlan.aux_names)
 
     def _c(self, device: Optional[bool]):
+        if len(self.aux) > N.MAX_AUX:
+            raise UnsupportedExpression(f"at most {N.MAX_AUX} aux operands")
+        aux = (N.Matrix * N.MAX_AUX)(*[matrix_of(x, device) for x in self.aux])
         return N.OperandsC(matrix_of(self.a, device), matrix_of(self.b, device),
                            matrix_of(self.r, device), matrix_of(self.thres, device),
-                           matrix_of(self.dis, device))
+                           matrix_of(self.dis, device), len(self.aux), aux)
 
 
 # ---------------------------------------------------------------------------
@@ -362,8 +366,16 @@ class Context:
                        thres_value)
 
     def plan_for(self, task: TaskPlan, dtype="f64") -> "GpuPlan":
+        if task.body == N.BODY_GENERIC:
+            return GpuPlan.from_source(self, task.source, dtype)
         return GpuPlan(self, task.body, dtype, task.accumulate, task.layout_a, task.layout_b,
                        task.thres_class, task.thres_value)
+
+    def plan_source(self, source: str, dtype="f64") -> "GpuPlan":
+        """amlt_gpu_plan_from_source: recognise + plan a task text; statements
+        that are not one of the fixed bodies get a generated body (compiled at
+        plan time, cached per statement)."""
+        return GpuPlan.from_source(self, source, dtype)
 
 
 BODIES = {"gemm": N.BODY_GEMM, "matmul": N.BODY_GEMM, "discount": N.BODY_DISCOUNT,
@@ -390,6 +402,23 @@ class GpuPlan:
         _raise(ctx._lib.amlt_gpu_plan_create(ctx.handle, C.byref(self.desc), C.byref(h)),
                ctx.handle)
         self.handle = h
+
+    @classmethod
+    def from_source(cls, ctx: Context, source: str, dtype="f64") -> "GpuPlan":
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self.dtype = DTYPES[dtype] if isinstance(dtype, str) else int(dtype)
+        info = N.TaskInfoC()
+        h = C.c_void_p()
+        self.handle = None
+        _raise(ctx._lib.amlt_gpu_plan_from_source(ctx.handle, source.encode(), self.dtype,
+                                                  C.byref(h), C.byref(info)), ctx.handle)
+        self.handle = h
+        self.desc = info.desc
+        self.body = info.desc.body
+        self.aux_names = tuple(info.aux_names[q].value.decode() for q in range(info.n_aux))
+        self.aux_classes = tuple(int(info.aux_class[q]) for q in range(info.n_aux))
+        return self
 
     def __del__(self):
         try:
@@ -666,4 +695,5 @@ def operands_of(task: TaskPlan, data: Dict[str, object]) -> Operands:
         return data[name]
     thres = need(task.thres_name) if task.thres_name else None
     dis = need(task.dis_name) if task.dis_name else None
-    return Operands(need(task.a_name), need(task.b_name), need(task.result_name), thres, dis)
+    aux = tuple(need(n) for n in task.aux_names)
+    return Operands(need(task.a_name), need(task.b_name), need(task.result_name), thres, dis, aux)

@@ -179,6 +179,11 @@ class TaskPlan:
     var_j: str
     var_k: str
     dims: Tuple[str, str, str]  # range-end identifiers bound to (M, K, N)
+    # generic statements (BODY_GENERIC): aux leaves in first-use order, their
+    # index classes (N.LEAF_*), the source the native planner compiles
+    aux_names: Tuple[str, ...] = ()
+    aux_classes: Tuple[int, ...] = ()
+    source: str = ""
 
 
 _TEMPLATES = [
@@ -314,8 +319,22 @@ def compile_task(source: str) -> TaskPlan:
                 result_name=target, thres_name=tname, dis_name=d[1] if d else None,
                 var_i=vi, var_j=vj, var_k=vk,
                 dims=(str(ends[vi]), str(ends[vk]), str(ends[vj])))
-    raise UnsupportedExpression("statement is an MMLT but not one of the GPU bodies "
-                                "(gemm, discount, boost, sqdiff, eqcount, thrcount)")
+    # Any other recognised statement: a generated body, compiled by the native
+    # planner at plan time (csrc/jit.cu); the aux leaf order comes from it.
+    import ctypes as C
+    info = N.TaskInfoC()
+    st = N.lib().amlt_gpu_recognize(source.encode(), C.byref(info))
+    if st != N.OK:
+        msg = N.lib().amlt_gpu_last_error(None)
+        raise UnsupportedExpression(msg.decode() if msg else "statement not recognised")
+    names = tuple(info.aux_names[q].value.decode() for q in range(info.n_aux))
+    return TaskPlan(
+        body=N.BODY_GENERIC, body_name="generic", accumulate=accumulate,
+        layout_a=roles[a_names[0]][1], layout_b=roles[b_names[0]][1],
+        thres_class=N.LEAF_CONSTANT, thres_value=0.0, a_name=a_names[0], b_name=b_names[0],
+        result_name=target, thres_name=None, dis_name=None, var_i=vi, var_j=vj, var_k=vk,
+        dims=(str(ends[vi]), str(ends[vk]), str(ends[vj])), aux_names=names,
+        aux_classes=tuple(int(info.aux_class[q]) for q in range(info.n_aux)), source=source)
 
 
 # ---------------------------------------------------------------------------

@@ -72,7 +72,7 @@ int main() {
         missing = true;
     }
     try {
-        Plan p2(ctx, "where(i in [0..M] and j in [0..N] and k in [0..K]) {\n  R[i][j] += A[i][k]*B[k][j] + u[i]*v[j];\n}\n",
+        Plan p2(ctx, "where(i in [0..M] and j in [0..N] and k in [0..K]) {\n  R[i][j] += A[i][k]*B[k][j]*u[k];\n}\n",
                 AMLT_F64);
     } catch (const UnsupportedExpression&) {
         unsupported = true;

@@ -15,7 +15,7 @@ from paper_2305_08872_b200 import cli
 from paper_2305_08872_b200 import matrix_io as io
 
 NOT_MMLT = ("where(i in [0..M] and j in [0..N] and k in [0..K]) {\n"
-            "  R[i][j] += A[i][k]*B[k][j] + A[i][k];\n}\n")
+            "  R[i][j] += A[i][k]*B[k][j]*u[k];\n}\n")  # a k-indexed aux: not an MMLT
 
 
 def run_cli(capsys, line: str):

@@ -215,9 +215,12 @@ def test_errors_map_to_reference_hierarchy(dry_ctx):
         tplan = dry_ctx.plan("gemm", "f64", **lay)
         assert P.run_subtask(tplan, big_ops(16, 16, 16, "gemm"), P.TileParams(),
                              P.Bounds(0, 16, 0, 16, 0, 16), clock=P.FakeClock([0.5])) == 0.5
-    with pytest.raises(P.UnsupportedExpression):  # not one of the bodies
+    with pytest.raises(P.UnsupportedExpression):  # u[k] is not an MMLT leaf
         P.compile_task("where(i in [0..M] and j in [0..N] and k in [0..K]) {\n"
-                       "  R[i][j] += A[i][k]*B[k][j] + u[i]*v[j];\n}\n")
+                       "  R[i][j] += A[i][k]*B[k][j]*u[k];\n}\n")
+    # a recognised statement outside the fixed bodies: a generated body
+    assert P.compile_task("where(i in [0..M] and j in [0..N] and k in [0..K]) {\n"
+                          "  R[i][j] += A[i][k]*B[k][j] + u[i]*v[j];\n}\n").body == N.BODY_GENERIC
     # thresholds indexed [i]: accepted, and the vector must cover i1
     iplan = dry_ctx.plan("discount", "f64", thres_class="i")
     assert all(v.name.endswith(("_ti", "_ti_u")) for v in iplan.variants())

@@ -55,15 +55,29 @@ def test_roles_and_forms():
     assert t.body_name == "gemm"
 
 
+@pytest.mark.parametrize("rhs,aux", [
+    ("A[i][k]*B[k][j] + u[i]*v[j]", (("u", N.LEAF_VEC_I), ("v", N.LEAF_VEC_J))),
+    ("A[i][k]*B[k][j]*s + u[i] - v[j]*W[i][j]",
+     (("s", N.LEAF_CONSTANT), ("u", N.LEAF_VEC_I), ("v", N.LEAF_VEC_J), ("W", N.LEAF_MAT_IJ))),
+    ("(A[i][k] + 1)*(B[k][j] - 1)/2 + W[i][j]", (("W", N.LEAF_MAT_IJ),)),
+    ("A[i][k]*B[k][j] - (A[i][k]*B[k][j] < thres[j])*A[i][k]*B[k][j]",
+     (("thres", N.LEAF_VEC_J),)),
+])
+def test_other_mmlt_statements_get_generated_bodies(rhs, aux):
+    """Recognised MMLT statements outside the six bodies (recognize.cpp:
+    84-166) plan a generated body; aux leaves in first-use order."""
+    t = compile_task(wrap(rhs))
+    assert t.body == N.BODY_GENERIC and t.body_name == "generic"
+    assert tuple(zip(t.aux_names, t.aux_classes)) == aux
+    assert (t.a_name, t.b_name) == ("A", "B")
+
+
 @pytest.mark.parametrize("rhs", [
-    "A[i][k]*B[k][j] + u[i]*v[j]",          # a recognised MMLT, but not one of the bodies
-    "A[i][k]*B[k][j]*s + u[i] - v[j]*W[i][j]",
-    "(A[i][k] + 1)*(B[k][j] - 1)/2 + W[i][j]",
-    "A[i][k]*B[k][j] - (A[i][k]*B[k][j] < thres[j])*A[i][k]*B[k][j]",
     "A[i][k]*C[k][j]*B[k][j]",               # two k-indexed B-role arrays
     "A[i][k]*u[k]",                          # u[k] does not fit the pattern
+    "A[i][k]*B[k][j]*W[j][i]",               # W[j][i] does not fit the pattern
 ])
-def test_non_bodies_are_unsupported(rhs):
+def test_non_mmlt_statements_are_unsupported(rhs):
     with pytest.raises(P.UnsupportedExpression):
         compile_task(wrap(rhs))
 
