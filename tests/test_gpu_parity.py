@@ -383,3 +383,34 @@ def test_run_sharded_single_process(gpu_ctx):
     with pytest.raises(P.UnsupportedExpression):
         P.engine.run_sharded_host(plan, P.Operands(np.ascontiguousarray(A.T), B, np.zeros((M, N)),
                                                    t, d), P.Bounds(0, M, 0, N, 0, K), [0])
+
+
+def test_config4_full_size_sampled_rows(gpu_ctx):
+    """BASELINE config 4 at full size (32768 x 32768 x 8192 discount f64, the
+    bench workload): inputs generated on the device with its distributions,
+    the tuned run over the whole task, then the oracle on sampled rows,
+    including the first and last row of every 8-way shard band."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 32768, 8192, 32768
+    g = torch.Generator(device="cuda").manual_seed(11)
+    A = torch.randint(0, 10, (M, K), device="cuda", generator=g).double()
+    B = torch.rand((K, N), device="cuda", dtype=torch.float64, generator=g) * 99 + 1
+    t = torch.rand(N, device="cuda", dtype=torch.float64, generator=g) * 400 + 50
+    d = torch.rand(N, device="cuda", dtype=torch.float64, generator=g) * 0.3
+    R = torch.zeros((M, N), device="cuda", dtype=torch.float64)
+    plan = gpu_ctx.plan("discount", "f64")
+    rep = P.adaptive_execute(plan, P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K))
+    assert sum((c.i1 - c.i0) for c in rep.coverage) == M
+    bands = [M * r // 8 for r in range(9)]
+    rows = sorted(set([b for b in bands[:-1]] + [b - 1 for b in bands[1:]]
+                      + list(np.random.default_rng(4).integers(0, M, 8))))
+    idx = torch.tensor(rows, device="cuda")
+    Ah = A[idx].cpu().numpy()
+    got = R[idx].cpu().numpy()
+    del R, A
+    Bh, th, dh = B.cpu().numpy(), t.cpu().numpy(), d.cpu().numpy()
+    want = oracle("discount", Ah, Bh, th, dh)
+    check("discount", "f64", got, want, what="config 4 sampled rows")
