@@ -14,10 +14,14 @@
 // interpreted on the device.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <sys/stat.h>
+#include <unistd.h>
 #include <nvrtc.h>
 
 #include <chrono>
+#include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -94,14 +98,17 @@ struct Shape {
 constexpr int kTma = 1, kElem = 0, kTout = 2;
 const Shape kShapesF64[] = {
     {4, 4, 8, 1, 16, 3, kTma, 2, "t4x4_w8x1"},
+    {4, 4, 4, 1, 16, 4, kTma, 3, "t4x4_w4x1"},
     {4, 2, 4, 1, 16, 4, kTma, 4, "t4x2_w4x1"},
     {4, 4, 8, 1, 16, 3, kElem, 2, "t4x4_w8x1_u"},
 };
 const Shape kShapesF32[] = {
+    {8, 4, 8, 1, 32, 3, kTma, 1, "t8x4_w8x1"},
     {4, 4, 8, 1, 32, 3, kTma, 2, "t4x4_w8x1"},
     {4, 4, 4, 1, 32, 4, kTma, 3, "t4x4_w4x1"},
     {4, 4, 8, 1, 32, 3, kElem, 2, "t4x4_w8x1_u"},
 };
+constexpr int kNumShapes = 4;
 
 const char* ctype(int dtype) { return dtype == AMLT_F64 ? "double" : "float"; }
 
@@ -127,6 +134,100 @@ std::string tile_name_expr(const Shape& sh, int dtype, bool tout) {
                   ctype(dtype), sh.tm, sh.tn, sh.wr, sh.wc, sh.bk, sh.stages,
                   sh.load | (tout ? kTout : 0), minb_of(sh, tout));
     return buf;
+}
+
+// On-disk cubin cache, so a generated body compiles once per machine rather
+// than once per process: $AMLT_GPU_JIT_CACHE (a directory; "0" disables),
+// else $XDG_CACHE_HOME/amlt_gpu or ~/.cache/amlt_gpu. Entries are keyed by a
+// 64-bit FNV-1a hash of the full source (header included) and verified
+// against the stored source text before use.
+uint64_t fnv1a64(const std::string& s) {
+    uint64_t h = 1469598103934665603ull;
+    for (unsigned char c : s) {
+        h ^= c;
+        h *= 1099511628211ull;
+    }
+    return h;
+}
+
+std::string disk_cache_path(const std::string& src) {
+    const char* env = std::getenv("AMLT_GPU_JIT_CACHE");
+    std::string dir;
+    if (env && *env) {
+        if (std::string(env) == "0") return "";
+        dir = env;
+    } else if (const char* x = std::getenv("XDG_CACHE_HOME"); x && *x) {
+        dir = std::string(x) + "/amlt_gpu";
+    } else if (const char* h = std::getenv("HOME"); h && *h) {
+        dir = std::string(h) + "/.cache/amlt_gpu";
+    } else {
+        return "";
+    }
+    std::string cur;
+    for (size_t i = 0; i <= dir.size(); ++i)  // mkdir -p
+        if (i == dir.size() || (dir[i] == '/' && i > 0)) {
+            cur = dir.substr(0, i);
+            mkdir(cur.c_str(), 0755);
+        }
+    char name[64];
+    std::snprintf(name, sizeof(name), "/jit-%016llx.bin", static_cast<unsigned long long>(fnv1a64(src)));
+    return dir + name + "|" + src;  // the source rides along for verification
+}
+
+// File layout: u64 source length, source, u64 name count, (u64 len, name)*,
+// u64 cubin length, cubin.
+bool disk_cache_read(const std::string& key, size_t n_names, std::vector<char>* cubin,
+                     std::vector<std::string>* lowered) {
+    const size_t bar = key.find('|');
+    const std::string path = key.substr(0, bar), src = key.substr(bar + 1);
+    FILE* f = std::fopen(path.c_str(), "rb");
+    if (!f) return false;
+    auto rd_u64 = [&](uint64_t* v) { return std::fread(v, 8, 1, f) == 1; };
+    auto rd_str = [&](std::string* out) {
+        uint64_t n = 0;
+        if (!rd_u64(&n) || n > (1ull << 28)) return false;
+        out->resize(n);
+        return n == 0 || std::fread(&(*out)[0], 1, n, f) == n;
+    };
+    bool ok = false;
+    std::string stored;
+    uint64_t names = 0, nc = 0;
+    if (rd_str(&stored) && stored == src && rd_u64(&names) && names == n_names) {
+        lowered->assign(names, "");
+        ok = true;
+        for (auto& l : *lowered) ok = ok && rd_str(&l);
+        if (ok && rd_u64(&nc) && nc > 0 && nc < (1ull << 30)) {
+            cubin->resize(nc);
+            ok = std::fread(cubin->data(), 1, nc, f) == nc;
+        } else {
+            ok = false;
+        }
+    }
+    std::fclose(f);
+    return ok;
+}
+
+void disk_cache_write(const std::string& key, const std::vector<char>& cubin,
+                      const std::vector<std::string>& lowered) {
+    const size_t bar = key.find('|');
+    const std::string path = key.substr(0, bar), src = key.substr(bar + 1);
+    const std::string tmp = path + ".tmp" + std::to_string(static_cast<long long>(getpid()));
+    FILE* f = std::fopen(tmp.c_str(), "wb");
+    if (!f) return;
+    auto wr_u64 = [&](uint64_t v) { std::fwrite(&v, 8, 1, f); };
+    auto wr_str = [&](const std::string& s) {
+        wr_u64(s.size());
+        std::fwrite(s.data(), 1, s.size(), f);
+    };
+    wr_str(src);
+    wr_u64(lowered.size());
+    for (const auto& l : lowered) wr_str(l);
+    wr_u64(cubin.size());
+    std::fwrite(cubin.data(), 1, cubin.size(), f);
+    const bool ok = std::fflush(f) == 0;
+    std::fclose(f);
+    if (ok) std::rename(tmp.c_str(), path.c_str());  // atomic publish
+    else std::remove(tmp.c_str());
 }
 
 struct Cache {
@@ -189,7 +290,7 @@ const JitBody& jit_body(const RecognizedTask& rt, int dtype, bool load) {
 
     const bool tout = has_at(rt);
     const Shape* shapes = dtype == AMLT_F64 ? kShapesF64 : kShapesF32;
-    const int nshapes = 3;
+    const int nshapes = kNumShapes;
     std::vector<std::string> exprs;
     for (int i = 0; i < nshapes; ++i) exprs.push_back(tile_name_expr(shapes[i], dtype, tout));
     exprs.push_back(std::string("amltk::mmlt_assign_kernel<amltk::BodyGen, ") + ctype(dtype) + ">");
@@ -199,12 +300,15 @@ const JitBody& jit_body(const RecognizedTask& rt, int dtype, bool load) {
     std::vector<char> cubin;
     std::vector<std::string> lowered(exprs.size());
     const auto t0 = std::chrono::steady_clock::now();
+    const std::string src = jit_source(rt, dtype);
+    const std::string disk = disk_cache_path(src);
     if (it != C.bodies.end()) {
         cubin = it->second.cubin;
         lowered = it->second.lowered;
+    } else if (!disk.empty() && disk_cache_read(disk, exprs.size(), &cubin, &lowered)) {
+        // compiled by an earlier process
     } else {
         const Nvrtc& N = nvrtc();
-        const std::string src = jit_source(rt, dtype);
         nvrtcProgram prog = nullptr;
         if (N.create(&prog, src.c_str(), "amlt_generated_body.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS)
             throw TaskError(AMLT_ERR_ENGINE, "nvrtcCreateProgram failed");
@@ -231,6 +335,7 @@ const JitBody& jit_body(const RecognizedTask& rt, int dtype, bool load) {
             lowered[i] = ln ? ln : "";
         }
         N.destroy(&prog);
+        if (!disk.empty()) disk_cache_write(disk, cubin, lowered);
     }
     const double secs =
         std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

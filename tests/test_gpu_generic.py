@@ -59,7 +59,7 @@ def test_generated_bodies_compile_for_sm100a_without_a_device(dry_ctx):
     assert plan.aux_names == ("u", "v", "s", "W")
     assert plan.aux_classes == (N.LEAF_VEC_I, N.LEAF_VEC_J, N.LEAF_CONSTANT, N.LEAF_MAT_IJ)
     vs = plan.variants()
-    assert len(vs) == 3 and all(v.name.startswith("generic_f64_") for v in vs)
+    assert len(vs) == 4 and all(v.name.startswith("generic_f64_") for v in vs)
     assert all(v.name.endswith(("_ti", "_u_ti")) for v in vs)  # per-output aux state
     # operand rules: every aux leaf must be bound, by position
     M, K, N_ = 16, 8, 24
@@ -102,7 +102,7 @@ def test_random_statements_recognised_and_compiled(dry_ctx, seed):
     t = P.compile_task(src)
     plan = dry_ctx.plan_for(t, "f64")
     if t.body == N.BODY_GENERIC:  # (a bare A*B core is the fixed GEMM body)
-        assert len(plan.variants()) == 3
+        assert len(plan.variants()) == 4
 
 
 # ---------------------------------------------------------------- GPU cases
@@ -182,3 +182,38 @@ def test_generated_body_naive_and_host_paths(gpu_ctx):
     assert np.array_equal(dev[t.result_name].cpu().numpy(), want)
     P.run_host(plan, P.operands_of(t, host), P.Bounds(0, M, 0, N_, 0, K))
     assert np.array_equal(host[t.result_name], want)
+
+
+def test_generated_kernels_are_cached_on_disk(tmp_path):
+    """A generated body compiles once per machine: the cubin lands in
+    $AMLT_GPU_JIT_CACHE and later processes load it; a damaged entry is
+    ignored (recompiled), and "0" disables the cache."""
+    import os
+    import subprocess
+    import sys
+
+    code = ("import paper_2305_08872_b200 as P\n"
+            "ctx = P.Context(0, dry_run=True)\n"
+            "p = ctx.plan_source('" + HEAD.replace("\n", "\\n") +
+            "+= A[i][k]*B[k][j] - v[j]*(B[k][j] > 2);\\n}\\n')\n"
+            "print(len(p.variants()))\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+    def run(cache):
+        env = dict(os.environ, AMLT_GPU_JIT_CACHE=str(cache))
+        r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        return r.stdout.strip()
+
+    d = tmp_path / "jit"
+    assert run(d) == "4"
+    files = list(d.glob("jit-*.bin"))
+    assert len(files) == 1 and files[0].stat().st_size > 10000
+    assert run(d) == "4"  # served from the cache
+    files[0].write_bytes(files[0].read_bytes()[:100])  # damaged entry: recompiled
+    assert run(d) == "4"
+    assert files[0].stat().st_size > 10000
+    off = tmp_path / "off"
+    env_dir = off / "x"
+    assert run("0") == "4" and not env_dir.exists()
