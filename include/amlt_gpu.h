@@ -410,7 +410,17 @@ amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_o
 amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const amlt_operands* host_ops,
                                  const amlt_bounds* bounds, int n_devices, const int* devices,
                                  int flags, double* elapsed_s);
-/* Message of the calling thread's last failing amlt_gpu_run_sharded. */
+/* The same from a task text: any recognised statement, generated bodies
+ * included (aux leaves bound by position as for amlt_gpu_plan_from_source).
+ * Operands indexed by i follow the row split: row-major [i][j] leaves (and
+ * thresholds) are copied band by band like R, [i] vectors are replicated
+ * and viewed from the band's first row; [j] and scalar leaves are
+ * replicated. */
+amlt_status amlt_gpu_run_sharded_source(const char* task_source, int dtype,
+                                        const amlt_operands* host_ops, const amlt_bounds* bounds,
+                                        int n_devices, const int* devices, int flags,
+                                        double* elapsed_s);
+/* Message of the calling thread's last failing amlt_gpu_run_sharded(_source). */
 const char* amlt_gpu_sharded_last_error(void);
 
 /* The reference's AMLT binary matrix files (README.md:146-157,

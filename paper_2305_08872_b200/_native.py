@@ -133,6 +133,7 @@ EXPORTS = [
     "amlt_gpu_run_sharded", "amlt_gpu_sharded_last_error", "amlt_matrix_file_info",
     "amlt_matrix_file_read", "amlt_matrix_file_write", "amlt_matrix_file_last_error",
     "amlt_operand_seed", "amlt_gen_matrix", "amlt_gpu_run_naive", "amlt_gpu_generated_source",
+    "amlt_gpu_run_sharded_source",
 ]
 HOST_R_ZERO = 1
 
@@ -186,6 +187,9 @@ def lib():
                                        C.POINTER(BoundsC), C.c_int, C.POINTER(C.c_int), C.c_int,
                                        C.POINTER(C.c_double)]
     L.amlt_gpu_sharded_last_error.restype = C.c_char_p
+    L.amlt_gpu_run_sharded_source.argtypes = [C.c_char_p, C.c_int, C.POINTER(OperandsC),
+                                              C.POINTER(BoundsC), C.c_int, C.POINTER(C.c_int),
+                                              C.c_int, C.POINTER(C.c_double)]
     L.amlt_matrix_file_info.argtypes = [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
                                         C.POINTER(C.c_int)]
     L.amlt_matrix_file_read.argtypes = [C.c_char_p, C.c_void_p, C.c_int, C.c_int]

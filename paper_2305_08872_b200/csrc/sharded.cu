@@ -82,20 +82,57 @@ struct DevState {
     amlt_ctx* ctx = nullptr;
     amlt_plan* plan = nullptr;
     cudaStream_t stream = nullptr;
-    void* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};  // A band, B, R band, thres, dis
+    void* buf[3] = {nullptr, nullptr, nullptr};  // A band, B, R band
+    std::vector<void*> xbuf;                     // per extra operand (see Extra)
     int64_t r0 = 0, r1 = 0;
     amlt_status st = AMLT_OK;
     std::string err;
 };
 
-}  // namespace
+// An operand besides A / B / R: thres, dis or a generated body's aux leaf.
+// Leaves indexed by i follow the row split: a row-major [i][j] matrix is
+// copied band by band like R; an [i] vector (or a col-major [i][j]) is
+// replicated and viewed from row r0. Everything else is replicated.
+struct Extra {
+    const amlt_matrix* host = nullptr;
+    int cls = AMLT_LEAF_VEC_J;
+    bool banded = false;  // row-major [i][j]: per-device band copies
+    size_t bytes = 0;     // replicated copy size
+};
+
+int64_t vec_step(const amlt_matrix& t) {
+    return (t.cols == 1) ? (t.order == AMLT_ROW_MAJOR ? t.ld : 1) : (t.order == AMLT_ROW_MAJOR ? 1 : t.ld);
+}
+
+// The device view of an extra operand on the device owning rows [r0, r1).
+amlt_matrix band_view(const Extra& x, void* dev, int64_t r0, int64_t r1) {
+    amlt_matrix m = *x.host;
+    m.data = dev;
+    if (!dev) return m;
+    const int es = es_of(m.dtype);
+    if (x.cls == AMLT_LEAF_VEC_I) {
+        m.data = static_cast<char*>(dev) + r0 * vec_step(*x.host) * es;
+        if (m.cols == 1) m.rows = std::max<int64_t>(m.rows - r0, 0);
+        else m.cols = std::max<int64_t>(m.cols - r0, 0);
+    } else if (x.cls == AMLT_LEAF_MAT_IJ) {
+        if (x.banded) {
+            m.rows = r1 - r0;
+        } else {  // col-major: element (i, j) at i + j * ld
+            m.data = static_cast<char*>(dev) + r0 * es;
+            m.rows = std::max<int64_t>(m.rows - r0, 0);
+        }
+    }
+    return m;
+}
 
 thread_local std::string g_sharded_error;
 
-extern "C" amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const amlt_operands* ho,
-                                            const amlt_bounds* bounds, int n, const int* devices,
-                                            int flags, double* elapsed_s) {
-    if (!desc || !ho || !bounds || n < 1 || !devices) return AMLT_ERR_INVALID_ARGUMENT;
+// Shared by the body-descriptor and task-text entries: make_plan creates
+// the per-device plan (and reports the aux classes of generated bodies).
+template <class MakePlan>
+amlt_status run_sharded_impl(int dtype, int layout_a, int thres_class, MakePlan make_plan,
+                             const amlt_operands* ho, const amlt_bounds* bounds, int n,
+                             const int* devices, int flags, double* elapsed_s) {
     std::vector<DevState> ds(static_cast<size_t>(n));
     std::vector<ncclComm_t> comms;
     auto cleanup = [&] {
@@ -103,6 +140,8 @@ extern "C" amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const am
             if (d.device >= 0) cudaSetDevice(d.device);
             if (d.stream) cudaStreamSynchronize(d.stream);
             for (void* p : d.buf)
+                if (p) cudaFree(p);
+            for (void* p : d.xbuf)
                 if (p) cudaFree(p);
             if (d.plan) amlt_gpu_plan_destroy(d.plan);
             if (d.ctx) amlt_gpu_ctx_destroy(d.ctx);
@@ -112,20 +151,20 @@ extern "C" amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const am
             if (c) nccl().destroy(c);
     };
     try {
-        const amlt_body_desc& bd = *desc;
-        const int es = es_of(bd.dtype);
+        const int es = es_of(dtype);
         const int64_t M = bounds->i1 - bounds->i0;
         // A: each statement row i must be a contiguous run along k (row stride lda)
-        const bool a_rows = (bd.layout_a == AMLT_LAYOUT_NORMAL && ho->a.order == AMLT_ROW_MAJOR) ||
-                            (bd.layout_a == AMLT_LAYOUT_TRANSPOSED && ho->a.order == AMLT_COL_MAJOR);
+        const bool a_rows = (layout_a == AMLT_LAYOUT_NORMAL && ho->a.order == AMLT_ROW_MAJOR) ||
+                            (layout_a == AMLT_LAYOUT_TRANSPOSED && ho->a.order == AMLT_COL_MAJOR);
         if (!a_rows || ho->r.order != AMLT_ROW_MAJOR)
             throw Fail(AMLT_ERR_UNSUPPORTED,
                        "run_sharded needs A rows (k) contiguous and a row-major R; use run_host per device");
         if (M < 0) throw Fail(AMLT_ERR_INVALID_ARGUMENT, "bad bounds");
         if (n > 1 && !nccl().ok) throw Fail(AMLT_ERR_CUDA, "libnccl.so.2 could not be loaded");
 
-        const size_t bB = bytes_of(ho->b), bT = bytes_of(ho->thres), bD = bytes_of(ho->dis);
+        const size_t bB = bytes_of(ho->b);
         const int64_t a_ld = ho->a.ld, r_ld = ho->r.ld;
+        std::vector<int> aux_class;
         for (int d = 0; d < n; ++d) {
             DevState& s = ds[static_cast<size_t>(d)];
             s.device = devices[d];
@@ -133,8 +172,24 @@ extern "C" amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const am
             s.r1 = bounds->i0 + M * (d + 1) / n;
             amlt_status st = amlt_gpu_ctx_create(s.device, 0, &s.ctx);
             if (st != AMLT_OK) throw Fail(st, amlt_gpu_last_error(nullptr));
-            st = amlt_gpu_plan_create(s.ctx, &bd, &s.plan);
+            st = make_plan(s.ctx, &s.plan, &aux_class);
             if (st != AMLT_OK) throw Fail(st, amlt_gpu_last_error(s.ctx));
+        }
+        // the extra operands: thres, dis, then the aux leaves by position
+        std::vector<Extra> ex;
+        auto add_extra = [&](const amlt_matrix* m, int cls) {
+            Extra x;
+            x.host = m;
+            x.cls = cls;
+            x.banded = cls == AMLT_LEAF_MAT_IJ && m->order == AMLT_ROW_MAJOR;
+            x.bytes = x.banded ? 0 : bytes_of(*m);
+            ex.push_back(x);
+        };
+        add_extra(&ho->thres, thres_class);
+        add_extra(&ho->dis, AMLT_LEAF_VEC_J);
+        for (size_t q = 0; q < aux_class.size() && static_cast<int>(q) < ho->n_aux; ++q)
+            add_extra(&ho->aux[q], aux_class[q]);
+        for (auto& s : ds) {
             ck(cudaSetDevice(s.device), "cudaSetDevice");
             ck(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking), "cudaStreamCreate");
             amlt_gpu_set_stream(s.ctx, s.stream);
@@ -143,8 +198,12 @@ extern "C" amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const am
             ck(cudaMalloc(&s.buf[0], std::max<size_t>(rows, 1) * a_ld * es), "cudaMalloc A band");
             ck(cudaMalloc(&s.buf[1], std::max<size_t>(bB, 16)), "cudaMalloc B");
             ck(cudaMalloc(&s.buf[2], std::max<size_t>(rows, 1) * r_ld * es), "cudaMalloc R band");
-            if (bT) ck(cudaMalloc(&s.buf[3], bT), "cudaMalloc thres");
-            if (bD) ck(cudaMalloc(&s.buf[4], bD), "cudaMalloc dis");
+            s.xbuf.assign(ex.size(), nullptr);
+            for (size_t x = 0; x < ex.size(); ++x) {
+                if (!ex[x].host->data) continue;
+                const size_t b = ex[x].banded ? std::max<size_t>(rows, 1) * ex[x].host->ld * es : ex[x].bytes;
+                ck(cudaMalloc(&s.xbuf[x], std::max<size_t>(b, 16)), "cudaMalloc extra operand");
+            }
         }
         if (n > 1) {
             comms.assign(static_cast<size_t>(n), nullptr);
@@ -152,7 +211,8 @@ extern "C" amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const am
         }
 
         auto t0 = std::chrono::steady_clock::now();
-        // H2D: A / R bands to their owners, B and the vectors to devices[0]
+        // H2D: A / R (and row-major [i][j]) bands to their owners, B and the
+        // replicated operands to devices[0]
         for (int d = 0; d < n; ++d) {
             DevState& s = ds[static_cast<size_t>(d)];
             ck(cudaSetDevice(s.device), "cudaSetDevice");
@@ -166,25 +226,33 @@ extern "C" amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const am
             else
                 ck(cudaMemcpyAsync(s.buf[2], r_src, rows * r_ld * es, cudaMemcpyHostToDevice, s.stream),
                    "H2D R band");
-            if (d == 0) {
-                ck(cudaMemcpyAsync(s.buf[1], ho->b.data, bB, cudaMemcpyHostToDevice, s.stream), "H2D B");
-                if (bT)
-                    ck(cudaMemcpyAsync(s.buf[3], ho->thres.data, bT, cudaMemcpyHostToDevice, s.stream),
-                       "H2D thres");
-                if (bD)
-                    ck(cudaMemcpyAsync(s.buf[4], ho->dis.data, bD, cudaMemcpyHostToDevice, s.stream),
-                       "H2D dis");
+            for (size_t x = 0; x < ex.size(); ++x) {
+                const amlt_matrix& m = *ex[x].host;
+                if (!m.data) continue;
+                if (ex[x].banded) {
+                    const size_t pitch = size_t(m.ld) * es;
+                    ck(cudaMemcpyAsync(s.xbuf[x], static_cast<const char*>(m.data) + size_t(s.r0) * pitch,
+                                       rows * pitch, cudaMemcpyHostToDevice, s.stream),
+                       "H2D [i][j] band");
+                } else if (d == 0) {
+                    ck(cudaMemcpyAsync(s.xbuf[x], m.data, ex[x].bytes, cudaMemcpyHostToDevice, s.stream),
+                       "H2D replicated operand");
+                }
             }
+            if (d == 0)
+                ck(cudaMemcpyAsync(s.buf[1], ho->b.data, bB, cudaMemcpyHostToDevice, s.stream), "H2D B");
         }
-        // replicate B / thres / dis over NVLink (byte broadcasts, in one group)
+        // replicate B and the replicated operands over NVLink (one group)
         if (n > 1) {
             nk(nccl().group_start(), "ncclGroupStart");
-            for (int slot : {1, 3, 4}) {
-                const size_t bytes = slot == 1 ? bB : slot == 3 ? bT : bD;
-                if (!bytes) continue;
-                for (int d = 0; d < n; ++d) {
-                    DevState& s = ds[static_cast<size_t>(d)];
-                    nk(nccl().bcast(s.buf[slot], s.buf[slot], bytes, ncclUint8, 0,
+            for (int d = 0; d < n; ++d) {
+                DevState& s = ds[static_cast<size_t>(d)];
+                nk(nccl().bcast(s.buf[1], s.buf[1], bB, ncclUint8, 0, comms[static_cast<size_t>(d)],
+                                s.stream),
+                   "ncclBroadcast");
+                for (size_t x = 0; x < ex.size(); ++x) {
+                    if (!ex[x].host->data || ex[x].banded || !ex[x].bytes) continue;
+                    nk(nccl().bcast(s.xbuf[x], s.xbuf[x], ex[x].bytes, ncclUint8, 0,
                                     comms[static_cast<size_t>(d)], s.stream),
                        "ncclBroadcast");
                 }
@@ -204,8 +272,10 @@ extern "C" amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const am
                 o.b.data = s.buf[1];
                 o.r.data = s.buf[2];
                 o.r.rows = s.r1 - s.r0;
-                o.thres.data = s.buf[3];
-                o.dis.data = s.buf[4];
+                o.thres = band_view(ex[0], s.xbuf[0], s.r0, s.r1);
+                o.dis = band_view(ex[1], s.xbuf[1], s.r0, s.r1);
+                for (size_t q = 2; q < ex.size(); ++q)
+                    o.aux[q - 2] = band_view(ex[q], s.xbuf[q], s.r0, s.r1);
                 // band-local bounds: rows [0, r1 - r0), same j / k ranges
                 amlt_bounds bb = *bounds;
                 bb.i0 = 0;
@@ -247,6 +317,46 @@ extern "C" amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const am
         cleanup();
         return AMLT_ERR_ENGINE;
     }
+}
+
+}  // namespace
+
+extern "C" amlt_status amlt_gpu_run_sharded(const amlt_body_desc* desc, const amlt_operands* ho,
+                                            const amlt_bounds* bounds, int n, const int* devices,
+                                            int flags, double* elapsed_s) {
+    if (!desc || !ho || !bounds || n < 1 || !devices) return AMLT_ERR_INVALID_ARGUMENT;
+    const bool needs_t = desc->body == AMLT_BODY_DISCOUNT || desc->body == AMLT_BODY_BOOST ||
+                         desc->body == AMLT_BODY_THRCOUNT;
+    return run_sharded_impl(
+        desc->dtype, desc->layout_a, needs_t ? desc->thres_class : AMLT_LEAF_VEC_J,
+        [&](amlt_ctx* ctx, amlt_plan** plan, std::vector<int>*) {
+            return amlt_gpu_plan_create(ctx, desc, plan);
+        },
+        ho, bounds, n, devices, flags, elapsed_s);
+}
+
+extern "C" amlt_status amlt_gpu_run_sharded_source(const char* task_source, int dtype,
+                                                   const amlt_operands* ho, const amlt_bounds* bounds,
+                                                   int n, const int* devices, int flags,
+                                                   double* elapsed_s) {
+    if (!task_source || !ho || !bounds || n < 1 || !devices) return AMLT_ERR_INVALID_ARGUMENT;
+    amlt_task_info info;
+    amlt_status st = amlt_gpu_recognize(task_source, &info);
+    if (st != AMLT_OK) {
+        g_sharded_error = amlt_gpu_last_error(nullptr);
+        return st;
+    }
+    const bool needs_t = info.desc.body == AMLT_BODY_DISCOUNT || info.desc.body == AMLT_BODY_BOOST ||
+                         info.desc.body == AMLT_BODY_THRCOUNT;
+    return run_sharded_impl(
+        dtype, info.desc.layout_a, needs_t ? info.desc.thres_class : AMLT_LEAF_VEC_J,
+        [&](amlt_ctx* ctx, amlt_plan** plan, std::vector<int>* aux_class) {
+            amlt_task_info ti;
+            amlt_status r = amlt_gpu_plan_from_source(ctx, task_source, dtype, plan, &ti);
+            if (r == AMLT_OK) aux_class->assign(ti.aux_class, ti.aux_class + ti.n_aux);
+            return r;
+        },
+        ho, bounds, n, devices, flags, elapsed_s);
 }
 
 extern "C" const char* amlt_gpu_sharded_last_error(void) { return g_sharded_error.c_str(); }

@@ -643,6 +643,24 @@ def run_sharded_host(desc_plan: GpuPlan, ops: Operands, bounds: Bounds, devices,
     return el.value
 
 
+def run_sharded_source(source: str, ops: Operands, bounds: Bounds, devices, dtype="f64",
+                       r_zero: bool = False) -> float:
+    """amlt_gpu_run_sharded_source: the single-process multi-GPU run for any
+    recognised task text (generated bodies included; aux leaves in
+    ops.aux by position). Returns elapsed seconds."""
+    devs = (C.c_int * len(devices))(*devices)
+    oc = ops._c(False)
+    bc = bounds._c()
+    el = C.c_double()
+    dt = DTYPES[dtype] if isinstance(dtype, str) else int(dtype)
+    st = N.lib().amlt_gpu_run_sharded_source(source.encode(), dt, C.byref(oc), C.byref(bc),
+                                             len(devices), devs, N.HOST_R_ZERO if r_zero else 0,
+                                             C.byref(el))
+    if st != N.OK:
+        raise _ERRS.get(st, EngineError)(N.lib().amlt_gpu_sharded_last_error().decode())
+    return el.value
+
+
 def run_fixed(plan: GpuPlan, ops: Operands, bounds: Bounds, kc: int, nc: int, pack=False,
               clock: Optional[Clock] = None, log: Optional[ExecLog] = None) -> float:
     """run_fixed (engine.hpp:67-68): one subtask over the whole bounds."""

@@ -217,3 +217,29 @@ def test_generated_kernels_are_cached_on_disk(tmp_path):
     off = tmp_path / "off"
     env_dir = off / "x"
     assert run("0") == "4" and not env_dir.exists()
+
+
+@pytest.mark.gpu
+@pytest.mark.skipif(not po.ref_available(), reason="reference engine not built")
+@pytest.mark.parametrize("w_order", ["C", "F"])
+def test_sharded_source_with_row_indexed_leaves(gpu_ctx, w_order):
+    """amlt_gpu_run_sharded_source on a sub-range of rows: [i] and [i][j]
+    leaves are viewed / copied from the band's first row (row-major W is
+    banded like R, col-major W replicated and offset)."""
+    src = HEAD + "+= A[i][k]*B[k][j] + u[i]*v[j] - (A[i][k] > s)*W[i][j]/4;\n}\n"
+    M, K, N_ = 64, 40, 72
+    ref = po.RefTask.create(src, M, K, N_, seed=9, int_valued=True)
+    t = P.compile_task(src)
+    host = {n: np.ascontiguousarray(ref.get(n)) for n in ref.names()}
+    host["W"] = np.asarray(host["W"], order=w_order)
+    R0 = np.arange(M * N_, dtype=np.float64).reshape(M, N_)
+    host[t.result_name] = R0.copy()
+    ref.set(t.result_name, R0)
+    i0, i1 = 7, 50
+    el = P.engine.run_sharded_source(src, P.operands_of(t, host), P.Bounds(i0, i1, 0, N_, 0, K), [0])
+    assert el > 0
+    ref.run_naive()
+    want = ref.get(ref.result_name())
+    got = host[t.result_name]
+    assert np.array_equal(got[i0:i1], want[i0:i1])
+    assert np.array_equal(got[:i0], R0[:i0]) and np.array_equal(got[i1:], R0[i1:])

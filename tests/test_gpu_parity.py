@@ -385,6 +385,30 @@ def test_run_sharded_single_process(gpu_ctx):
                                                    t, d), P.Bounds(0, M, 0, N, 0, K), [0])
 
 
+@pytest.mark.parametrize("form", ["i", "ij"])
+def test_run_sharded_row_indexed_thresholds(gpu_ctx, form):
+    """Thresholds indexed by i follow the row split: on a sub-range of rows
+    [i0, i1) the device sees thres from row i0 (a row-major [i][j] threshold
+    is copied band by band like R)."""
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 90, 70, 130
+    A, B, _, d = make_inputs("discount", M, K, N, "int", seed=62)
+    rng = np.random.default_rng(63)
+    t = rng.integers(-8, 9, M if form == "i" else (M, N)).astype(np.float64)
+    R0 = rng.integers(-8, 9, (M, N)).astype(np.float64)
+    i0, i1 = 13, 77
+    tv = np.broadcast_to(t[:, None], (M, N)) if form == "i" else t
+    want = R0.copy()
+    for i in range(i0, i1):
+        p = A[i][:, None] * B  # K x N
+        want[i] += (p - (p > tv[i]) * p * d).sum(axis=0)
+    plan = gpu_ctx.plan("discount", "f64", thres_class=form)
+    R = R0.copy()
+    P.engine.run_sharded_host(plan, P.Operands(A, B, R, t, d), P.Bounds(i0, i1, 0, N, 0, K), [0])
+    check("discount", "f64", R, want, exact=True, what=f"sharded thres[{form}]")
+
+
 def test_config4_full_size_sampled_rows(gpu_ctx):
     """BASELINE config 4 at full size (32768 x 32768 x 8192 discount f64, the
     bench workload): inputs generated on the device with its distributions,
