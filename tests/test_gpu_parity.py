@@ -412,8 +412,9 @@ def test_run_sharded_row_indexed_thresholds(gpu_ctx, form):
 def test_config4_full_size_sampled_rows(gpu_ctx):
     """BASELINE config 4 at full size (32768 x 32768 x 8192 discount f64, the
     bench workload): inputs generated on the device with its distributions,
-    the tuned run over the whole task, then the oracle on sampled rows,
-    including the first and last row of every 8-way shard band."""
+    the tuned run over the whole task, then the oracle on sampled rows
+    (including the first and last row of every 8-way shard band) x sampled
+    columns (including the first and last)."""
     import torch
 
     import paper_2305_08872_b200 as P
@@ -431,10 +432,11 @@ def test_config4_full_size_sampled_rows(gpu_ctx):
     bands = [M * r // 8 for r in range(9)]
     rows = sorted(set([b for b in bands[:-1]] + [b - 1 for b in bands[1:]]
                       + list(np.random.default_rng(4).integers(0, M, 8))))
+    cols = sorted(set([0, N - 1] + list(np.random.default_rng(5).integers(0, N, 510))))
     idx = torch.tensor(rows, device="cuda")
+    cdx = torch.tensor(cols, device="cuda")
     Ah = A[idx].cpu().numpy()
-    got = R[idx].cpu().numpy()
-    del R, A
-    Bh, th, dh = B.cpu().numpy(), t.cpu().numpy(), d.cpu().numpy()
-    want = oracle("discount", Ah, Bh, th, dh)
-    check("discount", "f64", got, want, what="config 4 sampled rows")
+    got = R[idx][:, cdx].cpu().numpy()
+    Bh, th, dh = B[:, cdx].cpu().numpy(), t[cdx].cpu().numpy(), d[cdx].cpu().numpy()
+    want = oracle("discount", Ah, Bh, th, dh)  # rows x sampled columns: exact oracle entries
+    check("discount", "f64", got, want, what="config 4 sampled rows x columns")
