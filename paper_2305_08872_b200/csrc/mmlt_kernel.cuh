@@ -379,6 +379,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
                  "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     uint32_t done;
     do {
@@ -424,7 +427,7 @@ struct MmltTile {
     static constexpr int BN = 32 * TN * WC;
     static constexpr int SMEM_A = BM * BK;  // elements per stage
     static constexpr int SMEM_B = BK * BN;
-    static constexpr int BAR_BYTES = 8 * STAGES;
+    static constexpr int BAR_BYTES = 16 * STAGES;  // full + empty mbarriers (within the +128)
     static constexpr int SMEM_BYTES = STAGES * (SMEM_A + SMEM_B) * (int)sizeof(T) + 128;
     static_assert(TN % VN == 0, "TN must be a multiple of the 16B vector width");
     static_assert(BK % VN == 0, "BK must be a multiple of the 16B vector width");
@@ -452,6 +455,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
     T* As = reinterpret_cast<T*>(smem_raw);
     T* Bs = As + STAGES * Cfg::SMEM_A;
     uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * Cfg::SMEM_B);
+    uint64_t* empty = full + STAGES;  // one arrival per warp when a stage is consumed
 
     // ---- tile coordinates: grouped raster (group_m row-tiles per group, about
     // 512 rows) so the B column panels of concurrently resident CTAs are
@@ -518,7 +522,10 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
     if constexpr ((LOAD & LOAD_TMA) != 0) {
         if (tid == 0) {
 #pragma unroll
-            for (int s = 0; s < STAGES; ++s) mbar_init(&full[s], 1);
+            for (int s = 0; s < STAGES; ++s) {
+                mbar_init(&full[s], 1);
+                mbar_init(&empty[s], THREADS / 32);
+            }
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -661,9 +668,15 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
                     }
         }
         if constexpr ((LOAD & LOAD_TMA) != 0) {
-            // every warp is done reading this stage: refill it with tile kt+STAGES
-            __syncthreads();
-            if (tid == 0 && kt + STAGES < nkt) tma_stage(stage, kt + STAGES);
+            // this warp is done reading the stage; the producer thread refills
+            // it with tile kt+STAGES once every warp has (no CTA-wide barrier:
+            // warps drift across the ready stages)
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (tid == 0 && kt + STAGES < nkt) {
+                mbar_wait(&empty[stage], static_cast<uint32_t>((kt / STAGES) & 1));
+                tma_stage(stage, kt + STAGES);
+            }
         }
     }
     if constexpr ((LOAD & LOAD_TMA) == 0) cp_async_wait<0>();
