@@ -455,6 +455,21 @@ amlt_status amlt_gpu_measure_peak(int pipe, double* ops_per_s, double* sm_ghz);
 /* Scaled processing rate M*K*N / (1e9 * seconds) (engine.cpp:212-216). */
 amlt_status amlt_spr(int64_t M, int64_t K, int64_t N, double seconds, double* out);
 
+/* Device matrices for callers without an allocator of their own (the
+ * reference hands over f64 MatrixBuffers). amlt_gpu_matrix_alloc returns a
+ * rows x cols matrix in the given order and dtype whose leading dimension is
+ * padded to 16 bytes (so the TMA-staged variants apply); upload / download
+ * convert between the caller's f64 values (storage order, leading dimension
+ * host_ld >= cols for row-major, >= rows for col-major) and the dtype.
+ * Synchronous on the context stream. */
+amlt_status amlt_gpu_matrix_alloc(amlt_ctx* ctx, int64_t rows, int64_t cols, int order, int dtype,
+                                  amlt_matrix* out);
+amlt_status amlt_gpu_matrix_free(amlt_ctx* ctx, amlt_matrix* m);
+amlt_status amlt_gpu_matrix_upload(amlt_ctx* ctx, const amlt_matrix* dev, const double* host,
+                                   int64_t host_ld);
+amlt_status amlt_gpu_matrix_download(amlt_ctx* ctx, const amlt_matrix* dev, double* host,
+                                     int64_t host_ld);
+
 #ifdef __cplusplus
 }
 #endif

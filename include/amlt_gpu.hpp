@@ -183,6 +183,40 @@ private:
     amlt_ctx* ctx_ = nullptr;
 };
 
+// A device matrix owned by the library's allocator (amlt_gpu_matrix_*):
+// f64 values in, stored in the plan's dtype, f64 values out.
+class DeviceMatrix {
+public:
+    DeviceMatrix(Context& ctx, std::int64_t rows, std::int64_t cols, amlt_order order,
+                 amlt_dtype dtype)
+        : ctx_(&ctx) {
+        check(amlt_gpu_matrix_alloc(ctx.get(), rows, cols, order, dtype, &m_), ctx.get());
+    }
+    ~DeviceMatrix() { amlt_gpu_matrix_free(ctx_->get(), &m_); }
+    DeviceMatrix(const DeviceMatrix&) = delete;
+    DeviceMatrix& operator=(const DeviceMatrix&) = delete;
+    void upload(const double* host, std::int64_t host_ld) {
+        check(amlt_gpu_matrix_upload(ctx_->get(), &m_, host, host_ld), ctx_->get());
+    }
+    void download(double* host, std::int64_t host_ld) const {
+        check(amlt_gpu_matrix_download(ctx_->get(), &m_, host, host_ld), ctx_->get());
+    }
+    Matrix view() const {
+        Matrix v;
+        v.data = m_.data;
+        v.rows = m_.rows;
+        v.cols = m_.cols;
+        v.ld = m_.ld;
+        v.order = static_cast<amlt_order>(m_.order);
+        v.dtype = static_cast<amlt_dtype>(m_.dtype);
+        return v;
+    }
+
+private:
+    Context* ctx_;
+    amlt_matrix m_{};
+};
+
 // The GPU counterpart of CompiledTask: immutable, shareable.
 class Plan {
 public:

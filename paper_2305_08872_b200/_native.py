@@ -133,7 +133,8 @@ EXPORTS = [
     "amlt_gpu_run_sharded", "amlt_gpu_sharded_last_error", "amlt_matrix_file_info",
     "amlt_matrix_file_read", "amlt_matrix_file_write", "amlt_matrix_file_last_error",
     "amlt_operand_seed", "amlt_gen_matrix", "amlt_gpu_run_naive", "amlt_gpu_generated_source",
-    "amlt_gpu_run_sharded_source",
+    "amlt_gpu_run_sharded_source", "amlt_gpu_matrix_alloc", "amlt_gpu_matrix_free",
+    "amlt_gpu_matrix_upload", "amlt_gpu_matrix_download",
 ]
 HOST_R_ZERO = 1
 
@@ -202,6 +203,10 @@ def lib():
                                   C.c_int, C.c_int]
     L.amlt_gpu_generated_source.argtypes = [C.c_char_p, C.c_int, C.c_char_p, C.c_int64]
     L.amlt_gpu_generated_source.restype = C.c_int64
+    L.amlt_gpu_matrix_alloc.argtypes = [P, C.c_int64, C.c_int64, C.c_int, C.c_int, C.POINTER(Matrix)]
+    L.amlt_gpu_matrix_free.argtypes = [P, C.POINTER(Matrix)]
+    L.amlt_gpu_matrix_upload.argtypes = [P, C.POINTER(Matrix), C.c_void_p, C.c_int64]
+    L.amlt_gpu_matrix_download.argtypes = [P, C.POINTER(Matrix), C.c_void_p, C.c_int64]
     L.amlt_gpu_recognize.argtypes = [C.c_char_p, C.POINTER(TaskInfoC)]
     L.amlt_gpu_plan_from_source.argtypes = [P, C.c_char_p, C.c_int, C.POINTER(P),
                                             C.POINTER(TaskInfoC)]

@@ -1532,6 +1532,117 @@ amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_o
     });
 }
 
+// ---------------------------------------------------------------------------
+// device matrices for callers without their own allocator (SURVEY §8b
+// "amlt_gpu_upload/alloc"): the reference's f64 MatrixBuffers in and out,
+// stored on the device in the plan's dtype.
+
+namespace {
+void convert_rows(const double* src, void* dst, int64_t n, int dtype) {
+    if (dtype == AMLT_F64) {
+        std::memcpy(dst, src, size_t(n) * 8);
+    } else if (dtype == AMLT_F32) {
+        float* d = static_cast<float*>(dst);
+        for (int64_t i = 0; i < n; ++i) d[i] = static_cast<float>(src[i]);
+    } else {
+        int32_t* d = static_cast<int32_t*>(dst);
+        for (int64_t i = 0; i < n; ++i) d[i] = static_cast<int32_t>(src[i]);
+    }
+}
+void widen_rows(const void* src, double* dst, int64_t n, int dtype) {
+    if (dtype == AMLT_F64) {
+        std::memcpy(dst, src, size_t(n) * 8);
+    } else if (dtype == AMLT_F32) {
+        const float* s = static_cast<const float*>(src);
+        for (int64_t i = 0; i < n; ++i) dst[i] = s[i];
+    } else {
+        const int32_t* s = static_cast<const int32_t*>(src);
+        for (int64_t i = 0; i < n; ++i) dst[i] = s[i];
+    }
+}
+}  // namespace
+
+amlt_status amlt_gpu_matrix_alloc(amlt_ctx* ctx, int64_t rows, int64_t cols, int order, int dtype,
+                                  amlt_matrix* out) {
+    if (!ctx || !out || rows < 0 || cols < 0 || (order != AMLT_ROW_MAJOR && order != AMLT_COL_MAJOR) ||
+        dtype < AMLT_F64 || dtype > AMLT_I32)
+        return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (ctx->dry()) fail(AMLT_ERR_NO_DEVICE, "amlt_gpu_matrix_alloc needs a device context");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const int es = dtype_size(dtype);
+        const int64_t inner = order == AMLT_ROW_MAJOR ? cols : rows;
+        const int64_t outer = order == AMLT_ROW_MAJOR ? rows : cols;
+        // leading dimension padded to 16 bytes: TMA-staged (aligned) variants apply
+        const int64_t vn = 16 / es;
+        const int64_t ld = std::max<int64_t>((inner + vn - 1) / vn * vn, vn);
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, size_t(std::max<int64_t>(outer, 1)) * size_t(ld) * es),
+                   "cudaMalloc(matrix)");
+        out->data = p;
+        out->rows = rows;
+        out->cols = cols;
+        out->ld = ld;
+        out->order = order;
+        out->dtype = dtype;
+    });
+}
+
+amlt_status amlt_gpu_matrix_free(amlt_ctx* ctx, amlt_matrix* m) {
+    if (!ctx || !m) return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (m->data) {
+            cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+            cuda_check(cudaFree(m->data), "cudaFree(matrix)");
+        }
+        m->data = nullptr;
+    });
+}
+
+amlt_status amlt_gpu_matrix_upload(amlt_ctx* ctx, const amlt_matrix* dev, const double* host,
+                                   int64_t host_ld) {
+    if (!ctx || !dev || !dev->data || (!host && dev->rows * dev->cols > 0))
+        return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const int64_t inner = dev->order == AMLT_ROW_MAJOR ? dev->cols : dev->rows;
+        const int64_t outer = dev->order == AMLT_ROW_MAJOR ? dev->rows : dev->cols;
+        if (host_ld < inner) fail(AMLT_ERR_INVALID_ARGUMENT, "host leading dimension too small");
+        if (inner == 0 || outer == 0) return;
+        const int es = dtype_size(dev->dtype);
+        std::vector<unsigned char> stage(size_t(outer) * size_t(dev->ld) * es, 0);
+        for (int64_t o = 0; o < outer; ++o)
+            convert_rows(host + o * host_ld, stage.data() + size_t(o) * size_t(dev->ld) * es, inner,
+                         dev->dtype);
+        cuda_check(cudaMemcpyAsync(dev->data, stage.data(), stage.size(), cudaMemcpyHostToDevice,
+                                   ctx->stream),
+                   "cudaMemcpyAsync H2D");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+    });
+}
+
+amlt_status amlt_gpu_matrix_download(amlt_ctx* ctx, const amlt_matrix* dev, double* host,
+                                     int64_t host_ld) {
+    if (!ctx || !dev || !dev->data || (!host && dev->rows * dev->cols > 0))
+        return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        const int64_t inner = dev->order == AMLT_ROW_MAJOR ? dev->cols : dev->rows;
+        const int64_t outer = dev->order == AMLT_ROW_MAJOR ? dev->rows : dev->cols;
+        if (host_ld < inner) fail(AMLT_ERR_INVALID_ARGUMENT, "host leading dimension too small");
+        if (inner == 0 || outer == 0) return;
+        const int es = dtype_size(dev->dtype);
+        std::vector<unsigned char> stage(size_t(outer) * size_t(dev->ld) * es);
+        cuda_check(cudaMemcpyAsync(stage.data(), dev->data, stage.size(), cudaMemcpyDeviceToHost,
+                                   ctx->stream),
+                   "cudaMemcpyAsync D2H");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+        for (int64_t o = 0; o < outer; ++o)
+            widen_rows(stage.data() + size_t(o) * size_t(dev->ld) * es, host + o * host_ld, inner,
+                       dev->dtype);
+    });
+}
+
 amlt_status amlt_spr(int64_t M, int64_t K, int64_t N, double seconds, double* out) {
     if (!out) return AMLT_ERR_INVALID_ARGUMENT;
     if (!(seconds > 0.0)) return AMLT_ERR_NON_POSITIVE_TIME;

@@ -440,3 +440,50 @@ def test_config4_full_size_sampled_rows(gpu_ctx):
     Bh, th, dh = B[:, cdx].cpu().numpy(), t[cdx].cpu().numpy(), d[cdx].cpu().numpy()
     want = oracle("discount", Ah, Bh, th, dh)  # rows x sampled columns: exact oracle entries
     check("discount", "f64", got, want, what="config 4 sampled rows x columns")
+
+
+@pytest.mark.parametrize("dtype,order", [("f64", 0), ("f32", 1), ("i32", 0)])
+def test_device_matrix_alloc_upload_download(gpu_ctx, dtype, order):
+    """amlt_gpu_matrix_*: the library's own device matrices (f64 host values
+    in, the plan's dtype on the device, f64 out), padded to 16 bytes, usable
+    as operands."""
+    import ctypes as C
+
+    import paper_2305_08872_b200 as P
+    from paper_2305_08872_b200 import _native as N
+
+    L = N.lib()
+    dt = {"f64": N.F64, "f32": N.F32, "i32": N.I32}[dtype]
+    body = "eqcount" if dtype == "i32" else "gemm"
+    M, K, N_ = 37, 29, 45
+    A, B, _, _ = make_inputs(body, M, K, N_, "int", seed=71)
+
+    def dev(x, order):
+        m = N.Matrix()
+        r, c = x.shape
+        assert L.amlt_gpu_matrix_alloc(gpu_ctx.handle, r, c, order, dt, C.byref(m)) == N.OK
+        assert m.ld * (8 if dt == N.F64 else 4) % 16 == 0
+        host = np.ascontiguousarray(x if order == 0 else x.T)
+        assert L.amlt_gpu_matrix_upload(gpu_ctx.handle, C.byref(m), host.ctypes.data,
+                                        host.shape[1]) == N.OK
+        return m, host
+
+    ma, _ = dev(A, order)
+    mb, _ = dev(B, 0)
+    mr, _ = dev(np.zeros((M, N_)), 0)
+    plan = gpu_ctx.plan(body, dtype)
+    ops = N.OperandsC(ma, mb, mr, N.Matrix(), N.Matrix(), 0)
+    b = N.BoundsC(0, M, 0, N_, 0, K)
+    tp = N.TileParamsC(0, 0, 0, -1)
+    el = C.c_double()
+    assert L.amlt_gpu_run_subtask(gpu_ctx.handle, plan.handle, C.byref(ops), C.byref(tp),
+                                  C.byref(b), N.CLOCK_FN(), None, None, C.byref(el)) == N.OK
+    out = np.empty((M, N_))
+    assert L.amlt_gpu_matrix_download(gpu_ctx.handle, C.byref(mr), out.ctypes.data, N_) == N.OK
+    want = oracle(body, A, B)
+    check(body, dtype, out, want, exact=True, what="device matrices")
+    back = np.empty_like(A if order == 0 else A.T)
+    L.amlt_gpu_matrix_download(gpu_ctx.handle, C.byref(ma), back.ctypes.data, back.shape[1])
+    assert np.array_equal(back, A if order == 0 else A.T)
+    for m in (ma, mb, mr):
+        assert L.amlt_gpu_matrix_free(gpu_ctx.handle, C.byref(m)) == N.OK and not m.data
