@@ -482,7 +482,7 @@ def test_device_matrix_alloc_upload_download(gpu_ctx, dtype, order):
     assert L.amlt_gpu_matrix_download(gpu_ctx.handle, C.byref(mr), out.ctypes.data, N_) == N.OK
     want = oracle(body, A, B)
     check(body, dtype, out, want, exact=True, what="device matrices")
-    back = np.empty_like(A if order == 0 else A.T)
+    back = np.empty((A if order == 0 else A.T).shape)  # C-ordered storage rows
     L.amlt_gpu_matrix_download(gpu_ctx.handle, C.byref(ma), back.ctypes.data, back.shape[1])
     assert np.array_equal(back, A if order == 0 else A.T)
     for m in (ma, mb, mr):
