@@ -198,3 +198,29 @@ def test_operand_files_override_generated_data(capsys, tmp_path):
     assert j["task"] == "matmul" and j["verify"] == "exact"
     code, _, err = run_cli(capsys, f"run --preset matmul --dims 9 9 9 --a-file {pa}")
     assert code == 2 and "9x9" in err
+
+
+GENERIC = ("where(i in [0..M] and j in [0..N] and k in [0..K]) {\n"
+           "  R[i][j] += A[k][i]*B[k][j] + u[i]*v[j] - (A[k][i] > s)*W[i][j]/4;\n}\n")
+
+
+def test_explain_a_generated_body(capsys, tmp_path):
+    p = tmp_path / "g.task"
+    p.write_text(GENERIC)
+    code, out, _ = run_cli(capsys, f"explain --task {p} --dims 64 32 48")
+    assert code == 0
+    assert "body: generated" in out and "aux={u [i], v [j], s constant, W [i][j]}" in out
+    assert "term: sub_rn(add_rn(mul_rn(a, b), mul_rn(c.v[0], c.v[1]))" in out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("extra", ["", "--mode naive", "--layout-a col --data real",
+                                   "--dtype f32"])
+def test_run_a_generated_body_verified(capsys, tmp_path, extra):
+    p = tmp_path / "g.task"
+    p.write_text(GENERIC)
+    code, out, err = run_cli(capsys, f"run --task {p} --dims 70 33 90 --verify --format json "
+                                     f"--trials 1 {extra}")
+    j = json.loads(out)
+    assert code == 0, err
+    assert j["verify"] in (("exact", "pass") if "real" in extra else ("exact",)), out
