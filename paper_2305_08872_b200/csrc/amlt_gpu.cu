@@ -108,6 +108,8 @@ struct amlt_ctx {
     size_t pack_bytes = 0;
     void* scratch = nullptr;  // scratch R for whole-task tuning trials
     size_t scratch_bytes = 0;
+    void* tc_ws = nullptr;    // split operands of the tcgen05 3xTF32 GEMM
+    size_t tc_ws_bytes = 0;
     // device staging for amlt_gpu_run_host
     // slots: A, B, R, thres, dis, then the aux leaves of generated bodies
     void* hbuf[5 + AMLT_MAX_AUX] = {};
@@ -490,7 +492,8 @@ Dispatch plan_dispatch(const amlt_ctx* ctx, const amlt_plan* plan, const amlt_ti
     Dispatch dp;
     dp.variant = choose_variant(ctx, plan, tile, rv);
     dp.kslice = rv.K;
-    if (tile && tile->kc > 0 && tile->kc < rv.K) {
+    if (tile && tile->kc > 0 && tile->kc < rv.K && !vdesc(dp.variant).run) {
+        // (variants with their own staging run the whole K range)
         // Segment starts stay multiples of 32 elements so every segment's
         // operand rows keep the 16-byte alignment the staged copies need.
         const int64_t kc = (tile->kc + 31) / 32 * 32;
@@ -562,6 +565,18 @@ void enqueue_compute(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const D
         return;
     }
     const VariantDesc& v = vdesc(dp.variant);
+    if (v.run) {  // own staging (tcgen05 3xTF32 GEMM): operand pre-pass + tensor-core GEMM
+        const size_t need = v.ws_bytes(kp);
+        if (need > ctx->tc_ws_bytes) {
+            if (ctx->tc_ws) cudaFree(ctx->tc_ws);
+            ctx->tc_ws = nullptr;
+            ctx->tc_ws_bytes = 0;
+            cuda_check(cudaMalloc(&ctx->tc_ws, need), "cudaMalloc(tensor-core operand workspace)");
+            ctx->tc_ws_bytes = need;
+        }
+        cuda_check(v.run(kp, ctx->tc_ws, ctx->stream), "tensor-core GEMM launch");
+        return;
+    }
     kp.tiles_m = static_cast<int32_t>((rv.M + v.bm - 1) / v.bm);
     kp.tiles_n = static_cast<int32_t>((rv.N + v.bn - 1) / v.bn);
     kp.group_m = std::min(64, std::max(8, 512 / v.bm));
@@ -669,6 +684,7 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
     const size_t bytes = size_t(whole.M) * size_t(whole.N) * dtype_size(plan->desc.dtype);
     if (bytes > ctx->scratch_bytes) {
         if (ctx->scratch) cudaFree(ctx->scratch);
+        if (ctx->tc_ws) cudaFree(ctx->tc_ws);
         ctx->scratch = nullptr;
         ctx->scratch_bytes = 0;
         cuda_check(cudaMalloc(&ctx->scratch, bytes), "cudaMalloc(tuning scratch)");

@@ -35,6 +35,10 @@ struct VariantDesc {
     const char* name = "";
     const void* func = nullptr;
     TileLaunchFn launch = nullptr;
+    // Variants with their own staging (tcgen05 3xTF32 GEMM): the whole
+    // subtask is run(), with ws_bytes() of context workspace.
+    size_t (*ws_bytes)(const KParams&) = nullptr;
+    cudaError_t (*run)(const KParams&, void* ws, cudaStream_t) = nullptr;
 };
 
 // Per (body, dtype) helpers that are not tile variants.
