@@ -263,6 +263,17 @@ def cpu_threads():
 # main
 
 
+def tensor_tf32_peak() -> float:
+    """Dense TF32 tensor-core TFLOP/s: the driver-measured dense bf16 figure
+    (MEASURED_PEAKS.json, burst) halved (TF32 runs at half the bf16 rate on
+    B200); the B200_PROFILING.md fallback (2250 bf16) when absent."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"]) / 2.0
+    except Exception:  # noqa: BLE001
+        return 2250.0 / 2.0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -405,6 +416,13 @@ def main():
     value = 2 * iters_total / el / 1e9
     kernel_s = sum(per_launch) / len(per_launch)
     achieved_tflops = 2 * rows * K * N / kernel_s / 1e12
+    win_name = plan.variants()[win.variant].name if win.variant is not None and win.variant >= 0 else ""
+    tensor_tf32 = "tcgen05_3xtf32" in win_name
+    if tensor_tf32:
+        # the winner runs on the tcgen05 tensor cores: 3 TF32 MMAs per
+        # product (3xTF32); TF32 dense is half the bf16 rate, so the
+        # effective ceiling is measured bf16 / 2 / 3 (MEASURED_PEAKS.json)
+        peak_tflops, pipe = tensor_tf32_peak() / 3.0, "tcgen05.kind::tf32 (3xTF32)"
 
     # ---- e2e leg: host buffers through the C-ABI host entry
     e2e = None
@@ -473,7 +491,8 @@ def main():
                                   else "planner default"),
                        "tuning_trials": [(variants[t.value].name, round(t.score * 1e6, 4))
                                          for t in tuned.trials] if tuned else []},
-            "roofline": {"bound": "fp64" if dtype == "f64" else ("fp32" if dtype == "f32" else "int32"),
+            "roofline": {"bound": "tensor" if tensor_tf32 else
+                         ("fp64" if dtype == "f64" else ("fp32" if dtype == "f32" else "int32")),
                          "pipe": pipe, "achieved": achieved_tflops, "peak": peak_tflops,
                          "unit": "TFLOP/s", "frac": achieved_tflops / peak_tflops,
                          "traffic": traffic_for(args.workload,
@@ -482,6 +501,10 @@ def main():
                                          "capture profiles/*/traffic.json)",
                          "algorithmic_bytes": algorithmic_bytes(body, dtype, M, K, N),
                          "accounting": (
+                             "2 flops per inner iteration (matmul-like); the tile runs 3 TF32 "
+                             "tensor-core products per iteration (3xTF32), peak = measured dense "
+                             "bf16 (MEASURED_PEAKS.json) / 2 (TF32 rate) / 3"
+                             if tensor_tf32 else
                              "2 ops per inner iteration (matmul-like); peak = the SM issue rate "
                              f"(128 lane-instructions/clk/SM) at the probe's {peak_ghz:.3f} GHz; the "
                              "body issues exactly 2 instructions per iteration"
@@ -489,7 +512,7 @@ def main():
                              "2 flops per inner iteration (matmul-like); peak = measured "
                              f"{pipe} probe x2 on this GPU at {peak_ghz:.3f} GHz"),
                          "body_pipe_ops_per_iter": ops_per_iter,
-                         "frac_of_body_ceiling": achieved_tflops / peak_tflops * ops_per_iter,
+                         "frac_of_body_ceiling": achieved_tflops / peak_tflops * (1 if tensor_tf32 else ops_per_iter),
                          "kernel_ms": kernel_s * 1e3},
             "cpu_baseline": cpu,
             "e2e": e2e,

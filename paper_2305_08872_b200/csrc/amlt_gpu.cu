@@ -507,6 +507,19 @@ Dispatch plan_dispatch(const amlt_ctx* ctx, const amlt_plan* plan, const amlt_ti
 void enqueue_compute(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch& dp,
                      KParams kp);
 
+// Workspace of the variants with their own staging, sized before any timed
+// region (an allocation inside it would be charged to the trial).
+void ensure_tc_ws(amlt_ctx* ctx, const VariantDesc& v, const KParams& kp) {
+    if (!v.ws_bytes || ctx->dry()) return;
+    const size_t need = v.ws_bytes(kp);
+    if (need <= ctx->tc_ws_bytes) return;
+    if (ctx->tc_ws) cudaFree(ctx->tc_ws);
+    ctx->tc_ws = nullptr;
+    ctx->tc_ws_bytes = 0;
+    cuda_check(cudaMalloc(&ctx->tc_ws, need), "cudaMalloc(tensor-core operand workspace)");
+    ctx->tc_ws_bytes = need;
+}
+
 void enqueue(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch& dp) {
     if (rv.M == 0 || rv.N == 0) return;
     if (rv.K == 0) return;  // empty k range: R untouched
@@ -555,6 +568,12 @@ void enqueue(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch&
 
 void enqueue_compute(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch& dp,
                      KParams kp) {
+    {
+        const cudaError_t pend = cudaPeekAtLastError();
+        if (pend != cudaSuccess)
+            fail(AMLT_ERR_CUDA, std::string("stale CUDA error from an earlier call: ") +
+                                    cudaGetErrorString(pend));
+    }
     if (!plan->desc.accumulate) {
         // "=": only the last k term reaches R.
         const int64_t total = rv.M * rv.N;
@@ -566,14 +585,7 @@ void enqueue_compute(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const D
     }
     const VariantDesc& v = vdesc(dp.variant);
     if (v.run) {  // own staging (tcgen05 3xTF32 GEMM): operand pre-pass + tensor-core GEMM
-        const size_t need = v.ws_bytes(kp);
-        if (need > ctx->tc_ws_bytes) {
-            if (ctx->tc_ws) cudaFree(ctx->tc_ws);
-            ctx->tc_ws = nullptr;
-            ctx->tc_ws_bytes = 0;
-            cuda_check(cudaMalloc(&ctx->tc_ws, need), "cudaMalloc(tensor-core operand workspace)");
-            ctx->tc_ws_bytes = need;
-        }
+        ensure_tc_ws(ctx, v, kp);
         cuda_check(v.run(kp, ctx->tc_ws, ctx->stream), "tensor-core GEMM launch");
         return;
     }
@@ -631,6 +643,7 @@ void log_dispatch(amlt_exec_log* log, const amlt_plan* plan, const Dispatch& dp,
 double timed_subtask(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch& dp,
                      const amlt_bounds& b, amlt_clock_fn clock, void* user, amlt_exec_log* log) {
     double el = 0.0;
+    if (!ctx->dry() && rv.M > 0 && rv.N > 0 && rv.K > 0) ensure_tc_ws(ctx, vdesc(dp.variant), rv.kp);
     if (clock) {
         const double t0 = clock(user);
         enqueue(ctx, plan, rv, dp);
@@ -684,7 +697,6 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
     const size_t bytes = size_t(whole.M) * size_t(whole.N) * dtype_size(plan->desc.dtype);
     if (bytes > ctx->scratch_bytes) {
         if (ctx->scratch) cudaFree(ctx->scratch);
-        if (ctx->tc_ws) cudaFree(ctx->tc_ws);
         ctx->scratch = nullptr;
         ctx->scratch_bytes = 0;
         cuda_check(cudaMalloc(&ctx->scratch, bytes), "cudaMalloc(tuning scratch)");
@@ -720,6 +732,7 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
     for (const Cand& c : trials) {
         amlt_tile_params tp{c.kc, 0, 0, plan_local_index(plan, c.variant)};
         Dispatch dp = plan_dispatch(ctx, plan, &tp, rs);
+        ensure_tc_ws(ctx, vdesc(dp.variant), rs.kp);
         cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
         enqueue(ctx, plan, rs, dp);
         cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
@@ -994,6 +1007,13 @@ template <class F>
 amlt_status guarded(amlt_ctx* ctx, F&& f) {
     try {
         f();
+        if (ctx && !ctx->dry()) {
+            // no CUDA error may outlive the call that caused it
+            const cudaError_t pend = cudaPeekAtLastError();
+            if (pend != cudaSuccess)
+                throw EngineError(AMLT_ERR_CUDA, std::string("CUDA error left by this call: ") +
+                                                     cudaGetErrorString(pend));
+        }
         if (ctx) ctx->err.clear();
         return AMLT_OK;
     } catch (const EngineError& e) {
@@ -1092,6 +1112,7 @@ void amlt_gpu_ctx_destroy(amlt_ctx* ctx) {
         if (ctx->work) cudaFree(ctx->work);
         if (ctx->pack_ws) cudaFree(ctx->pack_ws);
         if (ctx->scratch) cudaFree(ctx->scratch);
+        if (ctx->tc_ws) cudaFree(ctx->tc_ws);
         for (void* p : ctx->hbuf)
             if (p) cudaFree(p);
         if (ctx->ev0) cudaEventDestroy(ctx->ev0);
