@@ -388,18 +388,22 @@ def main():
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
     # timed steps: the tuned winner, enqueued back to back on the stream (one
-    # tile launch per step, plus the ordered split-K reduction if split)
+    # tile launch per step, plus the ordered split-K reduction if split; the
+    # tensor-core f32 GEMM is two operand-split launches plus the GEMM)
     last = reports[-1] if reports else None
     win = P.TileParams(kc=last.best_kc if last and last.best_kc < K else 0,
                        variant=last.best_variant if last else -1)
     split = bool(last and last.best_kc < K)
+    win_is_tc = last is not None and last.best_variant >= 0 and \
+        "tcgen05_3xtf32" in plan.variants()[last.best_variant].name
     for s in range(steps):
         if flush:
             flush_buf.zero_()  # evict L2 (outside the step's events)
         ev[s][0].record(stream)
         P.enqueue(plan, ops, win, bounds)
         ev[s][1].record(stream)
-        launches += 2 if split else 1
+        # tcgen05 3xTF32: operand split of A, of B, then the tensor-core GEMM
+        launches += 3 if win_is_tc else (2 if split else 1)
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
