@@ -71,9 +71,12 @@ struct TcParams {
 };
 
 __device__ __forceinline__ float tf32_round(float x) {
-    // round to 11 significant bits (nearest, ties away from zero); finite x
-    const uint32_t u = (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
-    return __uint_as_float(u);
+    // round to 11 significant bits (nearest, ties away from zero); a finite x
+    // that would round up to infinity is truncated instead, inf / nan pass
+    const uint32_t u = __float_as_uint(x);
+    uint32_t r = (u + 0x1000u) & 0xFFFFE000u;
+    if ((r & 0x7F800000u) == 0x7F800000u && (u & 0x7F800000u) != 0x7F800000u) r = u & 0xFFFFE000u;
+    return __uint_as_float(r);
 }
 
 // A' row i = [hi(A[i][:]) | hi(A[i][:]) | lo(A[i][:])]
