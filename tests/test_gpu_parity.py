@@ -487,3 +487,46 @@ def test_device_matrix_alloc_upload_download(gpu_ctx, dtype, order):
     assert np.array_equal(back, A if order == 0 else A.T)
     for m in (ma, mb, mr):
         assert L.amlt_gpu_matrix_free(gpu_ctx.handle, C.byref(m)) == N.OK and not m.data
+
+
+@pytest.mark.parametrize("name", ["gemm_f32_128x256_tcgen05_3xtf32",
+                                  "gemm_f32_128x128_tcgen05_3xtf32_acc4"])
+def test_tcgen05_gemm_edges(gpu_ctx, name):
+    """The tensor-core f32 GEMM forced through: ragged M/N tiles, a
+    sub-rectangle of a larger R (everything outside untouched, R0 accumulated),
+    transposed / col-major operands (packed first), and BASELINE data within
+    1e-5 normwise."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    rng = np.random.default_rng(81)
+    # ragged tiles, accumulate onto R0, sub-rectangle
+    M, K, N = 300, 136, 520
+    A = rng.integers(-8, 9, (M, K)).astype(np.float32)
+    B = rng.integers(-8, 9, (K, N)).astype(np.float32)
+    R0 = rng.integers(-100, 100, (M, N)).astype(np.float32)
+    b = (17, 290, 12, 500, 8, 128)  # i0, i1, j0, j1, k0, k1 (k0, j0 keep 16-byte alignment)
+    want = R0.astype(np.float64).copy()
+    want[b[0]:b[1], b[2]:b[3]] += A[b[0]:b[1], b[4]:b[5]].astype(np.float64) @ \
+        B[b[4]:b[5], b[2]:b[3]].astype(np.float64)
+    for layout_a, layout_b in ((0, 0), (1, 0), (0, 1), (1, 1)):
+        plan = gpu_ctx.plan("gemm", "f32", layout_a=layout_a, layout_b=layout_b)
+        vi = [v.name for v in plan.variants()].index(name)
+        Ab = torch.from_numpy(np.ascontiguousarray(A.T if layout_a else A)).cuda()
+        Bb = torch.from_numpy(np.ascontiguousarray(B.T if layout_b else B)).cuda()
+        R = torch.from_numpy(R0.copy()).cuda()
+        P.run_subtask(plan, P.Operands(Ab, Bb, R), P.TileParams(variant=vi), P.Bounds(*b))
+        assert np.array_equal(R.cpu().numpy().astype(np.float64), want), (name, layout_a, layout_b)
+    # BASELINE distribution (N(0,1)), normwise against the fp64 oracle
+    M, K, N = 512, 2048, 768
+    A = rng.standard_normal((M, K)).astype(np.float32)
+    B = rng.standard_normal((K, N)).astype(np.float32)
+    plan = gpu_ctx.plan("gemm", "f32")
+    vi = [v.name for v in plan.variants()].index(name)
+    R = torch.zeros((M, N), dtype=torch.float32, device="cuda")
+    P.run_subtask(plan, P.Operands(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), R),
+                  P.TileParams(variant=vi), P.Bounds(0, M, 0, N, 0, K))
+    want = A.astype(np.float64) @ B.astype(np.float64)
+    check("gemm", "f32", R.cpu().numpy(), want, A=A.astype(np.float64), B=B.astype(np.float64),
+          what=name)
