@@ -75,6 +75,7 @@ Registry& registry_storage() {
 const Registry& registry() { return registry_storage(); }
 
 const BodyAux* find_aux(int body, int dtype) {
+    std::lock_guard<std::mutex> lock(amltk::registry_mutex());
     for (const auto& a : registry().aux)
         if (a.body == body && a.dtype == dtype) return &a;
     return nullptr;
@@ -341,7 +342,12 @@ Resolved resolve(const amlt_plan* plan, const amlt_operands* ops, const amlt_bou
 // ---------------------------------------------------------------------------
 // variant choice
 
-const VariantDesc& vdesc(int idx) { return registry().variants.at(static_cast<size_t>(idx)); }
+// Registry reads take the registry lock: run-time compiled bodies append
+// entries from other threads (entries never move, so the reference stays valid).
+const VariantDesc& vdesc(int idx) {
+    std::lock_guard<std::mutex> lock(registry_mutex());
+    return registry().variants.at(static_cast<size_t>(idx));
+}
 
 // Resident CTAs per SM of a registry variant on this context; computed on
 // first use for variants added after the context was created (run-time
@@ -1047,6 +1053,7 @@ amlt_status amlt_gpu_ctx_create(int device, int flags, amlt_ctx** out) {
     ctx->device = device;
     ctx->flags = flags;
     const auto& reg = registry();
+    std::lock_guard<std::mutex> reg_lock(registry_mutex());  // a consistent snapshot of the registry
     amlt_status st = guarded(nullptr, [&] {
         if (ctx->dry()) {
             ctx->occupancy.assign(reg.variants.size(), 0);
@@ -1165,6 +1172,7 @@ amlt_status amlt_gpu_plan_create(amlt_ctx* ctx, const amlt_body_desc* desc, amlt
             fail(AMLT_ERR_UNSUPPORTED, std::string("no GPU kernel for body ") + body_name(d.body) +
                                            " in " + dtype_name(d.dtype));
         const auto& reg = registry();
+        std::lock_guard<std::mutex> reg_lock(registry_mutex());
         for (size_t i = 0; i < reg.variants.size(); ++i)
             if (reg.variants[i].body == d.body && reg.variants[i].dtype == d.dtype &&
                 reg.variants[i].tout == tout)
