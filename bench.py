@@ -283,6 +283,8 @@ def main():
     ap.add_argument("--workload", default="cfg4_discount_f64", choices=sorted(WORKLOADS))
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--f64-emulation", action="store_true",
+                    help="let the tuner use the int8-tensor-core f64 GEMM (AMLT_CTX_F64_EMULATION)")
     args = ap.parse_args()
     ws, rank, lrank = dist_env()
     body, dtype, M, K, N = WORKLOADS[args.workload]
@@ -326,7 +328,7 @@ def main():
     row0, row1 = row_band(M, ws, rank, align=64)
     rows = row1 - row0
 
-    ctx = P.Context(lrank)
+    ctx = P.Context(lrank, f64_emulation=args.f64_emulation)
     # one explicit (non-default) stream for torch and the kernels alike, so the
     # CUDA events below bracket exactly the launches
     stream = torch.cuda.Stream(device)
@@ -396,6 +398,8 @@ def main():
     split = bool(last and last.best_kc < K)
     win_is_tc = last is not None and last.best_variant >= 0 and \
         "tcgen05_3xtf32" in plan.variants()[last.best_variant].name
+    win_is_oz = last is not None and last.best_variant >= 0 and \
+        "ozaki" in plan.variants()[last.best_variant].name
     for s in range(steps):
         if flush:
             flush_buf.zero_()  # evict L2 (outside the step's events)
@@ -403,7 +407,8 @@ def main():
         P.enqueue(plan, ops, win, bounds)
         ev[s][1].record(stream)
         # tcgen05 3xTF32: operand split of A, of B, then the tensor-core GEMM
-        launches += 3 if win_is_tc else (2 if split else 1)
+        # Ozaki: row / column exponents, A / B slicing, then the int8 GEMM
+        launches += 3 if win_is_tc else (5 if win_is_oz else (2 if split else 1))
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -422,7 +427,13 @@ def main():
     achieved_tflops = 2 * rows * K * N / kernel_s / 1e12
     win_name = plan.variants()[win.variant].name if win.variant is not None and win.variant >= 0 else ""
     tensor_tf32 = "tcgen05_3xtf32" in win_name
-    if tensor_tf32:
+    ozaki = "ozaki" in win_name
+    if ozaki:
+        # int8 tensor cores, 28 slice GEMMs per f64 GEMM (7 slices, diagonals
+        # 2..8); int8 dense = 2 x bf16 dense on B200
+        peak_tflops, pipe = tensor_tf32_peak() * 4.0 / 28.0, "tcgen05.kind::i8 (Ozaki, 28 slice GEMMs)"
+        tensor_tf32 = True
+    elif tensor_tf32:
         # the winner runs on the tcgen05 tensor cores: 3 TF32 MMAs per
         # product (3xTF32); TF32 dense is half the bf16 rate, so the
         # effective ceiling is measured bf16 / 2 / 3 (MEASURED_PEAKS.json)
@@ -505,6 +516,10 @@ def main():
                                          "capture profiles/*/traffic.json)",
                          "algorithmic_bytes": algorithmic_bytes(body, dtype, M, K, N),
                          "accounting": (
+                             "2 flops per inner iteration (matmul-like); 28 int8 tensor-core "
+                             "slice products per iteration (Ozaki, 7 slices), peak = measured dense "
+                             "bf16 (MEASURED_PEAKS.json) x 2 (int8 rate) / 28"
+                             if ozaki else
                              "2 flops per inner iteration (matmul-like); the tile runs 3 TF32 "
                              "tensor-core products per iteration (3xTF32), peak = measured dense "
                              "bf16 (MEASURED_PEAKS.json) / 2 (TF32 rate) / 3"

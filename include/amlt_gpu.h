@@ -251,6 +251,13 @@ typedef struct amlt_plan amlt_plan;
  * logged and "timed" through the clock seam only (tests of the host logic
  * on machines without a GPU). Results are never produced in this mode. */
 #define AMLT_CTX_DRY_RUN 1
+/* F64_EMULATION: lets the tuner choose the f64 GEMM that runs on the int8
+ * tensor cores (Ozaki-style exact slicing, ~2x the fp64 DMMA rate). Its error
+ * is ~1e-14 normwise on BASELINE's data (bound 1e-12) and exact on integer
+ * data, but it scales each row of A / column of B by one power of two, so a
+ * row mixing magnitudes more than ~2^40 apart loses the small ones: opt-in.
+ * Without the flag the variant runs only when named in amlt_tile_params. */
+#define AMLT_CTX_F64_EMULATION 2
 
 int amlt_gpu_abi_version(void);
 

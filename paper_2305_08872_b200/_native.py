@@ -28,6 +28,7 @@ ROW_MAJOR, COL_MAJOR = 0, 1
 LAYOUT_NORMAL, LAYOUT_TRANSPOSED = 0, 1
 LEAF_CONSTANT, LEAF_VEC_I, LEAF_VEC_J, LEAF_MAT_IJ = range(4)
 CTX_DRY_RUN = 1
+CTX_F64_EMULATION = 2
 MAX_TRIALS = 32
 MAX_COVER = 64
 

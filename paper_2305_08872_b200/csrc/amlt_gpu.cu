@@ -774,6 +774,7 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
     std::vector<int> cands;
     for (int idx : plan->variants) {
         const VariantDesc& v = vdesc(idx);
+        if (v.emulated && !(ctx->flags & AMLT_CTX_F64_EMULATION)) continue;  // opt-in only
         if (v.vec == whole.aligned && (!v.tc || whole.aligned)) cands.push_back(idx);
     }
     // Band height per candidate: `waves` full waves of CTAs across all SMs

@@ -1,0 +1,484 @@
+// ozaki_gemm.cu — the plain-GEMM body in f64 on the int8 tensor cores
+// (tcgen05.mma kind::i8), Ozaki-style error-free splitting.
+//
+//   R[i][j] += sum_k A[i][k] * B[k][j]        (preset matmul, presets.cpp:64-65)
+//
+// tcgen05 has no f64 kind, and DMMA shares the FP64 units' throughput with
+// DFMA. The int8 tensor cores are far faster, and integer products are exact:
+//   * every row i of A is scaled by 2^-ea_i (ea_i: the smallest power of two
+//     with |a_ik| < 2^ea_i / 2 for all k) and cut into S signed 7-bit slices,
+//     a_ik = 2^ea_i * sum_p A_p[i][k] 2^-7p with A_p in [-64, 64] (each slice
+//     is the rounded next 7 bits; the remainders are exact in f64); every
+//     column j of B likewise with eb_j;
+//   * a_ik b_kj = 2^(ea_i + eb_j) sum_{p,q} A_p B_q 2^-7(p+q); the products of
+//     one diagonal d = p + q share a scale, so sum_k sum_{p+q=d} A_p B_q is ONE
+//     exact int32 accumulation in TMEM (|.| <= (d-1) K 64^2 < 2^31 for
+//     K <= 65536);
+//   * diagonals d = 2 .. S+1 are kept (S(S+1)/2 slice GEMMs); the dropped ones
+//     are below 2^-7(S+1) relative. The epilogue turns each diagonal into f64,
+//     scales it by 2^-7d exactly and sums, then R += 2^(ea_i+eb_j) * sum.
+// With S = 7 the normwise error is ~1e-15 (BASELINE's bound is 1e-12), and
+// integer-valued inputs (the reference's IntValued data) are exact: one slice
+// holds them and every step is exact.
+//
+// Kernel (one CTA per 128 x 128 tile of R, 320 threads, warp-specialised):
+//   warp 0, one lane   TMA producer over (diagonal, slice pair, k block):
+//                      A_p (128 x 128 int8) and B_q^T (128 x 128 int8) boxes,
+//                      128-byte swizzle, 6-stage full/empty mbarrier ring;
+//   warp 1             allocates 256 TMEM columns (two 128 x 128 int32
+//                      accumulators, one per diagonal in flight); one lane
+//                      issues tcgen05.mma kind::i8 (M=128, N=128, K=32) x 4 per
+//                      stage, commits stages and finished diagonals;
+//   warps 2-9          epilogue: per finished diagonal, tcgen05.ld their 32
+//                      lanes x 64 columns, fold them into f64 registers,
+//                      release the accumulator; finally R += scaled sums.
+#include <cudaTypedefs.h>
+
+#include <math_constants.h>
+
+#include <mutex>
+
+#include "variants.h"
+
+namespace amltk {
+namespace oz {
+
+constexpr int S = 7;                      // slices per operand
+constexpr int BM = 128, BN = 128, BK = 128;  // BK in int8 elements = one 128-byte swizzle row
+constexpr int STAGES = 6;
+constexpr int THREADS = 320;
+constexpr int STAGE_A = BM * BK, STAGE_B = BN * BK;  // bytes
+constexpr int SMEM = STAGES * (STAGE_A + STAGE_B) + 1024 + 256;
+constexpr uint32_t TMEM_COLS = 2 * BN;
+// kind::i8: signed A and B, s32 accumulate, K-major, M = 128, N = 128
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
+                           (uint32_t(BM >> 4) << 24);
+
+struct OzParams {
+    double* R;
+    int64_t ldr;
+    int64_t M, N, K;
+    const int32_t* ea;  // row exponents of A
+    const int32_t* eb;  // column exponents of B
+    int32_t tiles_m, tiles_n, group_m;
+};
+
+// ---- pre-pass: exponents and slices
+
+// A row / column holding inf or nan: its slices are zero and its outputs NaN
+// (IEEE arithmetic would give inf or nan there; integers cannot carry either).
+constexpr int32_t kNonFinite = 0x7fffffff;
+
+// ea_i: smallest e with |a_ik| < 2^(e-1) for all k (so a 2^-e lies in (-1/2, 1/2))
+__global__ void row_exp_kernel(const double* __restrict__ A, int64_t lda, int64_t M, int64_t K,
+                               int32_t* __restrict__ ea) {
+    const int64_t i = blockIdx.x;
+    if (i >= M) return;
+    double m = 0;
+    for (int64_t k = threadIdx.x; k < K; k += blockDim.x) {
+        const double x = fabs(A[i * lda + k]);
+        m = isfinite(x) ? fmax(m, x) : CUDART_INF;  // fmax would drop a nan
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));  // inf survives
+    __shared__ double wm[32];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (blockDim.x + 31) / 32; ++w) m = fmax(m, wm[w]);
+        int e = 0;
+        if (!isfinite(m)) {
+            e = kNonFinite;
+        } else if (m > 0) {
+            frexp(m, &e);  // m = f 2^e, f in [1/2, 1)
+            e += 1;        // m < 2^e / 2
+        }
+        ea[i] = e;
+    }
+}
+
+// eb_j over the columns of B (K x N, row-major): coalesced along j
+__global__ void col_exp_kernel(const double* __restrict__ B, int64_t ldb, int64_t K, int64_t N,
+                               int32_t* __restrict__ eb) {
+    const int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x;
+    if (j >= N) return;
+    double m = 0;
+    bool finite = true;
+    for (int64_t k = 0; k < K; ++k) {
+        const double x = fabs(B[k * ldb + j]);
+        finite = finite && isfinite(x);
+        m = fmax(m, x);
+    }
+    int e = 0;
+    if (!finite) {
+        e = kNonFinite;
+    } else if (m > 0) {
+        frexp(m, &e);
+        e += 1;
+    }
+    eb[j] = e;
+}
+
+__device__ __forceinline__ void slices_of(double x, int8_t (&q)[S]) {
+#pragma unroll
+    for (int p = 0; p < S; ++p) {
+        const double v = x * 128.0;  // exact (power of two)
+        const double r = rint(v);    // |r| <= 64
+        q[p] = static_cast<int8_t>(r);
+        x = v - r;                   // exact, in [-1/2, 1/2]
+    }
+}
+
+// A_p[i][k] (S planes of M x ldk int8, K contiguous)
+__global__ void slice_a_kernel(const double* __restrict__ A, int64_t lda, int64_t M, int64_t K,
+                               const int32_t* __restrict__ ea, int8_t* __restrict__ As, int64_t ldk) {
+    const int64_t total = M * K;
+    const int64_t plane = M * ldk;
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total;
+         idx += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = idx / K, k = idx - i * K;
+        int8_t q[S];
+        slices_of(ea[i] == kNonFinite ? 0.0 : ldexp(A[i * lda + k], -ea[i]), q);
+#pragma unroll
+        for (int p = 0; p < S; ++p) As[p * plane + i * ldk + k] = q[p];
+    }
+}
+
+// B_q^T[j][k] (S planes of N x ldk int8, K contiguous): 32 x 32 smem transpose
+__global__ void slice_bt_kernel(const double* __restrict__ B, int64_t ldb, int64_t K, int64_t N,
+                                const int32_t* __restrict__ eb, int8_t* __restrict__ Bs, int64_t ldk) {
+    __shared__ double tile[32][33];
+    const int64_t k0 = int64_t(blockIdx.y) * 32, j0 = int64_t(blockIdx.x) * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t k = k0 + r, j = j0 + threadIdx.x;
+        tile[r][threadIdx.x] = (k < K && j < N) ? B[k * ldb + j] : 0.0;
+    }
+    __syncthreads();
+    const int64_t plane = N * ldk;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t j = j0 + r, k = k0 + threadIdx.x;
+        if (j < N && k < K) {
+            int8_t q[S];
+            slices_of(eb[j] == kNonFinite ? 0.0 : ldexp(tile[threadIdx.x][r], -eb[j]), q);
+#pragma unroll
+            for (int p = 0; p < S; ++p) Bs[p * plane + j * ldk + k] = q[p];
+        }
+    }
+}
+
+// ---- PTX wrappers
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(b)), "r"(n));
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t done;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(su32(b)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y,
+                                       uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {  // K-major, 128-byte swizzle
+    uint64_t d = 0;
+    d |= uint64_t((addr & 0x3FFFF) >> 4);
+    d |= uint64_t(1) << 16;
+    d |= uint64_t(1024 >> 4) << 32;
+    d |= uint64_t(1) << 46;
+    d |= uint64_t(2) << 61;
+    return d;
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+        "l"(a), "l"(b), "r"(IDESC), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     su32(bar))
+                 : "memory");
+}
+
+// The (diagonal, slice pair) schedule: d = 2 .. S+1, p = 1 .. d-1 (q = d - p).
+constexpr int NDIAG = S;  // diagonals 2 .. S+1
+
+__global__ void __launch_bounds__(THREADS, 1)
+    ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                      const OzParams p) {
+    extern __shared__ unsigned char smem_raw[];
+    unsigned char* base = reinterpret_cast<unsigned char*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    unsigned char* sA = base;
+    unsigned char* sB = base + STAGES * STAGE_A;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * STAGE_B);
+    uint64_t* empty = full + STAGES;
+    uint64_t* acc_full = empty + STAGES;  // [2]
+    uint64_t* acc_empty = acc_full + 2;   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int G = p.group_m, bid = blockIdx.x, per_group = G * p.tiles_n;
+    const int group = bid / per_group, first_m = group * G;
+    const int gsize = min(p.tiles_m - first_m, G), in_group = bid - group * per_group;
+    const int64_t m0 = int64_t(first_m + in_group % gsize) * BM;
+    const int64_t n0 = int64_t(in_group / gsize) * BN;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nkb = static_cast<int>((p.K + BK - 1) / BK);
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            bar_init(&full[s], 1);
+            bar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            bar_init(&acc_full[b], 1);
+            bar_init(&acc_empty[b], 8);  // one arrival per epilogue warp
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         su32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA producer
+            int it = 0;
+            for (int d = 2; d <= S + 1; ++d)
+                for (int sa = 1; sa < d; ++sa) {
+                    const int sb = d - sa;
+                    if (sa > S || sb > S) continue;
+                    const int32_t ya = static_cast<int32_t>((sa - 1) * p.M + m0);
+                    const int32_t yb = static_cast<int32_t>((sb - 1) * p.N + n0);
+                    for (int kb = 0; kb < nkb; ++kb, ++it) {
+                        const int s = it % STAGES;
+                        bar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
+                        bar_expect(&full[s], STAGE_A + STAGE_B);
+                        tma_2d(sA + s * STAGE_A, &tmA, kb * BK, ya, &full[s]);
+                        tma_2d(sB + s * STAGE_B, &tmB, kb * BK, yb, &full[s]);
+                    }
+                }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            int it = 0;
+            for (int d = 2; d <= S + 1; ++d) {
+                const int buf = d & 1, use = (d - 2) >> 1;  // use-th time this buffer is filled
+                bar_wait(&acc_empty[buf], (use & 1) ^ 1);   // the epilogue has drained it
+                fence_after();
+                const uint32_t acc = tmem + uint32_t(buf * BN);
+                bool first = true;
+                for (int sa = 1; sa < d; ++sa) {
+                    const int sb = d - sa;
+                    if (sa > S || sb > S) continue;
+                    for (int kb = 0; kb < nkb; ++kb, ++it) {
+                        const int s = it % STAGES;
+                        bar_wait(&full[s], (it / STAGES) & 1);
+                        fence_after();
+                        const uint32_t a0 = su32(sA + s * STAGE_A), b0 = su32(sB + s * STAGE_B);
+#pragma unroll
+                        for (int k = 0; k < BK / 32; ++k) {
+                            mma_i8(acc, smem_desc(a0 + k * 32), smem_desc(b0 + k * 32), !first);
+                            first = false;
+                        }
+                        mma_commit(&empty[s]);
+                    }
+                }
+                mma_commit(&acc_full[buf]);  // diagonal d complete
+            }
+        }
+    } else {  // epilogue warps 2..9: lane quarter warp % 4, column half (warp - 2) / 4
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        const int64_t row = m0 + 32 * q + lane;
+        double sum[64];
+#pragma unroll
+        for (int c = 0; c < 64; ++c) sum[c] = 0.0;
+        for (int d = 2; d <= S + 1; ++d) {
+            const int buf = d & 1, use = (d - 2) >> 1;
+            bar_wait(&acc_full[buf], use & 1);
+            fence_after();
+            const double scale = ldexp(1.0, -7 * d);
+#pragma unroll
+            for (int c0 = 0; c0 < 64; c0 += 16) {
+                uint32_t v[16];
+                const uint32_t taddr = tmem + (uint32_t(32 * q) << 16) + uint32_t(buf * BN + h * 64 + c0);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
+                    "%10, %11, %12, %13, %14, %15}, [%16];\n"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                      "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                      "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                    sum[c0 + e] = fma(double(static_cast<int32_t>(v[e])), scale, sum[c0 + e]);
+            }
+            fence_before();
+            __syncwarp();
+            if (lane == 0) bar_arrive(&acc_empty[buf]);
+        }
+        if (row < p.M) {
+            const int ei = p.ea[row];
+            double* dst = p.R + row * p.ldr;
+#pragma unroll
+            for (int c = 0; c < 64; ++c) {
+                const int64_t col = n0 + h * 64 + c;
+                if (col < p.N) {
+                    const int32_t ej = p.eb[col];
+                    dst[col] += (ei == kNonFinite || ej == kNonFinite) ? CUDART_NAN
+                                                                        : ldexp(sum[c], ei + ej);
+                }
+            }
+        }
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+// ---- host side
+
+int64_t ldk_of(int64_t K) { return (K + 15) / 16 * 16; }
+
+size_t ws_bytes(const KParams& p) {
+    const int64_t ldk = ldk_of(p.K);
+    const size_t a = (size_t(S) * p.M * ldk + 255) / 256 * 256;
+    const size_t b = (size_t(S) * p.N * ldk + 255) / 256 * 256;
+    return a + b + (size_t(p.M) + size_t(p.N)) * 4 + 512;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+// S planes of rows x K int8 (row pitch ldk) as one (S*rows) x K tensor
+bool encode(CUtensorMap* m, const int8_t* base, int64_t K, int64_t rows_total, int64_t ldk) {
+    auto fn = encoder();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(rows_total)};
+    cuuint64_t strides[1] = {cuuint64_t(ldk)};
+    cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(BM)};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t run(const KParams& p, void* ws, cudaStream_t s) {
+    const int64_t M = p.M, N = p.N, K = p.K, ldk = ldk_of(K);
+    if (K > 65536) return cudaErrorInvalidValue;  // int32 diagonal sums need K <= 65536
+    char* w = static_cast<char*>(ws);
+    int8_t* As = reinterpret_cast<int8_t*>(w);
+    int8_t* Bs = reinterpret_cast<int8_t*>(w + (size_t(S) * M * ldk + 255) / 256 * 256);
+    int32_t* ea = reinterpret_cast<int32_t*>(
+        w + (size_t(S) * M * ldk + 255) / 256 * 256 + (size_t(S) * N * ldk + 255) / 256 * 256);
+    int32_t* eb = ea + M;
+    const double* A = static_cast<const double*>(p.A);
+    const double* B = static_cast<const double*>(p.B);
+    row_exp_kernel<<<static_cast<unsigned>(M), 256, 0, s>>>(A, p.lda, M, K, ea);
+    col_exp_kernel<<<static_cast<unsigned>((N + 255) / 256), 256, 0, s>>>(B, p.ldb, K, N, eb);
+    {
+        const int64_t total = M * K;
+        const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 32));
+        slice_a_kernel<<<blocks, 256, 0, s>>>(A, p.lda, M, K, ea, As, ldk);
+        dim3 g(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>((K + 31) / 32));
+        slice_bt_kernel<<<g, dim3(32, 8), 0, s>>>(B, p.ldb, K, N, eb, Bs, ldk);
+    }
+    CUtensorMap ma, mb;
+    if (!encode(&ma, As, K, int64_t(S) * M, ldk) || !encode(&mb, Bs, K, int64_t(S) * N, ldk))
+        return cudaErrorInvalidValue;
+    OzParams op;
+    op.R = static_cast<double*>(p.R);
+    op.ldr = p.ldr;
+    op.M = M;
+    op.N = N;
+    op.K = K;
+    op.ea = ea;
+    op.eb = eb;
+    op.tiles_m = static_cast<int32_t>((M + BM - 1) / BM);
+    op.tiles_n = static_cast<int32_t>((N + BN - 1) / BN);
+    op.group_m = 8;
+    const int64_t tiles = int64_t(op.tiles_m) * op.tiles_n;
+    ozaki_gemm_kernel<<<static_cast<unsigned>(tiles), THREADS, SMEM, s>>>(ma, mb, op);
+    return cudaGetLastError();
+}
+
+cudaError_t no_tile_launch(const KParams&, const CUtensorMap&, const CUtensorMap&, dim3, cudaStream_t) {
+    return cudaErrorNotSupported;  // launched through VariantDesc::run
+}
+
+}  // namespace oz
+
+void register_ozaki_gemm(Registry& reg) {
+    VariantDesc v;
+    v.body = 0;   // AMLT_BODY_GEMM
+    v.dtype = 0;  // AMLT_F64
+    v.bm = oz::BM;
+    v.bn = oz::BN;
+    v.bk = oz::BK;
+    v.tm = oz::BM;
+    v.tn = oz::BN;
+    v.threads = oz::THREADS;
+    v.stages = oz::STAGES;
+    v.smem = oz::SMEM;
+    v.minb = 1;
+    v.vec = true;
+    v.tc = true;
+    v.emulated = true;
+    v.name = "tcgen05_ozaki_i8";
+    v.func = reinterpret_cast<const void*>(&oz::ozaki_gemm_kernel);
+    v.launch = &oz::no_tile_launch;
+    v.ws_bytes = &oz::ws_bytes;
+    v.run = &oz::run;
+    reg.variants.push_back(v);
+}
+
+}  // namespace amltk

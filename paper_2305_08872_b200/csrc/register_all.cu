@@ -13,12 +13,14 @@ namespace amltk {
 AMLT_PAIRS(AMLT_DECL)
 void register_dmma_gemm(Registry&);
 void register_tcgen05_gemm(Registry&);
+void register_ozaki_gemm(Registry&);
 
 void register_all(Registry& reg) {
 #define AMLT_CALL(B, D) register_##B##_##D(reg);
     AMLT_PAIRS(AMLT_CALL)
     register_dmma_gemm(reg);
     register_tcgen05_gemm(reg);
+    register_ozaki_gemm(reg);
 }
 
 }  // namespace amltk

@@ -32,6 +32,7 @@ struct VariantDesc {
     bool vec = true;  // TMA staging (needs 16-byte aligned operands and strides)
     bool tc = false;  // tensor-core (DMMA) variant
     bool tout = false;  // per-output threshold state (T indexed by i or (i, j))
+    bool emulated = false;  // f64 via int8 tensor cores: tuner candidate only on opt-in
     const char* name = "";
     const void* func = nullptr;
     TileLaunchFn launch = nullptr;

@@ -324,12 +324,15 @@ class Operands:
 
 class Context:
     """One B200 device context (amlt_gpu_ctx_create). dry_run=True plans,
-    logs and clocks dispatches without touching a device (host-logic tests)."""
+    logs and clocks dispatches without touching a device (host-logic tests);
+    f64_emulation=True lets the tuner pick the int8-tensor-core f64 GEMM
+    (AMLT_CTX_F64_EMULATION)."""
 
-    def __init__(self, device: int = 0, dry_run: bool = False):
+    def __init__(self, device: int = 0, dry_run: bool = False, f64_emulation: bool = False):
         self._lib = N.lib()
         h = C.c_void_p()
-        st = self._lib.amlt_gpu_ctx_create(device, N.CTX_DRY_RUN if dry_run else 0, C.byref(h))
+        flags = (N.CTX_DRY_RUN if dry_run else 0) | (N.CTX_F64_EMULATION if f64_emulation else 0)
+        st = self._lib.amlt_gpu_ctx_create(device, flags, C.byref(h))
         _raise(st, None)
         self.handle = h
         self.device = device

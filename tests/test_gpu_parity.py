@@ -530,3 +530,69 @@ def test_tcgen05_gemm_edges(gpu_ctx, name):
     want = A.astype(np.float64) @ B.astype(np.float64)
     check("gemm", "f32", R.cpu().numpy(), want, A=A.astype(np.float64), B=B.astype(np.float64),
           what=name)
+
+
+def test_ozaki_f64_gemm_on_int8_tensor_cores():
+    """The f64 GEMM on the int8 tensor cores (Ozaki slicing): exact on integer
+    data (ragged tiles, sub-rectangles, every orientation), <= 1e-12 normwise
+    on N(0,1) data at BASELINE's K, NaN for rows/columns holding inf/nan, and
+    opt-in for the tuner (AMLT_CTX_F64_EMULATION)."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    ctx = P.Context(0)
+    rng = np.random.default_rng(91)
+    name = "gemm_f64_128x128_tcgen05_ozaki_i8"
+    M, K, N = 300, 136, 264
+    A = rng.integers(-8, 9, (M, K)).astype(np.float64)
+    B = rng.integers(-8, 9, (K, N)).astype(np.float64)
+    R0 = rng.integers(-100, 100, (M, N)).astype(np.float64)
+    b = (17, 290, 8, 250, 8, 128)
+    want = R0.copy()
+    want[b[0]:b[1], b[2]:b[3]] += A[b[0]:b[1], b[4]:b[5]] @ B[b[4]:b[5], b[2]:b[3]]
+    for layout_a, layout_b in ((0, 0), (1, 0), (0, 1), (1, 1)):
+        plan = ctx.plan("gemm", "f64", layout_a=layout_a, layout_b=layout_b)
+        vi = [v.name for v in plan.variants()].index(name)
+        R = torch.from_numpy(R0.copy()).cuda()
+        P.run_subtask(plan, P.Operands(torch.from_numpy(np.ascontiguousarray(A.T if layout_a else A)).cuda(),
+                                       torch.from_numpy(np.ascontiguousarray(B.T if layout_b else B)).cuda(), R),
+                      P.TileParams(variant=vi), P.Bounds(*b))
+        assert np.array_equal(R.cpu().numpy(), want), (layout_a, layout_b)
+    # N(0,1) at K = 8192 (BASELINE config 2's depth), normwise vs the fp64 oracle
+    plan = ctx.plan("gemm", "f64")
+    vi = [v.name for v in plan.variants()].index(name)
+    M, K, N = 256, 8192, 384
+    A = rng.standard_normal((M, K))
+    B = rng.standard_normal((K, N))
+    R = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+    P.run_subtask(plan, P.Operands(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), R),
+                  P.TileParams(variant=vi), P.Bounds(0, M, 0, N, 0, K))
+    check("gemm", "f64", R.cpu().numpy(), oracle("gemm", A, B), A=A, B=B, what="ozaki N(0,1)")
+    # non-finite inputs: the affected row / column becomes NaN, the rest is exact
+    A = rng.integers(-8, 9, (128, 64)).astype(np.float64)
+    B = rng.integers(-8, 9, (64, 128)).astype(np.float64)
+    A[5, 3] = np.inf
+    B[7, 9] = np.nan
+    R = torch.zeros((128, 128), dtype=torch.float64, device="cuda")
+    P.run_subtask(plan, P.Operands(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), R),
+                  P.TileParams(variant=vi), P.Bounds(0, 128, 0, 128, 0, 64))
+    got = R.cpu().numpy()
+    assert np.isnan(got[5]).all() and np.isnan(got[:, 9]).all()
+    mask = np.ones_like(got, dtype=bool)
+    mask[5] = False
+    mask[:, 9] = False
+    ref = np.nan_to_num(A, posinf=0.0) @ np.nan_to_num(B, nan=0.0)
+    assert np.array_equal(got[mask], ref[mask])
+    # opt-in: the default tuner never picks it; with the flag it is a candidate
+    M = K = N = 1024
+    A = torch.randn((M, K), device="cuda", dtype=torch.float64)
+    B = torch.randn((K, N), device="cuda", dtype=torch.float64)
+    R = torch.zeros((M, N), device="cuda", dtype=torch.float64)
+    rep = P.adaptive_execute(plan, P.Operands(A, B, R), P.Bounds(0, M, 0, N, 0, K))
+    assert all(plan.variants()[t.value].name != name for t in rep.trials)
+    ectx = P.Context(0, f64_emulation=True)
+    eplan = ectx.plan("gemm", "f64")
+    R.zero_()
+    rep = P.adaptive_execute(eplan, P.Operands(A, B, R), P.Bounds(0, M, 0, N, 0, K))
+    assert any(eplan.variants()[t.value].name == name for t in rep.trials)
