@@ -780,9 +780,15 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
     // Band height per candidate: `waves` full waves of CTAs across all SMs
     // (4 when the rows allow it, so partial-wave tails weigh little in the
     // score; otherwise 1).
+    // The bands must fit in a quarter of the rows (4-wave, then 1-wave bands);
+    // with many candidates, 1-wave bands may take up to 40% (their rows are
+    // real output, computed by the candidate under trial).
     std::vector<int64_t> band(cands.size());
     int64_t need = 0;
-    for (int waves : {4, 1}) {
+    int64_t cap = whole.M / 4;
+    for (int attempt = 0; attempt < 3; ++attempt) {
+        const int waves = attempt == 0 ? 4 : 1;
+        cap = attempt < 2 ? whole.M / 4 : whole.M * 2 / 5;
         need = 0;
         for (size_t c = 0; c < cands.size(); ++c) {
             const VariantDesc& v = vdesc(cands[c]);
@@ -793,11 +799,10 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
             band[c] = tiles_m * v.bm;
             need += band[c];
         }
-        if (need * 4 <= whole.M) break;
+        if (need <= cap) break;
     }
     const bool tunable = plan->desc.accumulate && !cands.empty() && whole.K > 0 && whole.N > 0 &&
-                         need * 4 <= whole.M &&  // tuning <= 25% of the rows
-                         ctx->tune_cache.find(key) == ctx->tune_cache.end();
+                         need <= cap && ctx->tune_cache.find(key) == ctx->tune_cache.end();
 
     auto run_rect = [&](const amlt_bounds& rb, int variant, int64_t kc) {
         amlt_tile_params tp{kc, 0, 0, plan_local_index(plan, variant)};
