@@ -109,8 +109,17 @@ struct amlt_ctx {
     size_t pack_bytes = 0;
     void* scratch = nullptr;  // scratch R for whole-task tuning trials
     size_t scratch_bytes = 0;
-    void* tc_ws = nullptr;    // split operands of the tcgen05 3xTF32 GEMM
+    void* tc_ws = nullptr;    // split / sliced operands of the tensor-core GEMMs
     size_t tc_ws_bytes = 0;
+    // B's preparation in tc_ws, valid within one C-ABI call (call_gen)
+    uint64_t call_gen = 0;
+    struct BPrep {
+        const void* B = nullptr;
+        int64_t ldb = 0, K = 0, N = 0;
+        int prep = 0;
+        uint64_t gen = ~uint64_t(0);
+        const void* ws = nullptr;
+    } bprep;
     // device staging for amlt_gpu_run_host
     // slots: A, B, R, thres, dis, then the aux leaves of generated bodies
     void* hbuf[5 + AMLT_MAX_AUX] = {};
@@ -522,8 +531,26 @@ void ensure_tc_ws(amlt_ctx* ctx, const VariantDesc& v, const KParams& kp) {
     if (ctx->tc_ws) cudaFree(ctx->tc_ws);
     ctx->tc_ws = nullptr;
     ctx->tc_ws_bytes = 0;
+    ctx->bprep.gen = ~uint64_t(0);
     cuda_check(cudaMalloc(&ctx->tc_ws, need), "cudaMalloc(tensor-core operand workspace)");
     ctx->tc_ws_bytes = need;
+}
+
+bool bprep_ready(const amlt_ctx* ctx, const VariantDesc& v, const KParams& kp) {
+    const auto& b = ctx->bprep;
+    return b.gen == ctx->call_gen && b.prep == v.prep_id && b.B == kp.B && b.ldb == kp.ldb &&
+           b.K == kp.K && b.N == kp.N && b.ws == ctx->tc_ws;
+}
+void bprep_mark(amlt_ctx* ctx, const VariantDesc& v, const KParams& kp) {
+    ctx->bprep = amlt_ctx::BPrep{kp.B, kp.ldb, kp.K, kp.N, v.prep_id, ctx->call_gen, ctx->tc_ws};
+}
+// B's preparation ahead of a timed trial, so trials measure the per-band work
+void prep_b_untimed(amlt_ctx* ctx, const VariantDesc& v, const KParams& kp) {
+    if (!v.prep_b || ctx->dry()) return;
+    ensure_tc_ws(ctx, v, kp);
+    if (bprep_ready(ctx, v, kp)) return;
+    cuda_check(v.prep_b(kp, ctx->tc_ws, ctx->stream), "tensor-core operand preparation");
+    bprep_mark(ctx, v, kp);
 }
 
 void enqueue(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch& dp) {
@@ -592,7 +619,8 @@ void enqueue_compute(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const D
     const VariantDesc& v = vdesc(dp.variant);
     if (v.run) {  // own staging (tcgen05 3xTF32 GEMM): operand pre-pass + tensor-core GEMM
         ensure_tc_ws(ctx, v, kp);
-        cuda_check(v.run(kp, ctx->tc_ws, ctx->stream), "tensor-core GEMM launch");
+        cuda_check(v.run(kp, ctx->tc_ws, bprep_ready(ctx, v, kp), ctx->stream), "tensor-core GEMM launch");
+        bprep_mark(ctx, v, kp);
         return;
     }
     kp.tiles_m = static_cast<int32_t>((rv.M + v.bm - 1) / v.bm);
@@ -649,7 +677,8 @@ void log_dispatch(amlt_exec_log* log, const amlt_plan* plan, const Dispatch& dp,
 double timed_subtask(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch& dp,
                      const amlt_bounds& b, amlt_clock_fn clock, void* user, amlt_exec_log* log) {
     double el = 0.0;
-    if (!ctx->dry() && rv.M > 0 && rv.N > 0 && rv.K > 0) ensure_tc_ws(ctx, vdesc(dp.variant), rv.kp);
+    if (!ctx->dry() && rv.M > 0 && rv.N > 0 && rv.K > 0 && !rv.packed())
+        prep_b_untimed(ctx, vdesc(dp.variant), rv.kp);
     if (clock) {
         const double t0 = clock(user);
         enqueue(ctx, plan, rv, dp);
@@ -738,7 +767,8 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
     for (const Cand& c : trials) {
         amlt_tile_params tp{c.kc, 0, 0, plan_local_index(plan, c.variant)};
         Dispatch dp = plan_dispatch(ctx, plan, &tp, rs);
-        ensure_tc_ws(ctx, vdesc(dp.variant), rs.kp);
+        if (!rs.packed()) prep_b_untimed(ctx, vdesc(dp.variant), rs.kp);
+        else ensure_tc_ws(ctx, vdesc(dp.variant), rs.kp);
         cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
         enqueue(ctx, plan, rs, dp);
         cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
@@ -1017,6 +1047,7 @@ struct AmuletTuner {
 
 template <class F>
 amlt_status guarded(amlt_ctx* ctx, F&& f) {
+    if (ctx) ++ctx->call_gen;  // operand preparations do not outlive the call
     try {
         f();
         if (ctx && !ctx->dry()) {

@@ -379,11 +379,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 int64_t ldk_of(int64_t K) { return (K + 15) / 16 * 16; }
 
+// Workspace: the B slices and column exponents first (shared by every row
+// band of one call), then the A slices and row exponents.
+size_t b_bytes(const KParams& p) {
+    return (size_t(S) * p.N * ldk_of(p.K) + 255) / 256 * 256 + (size_t(p.N) * 4 + 255) / 256 * 256;
+}
 size_t ws_bytes(const KParams& p) {
-    const int64_t ldk = ldk_of(p.K);
-    const size_t a = (size_t(S) * p.M * ldk + 255) / 256 * 256;
-    const size_t b = (size_t(S) * p.N * ldk + 255) / 256 * 256;
-    return a + b + (size_t(p.M) + size_t(p.N)) * 4 + 512;
+    return b_bytes(p) + (size_t(S) * p.M * ldk_of(p.K) + 255) / 256 * 256 + size_t(p.M) * 4 + 256;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
@@ -412,25 +414,35 @@ bool encode(CUtensorMap* m, const int8_t* base, int64_t K, int64_t rows_total, i
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-cudaError_t run(const KParams& p, void* ws, cudaStream_t s) {
+cudaError_t prep_b(const KParams& p, void* ws, cudaStream_t s) {
+    const int64_t N = p.N, K = p.K, ldk = ldk_of(K);
+    int8_t* Bs = static_cast<int8_t*>(ws);
+    int32_t* eb = reinterpret_cast<int32_t*>(static_cast<char*>(ws) + (size_t(S) * N * ldk + 255) / 256 * 256);
+    const double* B = static_cast<const double*>(p.B);
+    col_exp_kernel<<<static_cast<unsigned>((N + 255) / 256), 256, 0, s>>>(B, p.ldb, K, N, eb);
+    dim3 g(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>((K + 31) / 32));
+    slice_bt_kernel<<<g, dim3(32, 8), 0, s>>>(B, p.ldb, K, N, eb, Bs, ldk);
+    return cudaGetLastError();
+}
+
+cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
     const int64_t M = p.M, N = p.N, K = p.K, ldk = ldk_of(K);
     if (K > 65536) return cudaErrorInvalidValue;  // int32 diagonal sums need K <= 65536
     char* w = static_cast<char*>(ws);
-    int8_t* As = reinterpret_cast<int8_t*>(w);
-    int8_t* Bs = reinterpret_cast<int8_t*>(w + (size_t(S) * M * ldk + 255) / 256 * 256);
-    int32_t* ea = reinterpret_cast<int32_t*>(
-        w + (size_t(S) * M * ldk + 255) / 256 * 256 + (size_t(S) * N * ldk + 255) / 256 * 256);
-    int32_t* eb = ea + M;
+    int8_t* Bs = reinterpret_cast<int8_t*>(w);
+    int32_t* eb = reinterpret_cast<int32_t*>(w + (size_t(S) * N * ldk + 255) / 256 * 256);
+    int8_t* As = reinterpret_cast<int8_t*>(w + b_bytes(p));
+    int32_t* ea = reinterpret_cast<int32_t*>(w + b_bytes(p) + (size_t(S) * M * ldk + 255) / 256 * 256);
     const double* A = static_cast<const double*>(p.A);
-    const double* B = static_cast<const double*>(p.B);
+    if (!b_ready) {
+        const cudaError_t e = prep_b(p, ws, s);
+        if (e != cudaSuccess) return e;
+    }
     row_exp_kernel<<<static_cast<unsigned>(M), 256, 0, s>>>(A, p.lda, M, K, ea);
-    col_exp_kernel<<<static_cast<unsigned>((N + 255) / 256), 256, 0, s>>>(B, p.ldb, K, N, eb);
     {
         const int64_t total = M * K;
         const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 32));
         slice_a_kernel<<<blocks, 256, 0, s>>>(A, p.lda, M, K, ea, As, ldk);
-        dim3 g(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>((K + 31) / 32));
-        slice_bt_kernel<<<g, dim3(32, 8), 0, s>>>(B, p.ldb, K, N, eb, Bs, ldk);
     }
     CUtensorMap ma, mb;
     if (!encode(&ma, As, K, int64_t(S) * M, ldk) || !encode(&mb, Bs, K, int64_t(S) * N, ldk))
@@ -478,6 +490,8 @@ void register_ozaki_gemm(Registry& reg) {
     v.launch = &oz::no_tile_launch;
     v.ws_bytes = &oz::ws_bytes;
     v.run = &oz::run;
+    v.prep_b = &oz::prep_b;
+    v.prep_id = 2;  // int8 slices of B
     reg.variants.push_back(v);
 }
 

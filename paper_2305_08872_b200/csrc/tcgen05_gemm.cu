@@ -313,11 +313,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 int64_t ld3_of(int64_t K) { return (3 * K + 3) / 4 * 4; }  // 16-byte row pitch (TMA)
 
-size_t ws_bytes(const KParams& p) {
-    const int64_t ld3 = ld3_of(p.K);
-    const size_t a = (size_t(p.M) * ld3 * 4 + 255) / 256 * 256;
-    return a + size_t(p.N) * ld3 * 4 + 256;
-}
+// Workspace: B'^T first (the part shared by every row band of one call),
+// then A'.
+size_t b_bytes(const KParams& p) { return (size_t(p.N) * ld3_of(p.K) * 4 + 255) / 256 * 256; }
+size_t ws_bytes(const KParams& p) { return b_bytes(p) + size_t(p.M) * ld3_of(p.K) * 4 + 256; }
 
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -344,18 +343,28 @@ bool encode(CUtensorMap* m, const float* base, int64_t inner, int64_t outer, int
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+cudaError_t prep_b(const KParams& p, void* ws, cudaStream_t s) {
+    const int64_t N = p.N, K = p.K, ld3 = ld3_of(K);
+    float* Bt = static_cast<float*>(ws);
+    dim3 g(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>((K + 31) / 32));
+    split_bt_kernel<<<g, dim3(32, 8), 0, s>>>(static_cast<const float*>(p.B), p.ldb, K, N, Bt, ld3);
+    return cudaGetLastError();
+}
+
 template <class Cfg>
-cudaError_t run(const KParams& p, void* ws, cudaStream_t s) {
+cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
     constexpr int BN = Cfg::BN;
     const int64_t M = p.M, N = p.N, K = p.K, ld3 = ld3_of(K);
-    float* Ap = static_cast<float*>(ws);
-    float* Bt = reinterpret_cast<float*>(static_cast<char*>(ws) + (size_t(M) * ld3 * 4 + 255) / 256 * 256);
+    float* Bt = static_cast<float*>(ws);
+    float* Ap = reinterpret_cast<float*>(static_cast<char*>(ws) + b_bytes(p));
+    if (!b_ready) {
+        const cudaError_t e = prep_b(p, ws, s);
+        if (e != cudaSuccess) return e;
+    }
     {
         const int64_t total = M * K;
         const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 32));
         split_a_kernel<<<blocks, 256, 0, s>>>(static_cast<const float*>(p.A), p.lda, M, K, Ap, ld3);
-        dim3 g(static_cast<unsigned>((N + 31) / 32), static_cast<unsigned>((K + 31) / 32));
-        split_bt_kernel<<<g, dim3(32, 8), 0, s>>>(static_cast<const float*>(p.B), p.ldb, K, N, Bt, ld3);
     }
     CUtensorMap ma, mb;
     if (!encode(&ma, Ap, 3 * K, M, ld3, BM) || !encode(&mb, Bt, 3 * K, N, ld3, BN))
@@ -402,6 +411,8 @@ void add_tc(Registry& reg, const char* name) {
     v.launch = &tc::no_tile_launch;
     v.ws_bytes = &tc::ws_bytes;
     v.run = &tc::run<Cfg>;
+    v.prep_b = &tc::prep_b;
+    v.prep_id = 1;  // 3xTF32 split of B, shared by both tile shapes
     reg.variants.push_back(v);
 }
 

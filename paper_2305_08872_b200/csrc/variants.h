@@ -38,8 +38,13 @@ struct VariantDesc {
     TileLaunchFn launch = nullptr;
     // Variants with their own staging (tcgen05 3xTF32 GEMM): the whole
     // subtask is run(), with ws_bytes() of context workspace.
+    // B's preparation (split / slices) sits at the front of the workspace and
+    // is reused across the row bands of one call (b_ready); prep_id names its
+    // format, prep_b computes it alone (before a timed trial).
     size_t (*ws_bytes)(const KParams&) = nullptr;
-    cudaError_t (*run)(const KParams&, void* ws, cudaStream_t) = nullptr;
+    cudaError_t (*run)(const KParams&, void* ws, bool b_ready, cudaStream_t) = nullptr;
+    cudaError_t (*prep_b)(const KParams&, void* ws, cudaStream_t) = nullptr;
+    int prep_id = 0;
 };
 
 // Per (body, dtype) helpers that are not tile variants.
