@@ -1514,6 +1514,15 @@ amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_o
         const int64_t M = hv.M;
         int nb = 1;
         if (a_rows && r_rows && M >= 1024) nb = static_cast<int>(std::min<int64_t>(8, M / 256));
+        // Band edges: equal bands except a last one a quarter as tall, so the
+        // copy-out that trails the final compute is short; multiples of 64 rows.
+        std::vector<int64_t> edge(static_cast<size_t>(nb) + 1);
+        for (int bi = 0; bi <= nb; ++bi) {
+            const double f = nb == 1 ? double(bi) : std::min(1.0, bi / (nb - 0.75));
+            int64_t r = static_cast<int64_t>(f * double(M));
+            if (bi < nb) r = r / 64 * 64;
+            edge[static_cast<size_t>(bi)] = bounds->i0 + std::min<int64_t>(M, bi == nb ? M : r);
+        }
         // events: [0] shared inputs ready, [1] start, per band [2+3b] inputs
         // in, [3+3b] computed, and [2+3nb] all outputs out
         while (static_cast<int>(ctx->pipe_ev.size()) < 3 * nb + 3) {
@@ -1545,7 +1554,7 @@ amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_o
             cuda_check(cudaEventRecord(shared_ready, ctx->copy_in), "cudaEventRecord");
             const int64_t arow = host_ops->a.ld * es, rrow = host_ops->r.ld * es;
             for (int bi = 0; bi < nb; ++bi) {
-                const int64_t r0 = bounds->i0 + M * bi / nb, r1 = bounds->i0 + M * (bi + 1) / nb;
+                const int64_t r0 = edge[static_cast<size_t>(bi)], r1 = edge[static_cast<size_t>(bi) + 1];
                 cudaEvent_t in_ev = ctx->pipe_ev[2 + 3 * bi], done_ev = ctx->pipe_ev[3 + 3 * bi];
                 if (nb == 1) {
                     cuda_check(cudaMemcpyAsync(ctx->hbuf[0], src[0]->data, bytes[0],
