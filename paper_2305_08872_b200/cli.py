@@ -213,7 +213,7 @@ def _emit(a, text: str) -> None:
 def _setup(a):
     tp = _compile(a)
     M, K, N_ = _extents(tp, a.dims)
-    ctx = E.Context(a.device)
+    ctx = E.Context(a.device, f64_emulation=getattr(a, "f64_emulation", False))
     device = f"cuda:{a.device}"
     plan = ctx.plan_for(tp, a.dtype)
     data = TaskData(tp, M, K, N_, a, device)
@@ -430,6 +430,8 @@ def _parser() -> argparse.ArgumentParser:
         s.add_argument("--preset", default="")
         s.add_argument("--dtype", default="f64", choices=["f64", "f32", "i32"])
         s.add_argument("--device", type=int, default=0)
+        s.add_argument("--f64-emulation", action="store_true",
+                       help="let the tuner use the int8-tensor-core f64 GEMM (opt-in)")
         s.add_argument("--dims", type=int, nargs=3, default=[512, 512, 512],
                        metavar=("M", "K", "N"))
         s.add_argument("--out", default="")

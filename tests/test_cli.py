@@ -224,3 +224,15 @@ def test_run_a_generated_body_verified(capsys, tmp_path, extra):
     j = json.loads(out)
     assert code == 0, err
     assert j["verify"] in (("exact", "pass") if "real" in extra else ("exact",)), out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("extra", ["--dtype f32", "--f64-emulation"])
+def test_run_gemm_on_tensor_cores_verified(capsys, extra):
+    """matmul through the CLI where the tuner may choose a tensor-core GEMM
+    (tcgen05 3xTF32 for f32; the opt-in int8 Ozaki f64): integer data, exact."""
+    code, out, err = run_cli(capsys, f"run --preset matmul --dims 1024 512 768 --verify "
+                                     f"--format json --trials 1 {extra}")
+    j = json.loads(out)
+    assert code == 0, err
+    assert j["verify"] == "exact", out
