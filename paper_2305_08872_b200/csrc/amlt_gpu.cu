@@ -867,7 +867,8 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
             kc = it->second.kc;
             rep->from_cache = 1;
         } else if (!plan->desc.accumulate) {
-            v = plan->variants.empty() ? -1 : plan->variants[0];
+            // "=" runs the per-element assign kernel; any staging-compatible variant
+            v = default_variant(ctx, plan, whole.M, whole.N, whole.aligned);
         } else {
             v = default_variant(ctx, plan, whole.M, whole.N, whole.aligned);
             // Output too small to fill the GPU: split K so every SM has work

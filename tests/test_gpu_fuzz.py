@@ -1,0 +1,118 @@
+"""GPU: randomized parity sweep over the fixed bodies.
+
+Each case draws a body, dtype, shape (tiny and ragged included), a bounds
+sub-rectangle of a larger R holding prior values, operand orientations and
+storage orders, the threshold form, '=' or '+=', and how the task runs
+(tuned, a named tile variant, a forced split-K depth, or the host-buffer
+entry), on the reference's IntValued data so that every case must be
+bit-exact against the C oracle (and R outside the bounds untouched).
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from tests.helpers import NP_DT, oracle
+
+pytestmark = pytest.mark.gpu
+
+BODIES = [("gemm", "f64"), ("gemm", "f32"), ("discount", "f64"), ("discount", "f32"),
+          ("boost", "f64"), ("boost", "f32"), ("sqdiff", "f64"), ("sqdiff", "f32"),
+          ("eqcount", "f64"), ("eqcount", "i32"), ("thrcount", "f64"), ("thrcount", "i32")]
+
+
+def stored(x, transposed, col_major):
+    """The buffer holding the statement operand x (logical rows x cols)."""
+    buf = x.T if transposed else x
+    return np.asfortranarray(buf) if col_major else np.ascontiguousarray(buf)
+
+
+@pytest.mark.parametrize("case", range(192))
+def test_random_cases_bit_exact(gpu_ctx, case):
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    rng = np.random.default_rng(1000 + case)
+    body, dtype = BODIES[case % len(BODIES)]
+    M, K, N = (int(rng.integers(1, 200)), int(rng.integers(1, 160)), int(rng.integers(1, 220)))
+    if case % 5 == 0:
+        M, K, N = int(rng.integers(200, 700)), int(rng.integers(100, 600)), int(rng.integers(200, 700))
+    i0, j0, k0 = (int(rng.integers(0, max(1, M // 3))), int(rng.integers(0, max(1, N // 3))),
+                  int(rng.integers(0, max(1, K // 3))))
+    i1, j1, k1 = (int(rng.integers(i0 + 1, M + 1)), int(rng.integers(j0 + 1, N + 1)),
+                  int(rng.integers(k0 + 1, K + 1)))
+    at, bt = bool(rng.integers(0, 2)), bool(rng.integers(0, 2))
+    acm, bcm = bool(rng.integers(0, 2)), bool(rng.integers(0, 2))
+    accumulate = rng.random() < 0.8
+    tcls = "j"
+    if body in ("discount", "boost", "thrcount"):
+        tcls = str(rng.choice(["c", "i", "j", "ij"]))
+    A = rng.integers(-8, 9, (M, K)).astype(np.float64)
+    B = rng.integers(-8, 9, (K, N)).astype(np.float64)
+    if body == "eqcount":
+        A, B = np.abs(A) % 5, np.abs(B) % 5  # collisions likely
+    R0 = rng.integers(-50, 50, (M, N)).astype(np.float64)
+    tval = float(rng.integers(-8, 9))
+    thres = {"c": None, "i": rng.integers(-8, 9, M).astype(np.float64),
+             "j": rng.integers(-8, 9, N).astype(np.float64),
+             "ij": rng.integers(-8, 9, (M, N)).astype(np.float64)}[tcls] \
+        if body in ("discount", "boost", "thrcount") else None
+    dis = rng.integers(-8, 9, N).astype(np.float64) if body == "discount" else None
+
+    # oracle: thresholds as an (i, j) grid, one row at a time (its threshold
+    # vector runs over j)
+    b = (i0, i1, j0, j1, k0, k1)
+    if body in ("discount", "boost", "thrcount"):
+        T = {"c": np.full((M, N), tval), "i": None, "j": None, "ij": thres}[tcls]
+        if tcls == "i":
+            T = np.repeat(thres[:, None], N, 1)
+        elif tcls == "j":
+            T = np.repeat(thres[None, :], M, 0)
+        want = R0.copy()
+        for i in range(i0, i1):
+            want[i] = oracle(body, A[i:i + 1], B, T[i], dis, R0=R0[i:i + 1],
+                             bounds=(0, 1, j0, j1, k0, k1), accumulate=accumulate)[0]
+    else:
+        want = oracle(body, A, B, None, None, R0=R0, bounds=b, accumulate=accumulate)
+
+    td = {"f64": torch.float64, "f32": torch.float32, "i32": torch.int32}[dtype]
+    npd = NP_DT[dtype]
+    dev = lambda x: None if x is None else torch.from_numpy(  # noqa: E731
+        np.asarray(x.astype(npd), order="K")).to("cuda")
+    Ab = stored(A, at, acm).astype(npd, order="K")
+    Bb = stored(B, bt, bcm).astype(npd, order="K")
+    plan = gpu_ctx.plan(body, dtype, accumulate=accumulate, layout_a=int(at), layout_b=int(bt),
+                        thres_class=tcls, thres_value=tval)
+    mode = case % 4
+    if mode == 3:  # host-buffer entry
+        R = R0.astype(npd).copy()
+        ops = P.Operands(Ab, Bb, R, None if thres is None else thres.astype(npd),
+                         None if dis is None else dis.astype(npd))
+        P.run_host(plan, ops, P.Bounds(*b))
+        got = R.astype(np.float64)
+    else:
+        R = dev(R0)
+        At = torch.from_numpy(Ab).to("cuda") if Ab.flags.c_contiguous else \
+            torch.from_numpy(np.ascontiguousarray(Ab.T)).to("cuda").t()
+        Bt = torch.from_numpy(Bb).to("cuda") if Bb.flags.c_contiguous else \
+            torch.from_numpy(np.ascontiguousarray(Bb.T)).to("cuda").t()
+        ops = P.Operands(At, Bt, R, dev(thres), dev(dis))
+        if mode == 0:
+            P.adaptive_execute(plan, ops, P.Bounds(*b))
+        elif mode == 1:
+            vs = plan.variants()
+            vi = int(rng.integers(0, len(vs)))
+            try:
+                P.run_subtask(plan, ops, P.TileParams(variant=vi), P.Bounds(*b))
+            except P.EngineError:  # an aligned variant on unaligned operands: the planner's pick
+                P.run_subtask(plan, ops, P.TileParams(), P.Bounds(*b))
+        else:
+            P.run_subtask(plan, ops, P.TileParams(kc=int(rng.integers(1, max(2, k1 - k0 + 1)))),
+                          P.Bounds(*b))
+        got = R.cpu().numpy().astype(np.float64)
+    bad = np.argwhere(got != want)
+    assert bad.size == 0, (f"case {case}: {body}/{dtype} {M}x{K}x{N} bounds {b} at={at} bt={bt} "
+                           f"acm={acm} bcm={bcm} acc={accumulate} thres={tcls} mode={mode}: "
+                           f"{len(bad)} mismatches, first {tuple(bad[0])} got "
+                           f"{got[tuple(bad[0])]} want {want[tuple(bad[0])]}")
