@@ -3,8 +3,8 @@
 Each case draws a body, dtype, shape (tiny and ragged included), a bounds
 sub-rectangle of a larger R holding prior values, operand orientations and
 storage orders, the threshold form, '=' or '+=', and how the task runs
-(tuned, a named tile variant, a forced split-K depth, or the host-buffer
-entry), on the reference's IntValued data so that every case must be
+(tuned, a named tile variant, a forced split-K depth, the host-buffer
+entry, AMULET's tuner contract, or the per-element executor), on the reference's IntValued data so that every case must be
 bit-exact against the C oracle (and R outside the bounds untouched).
 """
 from __future__ import annotations
@@ -84,7 +84,7 @@ def test_random_cases_bit_exact(gpu_ctx, case):
     Bb = stored(B, bt, bcm).astype(npd, order="K")
     plan = gpu_ctx.plan(body, dtype, accumulate=accumulate, layout_a=int(at), layout_b=int(bt),
                         thres_class=tcls, thres_value=tval)
-    mode = case % 4
+    mode = case % 6
     if mode == 3:  # host-buffer entry
         R = R0.astype(npd).copy()
         ops = P.Operands(Ab, Bb, R, None if thres is None else thres.astype(npd),
@@ -100,6 +100,10 @@ def test_random_cases_bit_exact(gpu_ctx, case):
         ops = P.Operands(At, Bt, R, dev(thres), dev(dis))
         if mode == 0:
             P.adaptive_execute(plan, ops, P.Bounds(*b))
+        elif mode == 4:  # AMULET's own tuner contract over the GPU executor
+            P.engine.adaptive_execute_amulet(plan, ops, P.Bounds(*b))
+        elif mode == 5:  # the per-element executor
+            P.run_naive(plan, ops, P.Bounds(*b))
         elif mode == 1:
             vs = plan.variants()
             vi = int(rng.integers(0, len(vs)))
