@@ -170,3 +170,42 @@ def test_random_generated_statements_on_subrectangles(gpu_ctx, case):
     assert bad.size == 0, (f"{src} {M}x{K}x{N} bounds {(i0, i1, j0, j1, k0, k1)} how={how}: "
                            f"{len(bad)} mismatches, first {tuple(bad[0])}: {got[tuple(bad[0])]} "
                            f"vs {want[tuple(bad[0])]}")
+
+
+@pytest.mark.parametrize("case", range(48))
+def test_random_real_data_within_tolerance(gpu_ctx, case):
+    """BASELINE distributions (helpers.make_inputs 'baseline') on random shapes
+    with K up to 4096 and random entries: fp64 <= 1e-12, fp32 <= 1e-5
+    (normwise for GEMM) against the fp64 oracle, int32 exact."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+    from tests.helpers import cast, check, make_inputs
+
+    rng = np.random.default_rng(7000 + case)
+    body, dtype = BODIES[case % len(BODIES)]
+    M, N = int(rng.integers(1, 400)), int(rng.integers(1, 400))
+    K = int(rng.choice([int(rng.integers(1, 300)), int(rng.integers(300, 4097))]))
+    A, B, t, d = make_inputs(body, M, K, N, "baseline", seed=case)
+    A, B, t, d = (cast(x, dtype) for x in (A, B, t, d))
+    want = oracle(body, A, B, t, d)
+    td = {"f64": torch.float64, "f32": torch.float32, "i32": torch.int32}[dtype]
+    dev = lambda x: None if x is None else torch.from_numpy(x).to(td).cuda()  # noqa: E731
+    R = torch.zeros((M, N), dtype=td, device="cuda")
+    plan = gpu_ctx.plan(body, dtype)
+    ops = P.Operands(dev(A), dev(B), R, dev(t), dev(d))
+    mode = case % 3
+    if mode == 0:
+        P.adaptive_execute(plan, ops, P.Bounds(0, M, 0, N, 0, K))
+    elif mode == 1:
+        vs = plan.variants()
+        vi = int(rng.integers(0, len(vs)))
+        try:
+            P.run_subtask(plan, ops, P.TileParams(variant=vi), P.Bounds(0, M, 0, N, 0, K))
+        except P.EngineError:
+            P.run_subtask(plan, ops, P.TileParams(), P.Bounds(0, M, 0, N, 0, K))
+    else:
+        P.run_subtask(plan, ops, P.TileParams(kc=int(rng.integers(32, max(33, K)))),
+                      P.Bounds(0, M, 0, N, 0, K))
+    check(body, dtype, R.cpu().numpy(), want, A=A, B=B,
+          what=f"case {case} {body}/{dtype} {M}x{K}x{N} mode {mode}")
