@@ -14,5 +14,7 @@ from .engine import (Bounds, Clock, Context, CoverRect, EngineError, ExecLog, Ex
                      run_adaptive, run_fixed, run_host, run_naive, run_subtask,
                      spr)
 from .task import TaskPlan, compile_task  # noqa: F401
+from .taskdata import (TaskData, VerifyResult, bind_dims, load_operand_file,  # noqa: F401
+                       make_task_data, verify_against_naive)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

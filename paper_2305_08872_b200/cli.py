@@ -35,11 +35,12 @@ from __future__ import annotations
 import argparse
 import json
 import sys
-from typing import Dict, List, Optional, Tuple
+from typing import List, Optional, Tuple
 
 from . import _native as N
 from . import engine as E
 from . import matrix_io as io
+from . import taskdata as TD
 from .task import TaskError, TaskPlan, compile_task, preset_source
 
 # The reference's straight-line program per body (schedule.hpp:32-53; frozen
@@ -60,7 +61,6 @@ _LEDGER = {N.BODY_DISCOUNT: (11, 16, 31)}
 _DEFAULT_BLOCK = (12, 16, 31)
 _CLASS = {N.LEAF_CONSTANT: "constant", N.LEAF_VEC_I: "[i]", N.LEAF_VEC_J: "[j]",
           N.LEAF_MAT_IJ: "[i][j]"}
-_TOL = {"f64": 1e-12, "f32": 1e-5, "i32": 0.0}
 
 
 class UsageError(Exception):
@@ -105,89 +105,32 @@ def _compile(a) -> TaskPlan:
 
 
 def _extents(tp: TaskPlan, dims: List[int]) -> Tuple[int, int, int]:
-    """bind_dims (src/engine.cpp:104-126): numeric range ends are fixed;
-    named ends bind to --dims M K N by the loop they close; one name bound to
-    two different values is an error."""
-    bound: Dict[str, int] = {}
-    out = []
-    for end, value in zip(tp.dims, dims):
-        try:
-            out.append(int(float(end)))
-            continue
-        except ValueError:
-            pass
-        if end in bound and bound[end] != value:
-            raise E.EngineError(f"conflicting values for dimension '{end}': {bound[end]} vs {value}")
-        bound[end] = value
-        out.append(value)
-    return out[0], out[1], out[2]
+    """bind_dims (src/engine.cpp:104-126) over --dims M K N."""
+    return TD.bind_dims(tp, dims[0], dims[1], dims[2])[1]
 
 
-class TaskData:
-    """make_task_data (src/engine.cpp:128-151) on the device."""
-
-    def __init__(self, tp: TaskPlan, M: int, K: int, N_: int, a, device: str):
-        import torch
-        mode = io.REAL if a.data == "real" else io.INT_VALUED
-        if a.dtype == "i32" and mode == io.REAL:
-            raise E.EngineError("--dtype i32 needs --data int")
-        oa = io.COL_MAJOR if a.layout_a == "col" else io.ROW_MAJOR
-        ob = io.COL_MAJOR if a.layout_b == "col" else io.ROW_MAJOR
-        at = tp.layout_a == N.LAYOUT_TRANSPOSED
-        bt = tp.layout_b == N.LAYOUT_TRANSPOSED
-        shape_a = (K, M) if at else (M, K)
-        shape_b = (N_, K) if bt else (K, N_)
-
-        def gen(name, shape, order):
-            return io.gen_operand(a.seed, name, shape[0], shape[1], order, mode, a.dtype, device)
-
-        self.A = self._file(a.a_file, shape_a, a.dtype, device) if a.a_file else \
-            gen(tp.a_name, shape_a, oa)
-        self.B = self._file(a.b_file, shape_b, a.dtype, device) if a.b_file else \
-            gen(tp.b_name, shape_b, ob)
-        self.thres = self.dis = None
-        if tp.thres_name:
-            tshape = {N.LEAF_CONSTANT: (1, 1), N.LEAF_VEC_I: (M, 1), N.LEAF_VEC_J: (N_, 1),
-                      N.LEAF_MAT_IJ: (M, N_)}[tp.thres_class]
-            self.thres = gen(tp.thres_name, tshape, io.ROW_MAJOR)
-        if tp.dis_name:
-            self.dis = gen(tp.dis_name, (N_, 1), io.ROW_MAJOR)
-        shapes = {N.LEAF_CONSTANT: (1, 1), N.LEAF_VEC_I: (M, 1), N.LEAF_VEC_J: (N_, 1),
-                  N.LEAF_MAT_IJ: (M, N_)}
-        self.aux = tuple(gen(nm, shapes[cls], io.ROW_MAJOR)
-                         for nm, cls in zip(tp.aux_names, tp.aux_classes))
-        tdt = {"f64": torch.float64, "f32": torch.float32, "i32": torch.int32}[a.dtype]
-        self.R = torch.zeros((M, N_), dtype=tdt, device=device)
-
-    @staticmethod
-    def _file(path, shape, dtype, device):
-        info = io.matrix_file_info(path)
-        if (info.rows, info.cols) != tuple(shape):
-            raise E.EngineError(f"operand file {path} is {info.rows}x{info.cols}, task needs "
-                                f"{shape[0]}x{shape[1]}")
-        return io.read_matrix_file(path, dtype, device)
-
-    def operands(self, R=None) -> E.Operands:
-        return E.Operands(self.A, self.B, self.R if R is None else R, self.thres, self.dis,
-                          self.aux)
+def _task_data(tp: TaskPlan, M: int, K: int, N_: int, a, device: str) -> TD.TaskData:
+    """make_task_data (src/engine.cpp:128-151) on the device, then --a-file /
+    --b-file (amlt_main.cpp:117-134)."""
+    mode = io.REAL if a.data == "real" else io.INT_VALUED
+    if a.dtype == "i32" and mode == io.REAL:
+        raise E.EngineError("--dtype i32 needs --data int")
+    data = TD.make_task_data(tp, M, K, N_, seed=a.seed,
+                             order_a=io.COL_MAJOR if a.layout_a == "col" else io.ROW_MAJOR,
+                             order_b=io.COL_MAJOR if a.layout_b == "col" else io.ROW_MAJOR,
+                             mode=mode, dtype=a.dtype, device=device)
+    if a.a_file:
+        TD.load_operand_file(data, tp.a_name, a.a_file, device)
+    if a.b_file:
+        TD.load_operand_file(data, tp.b_name, a.b_file, device)
+    return data
 
 
-def _verify(plan, data: TaskData, bounds: E.Bounds, dtype: str, mode: str) -> str:
+def _verify(plan, data: TD.TaskData, bounds: E.Bounds, dtype: str, mode: str) -> str:
     """verify_against_naive (src/engine.cpp:186-210) with the per-element
     device executor as the naive side."""
-    import torch
-    scratch = torch.zeros_like(data.R)
-    E.run_naive(plan, data.operands(scratch), bounds)
-    got, want = data.R.double(), scratch.double()
-    if torch.equal(got, want):
-        return "exact"
-    err = (got - want).abs()
-    mag = torch.maximum(got.abs(), want.abs())
-    rel = torch.where(mag > 0, err / torch.where(mag > 0, mag, torch.ones_like(mag)),
-                      torch.zeros_like(mag))
-    if mode == "int":
-        return "fail"
-    return "pass" if float(rel.max()) <= _TOL[dtype] else "fail"
+    v = TD.verify_against_naive(plan, data, bounds, io.REAL if mode == "real" else io.INT_VALUED)
+    return "exact" if v.exact else ("pass" if v.passed else "fail")
 
 
 def _aggregate(times: List[float], agg: str) -> float:
@@ -216,7 +159,7 @@ def _setup(a):
     ctx = E.Context(a.device, f64_emulation=getattr(a, "f64_emulation", False))
     device = f"cuda:{a.device}"
     plan = ctx.plan_for(tp, a.dtype)
-    data = TaskData(tp, M, K, N_, a, device)
+    data = _task_data(tp, M, K, N_, a, device)
     return tp, ctx, plan, data, E.Bounds(0, M, 0, N_, 0, K), (M, K, N_)
 
 
@@ -250,7 +193,7 @@ def cmd_run(a) -> int:
     times: List[float] = []
     rep = None
     for _ in range(max(1, a.trials)):
-        data.R.zero_()
+        data.result().zero_()
         if a.mode == "adaptive":
             rep = E.adaptive_execute(plan, data.operands(), bounds, a.packing)
             times.append(rep.total_seconds)
@@ -347,11 +290,11 @@ def cmd_bench(a) -> int:
         for nc in ncs:
             times = []
             for _ in range(max(1, a.trials)):
-                data.R.zero_()
+                data.result().zero_()
                 times.append(E.run_fixed(plan, data.operands(), bounds, kc, nc, a.packing))
             cells.append(_g(_aggregate(times, a.agg)))
         lines.append(f"{kc}," + ",".join(cells))
-    data.R.zero_()
+    data.result().zero_()
     rep = E.adaptive_execute(plan, data.operands(), bounds, a.packing)
     kc = rep.best_kc if rep.best_kc > 0 else K
     nc = plan.variants()[rep.best_variant].block_n if rep.best_variant >= 0 else N_
