@@ -130,7 +130,10 @@ struct amlt_ctx {
         int variant;
         int64_t kc;
     };
-    std::map<std::tuple<int, int, int64_t, int64_t, int64_t>, Winner> tune_cache;
+    // keyed by (body, dtype, M, N, K, operands staging-aligned, variant family):
+    // a winner only serves calls its variant can run
+    using TuneKey = std::tuple<int, int, int64_t, int64_t, int64_t, int, int>;
+    std::map<TuneKey, Winner> tune_cache;
     std::string err;
     bool dry() const { return (flags & AMLT_CTX_DRY_RUN) != 0; }
 };
@@ -442,6 +445,11 @@ int choose_variant(const amlt_ctx* ctx, const amlt_plan* plan, const amlt_tile_p
         if (best >= 0) return best;
     }
     return default_variant(ctx, plan, rv.M, rv.N, rv.aligned);
+}
+
+amlt_ctx::TuneKey tune_key(const amlt_plan* plan, const Resolved& rv) {
+    return amlt_ctx::TuneKey(plan->desc.body, plan->desc.dtype, rv.M, rv.N, rv.K, rv.aligned ? 1 : 0,
+                             plan->variants.empty() ? -1 : plan->variants.front());
 }
 
 int plan_local_index(const amlt_plan* plan, int reg_idx) {
@@ -789,7 +797,7 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
         }
     }
     rep->scratch_tuned = 1;
-    ctx->tune_cache[std::make_tuple(plan->desc.body, plan->desc.dtype, whole.M, whole.N, whole.K)] =
+    ctx->tune_cache[tune_key(plan, whole)] =
         amlt_ctx::Winner{best.variant, best.kc};
 }
 
@@ -798,7 +806,7 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
     std::memset(rep, 0, sizeof(*rep));
     rep->best_variant = -1;
     Resolved whole = resolve(plan, ops, &b);
-    const auto key = std::make_tuple(plan->desc.body, plan->desc.dtype, whole.M, whole.N, whole.K);
+    const auto key = tune_key(plan, whole);
 
     // candidate list
     std::vector<int> cands;
@@ -1536,7 +1544,9 @@ amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_o
         amlt_tile_params tp{0, 0, 0, -1};
         if (tile) tp = *tile;
         else {
-            auto it = ctx->tune_cache.find(std::make_tuple(plan->desc.body, plan->desc.dtype, hv.M, hv.N, hv.K));
+            // (the device copies keep the host pitches and offsets, so the host
+            // description's alignment is the device's)
+            auto it = ctx->tune_cache.find(tune_key(plan, hv));
             if (it != ctx->tune_cache.end()) {
                 tp.variant = plan_local_index(plan, it->second.variant);
                 tp.kc = it->second.kc;

@@ -596,3 +596,41 @@ def test_ozaki_f64_gemm_on_int8_tensor_cores():
     R.zero_()
     rep = P.adaptive_execute(eplan, P.Operands(A, B, R), P.Bounds(0, M, 0, N, 0, K))
     assert any(eplan.variants()[t.value].name == name for t in rep.trials)
+
+
+def test_tuning_cache_across_layouts_alignment_and_threshold_forms(gpu_ctx):
+    """The per-shape tuning cache must not carry a winner into a call it cannot
+    serve: same (M, N, K) with aligned then unaligned operands, and with a plan
+    whose variants differ (thresholds indexed by i)."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 1500, 600, 700  # tunable size: the first call caches a winner
+    A, B, t, d = make_inputs("discount", M, K, N, "int", seed=71)
+    want = oracle("discount", A, B, t, d)
+    ctx = P.Context(0)
+    plan = ctx.plan("discount", "f64")
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
+    for rep in range(2):  # second run hits the cache
+        R = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+        P.adaptive_execute(plan, P.Operands(dev(A), dev(B), R, dev(t), dev(d)), P.Bounds(0, M, 0, N, 0, K))
+        check("discount", "f64", R.cpu().numpy(), want, exact=True, what=f"aligned run {rep}")
+    # unaligned: A and B as views with an odd leading dimension
+    Ab = torch.zeros((M, K + 1), dtype=torch.float64, device="cuda")
+    Ab[:, :K] = dev(A)
+    Bb = torch.zeros((K, N + 1), dtype=torch.float64, device="cuda")
+    Bb[:, :N] = dev(B)
+    R = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+    P.adaptive_execute(plan, P.Operands(Ab[:, :K], Bb[:, :N], R, dev(t), dev(d)), P.Bounds(0, M, 0, N, 0, K))
+    check("discount", "f64", R.cpu().numpy(), want, exact=True, what="unaligned after cached aligned")
+    # same shape, thresholds indexed by i: a different variant family
+    ti = np.random.default_rng(72).integers(-8, 9, M).astype(np.float64)
+    iplan = ctx.plan("discount", "f64", thres_class="i")
+    R = torch.zeros((M, N), dtype=torch.float64, device="cuda")
+    rep = P.adaptive_execute(iplan, P.Operands(dev(A), dev(B), R, dev(ti), dev(d)), P.Bounds(0, M, 0, N, 0, K))
+    wi = np.zeros((M, N))
+    for i in range(M):
+        wi[i] = oracle("discount", A[i:i + 1], B, np.full(N, ti[i]), d)[0]
+    check("discount", "f64", R.cpu().numpy(), wi, exact=True, what="thres[i] after cached thres[j]")
+    assert rep.best_variant >= 0
