@@ -430,6 +430,9 @@ int choose_variant(const amlt_ctx* ctx, const amlt_plan* plan, const amlt_tile_p
         if (vdesc(idx).vec && !rv.aligned)
             fail(AMLT_ERR_INVALID_ARGUMENT,
                  "variant needs 16-byte aligned operands with vector-multiple strides");
+        if (vdesc(idx).max_k && rv.K > vdesc(idx).max_k)
+            fail(AMLT_ERR_INVALID_ARGUMENT, std::string("variant accepts K <= ") +
+                                                std::to_string(vdesc(idx).max_k));
         return idx;
     }
     if (tile && tile->nc > 0) {
@@ -813,6 +816,7 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
     for (int idx : plan->variants) {
         const VariantDesc& v = vdesc(idx);
         if (v.emulated && !(ctx->flags & AMLT_CTX_F64_EMULATION)) continue;  // opt-in only
+        if (v.max_k && whole.K > v.max_k) continue;
         if (v.vec == whole.aligned && (!v.tc || whole.aligned)) cands.push_back(idx);
     }
     // Band height per candidate: `waves` full waves of CTAs across all SMs

@@ -485,6 +485,7 @@ void register_ozaki_gemm(Registry& reg) {
     v.vec = true;
     v.tc = true;
     v.emulated = true;
+    v.max_k = 65536;  // exact int32 diagonal sums
     v.name = "tcgen05_ozaki_i8";
     v.func = reinterpret_cast<const void*>(&oz::ozaki_gemm_kernel);
     v.launch = &oz::no_tile_launch;

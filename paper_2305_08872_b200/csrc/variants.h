@@ -33,6 +33,7 @@ struct VariantDesc {
     bool tc = false;  // tensor-core (DMMA) variant
     bool tout = false;  // per-output threshold state (T indexed by i or (i, j))
     bool emulated = false;  // f64 via int8 tensor cores: tuner candidate only on opt-in
+    int64_t max_k = 0;      // largest K range the variant accepts (0: any)
     const char* name = "";
     const void* func = nullptr;
     TileLaunchFn launch = nullptr;
