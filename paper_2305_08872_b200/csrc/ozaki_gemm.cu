@@ -21,17 +21,17 @@
 // integer-valued inputs (the reference's IntValued data) are exact: one slice
 // holds them and every step is exact.
 //
-// Kernel (one CTA per 128 x 128 tile of R, 320 threads, warp-specialised):
-//   warp 0, one lane   TMA producer over (diagonal, slice pair, k block):
-//                      A_p (128 x 128 int8) and B_q^T (128 x 128 int8) boxes,
-//                      128-byte swizzle, 6-stage full/empty mbarrier ring;
-//   warp 1             allocates 256 TMEM columns (two 128 x 128 int32
-//                      accumulators, one per diagonal in flight); one lane
-//                      issues tcgen05.mma kind::i8 (M=128, N=128, K=32) x 4 per
-//                      stage, commits stages and finished diagonals;
-//   warps 2-9          epilogue: per finished diagonal, tcgen05.ld their 32
-//                      lanes x 64 columns, fold them into f64 registers,
-//                      release the accumulator; finally R += scaled sums.
+// Kernel (one CTA per 128 x 64 tile of R, 192 threads, warp-specialised):
+//   warp 0, one lane   TMA producer: per 64-byte k block ONE 3-D box of all
+//                      seven A slices (64 x 128 x 7) and one of all seven B
+//                      slices (64 x 64 x 7), 64-byte swizzle, 2-stage ring;
+//   warp 1             allocates 512 TMEM columns: seven 128 x 64 int32
+//                      accumulators, one per diagonal; one lane issues the
+//                      28 slice pairs x 2 tcgen05.mma kind::i8 (M=128, N=64,
+//                      K=32) of each stage;
+//   warps 2-5          epilogue: tcgen05.ld each diagonal (32 lanes x 64
+//                      columns), fold into f64 registers with its exact
+//                      2^-7d scale, then R += 2^(ea_i+eb_j) * sum.
 #include <cudaTypedefs.h>
 
 #include <math_constants.h>
@@ -43,14 +43,19 @@
 namespace amltk {
 namespace oz {
 
-constexpr int S = 7;                      // slices per operand
-constexpr int BM = 128, BN = 128, BK = 128;  // BK in int8 elements = one 128-byte swizzle row
-constexpr int STAGES = 6;
-constexpr int THREADS = 320;
-constexpr int STAGE_A = BM * BK, STAGE_B = BN * BK;  // bytes
+constexpr int S = 7;  // slices per operand
+// One stage holds every slice of one 64-byte k block: A_1..A_7 (128 x 64 int8
+// each) and B_1..B_7 (64 x 64), so all 28 slice pairs of the block run from
+// one fill (the operand bytes per MAC drop ~3x against one pair per fill).
+constexpr int BM = 128, BN = 64, BK = 64;  // BK in int8 elements = one 64-byte swizzle row
+constexpr int STAGES = 2;
+constexpr int THREADS = 192;
+constexpr int PLANE_A = BM * BK, PLANE_B = BN * BK;  // bytes per slice plane
+constexpr int STAGE_A = S * PLANE_A, STAGE_B = S * PLANE_B;
 constexpr int SMEM = STAGES * (STAGE_A + STAGE_B) + 1024 + 256;
-constexpr uint32_t TMEM_COLS = 2 * BN;
-// kind::i8: signed A and B, s32 accumulate, K-major, M = 128, N = 128
+constexpr int NDIAG = S;                  // diagonals d = 2 .. S+1, one accumulator each
+constexpr uint32_t TMEM_COLS = 512;       // NDIAG x BN = 448 columns, allocated as 512
+// kind::i8: signed A and B, s32 accumulate, K-major, M = 128, N = 64
 constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | (uint32_t(BN >> 3) << 17) |
                            (uint32_t(BM >> 4) << 24);
 
@@ -205,14 +210,23 @@ __device__ __forceinline__ void fence_before() {
 __device__ __forceinline__ void fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 }
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {  // K-major, 128-byte swizzle
+// K-major operand in 64-byte-swizzled rows: 8-row atoms 512 B apart
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr) {
     uint64_t d = 0;
     d |= uint64_t((addr & 0x3FFFF) >> 4);
     d |= uint64_t(1) << 16;
-    d |= uint64_t(1024 >> 4) << 32;
+    d |= uint64_t(512 >> 4) << 32;
     d |= uint64_t(1) << 46;
-    d |= uint64_t(2) << 61;
+    d |= uint64_t(4) << 61;  // SWIZZLE_64B
     return d;
+}
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int32_t x, int32_t y,
+                                       int32_t z, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(su32(bar))
+        : "memory");
 }
 __device__ __forceinline__ void mma_i8(uint32_t tmem, uint64_t a, uint64_t b, uint32_t accumulate) {
     asm volatile(
@@ -227,9 +241,6 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
-// The (diagonal, slice pair) schedule: d = 2 .. S+1, p = 1 .. d-1 (q = d - p).
-constexpr int NDIAG = S;  // diagonals 2 .. S+1
-
 __global__ void __launch_bounds__(THREADS, 1)
     ozaki_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                       const OzParams p) {
@@ -240,9 +251,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     unsigned char* sB = base + STAGES * STAGE_A;
     uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * STAGE_B);
     uint64_t* empty = full + STAGES;
-    uint64_t* acc_full = empty + STAGES;  // [2]
-    uint64_t* acc_empty = acc_full + 2;   // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    uint64_t* acc_full = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
 
     const int G = p.group_m, bid = blockIdx.x, per_group = G * p.tiles_n;
     const int group = bid / per_group, first_m = group * G;
@@ -258,10 +268,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             bar_init(&full[s], 1);
             bar_init(&empty[s], 1);
         }
-        for (int b = 0; b < 2; ++b) {
-            bar_init(&acc_full[b], 1);
-            bar_init(&acc_empty[b], 8);  // one arrival per epilogue warp
-        }
+        bar_init(acc_full, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmB)) : "memory");
@@ -278,66 +285,56 @@ __global__ void __launch_bounds__(THREADS, 1)
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        if (lane == 0) {  // TMA producer
-            int it = 0;
-            for (int d = 2; d <= S + 1; ++d)
-                for (int sa = 1; sa < d; ++sa) {
-                    const int sb = d - sa;
-                    if (sa > S || sb > S) continue;
-                    const int32_t ya = static_cast<int32_t>((sa - 1) * p.M + m0);
-                    const int32_t yb = static_cast<int32_t>((sb - 1) * p.N + n0);
-                    for (int kb = 0; kb < nkb; ++kb, ++it) {
-                        const int s = it % STAGES;
-                        bar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
-                        bar_expect(&full[s], STAGE_A + STAGE_B);
-                        tma_2d(sA + s * STAGE_A, &tmA, kb * BK, ya, &full[s]);
-                        tma_2d(sB + s * STAGE_B, &tmB, kb * BK, yb, &full[s]);
-                    }
-                }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {  // MMA issuer
-            int it = 0;
-            for (int d = 2; d <= S + 1; ++d) {
-                const int buf = d & 1, use = (d - 2) >> 1;  // use-th time this buffer is filled
-                bar_wait(&acc_empty[buf], (use & 1) ^ 1);   // the epilogue has drained it
-                fence_after();
-                const uint32_t acc = tmem + uint32_t(buf * BN);
-                bool first = true;
-                for (int sa = 1; sa < d; ++sa) {
-                    const int sb = d - sa;
-                    if (sa > S || sb > S) continue;
-                    for (int kb = 0; kb < nkb; ++kb, ++it) {
-                        const int s = it % STAGES;
-                        bar_wait(&full[s], (it / STAGES) & 1);
-                        fence_after();
-                        const uint32_t a0 = su32(sA + s * STAGE_A), b0 = su32(sB + s * STAGE_B);
-#pragma unroll
-                        for (int k = 0; k < BK / 32; ++k) {
-                            mma_i8(acc, smem_desc(a0 + k * 32), smem_desc(b0 + k * 32), !first);
-                            first = false;
-                        }
-                        mma_commit(&empty[s]);
-                    }
-                }
-                mma_commit(&acc_full[buf]);  // diagonal d complete
+        if (lane == 0) {  // TMA producer: all slices of one k block per stage
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % STAGES;
+                bar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+                bar_expect(&full[s], STAGE_A + STAGE_B);
+                tma_3d(sA + s * STAGE_A, &tmA, kb * BK, static_cast<int32_t>(m0), 0, &full[s]);
+                tma_3d(sB + s * STAGE_B, &tmB, kb * BK, static_cast<int32_t>(n0), 0, &full[s]);
             }
         }
-    } else {  // epilogue warps 2..9: lane quarter warp % 4, column half (warp - 2) / 4
-        const int q = warp & 3, h = (warp - 2) >> 2;
-        const int64_t row = m0 + 32 * q + lane;
-        double sum[64];
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer: 28 slice pairs x 2 k steps per stage
+            for (int kb = 0; kb < nkb; ++kb) {
+                const int s = kb % STAGES;
+                bar_wait(&full[s], (kb / STAGES) & 1);
+                fence_after();
+                const uint32_t a0 = su32(sA + s * STAGE_A), b0 = su32(sB + s * STAGE_B);
+                uint32_t started = kb > 0 ? 0xffu : 0u;  // diagonals already holding a sum
 #pragma unroll
-        for (int c = 0; c < 64; ++c) sum[c] = 0.0;
+                for (int pa = 1; pa <= S; ++pa)
+#pragma unroll
+                    for (int pb = 1; pa + pb <= S + 1; ++pb) {
+                        const int d = pa + pb;  // 2 .. S+1
+                        const uint32_t acc = tmem + uint32_t((d - 2) * BN);
+#pragma unroll
+                        for (int k = 0; k < BK / 32; ++k) {
+                            const bool accumulate = (started >> (d - 2)) & 1u;
+                            mma_i8(acc, smem_desc(a0 + (pa - 1) * PLANE_A + k * 32),
+                                   smem_desc(b0 + (pb - 1) * PLANE_B + k * 32), accumulate);
+                            started |= 1u << (d - 2);
+                        }
+                    }
+                mma_commit(&empty[s]);
+            }
+            mma_commit(acc_full);
+        }
+    } else {  // epilogue warps 2..5: TMEM lane quarter warp % 4
+        const int q = warp & 3;
+        const int64_t row = m0 + 32 * q + lane;
+        double sum[BN];
+#pragma unroll
+        for (int c = 0; c < BN; ++c) sum[c] = 0.0;
+        bar_wait(acc_full, 0);
+        fence_after();
+#pragma unroll 1
         for (int d = 2; d <= S + 1; ++d) {
-            const int buf = d & 1, use = (d - 2) >> 1;
-            bar_wait(&acc_full[buf], use & 1);
-            fence_after();
             const double scale = ldexp(1.0, -7 * d);
 #pragma unroll
-            for (int c0 = 0; c0 < 64; c0 += 16) {
+            for (int c0 = 0; c0 < BN; c0 += 16) {
                 uint32_t v[16];
-                const uint32_t taddr = tmem + (uint32_t(32 * q) << 16) + uint32_t(buf * BN + h * 64 + c0);
+                const uint32_t taddr = tmem + (uint32_t(32 * q) << 16) + uint32_t((d - 2) * BN + c0);
                 asm volatile(
                     "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
                     "%10, %11, %12, %13, %14, %15}, [%16];\n"
@@ -350,16 +347,13 @@ __global__ void __launch_bounds__(THREADS, 1)
                 for (int e = 0; e < 16; ++e)
                     sum[c0 + e] = fma(double(static_cast<int32_t>(v[e])), scale, sum[c0 + e]);
             }
-            fence_before();
-            __syncwarp();
-            if (lane == 0) bar_arrive(&acc_empty[buf]);
         }
         if (row < p.M) {
             const int ei = p.ea[row];
             double* dst = p.R + row * p.ldr;
 #pragma unroll
-            for (int c = 0; c < 64; ++c) {
-                const int64_t col = n0 + h * 64 + c;
+            for (int c = 0; c < BN; ++c) {
+                const int64_t col = n0 + c;
                 if (col < p.N) {
                     const int32_t ej = p.eb[col];
                     dst[col] += (ei == kNonFinite || ej == kNonFinite) ? CUDART_NAN
@@ -401,16 +395,17 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
     return fn;
 }
 
-// S planes of rows x K int8 (row pitch ldk) as one (S*rows) x K tensor
-bool encode(CUtensorMap* m, const int8_t* base, int64_t K, int64_t rows_total, int64_t ldk) {
+// S planes of rows x K int8 (row pitch ldk, plane pitch rows*ldk) as a 3-D
+// tensor; one box carries a 64-byte k block of box_rows rows of every plane
+bool encode(CUtensorMap* m, const int8_t* base, int64_t K, int64_t rows, int64_t ldk, int box_rows) {
     auto fn = encoder();
     if (!fn) return false;
-    cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(rows_total)};
-    cuuint64_t strides[1] = {cuuint64_t(ldk)};
-    cuuint32_t box[2] = {cuuint32_t(BK), cuuint32_t(BM)};
-    cuuint32_t estr[2] = {1, 1};
-    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<int8_t*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+    cuuint64_t dims[3] = {cuuint64_t(K), cuuint64_t(rows), cuuint64_t(S)};
+    cuuint64_t strides[2] = {cuuint64_t(ldk), cuuint64_t(rows) * cuuint64_t(ldk)};
+    cuuint32_t box[3] = {cuuint32_t(BK), cuuint32_t(box_rows), cuuint32_t(S)};
+    cuuint32_t estr[3] = {1, 1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -445,7 +440,7 @@ cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
         slice_a_kernel<<<blocks, 256, 0, s>>>(A, p.lda, M, K, ea, As, ldk);
     }
     CUtensorMap ma, mb;
-    if (!encode(&ma, As, K, int64_t(S) * M, ldk) || !encode(&mb, Bs, K, int64_t(S) * N, ldk))
+    if (!encode(&ma, As, K, M, ldk, BM) || !encode(&mb, Bs, K, N, ldk, BN))
         return cudaErrorInvalidValue;
     OzParams op;
     op.R = static_cast<double*>(p.R);

@@ -543,7 +543,7 @@ def test_ozaki_f64_gemm_on_int8_tensor_cores():
 
     ctx = P.Context(0)
     rng = np.random.default_rng(91)
-    name = "gemm_f64_128x128_tcgen05_ozaki_i8"
+    name = "gemm_f64_128x64_tcgen05_ozaki_i8"
     M, K, N = 300, 136, 264
     A = rng.integers(-8, 9, (M, K)).astype(np.float64)
     B = rng.integers(-8, 9, (K, N)).astype(np.float64)

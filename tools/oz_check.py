@@ -4,7 +4,7 @@ import paper_2305_08872_b200 as P
 ctx = P.Context(0)
 plan = ctx.plan("gemm", "f64")
 names = [v.name for v in plan.variants()]
-vi = names.index("gemm_f64_128x128_tcgen05_ozaki_i8")
+vi = names.index("gemm_f64_128x64_tcgen05_ozaki_i8")
 dm = names.index("gemm_f64_64x64_dmma_w32x32_c2x2")
 print("variant", vi, flush=True)
 rng = np.random.default_rng(5)
