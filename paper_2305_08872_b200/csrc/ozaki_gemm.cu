@@ -182,9 +182,6 @@ __device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(b)), "r"(bytes)
                  : "memory");
 }
-__device__ __forceinline__ void bar_arrive(uint64_t* b) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(b)) : "memory");
-}
 __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
     uint32_t done;
     do {
@@ -195,14 +192,6 @@ __device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
             : "r"(su32(b)), "r"(parity)
             : "memory");
     } while (!done);
-}
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int32_t x, int32_t y,
-                                       uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(su32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(su32(bar))
-        : "memory");
 }
 __device__ __forceinline__ void fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
