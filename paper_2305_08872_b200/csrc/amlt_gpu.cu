@@ -822,13 +822,17 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
     // Band height per candidate: `waves` full waves of CTAs across all SMs
     // (4 when the rows allow it, so partial-wave tails weigh little in the
     // score; otherwise 1).
-    // The bands must fit in a quarter of the rows (4-wave, then 1-wave bands);
-    // with many candidates, 1-wave bands may take up to 40% (their rows are
-    // real output, computed by the candidate under trial).
+    // The bands must fit in a quarter of the rows (4-wave, then 1-wave bands).
+    // Tasks small enough are better measured whole on a scratch R (below);
+    // for larger ones with many candidates, 1-wave bands may take up to 40%
+    // of the rows (their rows are real output, computed by the candidate
+    // under trial).
+    const bool scratch_ok = double(whole.M) * double(whole.N) * double(whole.K) <= 1.5e11 &&
+                            whole.M * whole.N * dtype_size(plan->desc.dtype) <= (int64_t(1) << 30);
     std::vector<int64_t> band(cands.size());
     int64_t need = 0;
     int64_t cap = whole.M / 4;
-    for (int attempt = 0; attempt < 3; ++attempt) {
+    for (int attempt = 0; attempt < (scratch_ok ? 2 : 3); ++attempt) {
         const int waves = attempt == 0 ? 4 : 1;
         cap = attempt < 2 ? whole.M / 4 : whole.M * 2 / 5;
         need = 0;
@@ -864,8 +868,7 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
     // contexts and for tasks too large to repeat cheaply.
     if (!tunable && plan->desc.accumulate && !ctx->dry() && !cands.empty() && whole.M > 0 &&
         whole.N > 0 && whole.K > 0 && ctx->tune_cache.find(key) == ctx->tune_cache.end() &&
-        double(whole.M) * double(whole.N) * double(whole.K) <= 1.5e11 &&
-        whole.M * whole.N * dtype_size(plan->desc.dtype) <= (int64_t(1) << 30)) {
+        scratch_ok) {
         scratch_tune(ctx, plan, ops, b, whole, cands, rep);
     }
     if (!tunable) {
