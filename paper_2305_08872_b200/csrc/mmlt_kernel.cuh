@@ -455,7 +455,8 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
     T* As = reinterpret_cast<T*>(smem_raw);
     T* Bs = As + STAGES * Cfg::SMEM_A;
     uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * Cfg::SMEM_B);
-    uint64_t* empty = full + STAGES;  // one arrival per warp when a stage is consumed
+    // per-stage count of warps done reading it: the last one refills it
+    unsigned int* done = reinterpret_cast<unsigned int*>(full + STAGES);
 
     // ---- tile coordinates: grouped raster (group_m row-tiles per group, about
     // 512 rows) so the B column panels of concurrently resident CTAs are
@@ -524,7 +525,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
 #pragma unroll
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(&full[s], 1);
-                mbar_init(&empty[s], THREADS / 32);
+                done[s] = 0;
             }
             asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tmA)) : "memory");
@@ -668,14 +669,19 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
                     }
         }
         if constexpr ((LOAD & LOAD_TMA) != 0) {
-            // this warp is done reading the stage; the producer thread refills
-            // it with tile kt+STAGES once every warp has (no CTA-wide barrier:
-            // warps drift across the ready stages)
+            // this warp is done reading the stage; the LAST warp to finish it
+            // refills it with tile kt+STAGES (no CTA-wide barrier and nobody
+            // waits: warps drift across the ready stages)
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[stage]);
-            if (tid == 0 && kt + STAGES < nkt) {
-                mbar_wait(&empty[stage], static_cast<uint32_t>((kt / STAGES) & 1));
-                tma_stage(stage, kt + STAGES);
+            if (lane == 0) {
+                asm volatile("fence.acq_rel.cta;\n" ::: "memory");  // our reads before the count
+                if (atomicAdd(&done[stage], 1u) == THREADS / 32 - 1) {
+                    done[stage] = 0;
+                    // every warp's reads before the async-proxy (TMA) overwrite
+                    asm volatile("fence.acq_rel.cta;\n" ::: "memory");
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    if (kt + STAGES < nkt) tma_stage(stage, kt + STAGES);
+                }
             }
         }
     }
