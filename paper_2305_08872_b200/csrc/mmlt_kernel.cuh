@@ -73,6 +73,9 @@ struct KParams {
     const void* gaux[AMLT_KP_MAX_AUX];
     int64_t gaux_si[AMLT_KP_MAX_AUX];
     int64_t gaux_sj[AMLT_KP_MAX_AUX];
+    // Guarded variants (theta-form discount and its fallback): operand range
+    // statistics the kernels read to decide which of the two runs.
+    const int* guard;
 };
 
 // --------------------------------------------------------------------------
@@ -352,6 +355,27 @@ struct HasAt<Body, decltype(void(Body::HAS_AT))> {
     static constexpr bool value = Body::HAS_AT;
 };
 
+// Bodies whose B operand is a prepared multi-plane array (BPLANES planes of
+// K x N, one TMA box per stage covers all planes).
+template <class Body, class = void>
+struct BodyPlanes {
+    static constexpr int n = 1;
+};
+template <class Body>
+struct BodyPlanes<Body, decltype(void(Body::BPLANES))> {
+    static constexpr int n = Body::BPLANES;
+};
+
+// Bodies that run only when Body::guard(p) holds (checked once per CTA).
+template <class Body, class = void>
+struct BodyGuard {
+    __device__ static __forceinline__ bool run(const KParams&) { return true; }
+};
+template <class Body>
+struct BodyGuard<Body, decltype(void(Body::GUARDED))> {
+    __device__ static __forceinline__ bool run(const KParams& p) { return Body::guard(p); }
+};
+
 // Column state with the threshold of output (i, j) when T is indexed by i or
 // by (i, j): T(i, j) = thres[i * t_si + j * t_sj] (TCLS == 1 kernels).
 template <class Body, typename T>
@@ -402,6 +426,32 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// One body step with the B planes of the current (k, j): plane 0 is b itself
+// for single-plane bodies.
+template <class Body, int NPL>
+struct PlaneStep {
+    template <typename Acc, typename T, typename Col>
+    __device__ static __forceinline__ void go(Acc* acc, T a, T b0, T, T, const Col& col) {
+        Body::step(acc, a, b0, col);
+    }
+};
+template <class Body>
+struct PlaneStep<Body, 3> {
+    template <typename Acc, typename T, typename Col>
+    __device__ static __forceinline__ void go(Acc* acc, T a, T b0, T b1, T b2, const Col&) {
+        Body::step3(acc, a, b0, b1, b2);
+    }
+};
+
+__device__ __forceinline__ void tma_load_planes(void* dst, const CUtensorMap* map, int32_t x, int32_t y,
+                                                uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(0), "r"(smem_u32(bar))
+        : "memory");
+}
+
 // --------------------------------------------------------------------------
 // The tiled kernel
 //
@@ -426,7 +476,8 @@ struct MmltTile {
     static constexpr int BM = TM * WR;
     static constexpr int BN = 32 * TN * WC;
     static constexpr int SMEM_A = BM * BK;  // elements per stage
-    static constexpr int SMEM_B = BK * BN;
+    static constexpr int NPL = BodyPlanes<Body>::n;
+    static constexpr int SMEM_B = BK * BN * NPL;
     static constexpr int BAR_BYTES = 16 * STAGES;  // full + empty mbarriers (within the +128)
     static constexpr int SMEM_BYTES = STAGES * (SMEM_A + SMEM_B) * (int)sizeof(T) + 128;
     static_assert(TN % VN == 0, "TN must be a multiple of the 16B vector width");
@@ -434,6 +485,8 @@ struct MmltTile {
     static_assert(STAGES >= 2, "need at least double buffering");
     static_assert((SMEM_A * sizeof(T)) % 128 == 0, "TMA stage buffers must stay 128B aligned");
     static_assert(BN <= 256 && BM <= 256 && BK <= 256, "TMA box dims are at most 256");
+    static_assert(NPL == 1 || ((LOAD & LOAD_TMA) != 0 && (LOAD & LOAD_TOUT) == 0),
+                  "multi-plane B is TMA-staged with per-column state only");
 };
 
 template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, int LOAD,
@@ -450,6 +503,8 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
     using Vec = typename V16<T>::type;
     using Acc = typename Body::Acc;
     constexpr int NACC = Body::NACC;
+    constexpr int NPL = Cfg::NPL;
+    if (!BodyGuard<Body>::run(p)) return;  // CTA-uniform: before any barrier setup
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     T* As = reinterpret_cast<T*>(smem_raw);
@@ -493,7 +548,10 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
         mbar_expect_tx(&full[stage], STAGE_TX);
         const int32_t k = static_cast<int32_t>(kbeg + static_cast<int64_t>(kt) * BK);
         tma_load_2d(As + stage * Cfg::SMEM_A, &tmA, k, static_cast<int32_t>(m0), &full[stage]);
-        tma_load_2d(Bs + stage * Cfg::SMEM_B, &tmB, static_cast<int32_t>(n0), k, &full[stage]);
+        if constexpr (NPL == 1)
+            tma_load_2d(Bs + stage * Cfg::SMEM_B, &tmB, static_cast<int32_t>(n0), k, &full[stage]);
+        else
+            tma_load_planes(Bs + stage * Cfg::SMEM_B, &tmB, static_cast<int32_t>(n0), k, &full[stage]);
     };
     auto elem_stage = [&](int stage, int kt) {  // called by all threads
         T* as = As + stage * Cfg::SMEM_A;
@@ -571,8 +629,10 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
                                                            gj < p.N ? gj : 0);
                 }
     }
+#define STEP_PLANES(accv, a_, c_, col_) \
+    PlaneStep<Body, NPL>::go(accv, a_, b[c_], bx[0][c_], bx[NPL > 2 ? 1 : 0][c_], col_)
 #define COL(r, c) (TOUT ? colrc[TOUT ? (r) : 0][TOUT ? (c) : 0] : colst[c])
-#define STEP(accv, a_, c_, col_) Body::step(accv, a_, b[c_], col_)
+#define STEP(accv, a_, c_, col_) STEP_PLANES(accv, a_, c_, col_)
 
     Acc acc[TM][TN][NACC];
     Acc part[Body::TWO_LEVEL ? TM : 1][Body::TWO_LEVEL ? TN : 1][NACC];
@@ -616,11 +676,18 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
 #pragma unroll
                 for (int v = 0; v < VN; ++v) {
                     T b[TN];
+                    T bx[NPL > 1 ? NPL - 1 : 1][TN] = {};
 #pragma unroll
                     for (int q = 0; q < TN / VN; ++q) {
                         Vec bv = *reinterpret_cast<const Vec*>(bs + (kk + v) * BN + q * 32 * VN);
 #pragma unroll
                         for (int e = 0; e < VN; ++e) b[q * VN + e] = V16<T>::get(bv, e);
+#pragma unroll
+                        for (int pl = 1; pl < NPL; ++pl) {
+                            Vec xv = *reinterpret_cast<const Vec*>(bs + pl * BK * BN + (kk + v) * BN + q * 32 * VN);
+#pragma unroll
+                            for (int e = 0; e < VN; ++e) bx[pl - 1][q * VN + e] = V16<T>::get(xv, e);
+                        }
                     }
 #pragma unroll
                     for (int c = 0; c < TN; ++c) {
@@ -638,11 +705,18 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
         } else {
             for (int k = 0; k < kcount; ++k) {
                 T b[TN];
+                T bx[NPL > 1 ? NPL - 1 : 1][TN] = {};
 #pragma unroll
                 for (int q = 0; q < TN / VN; ++q) {
                     Vec bv = *reinterpret_cast<const Vec*>(bs + k * BN + q * 32 * VN);
 #pragma unroll
                     for (int e = 0; e < VN; ++e) b[q * VN + e] = V16<T>::get(bv, e);
+#pragma unroll
+                    for (int pl = 1; pl < NPL; ++pl) {
+                        Vec xv = *reinterpret_cast<const Vec*>(bs + pl * BK * BN + k * BN + q * 32 * VN);
+#pragma unroll
+                        for (int e = 0; e < VN; ++e) bx[pl - 1][q * VN + e] = V16<T>::get(xv, e);
+                    }
                 }
 #pragma unroll
                 for (int r = 0; r < TM; ++r) {
@@ -725,6 +799,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
 
 #undef COL
 #undef STEP
+#undef STEP_PLANES
 
 // R[i][j] (+)= sum over splits s = 0..S-1 (ascending) of work[s][i][j].
 template <typename T>

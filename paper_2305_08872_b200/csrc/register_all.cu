@@ -14,6 +14,7 @@ AMLT_PAIRS(AMLT_DECL)
 void register_dmma_gemm(Registry&);
 void register_tcgen05_gemm(Registry&);
 void register_ozaki_gemm(Registry&);
+void register_theta_discount(Registry&);
 
 void register_all(Registry& reg) {
 #define AMLT_CALL(B, D) register_##B##_##D(reg);
@@ -21,6 +22,7 @@ void register_all(Registry& reg) {
     register_dmma_gemm(reg);
     register_tcgen05_gemm(reg);
     register_ozaki_gemm(reg);
+    register_theta_discount(reg);
 }
 
 }  // namespace amltk

@@ -49,7 +49,7 @@ int main() {
     CHECK(el == 0.5 && fc.consumed() == 1);
 
     // tuner: scripted intervals -> argmin(score) wins, rows covered once
-    FakeClock tc({0.9, 0.2, 0.7, 0.8, 0.6, 0.4});
+    FakeClock tc({0.9, 0.2, 0.7, 0.8, 0.6, 0.4, 0.95, 0.85, 0.75, 0.65, 0.55, 0.45, 0.35, 0.99});
     ExecLog log;
     TuneReport rep = adaptive_execute(plan, ops, Bounds{0, M, 0, N, 0, K}, false, tc, &log);
     CHECK(rep.tuned && rep.trials.size() >= 2);

@@ -132,7 +132,7 @@ def test_tuner_ties_keep_earlier_candidate(dry_ctx):
 
 
 def test_tuner_cache_reused_on_second_call(dry_ctx):
-    plan, rep, clk, log = tuned_call(dry_ctx, [0.5, 0.1, 0.9, 0.9, 0.9, 0.9, 0.9, 0.9])
+    plan, rep, clk, log = tuned_call(dry_ctx, [0.5, 0.1] + [0.9] * 14)
     clk2 = P.FakeClock([0.3])
     log2 = P.ExecLog()
     rep2 = P.adaptive_execute(plan, big_ops(65536, 64, 1024), P.Bounds(0, 65536, 0, 1024, 0, 64),

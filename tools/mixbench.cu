@@ -4,6 +4,7 @@
 // SMSP for each mix.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mixbench tools/mixbench.cu
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 constexpr int NCH = 16;
@@ -33,6 +34,60 @@ __global__ void __launch_bounds__(256) mix(double* out, const double* in, int n)
         __syncthreads();
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if constexpr (MIX >= 22 && MIX <= 25) {
+        // theta form of discount: per (k, j) a threshold theta on a and the
+        // two candidate b values; P = a > theta; acc = fma(a, P ? x1 : x0, acc).
+        // 22: 4x4 tile, registers; 23: 4x4 tile from smem; 24: 8x4 from smem;
+        // 25: original discount 8x4 from smem (reference point for 24)
+        constexpr int RR = (MIX == 24 || MIX == 25) ? 8 : 4;
+        double th[4], x0[4], x1[4], aa[8], acc2[RR * 4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) { th[c] = in[18 + c]; x0[c] = in[22 + c]; x1[c] = in[26 + c]; }
+#pragma unroll
+        for (int c = 0; c < RR * 4; ++c) acc2[c] = 0;
+        __shared__ __align__(16) double sT[8 * 128 * 3];
+        for (int i = threadIdx.x; i < 8 * 128 * 3; i += blockDim.x) sT[i] = in[(i * 7) % 32];
+        for (int i = threadIdx.x; i < 16 * 8 * 4; i += blockDim.x) sA[i] = in[i % 16];
+        __syncthreads();
+        for (int it = 0; it < n; ++it) {
+            const int k = it & 7;
+            if constexpr (MIX == 22) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) { asm volatile("" : "+d"(th[c]), "+d"(x0[c]), "+d"(x1[c])); }
+#pragma unroll
+                for (int r = 0; r < 4; ++r) { aa[r] = a[r]; asm volatile("" : "+d"(aa[r])); }
+            } else {
+                const double* row = sT + k * 384;
+                const double2 t01 = *reinterpret_cast<const double2*>(row + lane * 2);
+                const double2 t23 = *reinterpret_cast<const double2*>(row + 64 + lane * 2);
+                const double2 p01 = *reinterpret_cast<const double2*>(row + 128 + lane * 2);
+                const double2 p23 = *reinterpret_cast<const double2*>(row + 192 + lane * 2);
+                const double2 q01 = *reinterpret_cast<const double2*>(row + 256 + lane * 2);
+                const double2 q23 = *reinterpret_cast<const double2*>(row + 320 + lane * 2);
+                th[0] = t01.x; th[1] = t01.y; th[2] = t23.x; th[3] = t23.y;
+                x0[0] = p01.x; x0[1] = p01.y; x0[2] = p23.x; x0[3] = p23.y;
+                x1[0] = q01.x; x1[1] = q01.y; x1[2] = q23.x; x1[3] = q23.y;
+#pragma unroll
+                for (int r = 0; r < RR; ++r) aa[r] = sA[(warp * 8 + r) % 32 * 16 + k];
+            }
+#pragma unroll
+            for (int c = 0; c < RR * 4; ++c) {
+                if constexpr (MIX == 25) {
+                    double p = __dmul_rn(aa[c / 4], x0[c % 4]);
+                    double f = p > th[c % 4] ? x1[c % 4] : 1.0;
+                    acc2[c] = __fma_rn(p, f, acc2[c]);
+                } else {
+                    double bs = aa[c / 4] > th[c % 4] ? x1[c % 4] : x0[c % 4];
+                    acc2[c] = __fma_rn(aa[c / 4], bs, acc2[c]);
+                }
+            }
+        }
+        double s = 0;
+#pragma unroll
+        for (int c = 0; c < RR * 4; ++c) s += acc2[c];
+        if (s == 1234.5) out[threadIdx.x] = s;
+        return;
+    }
     if constexpr (MIX == 11 || MIX == 12) {
         // B only from smem, A in registers. MIX 11: 4 x LDS.64 per k (one per
         // column); MIX 12: column-major B tile, one LDS.128 = 2 k values of a
@@ -200,7 +255,8 @@ void run(int sms, int blk, const char* name, double* out, const double* in) {
     cudaEventElapsedTime(&ms, e0, e1);
     int clk;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-    double warp_iters_per_smsp = double(blk) * 8 * NCH * ITERS / 4.0;
+    const int nch = (MIX == 24 || MIX == 25) ? 32 : NCH;
+    double warp_iters_per_smsp = double(blk) * 8 * nch * ITERS / 4.0;
     double cycles = ms * 1e-3 * clk * 1e3;  // at max clock
     printf("%-44s blk=%d  %.3f ms  %.2f cycles/warp-iter/SMSP (at max clock)\n", name, blk, ms,
            cycles / warp_iters_per_smsp);
@@ -215,6 +271,15 @@ int main() {
     double h[64];
     for (int i = 0; i < 64; ++i) h[i] = 1.0 + i * 0.25;
     cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
+    for (int blk : {1, 2}) {
+        run<7>(sms, blk, "discount 4x4 tile regs (reference point)", out, in);
+        run<22>(sms, blk, "theta form 4x4 regs: DSETP 2SEL DFMA", out, in);
+        run<8>(sms, blk, "discount 4x4 tile smem (reference point)", out, in);
+        run<23>(sms, blk, "theta form 4x4 smem (3 planes)", out, in);
+        run<25>(sms, blk, "discount 8x4 smem (reference point)", out, in);
+        run<24>(sms, blk, "theta form 8x4 smem (3 planes)", out, in);
+    }
+    if (getenv("MIX_ALL") == nullptr) return 0;
     for (int blk : {2, 4}) {
         run<13>(sms, blk, "DMUL only", out, in);
         run<14>(sms, blk, "DADD only", out, in);

@@ -16,7 +16,7 @@ from bench import gen_inputs  # noqa: E402
 
 body, dtype = sys.argv[1], sys.argv[2]
 M, K, N = (int(x) for x in sys.argv[3:6])
-variant = int(sys.argv[6]) if len(sys.argv) > 6 else -1
+variant = sys.argv[6] if len(sys.argv) > 6 else "-1"  # index or name
 reps = int(sys.argv[7]) if len(sys.argv) > 7 else 2
 dev = torch.device("cuda", 0)
 ctx = P.Context(0)
@@ -25,8 +25,11 @@ A, B, th, ds = gen_inputs(body, dtype, M, K, N, 0, 0, dev, False)
 R = torch.zeros((M, N), dtype=A.dtype, device=dev)
 ops = P.Operands(A, B, R, th, ds)
 vs = plan.variants()
-if variant < 0:
+if not variant.lstrip("-").isdigit():
+    variant = [v.name for v in vs].index(variant)
+elif int(variant) < 0:
     variant = plan.default_variant(M, N, K)
+variant = int(variant)
 print("variant", vs[variant].name, flush=True)
 for _ in range(reps):
     el = P.run_subtask(plan, ops, P.TileParams(variant=variant), P.Bounds(0, M, 0, N, 0, K))
