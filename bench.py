@@ -400,6 +400,8 @@ def main():
         "tcgen05_3xtf32" in plan.variants()[last.best_variant].name
     win_is_oz = last is not None and last.best_variant >= 0 and \
         "ozaki" in plan.variants()[last.best_variant].name
+    win_is_theta = last is not None and last.best_variant >= 0 and \
+        "_theta_" in plan.variants()[last.best_variant].name
     for s in range(steps):
         if flush:
             flush_buf.zero_()  # evict L2 (outside the step's events)
@@ -408,7 +410,8 @@ def main():
         ev[s][1].record(stream)
         # tcgen05 3xTF32: operand split of A, of B, then the tensor-core GEMM
         # Ozaki: row / column exponents, A / B slicing, then the int8 GEMM
-        launches += 3 if win_is_tc else (5 if win_is_oz else (2 if split else 1))
+        # theta-form discount: B planes, A range scan, theta tile, guard-exited fallback
+        launches += 3 if win_is_tc else (5 if win_is_oz else (4 if win_is_theta else (2 if split else 1)))
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -488,6 +491,8 @@ def main():
         # pipe instructions per inner iteration of the body's kernel; the
         # ceiling under 2-op accounting is 1/ops of the pipe peak
         ops_per_iter = {"discount": 3, "boost": 3, "gemm": 1, "sqdiff": 2, "eqcount": 1}[body]
+        if best >= 0 and "_theta_" in variants[best].name:
+            ops_per_iter = 2  # theta form: DSETP + DFMA per iteration (csrc/theta_discount.cu)
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s",
             "inner_iters_per_s": iters_total / el,

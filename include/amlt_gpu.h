@@ -217,7 +217,9 @@ typedef struct {
     int64_t value;  /* variant index tried                                   */
     int64_t rows;   /* row band the trial computed (its share of the output) */
     double elapsed; /* seconds                                               */
-    double score;   /* elapsed / rows: lower is better                       */
+    double score;   /* elapsed / rows, the band's partial last CTA round
+                       counted as full (ceil(c)/c, c = CTAs per SM): lower
+                       is better                                         */
 } amlt_trial;
 
 /* A completed output region (CoverRect, autotuner.hpp:19-24, extended with

@@ -916,7 +916,16 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
         t.value = plan_local_index(plan, cands[c]);
         t.rows = band[c];
         t.elapsed = el;
-        t.score = el / double(band[c]);
+        // A band cannot hold a whole number of waves for every tile shape
+        // (e.g. 3 x 256 CTAs of 96 x 128 on 148 SMs is 5.19 CTAs per SM,
+        // run as 6): score the band as if its busiest SM's last CTA round
+        // were full, which is what the many-wave remainder sees.
+        {
+            const VariantDesc& v = vdesc(cands[c]);
+            const double per_sm = double(ctas_for(v, band[c], whole.N)) / double(ctx->num_sms);
+            const double full = per_sm > 0.0 ? per_sm / std::ceil(per_sm) : 1.0;
+            t.score = el * full / double(band[c]);
+        }
         if (best < 0 || t.score < best_score) {
             best = cands[c];
             best_score = t.score;
