@@ -257,9 +257,9 @@ bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, 
 constexpr int FB_TM = 4, FB_TN = 4, FB_WR = 8, FB_WC = 1, FB_BK = 16, FB_ST = 3, FB_MINB = 2;
 using FbCfg = MmltTile<BodyDiscountFallback, double, FB_TM, FB_TN, FB_WR, FB_WC, FB_BK, FB_ST, LOAD_TMA, FB_MINB>;
 
-template <int TM, int TN, int WR, int WC, int BK, int ST, int MINB>
+template <class Body, int TM, int TN, int WR, int WC, int BK, int ST, int MINB>
 cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
-    using Cfg = MmltTile<BodyTheta, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>;
+    using Cfg = MmltTile<Body, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>;
     int* g = static_cast<int*>(ws);
     const double* planes = reinterpret_cast<const double*>(static_cast<char*>(ws) + HEADER);
     const int64_t npad = npad_of(p.N);
@@ -291,7 +291,7 @@ cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
     q.tiles_m = static_cast<int32_t>((p.M + Cfg::BM - 1) / Cfg::BM);
     q.tiles_n = static_cast<int32_t>((p.N + Cfg::BN - 1) / Cfg::BN);
     q.group_m = std::min(64, std::max(8, 512 / Cfg::BM));
-    auto kt = &mmlt_tile_kernel<BodyTheta, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>;
+    auto kt = &mmlt_tile_kernel<Body, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>;
     if ((e = cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES)) != cudaSuccess)
         return e;
     kt<<<static_cast<unsigned>(int64_t(q.tiles_m) * q.tiles_n), Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(q, ma, mb);
@@ -327,9 +327,9 @@ cudaError_t no_tile_launch(const KParams&, const CUtensorMap&, const CUtensorMap
 
 }  // namespace th
 
-template <int TM, int TN, int WR, int WC, int BK, int ST, int MINB>
+template <int TM, int TN, int WR, int WC, int BK, int ST, int MINB, class Body = th::BodyTheta>
 void add_theta(Registry& reg, const char* name) {
-    using Cfg = MmltTile<th::BodyTheta, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>;
+    using Cfg = MmltTile<Body, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>;
     VariantDesc v;
     v.body = 1;   // AMLT_BODY_DISCOUNT
     v.dtype = 0;  // AMLT_F64
@@ -345,24 +345,25 @@ void add_theta(Registry& reg, const char* name) {
     v.vec = true;
     v.name = name;
     v.func = reinterpret_cast<const void*>(
-        &mmlt_tile_kernel<th::BodyTheta, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>);
+        &mmlt_tile_kernel<Body, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>);
     v.launch = &th::no_tile_launch;
     v.ws_bytes = &th::ws_bytes;
-    v.run = &th::run<TM, TN, WR, WC, BK, ST, MINB>;
+    v.run = &th::run<Body, TM, TN, WR, WC, BK, ST, MINB>;
     v.prep_b = &th::prep_b;
     v.prep_id = 3;  // (theta, x0, x1) planes of B, shared by every theta tile
     reg.variants.push_back(v);
 }
 
 void register_theta_discount(Registry& reg) {
+    // 1 CTA per SM for the 8 x 4 micro-tiles (150+ registers); the 96-row
+    // tiles run 12 warps per SM, the most that fit
     //                 TM TN WR WC BK ST MINB
     add_theta<4, 4, 8, 1, 8, 4, 2>(reg, "theta_t4x4_w8x1");
-    add_theta<8, 4, 8, 1, 8, 3, 2>(reg, "theta_t8x4_w8x1");
-    add_theta<8, 4, 8, 1, 16, 3, 1>(reg, "theta_t8x4_w8x1_k16");
     add_theta<8, 2, 8, 1, 16, 3, 2>(reg, "theta_t8x2_w8x1");
-    add_theta<8, 4, 12, 1, 16, 3, 1>(reg, "theta_t8x4_w12x1");
-    add_theta<16, 2, 8, 1, 16, 3, 1>(reg, "theta_t16x2_w8x1");
+    add_theta<8, 4, 8, 1, 16, 3, 1>(reg, "theta_t8x4_w8x1");
     add_theta<8, 4, 4, 2, 16, 2, 1>(reg, "theta_t8x4_w4x2");
+    add_theta<8, 4, 12, 1, 16, 3, 1>(reg, "theta_t8x4_w12x1");
+    add_theta<8, 4, 12, 1, 16, 2, 1>(reg, "theta_t8x4_w12x1_s2");
 }
 
 }  // namespace amltk
