@@ -281,6 +281,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="cfg4_discount_f64", choices=sorted(WORKLOADS))
+    ap.add_argument("--tile", default=None,
+                    help="skip the tuner and run this tile variant (name from plan.variants()); "
+                         "used to pin the tuned winner under ncu, whose serialised launches "
+                         "change the trial timings")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--f64-emulation", action="store_true",
@@ -363,8 +367,17 @@ def main():
     # warm-up: the first call tunes on row bands (AMULET-style), later calls
     # reuse the cached winner
     reports = []
-    for _ in range(warmup):
-        reports.append(P.adaptive_execute(plan, ops, bounds))
+    if args.tile:
+        from types import SimpleNamespace
+
+        vi = [v.name for v in plan.variants()].index(args.tile)
+        for _ in range(warmup):
+            P.run_subtask(plan, ops, P.TileParams(variant=vi), bounds)
+        reports.append(SimpleNamespace(best_variant=vi, best_kc=K, tuned=False, scratch_tuned=False,
+                                       trials=[]))
+    else:
+        for _ in range(warmup):
+            reports.append(P.adaptive_execute(plan, ops, bounds))
     torch.cuda.synchronize()
     tuned = reports[0] if reports else None
 
@@ -506,7 +519,8 @@ def main():
                               if flush else "inputs larger than L2 (no flush)"),
                        "tile": variants[best].name if best >= 0 else None,
                        "split_k_kc": win.kc or None,
-                       "tuning": ("row-band trials" if tuned and tuned.tuned else
+                       "tuning": ("pinned by --tile" if args.tile else
+                                  "row-band trials" if tuned and tuned.tuned else
                                   "whole-task trials on scratch R" if tuned and tuned.scratch_tuned
                                   else "planner default"),
                        "tuning_trials": [(variants[t.value].name, round(t.score * 1e6, 4))
