@@ -1568,6 +1568,24 @@ amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_o
                 tp.kc = it->second.kc;
             }
         }
+        // Fewer bands when one band would not fill the SMs (a band is one
+        // launch of the variant; split-K multiplies its CTAs).
+        if (nb > 1) {
+            const int vi = tp.variant >= 0 ? plan->variants[static_cast<size_t>(tp.variant)]
+                                           : default_variant(ctx, plan, hv.M, hv.N, hv.aligned);
+            const VariantDesc& v = vdesc(vi);
+            const int64_t splits = (!v.run && tp.kc > 0 && tp.kc < hv.K) ? (hv.K + tp.kc - 1) / tp.kc : 1;
+            const int64_t slots = int64_t(ctx->num_sms) * occ_of(ctx, vi);
+            const int64_t fill = ctas_for(v, hv.M, hv.N) * splits / std::max<int64_t>(1, slots);
+            nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nb, fill)));
+            for (int bi = 0; bi <= nb; ++bi) {
+                const double f = nb == 1 ? double(bi) : std::min(1.0, bi / (nb - 0.75));
+                int64_t r = static_cast<int64_t>(f * double(M));
+                if (bi < nb) r = r / 64 * 64;
+                edge[static_cast<size_t>(bi)] = bounds->i0 + std::min<int64_t>(M, bi == nb ? M : r);
+            }
+            edge.resize(static_cast<size_t>(nb) + 1);
+        }
         auto body = [&] {
             cudaEvent_t shared_ready = ctx->pipe_ev[0];
             cudaEvent_t start_ev = ctx->pipe_ev[1];

@@ -35,6 +35,9 @@
 #include <math_constants.h>
 
 #include <cfloat>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "variants.h"
 
@@ -253,6 +256,20 @@ bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// cudaFuncSetAttribute once per (kernel, device)
+cudaError_t smem_attr_once(const void* kernel, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void*, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({kernel, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({kernel, dev});
+    return e;
+}
+
 // the fallback's tile: the shipped discount f64 tile (32 x 128, 4 x 4 per thread)
 constexpr int FB_TM = 4, FB_TN = 4, FB_WR = 8, FB_WC = 1, FB_BK = 16, FB_ST = 3, FB_MINB = 2;
 using FbCfg = MmltTile<BodyDiscountFallback, double, FB_TM, FB_TN, FB_WR, FB_WC, FB_BK, FB_ST, LOAD_TMA, FB_MINB>;
@@ -294,8 +311,7 @@ cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
     // measured 690 GB of DRAM reads per config-4 launch against 632 GB)
     q.group_m = std::min(64, std::max(8, 512 / Cfg::BM));
     auto kt = &mmlt_tile_kernel<Body, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>;
-    if ((e = cudaFuncSetAttribute(kt, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM_BYTES)) != cudaSuccess)
-        return e;
+    if ((e = smem_attr_once(reinterpret_cast<const void*>(kt), Cfg::SMEM_BYTES)) != cudaSuccess) return e;
     kt<<<static_cast<unsigned>(int64_t(q.tiles_m) * q.tiles_n), Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(q, ma, mb);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
@@ -316,9 +332,7 @@ cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
     f.group_m = std::min(64, std::max(8, 512 / FbCfg::BM));
     auto kf = &mmlt_tile_kernel<BodyDiscountFallback, double, FB_TM, FB_TN, FB_WR, FB_WC, FB_BK, FB_ST, LOAD_TMA,
                                 FB_MINB>;
-    if ((e = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, FbCfg::SMEM_BYTES)) !=
-        cudaSuccess)
-        return e;
+    if ((e = smem_attr_once(reinterpret_cast<const void*>(kf), FbCfg::SMEM_BYTES)) != cudaSuccess) return e;
     kf<<<static_cast<unsigned>(int64_t(f.tiles_m) * f.tiles_n), FbCfg::THREADS, FbCfg::SMEM_BYTES, s>>>(f, fa, fb);
     return cudaGetLastError();
 }
