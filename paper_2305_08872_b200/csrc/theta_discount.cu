@@ -371,15 +371,15 @@ void add_theta(Registry& reg, const char* name) {
 }
 
 void register_theta_discount(Registry& reg) {
-    // 1 CTA per SM for the 8 x 4 micro-tiles (150+ registers); the 96-row
-    // tiles run 12 warps per SM, the most that fit
+    // 8 x 4 micro-tiles take 150+ registers (one CTA per SM; the 96-row tile
+    // runs 12 warps), 6 x 4 ones 126 (two 8-warp CTAs per SM: 16 warps)
     //                 TM TN WR WC BK ST MINB
     add_theta<4, 4, 8, 1, 8, 4, 2>(reg, "theta_t4x4_w8x1");
     add_theta<8, 2, 8, 1, 16, 3, 2>(reg, "theta_t8x2_w8x1");
     add_theta<8, 4, 8, 1, 16, 3, 1>(reg, "theta_t8x4_w8x1");
     add_theta<8, 4, 4, 2, 16, 2, 1>(reg, "theta_t8x4_w4x2");
-    add_theta<8, 4, 12, 1, 16, 3, 1>(reg, "theta_t8x4_w12x1");
-    add_theta<8, 4, 12, 1, 16, 2, 1>(reg, "theta_t8x4_w12x1_s2");
+    add_theta<8, 4, 12, 1, 16, 2, 1>(reg, "theta_t8x4_w12x1");
+    add_theta<6, 4, 8, 1, 16, 2, 2>(reg, "theta_t6x4_w8x1");
 }
 
 }  // namespace amltk

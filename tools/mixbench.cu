@@ -34,12 +34,12 @@ __global__ void __launch_bounds__(256) mix(double* out, const double* in, int n)
         __syncthreads();
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if constexpr (MIX >= 22 && MIX <= 25) {
+    if constexpr (MIX >= 22 && MIX <= 27) {
         // theta form of discount: per (k, j) a threshold theta on a and the
         // two candidate b values; P = a > theta; acc = fma(a, P ? x1 : x0, acc).
         // 22: 4x4 tile, registers; 23: 4x4 tile from smem; 24: 8x4 from smem;
         // 25: original discount 8x4 from smem (reference point for 24)
-        constexpr int RR = (MIX == 24 || MIX == 25) ? 8 : 4;
+        constexpr int RR = (MIX == 24 || MIX == 25 || MIX == 26 || MIX == 27) ? 8 : 4;
         double th[4], x0[4], x1[4], aa[8], acc2[RR * 4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) { th[c] = in[18 + c]; x0[c] = in[22 + c]; x1[c] = in[26 + c]; }
@@ -72,7 +72,15 @@ __global__ void __launch_bounds__(256) mix(double* out, const double* in, int n)
             }
 #pragma unroll
             for (int c = 0; c < RR * 4; ++c) {
-                if constexpr (MIX == 25) {
+                if constexpr (MIX == 26) {  // predicated DFMA pair, no select
+                    asm("{ .reg .pred P; setp.gt.f64 P, %1, %2; @P fma.rn.f64 %0, %1, %3, %0; "
+                        "@!P fma.rn.f64 %0, %1, %4, %0; }"
+                        : "+d"(acc2[c]) : "d"(aa[c / 4]), "d"(th[c % 4]), "d"(x1[c % 4]), "d"(x0[c % 4]));
+                } else if constexpr (MIX == 27) {  // theta form via selp.f64
+                    asm("{ .reg .pred P; .reg .f64 s; setp.gt.f64 P, %1, %2; selp.f64 s, %3, %4, P; "
+                        "fma.rn.f64 %0, %1, s, %0; }"
+                        : "+d"(acc2[c]) : "d"(aa[c / 4]), "d"(th[c % 4]), "d"(x1[c % 4]), "d"(x0[c % 4]));
+                } else if constexpr (MIX == 25) {
                     double p = __dmul_rn(aa[c / 4], x0[c % 4]);
                     double f = p > th[c % 4] ? x1[c % 4] : 1.0;
                     acc2[c] = __fma_rn(p, f, acc2[c]);
@@ -255,7 +263,7 @@ void run(int sms, int blk, const char* name, double* out, const double* in) {
     cudaEventElapsedTime(&ms, e0, e1);
     int clk;
     cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
-    const int nch = (MIX == 24 || MIX == 25) ? 32 : NCH;
+    const int nch = (MIX == 24 || MIX == 25 || MIX == 26 || MIX == 27) ? 32 : NCH;
     double warp_iters_per_smsp = double(blk) * 8 * nch * ITERS / 4.0;
     double cycles = ms * 1e-3 * clk * 1e3;  // at max clock
     printf("%-44s blk=%d  %.3f ms  %.2f cycles/warp-iter/SMSP (at max clock)\n", name, blk, ms,
@@ -278,6 +286,8 @@ int main() {
         run<23>(sms, blk, "theta form 4x4 smem (3 planes)", out, in);
         run<25>(sms, blk, "discount 8x4 smem (reference point)", out, in);
         run<24>(sms, blk, "theta form 8x4 smem (3 planes)", out, in);
+        run<26>(sms, blk, "theta 8x4 smem, predicated DFMA pair", out, in);
+        run<27>(sms, blk, "theta 8x4 smem, selp.f64", out, in);
     }
     if (getenv("MIX_ALL") == nullptr) return 0;
     for (int blk : {2, 4}) {
