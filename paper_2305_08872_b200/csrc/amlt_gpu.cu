@@ -398,7 +398,7 @@ int default_variant(const amlt_ctx* ctx, const amlt_plan* plan, int64_t M, int64
     for (int idx : plan->variants) {
         const VariantDesc& v = vdesc(idx);
         if (v.vec != aligned) continue;
-        if (v.tc) continue;
+        if (v.tc || v.run) continue;  // own staging + workspace: tuner candidates only
         const int occ = occ_of(ctx, idx);
         const int sms = ctx ? ctx->num_sms : 148;
         const double waves = double(ctas_for(v, M, N)) / double(sms * occ);
@@ -545,6 +545,22 @@ void ensure_tc_ws(amlt_ctx* ctx, const VariantDesc& v, const KParams& kp) {
     ctx->bprep.gen = ~uint64_t(0);
     cuda_check(cudaMalloc(&ctx->tc_ws, need), "cudaMalloc(tensor-core operand workspace)");
     ctx->tc_ws_bytes = need;
+}
+
+// Whether a variant's workspace (prepared B, split A, ...) can be allocated:
+// what it needs beyond the current workspace must stay under 90% of free HBM
+// with 1 GiB to spare.
+bool ws_fits(const amlt_ctx* ctx, const VariantDesc& v, const KParams& kp) {
+    if (!v.ws_bytes || ctx->dry()) return true;
+    const size_t need = v.ws_bytes(kp);
+    if (need <= ctx->tc_ws_bytes) return true;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        (void)cudaGetLastError();
+        return false;
+    }
+    const double avail = 0.9 * double(free_b + ctx->tc_ws_bytes) - double(size_t(1) << 30);
+    return double(need) <= avail;
 }
 
 bool bprep_ready(const amlt_ctx* ctx, const VariantDesc& v, const KParams& kp) {
@@ -759,7 +775,8 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
         const int occ = occ_of(ctx, v);
         const int64_t ctas = ctas_for(vd, whole.M, whole.N);
         const int64_t slots = int64_t(ctx->num_sms) * occ;
-        if (ctas < 2 * slots && whole.K >= 512) {  // split-K forms for small outputs
+        // split-K forms for small outputs (variants with their own staging run whole K)
+        if (!vd.run && ctas < 2 * slots && whole.K >= 512) {
             for (int64_t splits : {int64_t(2), (2 * slots + ctas - 1) / ctas}) {
                 splits = std::min<int64_t>(splits, whole.K / 128);
                 if (splits < 2) continue;
@@ -817,6 +834,7 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
         const VariantDesc& v = vdesc(idx);
         if (v.emulated && !(ctx->flags & AMLT_CTX_F64_EMULATION)) continue;  // opt-in only
         if (v.max_k && whole.K > v.max_k) continue;
+        if (!ws_fits(ctx, v, whole.kp)) continue;  // prepared operands would not fit in HBM
         if (v.vec == whole.aligned && (!v.tc || whole.aligned)) cands.push_back(idx);
     }
     // Band height per candidate: `waves` full waves of CTAs across all SMs

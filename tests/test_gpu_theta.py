@@ -166,3 +166,35 @@ def test_nonfinite_a_in_theta_form(gpu_ctx):
     for vi, name in theta_variants(plan):
         got = run(gpu_ctx, A, B, t, d, vi)
         np.testing.assert_array_equal(got, base, err_msg=name)
+
+
+def test_theta_skipped_when_planes_do_not_fit():
+    """The tuner leaves out variants whose prepared operands would not fit in
+    free HBM (here 1.6 GB of theta planes with ~1.5 GB free) instead of
+    failing the call on cudaMalloc."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 2048, 4096, 16384
+    g = torch.Generator(device="cuda").manual_seed(3)
+    A = torch.randint(0, 10, (M, K), device="cuda", generator=g).double()
+    B = torch.rand((K, N), device="cuda", dtype=torch.float64, generator=g) * 99 + 1
+    t = torch.rand(N, device="cuda", dtype=torch.float64, generator=g) * 400 + 50
+    d = torch.rand(N, device="cuda", dtype=torch.float64, generator=g) * 0.3
+    R = torch.zeros((M, N), device="cuda", dtype=torch.float64)
+    ctx = P.Context(0)
+    plan = ctx.plan("discount", "f64")
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    hog = torch.empty(max(0, free - (1536 << 20)), dtype=torch.uint8, device="cuda")
+    try:
+        rep = P.adaptive_execute(plan, P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K))
+    finally:
+        del hog
+        torch.cuda.empty_cache()
+    names = [plan.variants()[tr.value].name for tr in rep.trials]
+    assert names and not any("_theta_" in n for n in names), names
+    rows = [0, 777, M - 1]
+    want = oracle("discount", A[rows].cpu().numpy(), B.cpu().numpy(), t.cpu().numpy(), d.cpu().numpy())
+    check("discount", "f64", R[rows].cpu().numpy(), want, what="fallback tiles under memory pressure")
