@@ -119,6 +119,7 @@ struct amlt_ctx {
         int prep = 0;
         uint64_t gen = ~uint64_t(0);
         const void* ws = nullptr;
+        double seconds = 0.0;  // measured cost of the preparation (tuning trials)
     } bprep;
     // device staging for amlt_gpu_run_host
     // slots: A, B, R, thres, dis, then the aux leaves of generated bodies
@@ -568,16 +569,29 @@ bool bprep_ready(const amlt_ctx* ctx, const VariantDesc& v, const KParams& kp) {
     return b.gen == ctx->call_gen && b.prep == v.prep_id && b.B == kp.B && b.ldb == kp.ldb &&
            b.K == kp.K && b.N == kp.N && b.ws == ctx->tc_ws;
 }
-void bprep_mark(amlt_ctx* ctx, const VariantDesc& v, const KParams& kp) {
-    ctx->bprep = amlt_ctx::BPrep{kp.B, kp.ldb, kp.K, kp.N, v.prep_id, ctx->call_gen, ctx->tc_ws};
+void bprep_mark(amlt_ctx* ctx, const VariantDesc& v, const KParams& kp, double seconds = 0.0) {
+    ctx->bprep = amlt_ctx::BPrep{kp.B, kp.ldb, kp.K, kp.N, v.prep_id, ctx->call_gen, ctx->tc_ws, seconds};
 }
-// B's preparation ahead of a timed trial, so trials measure the per-band work
+// B's preparation ahead of a timed trial, so trials measure the per-band
+// work; its own (event-timed) cost is kept in ctx->bprep.seconds, and the
+// trial scores charge it back once per call (a cached winner pays it on
+// every later call).
 void prep_b_untimed(amlt_ctx* ctx, const VariantDesc& v, const KParams& kp) {
     if (!v.prep_b || ctx->dry()) return;
     ensure_tc_ws(ctx, v, kp);
     if (bprep_ready(ctx, v, kp)) return;
+    cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
     cuda_check(v.prep_b(kp, ctx->tc_ws, ctx->stream), "tensor-core operand preparation");
-    bprep_mark(ctx, v, kp);
+    cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
+    cuda_check(cudaEventSynchronize(ctx->ev1), "cudaEventSynchronize");
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "cudaEventElapsedTime");
+    bprep_mark(ctx, v, kp, ms * 1e-3);
+}
+// The preparation cost a trial of variant v leaves out (0 without one).
+double prep_seconds(const amlt_ctx* ctx, const VariantDesc& v) {
+    return v.prep_b && ctx->bprep.prep == v.prep_id && ctx->bprep.gen == ctx->call_gen ? ctx->bprep.seconds
+                                                                                          : 0.0;
 }
 
 void enqueue(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const Dispatch& dp) {
@@ -646,8 +660,9 @@ void enqueue_compute(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const D
     const VariantDesc& v = vdesc(dp.variant);
     if (v.run) {  // own staging (tcgen05 3xTF32 GEMM): operand pre-pass + tensor-core GEMM
         ensure_tc_ws(ctx, v, kp);
-        cuda_check(v.run(kp, ctx->tc_ws, bprep_ready(ctx, v, kp), ctx->stream), "tensor-core GEMM launch");
-        bprep_mark(ctx, v, kp);
+        const bool ready = bprep_ready(ctx, v, kp);
+        cuda_check(v.run(kp, ctx->tc_ws, ready, ctx->stream), "tensor-core GEMM launch");
+        if (!ready) bprep_mark(ctx, v, kp);
         return;
     }
     kp.tiles_m = static_cast<int32_t>((rv.M + v.bm - 1) / v.bm);
@@ -803,7 +818,8 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
         cuda_check(cudaEventSynchronize(ctx->ev1), "cudaEventSynchronize");
         float ms = 0;
         cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "cudaEventElapsedTime");
-        const double el = ms * 1e-3;
+        // the whole task: its B preparation is part of every call
+        const double el = ms * 1e-3 + (rs.packed() ? 0.0 : prep_seconds(ctx, vdesc(dp.variant)));
         if (rep->n_trials < AMLT_MAX_TRIALS) {
             amlt_trial& t = rep->trials[rep->n_trials++];
             t.value = plan_local_index(plan, c.variant);
@@ -942,7 +958,8 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
             const VariantDesc& v = vdesc(cands[c]);
             const double per_sm = double(ctas_for(v, band[c], whole.N)) / double(ctx->num_sms);
             const double full = per_sm > 0.0 ? per_sm / std::ceil(per_sm) : 1.0;
-            t.score = el * full / double(band[c]);
+            // plus the variant's B preparation spread over the whole task
+            t.score = el * full / double(band[c]) + prep_seconds(ctx, v) / double(whole.M);
         }
         if (best < 0 || t.score < best_score) {
             best = cands[c];
