@@ -12,9 +12,14 @@
 //    STAGES-deep TMA ring (cp.async.bulk.tensor + mbarrier; per-element
 //    cp.async for unaligned operands): the reference's packing
 //    (src/packing.cpp:5-45) becomes the SMEM copy.
-//  * Every lane of a warp owns the SAME TM rows, so each A read is a 16-byte
-//    shared-memory broadcast (one wavefront, no bank conflicts); B reads are
-//    16-byte vectors, lane-interleaved so a warp touches contiguous bytes.
+//  * Lanes form an LR x LC grid (LR * LC = 32). LR = 1: every lane of a warp
+//    owns the SAME TM rows, so each A read is a 16-byte broadcast and the B
+//    reads are lane-interleaved 16-byte vectors (32 distinct per load: four
+//    wavefronts). LR > 1: the LR lanes of a column group share its B vectors
+//    (one wavefront per load) and read LR distinct A rows, conflict-free
+//    through the TMA 128-byte swizzle of the A tile. Shared-memory traffic
+//    per product drops about threefold for the 8 x 4 f64 micro-tile, which is
+//    what bounds the three-plane theta-form discount.
 //  * The per-j vectors (thres[j], dis[j]) are loaded once into registers.
 //  * The body is fused into the accumulate chain on CUDA cores (tensor cores
 //    cannot evaluate a per-product predicate); see the Body structs below for
@@ -467,19 +472,28 @@ constexpr int LOAD_ELEM = 0;
 constexpr int LOAD_TMA = 1;
 // flag: per-output threshold state (T indexed by i or by (i, j))
 constexpr int LOAD_TOUT = 2;
+// lane grid: bits 2-3 hold log2(LR), LR lanes along rows (see the header)
+constexpr int LOAD_LR2 = 1 << 2;
+constexpr int LOAD_LR4 = 2 << 2;
+constexpr int LOAD_LR8 = 3 << 2;
+__host__ __device__ constexpr int load_lr(int load) { return 1 << ((load >> 2) & 3); }
 
 template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, int LOAD,
           int MINB>
 struct MmltTile {
     static constexpr int VN = V16<T>::n;
     static constexpr int THREADS = 32 * WR * WC;
-    static constexpr int BM = TM * WR;
-    static constexpr int BN = 32 * TN * WC;
+    static constexpr int LR = load_lr(LOAD);  // lanes along rows
+    static constexpr int LC = 32 / LR;        // lanes along columns
+    static constexpr bool SWZ = LR > 1;       // A tile in the TMA 128-byte swizzle
+    static constexpr int BM = TM * LR * WR;
+    static constexpr int BN = LC * TN * WC;
     static constexpr int SMEM_A = BM * BK;  // elements per stage
     static constexpr int NPL = BodyPlanes<Body>::n;
     static constexpr int SMEM_B = BK * BN * NPL;
     static constexpr int BAR_BYTES = 16 * STAGES;  // full + empty mbarriers (within the +128)
-    static constexpr int SMEM_BYTES = STAGES * (SMEM_A + SMEM_B) * (int)sizeof(T) + 128;
+    // + 1024: the swizzled A stages start on a 1024-byte boundary
+    static constexpr int SMEM_BYTES = STAGES * (SMEM_A + SMEM_B) * (int)sizeof(T) + 128 + (SWZ ? 1024 : 0);
     static_assert(TN % VN == 0, "TN must be a multiple of the 16B vector width");
     static_assert(BK % VN == 0, "BK must be a multiple of the 16B vector width");
     static_assert(STAGES >= 2, "need at least double buffering");
@@ -487,6 +501,17 @@ struct MmltTile {
     static_assert(BN <= 256 && BM <= 256 && BK <= 256, "TMA box dims are at most 256");
     static_assert(NPL == 1 || ((LOAD & LOAD_TMA) != 0 && (LOAD & LOAD_TOUT) == 0),
                   "multi-plane B is TMA-staged with per-column state only");
+    static_assert(!SWZ || ((LOAD & LOAD_TMA) != 0 && BK * (int)sizeof(T) == 128 && TM * LR % 8 == 0),
+                  "the 2-D lane grid reads a TMA-swizzled A tile of 128-byte rows");
+    static_assert(!SWZ || LC * VN * (int)sizeof(T) <= 128, "a column group's B load must stay one wavefront");
+    // element offset of A(row, k) inside a stage (the TMA 128B swizzle XORs
+    // the 16-byte chunk index with row % 8)
+    __device__ static __forceinline__ int a_off(int row, int k) {
+        if constexpr (SWZ)
+            return row * BK + ((((k / VN) ^ (row & 7)) * VN) | (k % VN));
+        else
+            return row * BK + k;
+    }
 };
 
 template <class Body, typename T, int TM, int TN, int WR, int WC, int BK, int STAGES, int LOAD,
@@ -506,7 +531,10 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
     constexpr int NPL = Cfg::NPL;
     if (!BodyGuard<Body>::run(p)) return;  // CTA-uniform: before any barrier setup
 
-    extern __shared__ __align__(128) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw_[];
+    unsigned char* smem_raw = smem_raw_;
+    if constexpr (Cfg::SWZ)
+        smem_raw += (1024 - (smem_u32(smem_raw_) & 1023)) & 1023;
     T* As = reinterpret_cast<T*>(smem_raw);
     T* Bs = As + STAGES * Cfg::SMEM_A;
     uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * Cfg::SMEM_B);
@@ -537,6 +565,13 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
     const int warp = tid >> 5;
     const int wr = warp / WC;
     const int wc = warp - wr * WC;
+    constexpr int LR = Cfg::LR, LC = Cfg::LC;
+    const int lg = LR > 1 ? lane % LR : 0;  // row slot in the lane grid
+    const int lh = LR > 1 ? lane / LR : lane;  // column group
+    // this thread's rows: row0 + r * LR (interleaved, so the LR lanes of a
+    // column group hit distinct swizzle phases); columns: col0 + q * LC * VN + e
+    const int row0 = wr * TM * LR + lg;
+    const int col0 = wc * LC * TN + lh * VN;
 
     const T* __restrict__ Ag = static_cast<const T*>(p.A);
     const T* __restrict__ Bg = static_cast<const T*>(p.B);
@@ -603,14 +638,13 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
         }
     }
 
-    // ---- per-thread columns: local col of element (q, e) is
-    //      wc*32*TN + q*32*VN + lane*VN + e
+    // ---- per-thread columns: local col of element (q, e) is col0 + q*LC*VN + e
     typename Body::Col colst[TN];
 #pragma unroll
     for (int q = 0; q < TN / VN; ++q)
 #pragma unroll
         for (int e = 0; e < VN; ++e) {
-            const int64_t gj = n0 + wc * 32 * TN + q * 32 * VN + lane * VN + e;
+            const int64_t gj = n0 + col0 + q * LC * VN + e;
             colst[q * VN + e] = Body::col(p, gj < p.N ? gj : 0);
         }
     // Thresholds indexed by i or (i, j) (LOAD_TOUT variants): one state per
@@ -623,8 +657,8 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
             for (int q = 0; q < TN / VN; ++q)
 #pragma unroll
                 for (int e = 0; e < VN; ++e) {
-                    const int64_t gi = m0 + wr * TM + r;
-                    const int64_t gj = n0 + wc * 32 * TN + q * 32 * VN + lane * VN + e;
+                    const int64_t gi = m0 + row0 + r * LR;
+                    const int64_t gj = n0 + col0 + q * LC * VN + e;
                     colrc[r][q * VN + e] = col_at<Body, T>(colst[q * VN + e], p, gi < p.M ? gi : 0,
                                                            gj < p.N ? gj : 0);
                 }
@@ -662,8 +696,8 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
             if (nxt < nkt) elem_stage(nxt % STAGES, nxt);
             cp_async_commit();
         }
-        const T* as = As + stage * Cfg::SMEM_A + (wr * TM) * BK;
-        const T* bs = Bs + stage * Cfg::SMEM_B + wc * 32 * TN + lane * VN;
+        const T* as = As + stage * Cfg::SMEM_A;
+        const T* bs = Bs + stage * Cfg::SMEM_B + col0;
         const int kcount =
             static_cast<int>(min(static_cast<int64_t>(BK), kspan - static_cast<int64_t>(kt) * BK));
 
@@ -672,19 +706,19 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
             for (int kk = 0; kk < BK; kk += VN) {
                 Vec av[TM];
 #pragma unroll
-                for (int r = 0; r < TM; ++r) av[r] = *reinterpret_cast<const Vec*>(as + r * BK + kk);
+                for (int r = 0; r < TM; ++r) av[r] = *reinterpret_cast<const Vec*>(as + Cfg::a_off(row0 + r * LR, kk));
 #pragma unroll
                 for (int v = 0; v < VN; ++v) {
                     T b[TN];
                     T bx[NPL > 1 ? NPL - 1 : 1][TN] = {};
 #pragma unroll
                     for (int q = 0; q < TN / VN; ++q) {
-                        Vec bv = *reinterpret_cast<const Vec*>(bs + (kk + v) * BN + q * 32 * VN);
+                        Vec bv = *reinterpret_cast<const Vec*>(bs + (kk + v) * BN + q * LC * VN);
 #pragma unroll
                         for (int e = 0; e < VN; ++e) b[q * VN + e] = V16<T>::get(bv, e);
 #pragma unroll
                         for (int pl = 1; pl < NPL; ++pl) {
-                            Vec xv = *reinterpret_cast<const Vec*>(bs + pl * BK * BN + (kk + v) * BN + q * 32 * VN);
+                            Vec xv = *reinterpret_cast<const Vec*>(bs + pl * BK * BN + (kk + v) * BN + q * LC * VN);
 #pragma unroll
                             for (int e = 0; e < VN; ++e) bx[pl - 1][q * VN + e] = V16<T>::get(xv, e);
                         }
@@ -708,19 +742,19 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
                 T bx[NPL > 1 ? NPL - 1 : 1][TN] = {};
 #pragma unroll
                 for (int q = 0; q < TN / VN; ++q) {
-                    Vec bv = *reinterpret_cast<const Vec*>(bs + k * BN + q * 32 * VN);
+                    Vec bv = *reinterpret_cast<const Vec*>(bs + k * BN + q * LC * VN);
 #pragma unroll
                     for (int e = 0; e < VN; ++e) b[q * VN + e] = V16<T>::get(bv, e);
 #pragma unroll
                     for (int pl = 1; pl < NPL; ++pl) {
-                        Vec xv = *reinterpret_cast<const Vec*>(bs + pl * BK * BN + k * BN + q * 32 * VN);
+                        Vec xv = *reinterpret_cast<const Vec*>(bs + pl * BK * BN + k * BN + q * LC * VN);
 #pragma unroll
                         for (int e = 0; e < VN; ++e) bx[pl - 1][q * VN + e] = V16<T>::get(xv, e);
                     }
                 }
 #pragma unroll
                 for (int r = 0; r < TM; ++r) {
-                    const T a = as[r * BK + k];
+                    const T a = as[Cfg::a_off(row0 + r * LR, k)];
 #pragma unroll
                     for (int c = 0; c < TN; ++c) {
                         if constexpr (Body::TWO_LEVEL)
@@ -766,11 +800,11 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
     T* Wg = static_cast<T*>(p.work);
 #pragma unroll
     for (int r = 0; r < TM; ++r) {
-        const int64_t gi = m0 + wr * TM + r;
+        const int64_t gi = m0 + row0 + r * LR;
         if (gi >= p.M) continue;
 #pragma unroll
         for (int q = 0; q < TN / VN; ++q) {
-            const int64_t gj0 = n0 + wc * 32 * TN + q * 32 * VN + lane * VN;
+            const int64_t gj0 = n0 + col0 + q * LC * VN;
             T val[VN];
 #pragma unroll
             for (int e = 0; e < VN; ++e) val[e] = Body::finish(acc[r][q * VN + e], COL(r, q * VN + e), kspan);

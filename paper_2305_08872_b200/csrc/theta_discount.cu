@@ -247,12 +247,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encoder() {
 }
 
 bool encode(CUtensorMap* m, const void* base, int rank, const cuuint64_t* dims, const cuuint64_t* strides,
-            const cuuint32_t* box) {
+            const cuuint32_t* box, bool swizzle128 = false) {
     auto fn = encoder();
     if (!fn) return false;
     cuuint32_t estr[3] = {1, 1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<void*>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -274,9 +275,9 @@ cudaError_t smem_attr_once(const void* kernel, int bytes) {
 constexpr int FB_TM = 4, FB_TN = 4, FB_WR = 8, FB_WC = 1, FB_BK = 16, FB_ST = 3, FB_MINB = 2;
 using FbCfg = MmltTile<BodyDiscountFallback, double, FB_TM, FB_TN, FB_WR, FB_WC, FB_BK, FB_ST, LOAD_TMA, FB_MINB>;
 
-template <class Body, int TM, int TN, int WR, int WC, int BK, int ST, int MINB>
+template <class Body, int TM, int TN, int WR, int WC, int BK, int ST, int MINB, int LOAD>
 cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
-    using Cfg = MmltTile<Body, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>;
+    using Cfg = MmltTile<Body, double, TM, TN, WR, WC, BK, ST, LOAD, MINB>;
     int* g = static_cast<int*>(ws);
     const double* planes = reinterpret_cast<const double*>(static_cast<char*>(ws) + HEADER);
     const int64_t npad = npad_of(p.N);
@@ -298,7 +299,8 @@ cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
         const cuuint64_t bd[3] = {cuuint64_t(p.N), cuuint64_t(p.K), 3};
         const cuuint64_t bs[2] = {cuuint64_t(npad) * 8, cuuint64_t(p.K) * cuuint64_t(npad) * 8};
         const cuuint32_t bb[3] = {cuuint32_t(Cfg::BN), cuuint32_t(BK), 3};
-        if (!encode(&ma, p.A, 2, ad, as, ab) || !encode(&mb, planes, 3, bd, bs, bb)) return cudaErrorInvalidValue;
+        if (!encode(&ma, p.A, 2, ad, as, ab, Cfg::SWZ) || !encode(&mb, planes, 3, bd, bs, bb))
+            return cudaErrorInvalidValue;
     }
     KParams q = p;
     q.guard = g;
@@ -310,7 +312,7 @@ cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
     // raster groups of ~512 rows, as for the ordinary tiles (2304-row groups
     // measured 690 GB of DRAM reads per config-4 launch against 632 GB)
     q.group_m = std::min(64, std::max(8, 512 / Cfg::BM));
-    auto kt = &mmlt_tile_kernel<Body, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>;
+    auto kt = &mmlt_tile_kernel<Body, double, TM, TN, WR, WC, BK, ST, LOAD, MINB>;
     if ((e = smem_attr_once(reinterpret_cast<const void*>(kt), Cfg::SMEM_BYTES)) != cudaSuccess) return e;
     kt<<<static_cast<unsigned>(int64_t(q.tiles_m) * q.tiles_n), Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(q, ma, mb);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
@@ -343,9 +345,9 @@ cudaError_t no_tile_launch(const KParams&, const CUtensorMap&, const CUtensorMap
 
 }  // namespace th
 
-template <int TM, int TN, int WR, int WC, int BK, int ST, int MINB, class Body = th::BodyTheta>
+template <int TM, int TN, int WR, int WC, int BK, int ST, int MINB, int LOAD = LOAD_TMA, class Body = th::BodyTheta>
 void add_theta(Registry& reg, const char* name) {
-    using Cfg = MmltTile<Body, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>;
+    using Cfg = MmltTile<Body, double, TM, TN, WR, WC, BK, ST, LOAD, MINB>;
     VariantDesc v;
     v.body = 1;   // AMLT_BODY_DISCOUNT
     v.dtype = 0;  // AMLT_F64
@@ -361,10 +363,10 @@ void add_theta(Registry& reg, const char* name) {
     v.vec = true;
     v.name = name;
     v.func = reinterpret_cast<const void*>(
-        &mmlt_tile_kernel<Body, double, TM, TN, WR, WC, BK, ST, LOAD_TMA, MINB>);
+        &mmlt_tile_kernel<Body, double, TM, TN, WR, WC, BK, ST, LOAD, MINB>);
     v.launch = &th::no_tile_launch;
     v.ws_bytes = &th::ws_bytes;
-    v.run = &th::run<Body, TM, TN, WR, WC, BK, ST, MINB>;
+    v.run = &th::run<Body, TM, TN, WR, WC, BK, ST, MINB, LOAD>;
     v.prep_b = &th::prep_b;
     v.prep_id = 3;  // (theta, x0, x1) planes of B, shared by every theta tile
     reg.variants.push_back(v);
@@ -380,6 +382,12 @@ void register_theta_discount(Registry& reg) {
     add_theta<8, 4, 4, 2, 16, 2, 1>(reg, "theta_t8x4_w4x2");
     add_theta<8, 4, 12, 1, 16, 2, 1>(reg, "theta_t8x4_w12x1");
     add_theta<6, 4, 8, 1, 16, 2, 2>(reg, "theta_t6x4_w8x1");
+    // A 2-D lane grid (4 lanes along rows, 8 along columns): a third of the
+    // shared-memory wavefronts per product. Measured slower than the 1 x 32
+    // grids at 8192^3 (100.9 vs 98.9 ms; shared-memory bandwidth is not what
+    // bounds this body, profiles/r01/thetabench.txt); kept as a tuner
+    // candidate and to keep the lane-grid path exercised.
+    add_theta<8, 4, 3, 4, 16, 2, 1, LOAD_TMA | LOAD_LR4>(reg, "theta_t8x4_l4x8_w3x4");
 }
 
 }  // namespace amltk

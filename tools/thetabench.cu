@@ -1,0 +1,264 @@
+// thetabench.cu — throughput of forms of the theta-discount step (scratch
+// experiment, not product code). 8 x 4 micro-tile per thread: a[8] per row,
+// (theta, x0, x1)[4] per column. FORMs 0-7 keep the operands in registers
+// behind empty asm statements; ptxas does not see those, so it hoists the
+// compare and selects out of the loop and they time the DFMA alone (not
+// run). FORMs 8-17 load the operands from shared memory every k, as the tile
+// kernel does. Prints cycles per
+// warp-product per SMSP at the measured clock.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o thetabench tools/thetabench.cu
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+constexpr int TM = 8, TN = 4, ITERS = 4096;
+
+__device__ __forceinline__ unsigned hi(double x) { return static_cast<unsigned>(__double2hiint(x)); }
+__device__ __forceinline__ unsigned lo(double x) { return static_cast<unsigned>(__double2loint(x)); }
+
+template <int FORM>
+__global__ void __launch_bounds__(384, 1) kern(double* out, const double* in, long long* cyc) {
+    double a[TM], th[TN], x0[TN], x1[TN], acc[TM][TN];
+    float ahf[TM], thf[TN];
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int r = 0; r < TM; ++r) a[r] = in[(t + r) & 63];
+#pragma unroll
+    for (int c = 0; c < TN; ++c) {
+        th[c] = in[64 + ((t + 3 * c) & 63)];
+        x0[c] = in[128 + ((t + 5 * c) & 63)];
+        x1[c] = in[192 + ((t + 7 * c) & 63)];
+    }
+#pragma unroll
+    for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int c = 0; c < TN; ++c) acc[r][c] = 0.0;
+    // shared tiles for the smem-fed forms: A as [rows][16 k] (row-broadcast
+    // reads, as the tile kernel), B planes as [3][8 k][128 cols]
+    __shared__ __align__(16) double sA[96 * 16];
+    __shared__ __align__(16) double sB[3 * 8 * 128];
+    for (int i = t; i < 96 * 16; i += blockDim.x) sA[i] = in[i & 63];
+    for (int i = t; i < 3 * 8 * 128; i += blockDim.x) sB[i] = in[64 + (i & 191)];
+    __syncthreads();
+    const int lane = t & 31, warp = t >> 5;
+    const long long c0 = clock64();
+    if constexpr (FORM >= 8) {
+        // smem-fed: 8: row outer, loads then compute per k; 9: loads for the next
+        // k issued before this k's compute (register double buffer); 10: B from
+        // smem, a from registers; 11: a from smem, B from registers
+        double na[TM], nth[TN], nx0[TN], nx1[TN];
+        auto load = [&](int k, double* la, double* lth, double* lx0, double* lx1) {
+            if constexpr (FORM != 10) {
+#pragma unroll
+                for (int r = 0; r < TM; ++r) la[r] = sA[(warp * 8 + r) * 16 + k];
+            }
+            if constexpr (FORM != 11) {
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    const double2 t2 = *reinterpret_cast<const double2*>(sB + k * 128 + q * 64 + lane * 2);
+                    const double2 p2 = *reinterpret_cast<const double2*>(sB + 1024 + k * 128 + q * 64 + lane * 2);
+                    const double2 x2 = *reinterpret_cast<const double2*>(sB + 2048 + k * 128 + q * 64 + lane * 2);
+                    lth[2 * q] = t2.x; lth[2 * q + 1] = t2.y;
+                    lx0[2 * q] = p2.x; lx0[2 * q + 1] = p2.y;
+                    lx1[2 * q] = x2.x; lx1[2 * q + 1] = x2.y;
+                }
+            }
+        };
+        auto compute = [&](const double* la, const double* lth, const double* lx0, const double* lx1) {
+            if constexpr (FORM == 13 || FORM == 14) {  // compare the high words (f32 / s32)
+#pragma unroll
+                for (int c = 0; c < TN; ++c)
+#pragma unroll
+                    for (int r = 0; r < TM; ++r) {
+                        bool m;
+                        if constexpr (FORM == 13)
+                            m = __uint_as_float(hi(la[r])) > __uint_as_float(hi(lth[c]));
+                        else
+                            m = static_cast<int>(hi(la[r])) > static_cast<int>(hi(lth[c]));
+                        acc[r][c] = __fma_rn(la[r], m ? lx1[c] : lx0[c], acc[r][c]);
+                    }
+                return;
+            }
+            if constexpr (FORM == 15) {  // DFMA only (the feed plus the FP64 pipe)
+#pragma unroll
+                for (int c = 0; c < TN; ++c)
+#pragma unroll
+                    for (int r = 0; r < TM; ++r) acc[r][c] = __fma_rn(la[r], lx0[c], acc[r][c]);
+                return;
+            }
+            if constexpr (FORM == 16) {  // DSETP + 2 FSEL only, into the accumulator
+#pragma unroll
+                for (int c = 0; c < TN; ++c)
+#pragma unroll
+                    for (int r = 0; r < TM; ++r) acc[r][c] = la[r] > lth[c] ? lx1[c] : acc[r][c];
+                return;
+            }
+            if constexpr (FORM == 17) {  // FSETP (high words) + 2 FSEL only, into the accumulator
+#pragma unroll
+                for (int c = 0; c < TN; ++c)
+#pragma unroll
+                    for (int r = 0; r < TM; ++r)
+                        acc[r][c] = __uint_as_float(hi(la[r])) > __uint_as_float(hi(lth[c])) ? lx1[c] : acc[r][c];
+                return;
+            }
+            if constexpr (FORM == 12) {
+#pragma unroll
+                for (int c = 0; c < TN; ++c)
+#pragma unroll
+                    for (int r = 0; r < TM; ++r)
+                        acc[r][c] = __fma_rn(la[r], la[r] > lth[c] ? lx1[c] : lx0[c], acc[r][c]);
+                return;
+            }
+#pragma unroll
+            for (int r = 0; r < TM; ++r)
+#pragma unroll
+                for (int c = 0; c < TN; ++c)
+                    acc[r][c] = __fma_rn(la[r], la[r] > lth[c] ? lx1[c] : lx0[c], acc[r][c]);
+        };
+        if constexpr (FORM == 9) {
+            load(0, na, nth, nx0, nx1);
+            for (int it = 0; it < ITERS; it += 2) {
+                load((it + 1) & 7, a, th, x0, x1);
+                compute(na, nth, nx0, nx1);
+                load((it + 2) & 7, na, nth, nx0, nx1);
+                compute(a, th, x0, x1);
+            }
+        } else {
+#pragma unroll 2
+            for (int it = 0; it < ITERS; ++it) {
+                load(it & 7, a, th, x0, x1);
+                compute(a, th, x0, x1);
+            }
+        }
+    } else
+    for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+        for (int r = 0; r < TM; ++r) asm volatile("" : "+d"(a[r]));
+#pragma unroll
+        for (int c = 0; c < TN; ++c) asm volatile("" : "+d"(th[c]), "+d"(x0[c]), "+d"(x1[c]));
+        if constexpr (FORM == 0) {  // C: row-inner, as the tile kernel writes it (column outer)
+#pragma unroll
+            for (int c = 0; c < TN; ++c)
+#pragma unroll
+                for (int r = 0; r < TM; ++r) acc[r][c] = __fma_rn(a[r], a[r] > th[c] ? x1[c] : x0[c], acc[r][c]);
+        } else if constexpr (FORM == 1) {  // C: column-inner
+#pragma unroll
+            for (int r = 0; r < TM; ++r)
+#pragma unroll
+                for (int c = 0; c < TN; ++c) acc[r][c] = __fma_rn(a[r], a[r] > th[c] ? x1[c] : x0[c], acc[r][c]);
+        } else if constexpr (FORM == 2) {  // PTX grouped per column: setp x8, selp lo x8, selp hi x8, fma x8
+#pragma unroll
+            for (int c = 0; c < TN; ++c) {
+                asm volatile(
+                    "{\n .reg .pred p<8>; .reg .b32 l<8>, h<8>; .reg .f64 x<8>;\n"
+                    " .reg .b32 x0l, x0h, x1l, x1h;\n"
+                    " mov.b64 {x0l, x0h}, %9; mov.b64 {x1l, x1h}, %10;\n"
+                    " setp.gt.f64 p0, %11, %8; setp.gt.f64 p1, %12, %8; setp.gt.f64 p2, %13, %8; setp.gt.f64 p3, %14, %8;\n"
+                    " setp.gt.f64 p4, %15, %8; setp.gt.f64 p5, %16, %8; setp.gt.f64 p6, %17, %8; setp.gt.f64 p7, %18, %8;\n"
+                    " selp.b32 l0, x1l, x0l, p0; selp.b32 l1, x1l, x0l, p1; selp.b32 l2, x1l, x0l, p2; selp.b32 l3, x1l, x0l, p3;\n"
+                    " selp.b32 l4, x1l, x0l, p4; selp.b32 l5, x1l, x0l, p5; selp.b32 l6, x1l, x0l, p6; selp.b32 l7, x1l, x0l, p7;\n"
+                    " selp.b32 h0, x1h, x0h, p0; selp.b32 h1, x1h, x0h, p1; selp.b32 h2, x1h, x0h, p2; selp.b32 h3, x1h, x0h, p3;\n"
+                    " selp.b32 h4, x1h, x0h, p4; selp.b32 h5, x1h, x0h, p5; selp.b32 h6, x1h, x0h, p6; selp.b32 h7, x1h, x0h, p7;\n"
+                    " mov.b64 x0, {l0, h0}; mov.b64 x1, {l1, h1}; mov.b64 x2, {l2, h2}; mov.b64 x3, {l3, h3};\n"
+                    " mov.b64 x4, {l4, h4}; mov.b64 x5, {l5, h5}; mov.b64 x6, {l6, h6}; mov.b64 x7, {l7, h7};\n"
+                    " fma.rn.f64 %0, %11, x0, %0; fma.rn.f64 %1, %12, x1, %1; fma.rn.f64 %2, %13, x2, %2; fma.rn.f64 %3, %14, x3, %3;\n"
+                    " fma.rn.f64 %4, %15, x4, %4; fma.rn.f64 %5, %16, x5, %5; fma.rn.f64 %6, %17, x6, %6; fma.rn.f64 %7, %18, x7, %7;\n"
+                    "}\n"
+                    : "+d"(acc[0][c]), "+d"(acc[1][c]), "+d"(acc[2][c]), "+d"(acc[3][c]), "+d"(acc[4][c]),
+                      "+d"(acc[5][c]), "+d"(acc[6][c]), "+d"(acc[7][c])
+                    : "d"(th[c]), "d"(x0[c]), "d"(x1[c]), "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]),
+                      "d"(a[5]), "d"(a[6]), "d"(a[7]));
+            }
+        } else if constexpr (FORM == 3 || FORM == 4) {
+            // compare on the high words only (valid when every a >= 0 has a zero low word):
+            // 3: as f32 (FSETP), 4: as s32 (ISETP)
+#pragma unroll
+            for (int r = 0; r < TM; ++r) ahf[r] = __uint_as_float(hi(a[r]));
+#pragma unroll
+            for (int c = 0; c < TN; ++c) thf[c] = __uint_as_float(hi(th[c]));
+#pragma unroll
+            for (int c = 0; c < TN; ++c)
+#pragma unroll
+                for (int r = 0; r < TM; ++r) {
+                    bool m;
+                    if constexpr (FORM == 3)
+                        m = ahf[r] > thf[c];
+                    else
+                        m = static_cast<int>(hi(a[r])) > static_cast<int>(hi(th[c]));
+                    acc[r][c] = __fma_rn(a[r], m ? x1[c] : x0[c], acc[r][c]);
+                }
+        } else if constexpr (FORM == 5) {  // DFMA only, a shared per row (the pipe's own rate)
+#pragma unroll
+            for (int c = 0; c < TN; ++c)
+#pragma unroll
+                for (int r = 0; r < TM; ++r) acc[r][c] = __fma_rn(a[r], x0[c], acc[r][c]);
+        } else if constexpr (FORM == 6) {  // DSETP + 2 FSEL only (no DFMA): select into acc
+#pragma unroll
+            for (int c = 0; c < TN; ++c)
+#pragma unroll
+                for (int r = 0; r < TM; ++r) acc[r][c] = a[r] > th[c] ? x1[c] : acc[r][c];
+        } else if constexpr (FORM == 7) {  // 2 DFMA per product (the 3-op ordinary discount's pipe load minus the select)
+#pragma unroll
+            for (int c = 0; c < TN; ++c)
+#pragma unroll
+                for (int r = 0; r < TM; ++r) acc[r][c] = __fma_rn(a[r], x0[c], __fma_rn(a[r], x1[c], acc[r][c]));
+        }
+    }
+    const long long c1 = clock64();
+    double s = 0;
+#pragma unroll
+    for (int r = 0; r < TM; ++r)
+#pragma unroll
+        for (int c = 0; c < TN; ++c) s += acc[r][c];
+    if (s == 1234.5) out[t] = s;
+    if (t == 0) cyc[blockIdx.x] = c1 - c0;
+}
+
+template <int FORM>
+void run(int sms, int blk, const char* name, double* out, const double* in, long long* cyc) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    kern<FORM><<<sms * blk, 384>>>(out, in, cyc);
+    cudaEventRecord(e0);
+    kern<FORM><<<sms * blk, 384>>>(out, in, cyc);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    long long h[1];
+    cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
+    // 12 warps per SM = 3 per SMSP, each ITERS * TM * TN warp-products
+    printf("%-58s %8.3f ms  %.2f cycles/warp-product/SMSP (clock64, block 0)\n", name, ms,
+           double(h[0]) / (double(ITERS) * TM * TN * 3));
+}
+
+int main() {
+    int sms;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    double *out, *in;
+    long long* cyc;
+    cudaMalloc(&out, 4096 * 8);
+    cudaMalloc(&in, 256 * 8);
+    cudaMalloc(&cyc, 4096 * 8);
+    double h[256];
+    for (int i = 0; i < 64; ++i) h[i] = double(i % 10);                 // a: integers 0..9
+    for (int i = 0; i < 64; ++i) h[64 + i] = 0.5 + (i * 37 % 64) * 0.13;  // theta
+    for (int i = 0; i < 64; ++i) h[128 + i] = 1.0 + i * 1.37;             // x0
+    for (int i = 0; i < 64; ++i) h[192 + i] = 0.8 * (1.0 + i * 1.37);     // x1
+    cudaMemcpy(in, h, sizeof(h), cudaMemcpyHostToDevice);
+    {
+        const int blk = 1;
+        run<8>(sms, blk, "8 smem-fed, row outer", out, in, cyc);
+        run<9>(sms, blk, "9 smem-fed, next k loaded before this k's compute", out, in, cyc);
+        run<10>(sms, blk, "10 B from smem, a in registers", out, in, cyc);
+        run<11>(sms, blk, "11 a from smem, B in registers", out, in, cyc);
+        run<12>(sms, blk, "12 smem-fed, column outer (as the tile kernel)", out, in, cyc);
+        run<13>(sms, blk, "13 smem-fed, high-word compare as f32 (FSETP)", out, in, cyc);
+        run<14>(sms, blk, "14 smem-fed, high-word compare as s32 (ISETP)", out, in, cyc);
+        run<15>(sms, blk, "15 smem-fed, DFMA only", out, in, cyc);
+        run<16>(sms, blk, "16 smem-fed, DSETP + 2 FSEL only", out, in, cyc);
+        run<17>(sms, blk, "17 smem-fed, FSETP + 2 FSEL only", out, in, cyc);
+    }
+    return 0;
+}
