@@ -413,6 +413,8 @@ def main():
         "tcgen05_3xtf32" in plan.variants()[last.best_variant].name
     win_is_oz = last is not None and last.best_variant >= 0 and \
         "ozaki" in plan.variants()[last.best_variant].name
+    win_is_swar = last is not None and last.best_variant >= 0 and \
+        "_swar_" in plan.variants()[last.best_variant].name
     win_is_theta = last is not None and last.best_variant >= 0 and \
         "_theta_" in plan.variants()[last.best_variant].name
     for s in range(steps):
@@ -424,7 +426,9 @@ def main():
         # tcgen05 3xTF32: operand split of A, of B, then the tensor-core GEMM
         # Ozaki: row / column exponents, A / B slicing, then the int8 GEMM
         # theta-form discount: B planes, A range scan, theta tile, guard-exited fallback
-        launches += 3 if win_is_tc else (5 if win_is_oz else (4 if win_is_theta else (2 if split else 1)))
+        # byte-packed eqcount: B packing, A packing, packed tile, guard-exited fallback
+        launches += 3 if win_is_tc else (5 if win_is_oz else (4 if (win_is_theta or win_is_swar)
+                                                              else (2 if split else 1)))
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -506,6 +510,10 @@ def main():
         ops_per_iter = {"discount": 3, "boost": 3, "gemm": 1, "sqdiff": 2, "eqcount": 1}[body]
         if best >= 0 and "_theta_" in variants[best].name:
             ops_per_iter = 2  # theta form: DSETP + DFMA per iteration (csrc/theta_discount.cu)
+        if best >= 0 and "_swar_" in variants[best].name:
+            # byte-packed eqcount: XOR, AND, LEA.HI on the ALU per packed word of
+            # 4 iterations (the add runs on the FMA pipe; csrc/swar_eqcount.cu)
+            ops_per_iter = 0.75
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s",
             "inner_iters_per_s": iters_total / el,
@@ -543,6 +551,12 @@ def main():
                              "tensor-core products per iteration (3xTF32), peak = measured dense "
                              "bf16 (MEASURED_PEAKS.json) / 2 (TF32 rate) / 3"
                              if tensor_tf32 else
+                             "2 ops per inner iteration (matmul-like); peak = the SM issue rate "
+                             f"(128 lane-instructions/clk/SM) at the probe's {peak_ghz:.3f} GHz; the "
+                             "byte-packed body runs 3 ALU instructions per 4 iterations (XOR, AND, "
+                             "LEA.HI; the add on the FMA pipe), the ALU taking 64 "
+                             "lane-instructions/clk/SM: a ceiling of 4/3 of that peak"
+                             if pipe == "alu" and "_swar_" in win_name else
                              "2 ops per inner iteration (matmul-like); peak = the SM issue rate "
                              f"(128 lane-instructions/clk/SM) at the probe's {peak_ghz:.3f} GHz; the "
                              "body issues exactly 2 instructions per iteration"

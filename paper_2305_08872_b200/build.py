@@ -59,7 +59,7 @@ def _jobs():
         out = os.path.join(OBJ, f"k_{body}_{dt}.o")
         defs = [f"-DAMLT_BODY={body}", f"-DAMLT_BODY_ID={bid}", f"-DAMLT_T={ctype}", f"-DAMLT_DT={dt}"]
         jobs.append((inst, out, defs))
-    for src in ("dmma_gemm.cu", "tcgen05_gemm.cu", "ozaki_gemm.cu", "theta_discount.cu", "register_all.cu", "amlt_gpu.cu", "peak.cu", "task.cpp",
+    for src in ("dmma_gemm.cu", "tcgen05_gemm.cu", "ozaki_gemm.cu", "theta_discount.cu", "swar_eqcount.cu", "register_all.cu", "amlt_gpu.cu", "peak.cu", "task.cpp",
                 "sharded.cu", "matrix_file.cpp", "naive.cu", "jit.cu"):
         obj = os.path.splitext(src)[0] + ".o"
         jobs.append((os.path.join(CSRC, src), os.path.join(OBJ, obj), []))

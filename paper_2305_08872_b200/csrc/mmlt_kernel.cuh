@@ -360,6 +360,23 @@ struct HasAt<Body, decltype(void(Body::HAS_AT))> {
     static constexpr bool value = Body::HAS_AT;
 };
 
+// Two-level bodies may fold the per-BK-tile partial into the running
+// accumulator their own way (FOLD: Body::fold(acc, part)); the default adds.
+template <class Body, class = void>
+struct BodyFold {
+    template <typename Acc>
+    __device__ static __forceinline__ void go(Acc& acc, const Acc& part) {
+        acc += part;
+    }
+};
+template <class Body>
+struct BodyFold<Body, decltype(void(Body::FOLD))> {
+    template <typename Acc>
+    __device__ static __forceinline__ void go(Acc& acc, const Acc& part) {
+        Body::fold(acc, part);
+    }
+};
+
 // Bodies whose B operand is a prepared multi-plane array (BPLANES planes of
 // K x N, one TMA box per stage covers all planes).
 template <class Body, class = void>
@@ -772,7 +789,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
                 for (int c = 0; c < TN; ++c)
 #pragma unroll
                     for (int n = 0; n < NACC; ++n) {
-                        acc[r][c][n] += part[r][c][n];
+                        BodyFold<Body>::go(acc[r][c][n], part[r][c][n]);
                         part[r][c][n] = Acc(0);
                     }
         }

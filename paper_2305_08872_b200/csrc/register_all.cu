@@ -15,6 +15,7 @@ void register_dmma_gemm(Registry&);
 void register_tcgen05_gemm(Registry&);
 void register_ozaki_gemm(Registry&);
 void register_theta_discount(Registry&);
+void register_swar_eqcount(Registry&);
 
 void register_all(Registry& reg) {
 #define AMLT_CALL(B, D) register_##B##_##D(reg);
@@ -23,6 +24,7 @@ void register_all(Registry& reg) {
     register_tcgen05_gemm(reg);
     register_ozaki_gemm(reg);
     register_theta_discount(reg);
+    register_swar_eqcount(reg);
 }
 
 }  // namespace amltk
