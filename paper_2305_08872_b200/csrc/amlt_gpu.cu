@@ -881,8 +881,15 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
         }
         if (need <= cap) break;
     }
-    const bool tunable = plan->desc.accumulate && !cands.empty() && whole.K > 0 && whole.N > 0 &&
-                         need <= cap && ctx->tune_cache.find(key) == ctx->tune_cache.end();
+    // Tasks cheap enough to repeat are measured whole on the scratch R even
+    // when row bands would fit: a band of a few waves sees a different L2
+    // (its B panels stay resident, the whole task's do not), and at config
+    // 1's shape that misranked the tiles by up to 12% (tools/tuner_stability.py,
+    // profiles/r01/tuner_stability.txt). A caller-supplied clock keeps the
+    // band trials: its readings are the AMULET contract's scores.
+    const bool prefer_scratch = scratch_ok && !clock && !ctx->dry();
+    const bool tunable = !prefer_scratch && plan->desc.accumulate && !cands.empty() && whole.K > 0 &&
+                         whole.N > 0 && need <= cap && ctx->tune_cache.find(key) == ctx->tune_cache.end();
 
     auto run_rect = [&](const amlt_bounds& rb, int variant, int64_t kc) {
         amlt_tile_params tp{kc, 0, 0, plan_local_index(plan, variant)};
