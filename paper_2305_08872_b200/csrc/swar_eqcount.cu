@@ -37,14 +37,17 @@
 namespace amltk {
 namespace sw {
 
-// Header ints: min / max of B (prepared once per call), min / max of A (per run).
+// Header words: min / max of B (prepared once per call), min / max of A (per
+// run), as order-preserving unsigned keys v ^ 0x80000000, so the sentinels
+// are plain byte fills (0xFF.. for min, 0 for max) below / above any value.
 enum { G_BMIN = 0, G_BMAX, G_AMIN, G_AMAX };
+__host__ __device__ __forceinline__ unsigned okey32(int v) { return static_cast<unsigned>(v) ^ 0x80000000u; }
 constexpr int HEADER = 256;  // bytes before the packed operands
 
 __device__ __forceinline__ bool window_ok(const KParams& p) {
-    const int* g = p.guard;
-    const long long mn = min(g[G_BMIN], g[G_AMIN]), mx = max(g[G_BMAX], g[G_AMAX]);
-    return mx - mn <= 127;  // (no elements: mx < mn)
+    const unsigned* g = reinterpret_cast<const unsigned*>(p.guard);
+    const unsigned mn = min(g[G_BMIN], g[G_AMIN]), mx = max(g[G_BMAX], g[G_AMAX]);
+    return mx < mn || mx - mn <= 127u;  // (mx < mn: no elements)
 }
 
 // (Moving the add or the count onto the FMA pipe as integer multiply-adds
@@ -83,8 +86,9 @@ struct BodyEqFallback : BodyEqcount<int> {
 int64_t kw_of(int64_t K) { return ((K + 3) / 4 + 3) / 4 * 4; }  // words per packed row (16-byte pitch)
 int64_t npad_of(int64_t N) { return (N + 3) / 4 * 4; }
 
-__device__ __forceinline__ void block_minmax(int mn, int mx, int* g, int slot_min) {
-    __shared__ int red[2][8];
+__device__ __forceinline__ void block_minmax(unsigned mn, unsigned mx, int* gi, int slot_min) {
+    unsigned* g = reinterpret_cast<unsigned*>(gi);
+    __shared__ unsigned red[2][8];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     mn = __reduce_min_sync(0xffffffffu, mn);
     mx = __reduce_max_sync(0xffffffffu, mx);
@@ -98,8 +102,8 @@ __device__ __forceinline__ void block_minmax(int mn, int mx, int* g, int slot_mi
             mn = min(mn, red[0][w]);
             mx = max(mx, red[1][w]);
         }
-        if (mn != INT_MAX) atomicMin(g + slot_min, mn);
-        if (mx != INT_MIN) atomicMax(g + slot_min + 1, mx);
+        if (mn != 0xFFFFFFFFu) atomicMin(g + slot_min, mn);
+        if (mx != 0u) atomicMax(g + slot_min + 1, mx);
     }
 }
 
@@ -107,7 +111,7 @@ __device__ __forceinline__ void block_minmax(int mn, int mx, int* g, int slot_mi
 __global__ void __launch_bounds__(256) pack_b_kernel(const KParams p, unsigned* B4, int64_t kw, int64_t npad,
                                                      int* g) {
     const int* B = static_cast<const int*>(p.B);
-    int mn = INT_MAX, mx = INT_MIN;
+    unsigned mn = 0xFFFFFFFFu, mx = 0u;
     const int64_t total = kw * npad;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -119,8 +123,8 @@ __global__ void __launch_bounds__(256) pack_b_kernel(const KParams p, unsigned* 
             unsigned byte = 1u;
             if (k < p.K && j < p.N) {
                 const int v = B[k * p.ldb + j];
-                mn = min(mn, v);
-                mx = max(mx, v);
+                mn = min(mn, okey32(v));
+                mx = max(mx, okey32(v));
                 byte = static_cast<unsigned>(v) & 0x7Fu;
             }
             word |= byte << (8 * e);
@@ -133,7 +137,7 @@ __global__ void __launch_bounds__(256) pack_b_kernel(const KParams p, unsigned* 
 // A4[i][w] = bytes (A[i][4w + e] & 0x7F); 0 past K
 __global__ void __launch_bounds__(256) pack_a_kernel(const KParams p, unsigned* A4, int64_t kw, int* g) {
     const int* A = static_cast<const int*>(p.A);
-    int mn = INT_MAX, mx = INT_MIN;
+    unsigned mn = 0xFFFFFFFFu, mx = 0u;
     const int64_t total = p.M * kw;
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -141,8 +145,8 @@ __global__ void __launch_bounds__(256) pack_a_kernel(const KParams p, unsigned* 
         unsigned word = 0;
         if (4 * w + 3 < p.K) {  // one 16-byte load (the variants take 16-byte aligned operands)
             const int4 v = *reinterpret_cast<const int4*>(A + i * p.lda + 4 * w);
-            mn = min(mn, min(min(v.x, v.y), min(v.z, v.w)));
-            mx = max(mx, max(max(v.x, v.y), max(v.z, v.w)));
+            mn = min(mn, okey32(min(min(v.x, v.y), min(v.z, v.w))));
+            mx = max(mx, okey32(max(max(v.x, v.y), max(v.z, v.w))));
             word = (static_cast<unsigned>(v.x) & 0x7Fu) | ((static_cast<unsigned>(v.y) & 0x7Fu) << 8) |
                    ((static_cast<unsigned>(v.z) & 0x7Fu) << 16) | ((static_cast<unsigned>(v.w) & 0x7Fu) << 24);
         } else {
@@ -151,8 +155,8 @@ __global__ void __launch_bounds__(256) pack_a_kernel(const KParams p, unsigned* 
                 const int64_t k = 4 * w + e;
                 if (k < p.K) {
                     const int v = A[i * p.lda + k];
-                    mn = min(mn, v);
-                    mx = max(mx, v);
+                    mn = min(mn, okey32(v));
+                    mx = max(mx, okey32(v));
                     word |= (static_cast<unsigned>(v) & 0x7Fu) << (8 * e);
                 }
             }
@@ -165,10 +169,10 @@ __global__ void __launch_bounds__(256) pack_a_kernel(const KParams p, unsigned* 
 size_t b_bytes(const KParams& p) { return size_t(kw_of(p.K)) * size_t(npad_of(p.N)) * 4; }
 size_t ws_bytes(const KParams& p) { return HEADER + b_bytes(p) + size_t(p.M) * size_t(kw_of(p.K)) * 4; }
 
-// min slots start at INT_MAX-ish (0x7F7F7F7F), max slots at INT_MIN-ish (0x80808080)
+// min slot starts at the largest key, max slot at the smallest
 cudaError_t reset_stats(int* g, int slot_min, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(g + slot_min, 0x7F, sizeof(int), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(g + slot_min + 1, 0x80, sizeof(int), s);
+    cudaError_t e = cudaMemsetAsync(g + slot_min, 0xFF, sizeof(int), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(g + slot_min + 1, 0x00, sizeof(int), s);
     return e;
 }
 
