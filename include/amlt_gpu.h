@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define AMLT_GPU_ABI_VERSION 2
+#define AMLT_GPU_ABI_VERSION 3
 
 /* Aux arrays one generated (AMLT_BODY_GENERIC) statement may name. */
 #define AMLT_MAX_AUX 8
@@ -274,6 +274,13 @@ amlt_status amlt_gpu_set_stream(amlt_ctx* ctx, void* stream);
 /* Forget tuning winners cached by amlt_gpu_adaptive_execute. */
 void amlt_gpu_clear_tuning_cache(amlt_ctx* ctx);
 
+/* Pseudo-program opcodes (schedule.hpp:11-15, POpcode order). */
+enum {
+    AMLT_PROG_MOV = 0, AMLT_PROG_ADD, AMLT_PROG_SUB, AMLT_PROG_MUL, AMLT_PROG_DIV,
+    AMLT_PROG_GTCMP, AMLT_PROG_GECMP, AMLT_PROG_LTCMP, AMLT_PROG_LECMP, AMLT_PROG_EQCMP,
+    AMLT_PROG_MASKSUB, AMLT_PROG_MASKADD, AMLT_PROG_NOPS
+};
+
 /* The compile_task boundary (src/engine.cpp:86-102): which GPU body a task
  * text is, and which arrays play A, B, R, the threshold and the discount
  * vector. Names are "" for absent roles. GENERIC statements list their aux
@@ -288,6 +295,16 @@ typedef struct {
     int32_t n_aux;
     char aux_names[AMLT_MAX_AUX][64];
     int32_t aux_class[AMLT_MAX_AUX]; /* amlt_leaf_class */
+    /* The reference's compiled program for this statement (build_dag +
+     * schedule_labelfs: one pseudo-instruction per DAG op node with equal
+     * subexpressions shared, plus the final accumulate; expr_dag.cpp:63-245,
+     * schedule.cpp:265-273): instructions per opcode (AMLT_PROG_*), their
+     * total, and the body-op flops per inner iteration (add / sub / mul / div /
+     * compare 1, masksub / maskadd 2, the final add 1, mov 0): SURVEY §8(d)'s
+     * measure (B). */
+    int32_t prog_counts[AMLT_PROG_NOPS];
+    int32_t prog_instrs;
+    int32_t prog_flops;
 } amlt_task_info;
 
 /* Parses and recognises a task in the reference DSL. UNSUPPORTED for a task
@@ -346,6 +363,13 @@ amlt_status amlt_gpu_adaptive_execute(amlt_ctx* ctx, const amlt_plan* plan,
 
 /* run_host flags */
 #define AMLT_HOST_R_ZERO 1 /* R starts at zero: device R is zero-filled, not copied in */
+/* With a communicator attached (amlt_gpu_comm_attach, or a rank of an
+ * amlt_sharded group): B and the operands every rank shares (thresholds and
+ * leaves indexed by nothing or by j) are read from host memory on rank 0 only
+ * and broadcast to the other ranks over NVLink / NVSwitch (NCCL), panel by
+ * panel as they land, overlapping compute. Other ranks pass the shapes of
+ * those operands with data == NULL; every rank passes its own A / R rows. */
+#define AMLT_HOST_BCAST_SHARED 2
 
 /* AMULET's own tuner contract, restated on the GPU executor
  * (src/autotuner.cpp:8-151): find_kc lays kc candidates (K, then repeated
@@ -392,18 +416,46 @@ amlt_status amlt_gpu_adaptive_execute_amulet(amlt_ctx* ctx, const amlt_plan* pla
                                              void* clock_user, amlt_exec_log* log,
                                              amlt_amulet_report* report);
 
-/* Host-buffer entry (the reference's callers hold host MatrixBuffers):
- * operands' `data` are HOST pointers (pinned for full copy bandwidth).
- * Copies B and the aux vectors, then streams A (and R, unless
- * AMLT_HOST_R_ZERO) to the device in row bands on a copy stream while the
- * previous band computes, and streams finished R bands back on a second
- * copy stream. The tile: `tile` if given, else the winner cached by an
- * earlier amlt_gpu_adaptive_execute of the same shape, else the planner
+/* Host-buffer entry (the reference's callers hold host MatrixBuffers:
+ * run_fixed / run_adaptive, src/engine.cpp:165-175): operands' `data` are
+ * HOST pointers (pinned for full copy bandwidth). A copy / compute pipeline:
+ * A (and R, unless AMLT_HOST_R_ZERO) in row bands and B in K panels go H2D on
+ * a copy stream; compute starts once the first band and the first panel
+ * are resident and runs panel by panel over the bands (the kernels
+ * accumulate into R); each R band goes back D2H on a second copy stream as
+ * soon as its last panel is done. B is cut into K panels when its k rows are
+ * contiguous (B[k][j] row-major, B[j][k] col-major), the winner is not
+ * split-K and the statement accumulates. The tile: `tile` if given, else the
+ * winner cached by an earlier tuning of the same shape, else the planner
  * default. *elapsed_s covers all copies and compute (the clock, if any, is
  * read exactly twice around all of it). */
 amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* host_ops,
                               const amlt_tile_params* tile, const amlt_bounds* bounds, int flags,
                               amlt_clock_fn clock, void* clock_user, double* elapsed_s);
+/* run_adaptive over host buffers: amlt_gpu_run_host whose tile comes from
+ * the runtime tuner. When no winner is cached for the shape, the operands
+ * are copied whole and the task runs through amlt_gpu_adaptive_execute
+ * (row-band or scratch trials, the remainder with the winner; a caller clock
+ * scores the trials, read twice around each of them); later calls of the
+ * shape reuse the winner through the pipeline. *report: the trials (empty
+ * when the winner was cached: from_cache = 1), the winner, and coverage
+ * rectangles that are disjoint with union = bounds. */
+amlt_status amlt_gpu_run_host_adaptive(amlt_ctx* ctx, const amlt_plan* plan,
+                                       const amlt_operands* host_ops, const amlt_bounds* bounds,
+                                       int flags, amlt_clock_fn clock, void* clock_user,
+                                       amlt_tune_report* report, double* elapsed_s);
+
+/* Multi-process (one process per GPU, e.g. torchrun) communicator for
+ * AMLT_HOST_BCAST_SHARED: rank 0 makes an id (AMLT_NCCL_ID_BYTES opaque
+ * bytes), the caller hands it to every rank by its own means, and every rank
+ * attaches it to its context (collective: blocks until all ranks attach).
+ * NCCL (libnccl.so.2) is loaded at run time. */
+#define AMLT_NCCL_ID_BYTES 128
+amlt_status amlt_gpu_comm_unique_id(void* id_out);
+amlt_status amlt_gpu_comm_attach(amlt_ctx* ctx, const void* id, int rank, int nranks);
+amlt_status amlt_gpu_comm_detach(amlt_ctx* ctx);
+/* Ranks of the attached communicator (1 when none). */
+int amlt_gpu_comm_size(const amlt_ctx* ctx);
 
 /* Row-band multi-GPU execution of one task from a single process (the
  * reference engine's process model). Device d of n owns rows
@@ -431,6 +483,28 @@ amlt_status amlt_gpu_run_sharded_source(const char* task_source, int dtype,
                                         double* elapsed_s);
 /* Message of the calling thread's last failing amlt_gpu_run_sharded(_source). */
 const char* amlt_gpu_sharded_last_error(void);
+
+/* The persistent form of amlt_gpu_run_sharded: a row-band group over n
+ * devices of this process, made once (one context per device, one NCCL
+ * communicator from ncclCommInitAll). Plans and tuning winners persist
+ * across runs, so only the first run of a shape tunes. Each run: device d of
+ * n owns rows [i0 + M d/n, i0 + M (d+1)/n) (edges on multiples of 64 rows);
+ * every device runs the host pipeline of amlt_gpu_run_host_adaptive on its
+ * band, device 0 reading B and the shared operands from host memory and
+ * broadcasting them panel by panel (AMLT_HOST_BCAST_SHARED); R bands stream
+ * back as they finish. The plan is `desc` when task_source is NULL, else the
+ * task text (generated bodies included). reports: NULL or n entries, one per
+ * device. *elapsed_s: wall time of the whole run. */
+typedef struct amlt_sharded amlt_sharded;
+amlt_status amlt_sharded_create(int n_devices, const int* devices, int ctx_flags, amlt_sharded** out);
+void amlt_sharded_destroy(amlt_sharded* group);
+amlt_status amlt_sharded_run(amlt_sharded* group, const amlt_body_desc* desc, const char* task_source,
+                             int dtype, const amlt_operands* host_ops, const amlt_bounds* bounds,
+                             int flags, amlt_tune_report* reports, double* elapsed_s);
+int amlt_sharded_size(const amlt_sharded* group);
+/* Message of the group's last failing call (or of amlt_sharded_create when
+ * group == NULL). Never NULL. */
+const char* amlt_sharded_last_error(const amlt_sharded* group);
 
 /* The reference's AMLT binary matrix files (README.md:146-157,
  * src/matrix.cpp:64-114; the CLI's --a-file / --b-file): 24-byte header

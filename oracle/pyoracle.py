@@ -151,7 +151,8 @@ def ref_lib():
                    "ref_task_array_name", "ref_task_result_name", "ref_task_array_shape",
                    "ref_task_array_get", "ref_task_array_set", "ref_task_bounds",
                    "ref_task_run_naive", "ref_task_run_adaptive", "ref_task_run_fixed",
-                   "ref_task_run_scalar_region", "ref_task_run_adaptive_bands", "ref_task_roles"):
+                   "ref_task_run_scalar_region", "ref_task_run_adaptive_bands", "ref_task_roles",
+                   "ref_task_program"):
             getattr(lib, fn).argtypes = None
         lib.ref_task_array_name.restype = C.c_char_p
         lib.ref_task_result_name.restype = C.c_char_p
@@ -271,6 +272,15 @@ class RefTask:
 
     def result_name(self) -> str:
         return ref_lib().ref_task_result_name(self._h).decode()
+
+    def program(self) -> list:
+        """The reference's compiled pseudo-program (schedule_labelfs +
+        print_program): one "opcode dst src..." string per instruction."""
+        buf = C.create_string_buffer(1 << 14)
+        n = ref_lib().ref_task_program(self._h, buf, C.c_int(len(buf)))
+        if n < 0:
+            raise RuntimeError("not an MMLT task")
+        return [ln for ln in buf.value.decode().splitlines() if ln.strip()]
 
     def roles(self):
         a, b, aux = (C.create_string_buffer(256) for _ in range(3))

@@ -30,6 +30,7 @@
 #include "amlt/errors.hpp"
 #include "amlt/matrix.hpp"
 #include "amlt/presets.hpp"
+#include "amlt/schedule.hpp"
 
 using namespace amlt;
 
@@ -104,6 +105,19 @@ void* ref_task_new(const char* src, std::int64_t M, std::int64_t K, std::int64_t
 void ref_task_free(void* h) { delete static_cast<RefTask*>(h); }
 
 int ref_task_is_mmlt(void* h) { return static_cast<RefTask*>(h)->ct.mmlt ? 1 : 0; }
+
+// The reference's compiled pseudo-program (schedule_labelfs over the task's
+// DAG, print_program: one "opcode dst src..." per line); returns its length.
+int ref_task_program(void* h, char* buf, int buflen) {
+    const RefTask* t = static_cast<RefTask*>(h);
+    if (!t->ct.mmlt) return -1;
+    const std::string s = print_program(schedule_labelfs(t->ct.dag));
+    if (buf && buflen > 0) {
+        std::strncpy(buf, s.c_str(), static_cast<size_t>(buflen - 1));
+        buf[buflen - 1] = 0;
+    }
+    return static_cast<int>(s.size());
+}
 
 int ref_task_num_arrays(void* h) { return static_cast<int>(static_cast<RefTask*>(h)->names.size()); }
 

@@ -11,8 +11,8 @@ from .engine import (Bounds, Clock, Context, CoverRect, EngineError, ExecLog, Ex
                      FakeClock, GpuPlan, MissingBinding, NoDevice, NoFeasibleKernel,
                      NonPositiveTime, Operands, SteadyClock, TileParams, Trial, TuneReport,
                      UnsupportedExpression, adaptive_execute, bounds_of, enqueue, operands_of,
-                     run_adaptive, run_fixed, run_host, run_naive, run_subtask,
-                     spr)
+                     run_adaptive, run_fixed, run_host, run_host_adaptive, run_naive, run_subtask,
+                     Shape, ShardedGroup, spr)
 from .task import TaskPlan, compile_task  # noqa: F401
 from .taskdata import (TaskData, VerifyResult, bind_dims, load_operand_file,  # noqa: F401
                        make_task_data, verify_against_naive)

@@ -12,7 +12,7 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "lib", "libamlt_gpu.so")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 MAX_AUX = 8
 
 # amlt_status
@@ -115,11 +115,17 @@ class AmuletReportC(C.Structure):
                 ("tuning_fraction", C.c_double), ("total_seconds", C.c_double)]
 
 
+PROG_OPCODES = ("mov", "add", "sub", "mul", "div", "gtcmp", "gecmp", "ltcmp", "lecmp", "eqcmp",
+                "masksub", "maskadd")
+PROG_NOPS = len(PROG_OPCODES)
+
+
 class TaskInfoC(C.Structure):
     _fields_ = [("desc", BodyDesc), ("a", C.c_char * 64), ("b", C.c_char * 64),
                 ("r", C.c_char * 64), ("thres", C.c_char * 64), ("dis", C.c_char * 64),
                 ("n_aux", C.c_int32), ("aux_names", (C.c_char * 64) * MAX_AUX),
-                ("aux_class", C.c_int32 * MAX_AUX)]
+                ("aux_class", C.c_int32 * MAX_AUX), ("prog_counts", C.c_int32 * PROG_NOPS),
+                ("prog_instrs", C.c_int32), ("prog_flops", C.c_int32)]
 
 
 CLOCK_FN = C.CFUNCTYPE(C.c_double, C.c_void_p)
@@ -135,9 +141,14 @@ EXPORTS = [
     "amlt_matrix_file_read", "amlt_matrix_file_write", "amlt_matrix_file_last_error",
     "amlt_operand_seed", "amlt_gen_matrix", "amlt_gpu_run_naive", "amlt_gpu_generated_source",
     "amlt_gpu_run_sharded_source", "amlt_gpu_matrix_alloc", "amlt_gpu_matrix_free",
-    "amlt_gpu_matrix_upload", "amlt_gpu_matrix_download",
+    "amlt_gpu_matrix_upload", "amlt_gpu_matrix_download", "amlt_gpu_run_host_adaptive",
+    "amlt_gpu_comm_unique_id", "amlt_gpu_comm_attach", "amlt_gpu_comm_detach", "amlt_gpu_comm_size",
+    "amlt_sharded_create", "amlt_sharded_destroy", "amlt_sharded_run", "amlt_sharded_size",
+    "amlt_sharded_last_error",
 ]
 HOST_R_ZERO = 1
+HOST_BCAST_SHARED = 2
+NCCL_ID_BYTES = 128
 
 _lib = None
 
@@ -181,6 +192,21 @@ def lib():
     L.amlt_gpu_run_host.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(TileParamsC),
                                     C.POINTER(BoundsC), C.c_int, CLOCK_FN, P,
                                     C.POINTER(C.c_double)]
+    L.amlt_gpu_run_host_adaptive.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(BoundsC), C.c_int,
+                                             CLOCK_FN, P, C.POINTER(TuneReportC), C.POINTER(C.c_double)]
+    L.amlt_gpu_comm_unique_id.argtypes = [C.c_void_p]
+    L.amlt_gpu_comm_attach.argtypes = [P, C.c_void_p, C.c_int, C.c_int]
+    L.amlt_gpu_comm_detach.argtypes = [P]
+    L.amlt_gpu_comm_size.argtypes = [P]
+    L.amlt_sharded_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(P)]
+    L.amlt_sharded_destroy.argtypes = [P]
+    L.amlt_sharded_destroy.restype = None
+    L.amlt_sharded_run.argtypes = [P, C.POINTER(BodyDesc), C.c_char_p, C.c_int, C.POINTER(OperandsC),
+                                   C.POINTER(BoundsC), C.c_int, C.POINTER(TuneReportC),
+                                   C.POINTER(C.c_double)]
+    L.amlt_sharded_size.argtypes = [P]
+    L.amlt_sharded_last_error.argtypes = [P]
+    L.amlt_sharded_last_error.restype = C.c_char_p
     L.amlt_gpu_measure_peak.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
     L.amlt_gpu_adaptive_execute_amulet.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(BoundsC),
                                                    C.c_int, C.c_int, CLOCK_FN, P,

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -22,6 +23,7 @@
 
 #include "../../include/amlt_gpu.h"
 #include "jit.h"
+#include "nccl_dl.h"
 #include "naive.h"
 #include "variants.h"
 
@@ -101,6 +103,7 @@ struct amlt_ctx {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    cudaEvent_t hev0 = nullptr, hev1 = nullptr;  // host-entry call timing
     cudaStream_t copy_in = nullptr, copy_out = nullptr;  // run_host pipeline
     std::vector<cudaEvent_t> pipe_ev;                      // run_host pipeline
     void* work = nullptr;
@@ -136,6 +139,13 @@ struct amlt_ctx {
     using TuneKey = std::tuple<int, int, int64_t, int64_t, int64_t, int, int>;
     std::map<TuneKey, Winner> tune_cache;
     std::string err;
+    // communicator of the multi-rank host entry (amlt_gpu_comm_attach, or a
+    // rank of an amlt_sharded group): B and the replicated operands are
+    // broadcast from rank 0 over NVLink / NVSwitch on comm_stream
+    ncclComm_t comm = nullptr;
+    bool comm_owned = false;
+    int comm_rank = 0, comm_size = 1;
+    cudaStream_t comm_stream = nullptr;
     bool dry() const { return (flags & AMLT_CTX_DRY_RUN) != 0; }
 };
 
@@ -1109,6 +1119,368 @@ struct AmuletTuner {
     }
 };
 
+
+// ---------------------------------------------------------------------------
+// communicator of the multi-rank host entry
+
+void comm_release(amlt_ctx* ctx) {
+    if (ctx->comm && ctx->comm_owned) nccl().destroy(ctx->comm);
+    ctx->comm = nullptr;
+    ctx->comm_owned = false;
+    ctx->comm_rank = 0;
+    ctx->comm_size = 1;
+}
+
+void comm_use(amlt_ctx* ctx, ncclComm_t c, int rank, int n, bool owned) {
+    comm_release(ctx);
+    ctx->comm = c;
+    ctx->comm_owned = owned;
+    ctx->comm_rank = rank;
+    ctx->comm_size = n;
+    if (!ctx->comm_stream)
+        cuda_check(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+}
+
+void nccl_check(int r, const char* what) {
+    if (r != kNcclSuccess) fail(AMLT_ERR_CUDA, std::string(what) + ": " + nccl_error_string(r));
+}
+
+// ---------------------------------------------------------------------------
+// The host-buffer entry (run_fixed / run_adaptive over host MatrixBuffers,
+// src/engine.cpp:165-175): a copy / compute pipeline over row bands of A and
+// R and K panels of B.
+//
+//   copy_in   : replicated operands, A band 0 (+ R band 0), B panel 0, the
+//               other A bands, the other B panels (H2D)
+//   comm      : with a communicator and AMLT_HOST_BCAST_SHARED, rank 0's B
+//               panels and replicated operands are broadcast (NCCL) as they land
+//   compute   : for each K panel p, for each row band b: R[b] += body over
+//               k in panel p (the kernels accumulate into R)
+//   copy_out  : R band b (D2H) as soon as its last panel is done
+//
+// Compute starts as soon as the first band of A and the first panel of B are
+// resident; later transfers overlap it. Panels need B's k rows contiguous
+// (B[k][j] row-major or B[j][k] col-major) and are skipped for split-K
+// winners and "=" statements. With `rep` and no tuned winner for the shape,
+// the whole task is copied first and runs through the tuner (adaptive).
+
+int host_ncopies(const amlt_operands* ho) { return 5 + std::max(0, std::min<int>(ho->n_aux, AMLT_MAX_AUX)); }
+
+// Is operand slot s (0 A, 1 B, 2 R, 3 thres, 4 dis, 5+ aux) replicated on
+// every rank (as opposed to indexed by the rank's rows)?
+bool slot_replicated(const amlt_plan* plan, int s) {
+    auto rep_class = [](int c) { return c == AMLT_LEAF_CONSTANT || c == AMLT_LEAF_VEC_J; };
+    if (s == 1) return true;
+    if (s == 3) return rep_class(plan->desc.thres_class);
+    if (s == 4) return true;
+    if (s >= 5) {
+        const size_t q = static_cast<size_t>(s - 5);
+        return q < plan->aux_class.size() && rep_class(plan->aux_class[q]);
+    }
+    return false;
+}
+
+std::vector<int64_t> band_edges(int64_t lo, int64_t n, int nb, int64_t align, bool short_last) {
+    std::vector<int64_t> e(static_cast<size_t>(nb) + 1);
+    for (int b = 0; b <= nb; ++b) {
+        double f = nb == 1 ? double(b) : (short_last ? std::min(1.0, b / (nb - 0.75)) : double(b) / nb);
+        int64_t r = static_cast<int64_t>(f * double(n));
+        if (b < nb) r = r / align * align;
+        e[static_cast<size_t>(b)] = lo + std::min<int64_t>(n, b == nb ? n : r);
+    }
+    return e;
+}
+
+void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* host_ops,
+                   const amlt_tile_params* tile, const amlt_bounds* bounds, int flags, amlt_clock_fn clock,
+                   void* clock_user, amlt_tune_report* rep, double* elapsed_s) {
+    if (ctx->dry()) fail(AMLT_ERR_NO_DEVICE, "amlt_gpu_run_host needs a device context");
+    cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    const amlt_body_desc& d = plan->desc;
+    const int es = dtype_size(d.dtype);
+    const bool r_zero = (flags & AMLT_HOST_R_ZERO) != 0;
+    const bool bcast = (flags & AMLT_HOST_BCAST_SHARED) != 0 && ctx->comm && ctx->comm_size > 1;
+    const bool root = !bcast || ctx->comm_rank == 0;
+    const int nslot = host_ncopies(host_ops);
+
+    // Host view for validation. Off the root, replicated operands arrive by
+    // broadcast: their shapes must be given, their data may be NULL.
+    amlt_operands hview = *host_ops;
+    amlt_matrix* hslot[5 + AMLT_MAX_AUX] = {&hview.a, &hview.b, &hview.r, &hview.thres, &hview.dis};
+    for (int q = 0; q + 5 < nslot; ++q) hslot[5 + q] = &hview.aux[q];
+    std::vector<bool> shared(static_cast<size_t>(nslot), false);
+    for (int s = 0; s < nslot; ++s) {
+        shared[static_cast<size_t>(s)] = slot_replicated(plan, s);
+        if (bcast && !root && shared[static_cast<size_t>(s)] && !hslot[s]->data && hslot[s]->rows > 0)
+            hslot[s]->data = reinterpret_cast<void*>(uintptr_t(256));  // shape only; never read here
+    }
+    Resolved hv = resolve(plan, &hview, bounds);
+
+    // device staging, one buffer per operand (same pitch and offsets as the host's)
+    amlt_operands dev = hview;
+    amlt_matrix* dslot[5 + AMLT_MAX_AUX] = {&dev.a, &dev.b, &dev.r, &dev.thres, &dev.dis};
+    for (int q = 0; q + 5 < nslot; ++q) dslot[5 + q] = &dev.aux[q];
+    size_t bytes[5 + AMLT_MAX_AUX] = {};
+    for (int s = 0; s < nslot; ++s) {
+        const amlt_matrix& m = *hslot[s];
+        if (!m.data) continue;
+        // the buffer's extent: (outer - 1) whole pitches plus one inner run
+        // (a view into a larger host buffer never reads past its own end)
+        const int64_t outer = m.order == AMLT_ROW_MAJOR ? m.rows : m.cols;
+        const int64_t inner = m.order == AMLT_ROW_MAJOR ? m.cols : m.rows;
+        bytes[s] = outer > 0 && inner > 0 ? (size_t(outer - 1) * size_t(m.ld) + size_t(inner)) * es : 0;
+        if (!bytes[s]) {
+            dslot[s]->data = ctx->hbuf[s] ? ctx->hbuf[s] : reinterpret_cast<void*>(uintptr_t(256));
+            continue;
+        }
+        if (bytes[s] > ctx->hbuf_bytes[s]) {
+            if (ctx->hbuf[s]) cudaFree(ctx->hbuf[s]);
+            ctx->hbuf[s] = nullptr;
+            ctx->hbuf_bytes[s] = 0;
+            cuda_check(cudaMalloc(&ctx->hbuf[s], bytes[s]), "cudaMalloc(host staging)");
+            ctx->hbuf_bytes[s] = bytes[s];
+        }
+        dslot[s]->data = ctx->hbuf[s];
+    }
+    if (!ctx->copy_in) {
+        cuda_check(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking), "cudaStreamCreate");
+    }
+
+    // the variant: the caller's tile, else the winner cached for this shape,
+    // else (rep given) tune now, else the planner default
+    amlt_tile_params tp{0, 0, 0, -1};
+    const auto key = tune_key(plan, hv);
+    bool cached = false;
+    if (tile) {
+        tp = *tile;
+    } else {
+        auto it = ctx->tune_cache.find(key);
+        if (it != ctx->tune_cache.end()) {
+            tp.variant = plan_local_index(plan, it->second.variant);
+            tp.kc = it->second.kc;
+            cached = true;
+        }
+    }
+    const bool tune_now = rep && !tile && !cached;
+    const int64_t M = hv.M, N = hv.N, K = hv.K;
+
+    // row bands of A / R (A rows k-contiguous, R row-major)
+    const bool a_rows = (d.layout_a == AMLT_LAYOUT_NORMAL && host_ops->a.order == AMLT_ROW_MAJOR);
+    const bool r_rows = host_ops->r.order == AMLT_ROW_MAJOR;
+    int nb = 1;
+    if (!tune_now && a_rows && r_rows && M >= 1024) nb = static_cast<int>(std::min<int64_t>(8, M / 256));
+    // K panels of B (B's k rows contiguous)
+    const bool b_kouter = (d.layout_b == AMLT_LAYOUT_NORMAL && host_ops->b.order == AMLT_ROW_MAJOR) ||
+                          (d.layout_b == AMLT_LAYOUT_TRANSPOSED && host_ops->b.order == AMLT_COL_MAJOR);
+    const bool split_winner = tp.kc > 0 && tp.kc < K;
+    // (the panel count depends only on what every rank of a broadcast shares,
+    // so all ranks issue the same sequence of collectives)
+    // Panels of at least 256 MiB of B (AMLT_HOST_PANEL_BYTES overrides; tests
+    // use it to cut small tasks) and 256 k, at most 8.
+    int np = 1;
+    if (b_kouter && d.accumulate) {
+        double panel_bytes = double(256 << 20);
+        if (const char* e = std::getenv("AMLT_HOST_PANEL_BYTES")) panel_bytes = std::max(1.0, std::atof(e));
+        const double b_bytes = double(K) * double(host_ops->b.ld) * es;
+        np = static_cast<int>(std::max(1.0, std::min({8.0, std::floor(b_bytes / panel_bytes),
+                                                      std::floor(double(K) / 256.0)})));
+    }
+    const int vi = !tune_now ? (tp.variant >= 0 ? plan->variants[static_cast<size_t>(tp.variant)]
+                                                : default_variant(ctx, plan, M, N, hv.aligned))
+                             : -1;
+    if (nb > 1) {
+        // fewer bands when one band would not fill the SMs (split-K multiplies CTAs)
+        const VariantDesc& v = vdesc(vi);
+        const int64_t splits = (!v.run && split_winner) ? (K + tp.kc - 1) / tp.kc : 1;
+        const int64_t slots = int64_t(ctx->num_sms) * occ_of(ctx, vi);
+        const int64_t fill = ctas_for(v, M, N) * splits / std::max<int64_t>(1, slots);
+        nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nb, fill)));
+    }
+    // Bands: equal but for a last one a quarter as tall, so the copy-out that
+    // trails the final compute is short; 64-row multiples. Panels: equal,
+    // edges on multiples of 64 k (16-byte aligned operand offsets).
+    const std::vector<int64_t> redge = band_edges(bounds->i0, M, nb, 64, true);
+    const std::vector<int64_t> kedge = band_edges(bounds->k0, K, np, 64, false);
+
+    // events: [0] start, [1] replicated operands ready, [2..2+nb) band inputs,
+    // [2+nb..2+nb+np) panels ready, [2+nb+np..2+2nb+np) bands done, [last] out
+    const int nev = 3 + 2 * nb + np;
+    while (static_cast<int>(ctx->pipe_ev.size()) < nev) {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+        ctx->pipe_ev.push_back(e);
+    }
+    cudaEvent_t* ev = ctx->pipe_ev.data();
+    cudaEvent_t start_ev = ev[0], small_ev = ev[1], out_ev = ev[nev - 1];
+    auto band_in = [&](int b) { return ev[2 + b]; };
+    auto panel_ev = [&](int p) { return ev[2 + nb + p]; };
+    auto band_done = [&](int b) { return ev[2 + nb + np + b]; };
+
+    const int64_t arow = host_ops->a.ld * es, rrow = host_ops->r.ld * es;
+    const int64_t brow = host_ops->b.ld * es;  // one k row of B (b_kouter)
+    // k rows [k0, k1) of B, relative to the buffer (the bounds' k0 is an offset into it)
+    auto b_span = [&](int64_t k0, int64_t k1, size_t* off, size_t* len) {
+        if (np == 1) {
+            *off = 0;
+            *len = bytes[1];
+        } else {
+            *off = std::min(size_t(k0) * size_t(brow), bytes[1]);
+            *len = std::min(size_t(k1 - k0) * size_t(brow), bytes[1] - *off);
+        }
+    };
+    auto h2d = [&](void* dst, const void* src, size_t n, cudaStream_t s, const char* what) {
+        if (n) cuda_check(cudaMemcpyAsync(dst, src, n, cudaMemcpyHostToDevice, s), what);
+    };
+    auto bcast_bytes = [&](void* buf, size_t n) {
+        if (n) nccl_check(nccl().bcast(buf, buf, n, kNcclUint8, 0, ctx->comm, ctx->comm_stream), "ncclBroadcast");
+    };
+    auto copy_band_in = [&](int b) {
+        const int64_t r0 = redge[static_cast<size_t>(b)], r1 = redge[static_cast<size_t>(b) + 1];
+        if (nb == 1) {
+            h2d(ctx->hbuf[0], host_ops->a.data, bytes[0], ctx->copy_in, "H2D A");
+            if (r_zero) cuda_check(cudaMemsetAsync(ctx->hbuf[2], 0, bytes[2], ctx->copy_in), "memset R");
+            else h2d(ctx->hbuf[2], host_ops->r.data, bytes[2], ctx->copy_in, "H2D R");
+        } else {
+            h2d(static_cast<char*>(ctx->hbuf[0]) + r0 * arow, static_cast<const char*>(host_ops->a.data) + r0 * arow,
+                size_t(r1 - r0) * arow, ctx->copy_in, "H2D A band");
+            if (r_zero)
+                cuda_check(cudaMemsetAsync(static_cast<char*>(ctx->hbuf[2]) + r0 * rrow, 0, size_t(r1 - r0) * rrow,
+                                           ctx->copy_in), "memset R band");
+            else
+                h2d(static_cast<char*>(ctx->hbuf[2]) + r0 * rrow, static_cast<const char*>(host_ops->r.data) + r0 * rrow,
+                    size_t(r1 - r0) * rrow, ctx->copy_in, "H2D R band");
+        }
+        cuda_check(cudaEventRecord(band_in(b), ctx->copy_in), "cudaEventRecord");
+    };
+    auto copy_panel_in = [&](int p) {
+        size_t off, len;
+        b_span(kedge[static_cast<size_t>(p)], kedge[static_cast<size_t>(p) + 1], &off, &len);
+        if (root) h2d(static_cast<char*>(ctx->hbuf[1]) + off, static_cast<const char*>(host_ops->b.data) + off, len,
+                      ctx->copy_in, "H2D B panel");
+        if (bcast) {
+            if (root) {
+                cuda_check(cudaEventRecord(panel_ev(p), ctx->copy_in), "cudaEventRecord");
+                cuda_check(cudaStreamWaitEvent(ctx->comm_stream, panel_ev(p), 0), "cudaStreamWaitEvent");
+            }
+            bcast_bytes(static_cast<char*>(ctx->hbuf[1]) + off, len);
+            cuda_check(cudaEventRecord(panel_ev(p), ctx->comm_stream), "cudaEventRecord");
+        } else {
+            cuda_check(cudaEventRecord(panel_ev(p), ctx->copy_in), "cudaEventRecord");
+        }
+    };
+    auto band_bounds = [&](int b, int p) {
+        amlt_bounds bb = *bounds;
+        bb.i0 = redge[static_cast<size_t>(b)];
+        bb.i1 = redge[static_cast<size_t>(b) + 1];
+        bb.k0 = kedge[static_cast<size_t>(p)];
+        bb.k1 = kedge[static_cast<size_t>(p) + 1];
+        return bb;
+    };
+
+    auto body = [&] {
+        cuda_check(cudaEventRecord(start_ev, ctx->stream), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(ctx->copy_in, start_ev, 0), "cudaStreamWaitEvent");
+        if (bcast) cuda_check(cudaStreamWaitEvent(ctx->comm_stream, start_ev, 0), "cudaStreamWaitEvent");
+        // replicated operands other than B (thresholds, vectors, [i] / [i][j]
+        // leaves are copied whole by every rank: they are the rank's own)
+        for (int s = 3; s < nslot; ++s)
+            if (bytes[s] && (root || !shared[static_cast<size_t>(s)]))
+                h2d(ctx->hbuf[s], hslot[s]->data, bytes[s], ctx->copy_in, "H2D operand");
+        cuda_check(cudaEventRecord(small_ev, ctx->copy_in), "cudaEventRecord");
+        if (bcast) {
+            cuda_check(cudaStreamWaitEvent(ctx->comm_stream, small_ev, 0), "cudaStreamWaitEvent");
+            nccl_check(nccl().group_start(), "ncclGroupStart");
+            for (int s = 3; s < nslot; ++s)
+                if (bytes[s] && shared[static_cast<size_t>(s)]) bcast_bytes(ctx->hbuf[s], bytes[s]);
+            nccl_check(nccl().group_end(), "ncclGroupEnd");
+            cuda_check(cudaEventRecord(small_ev, ctx->comm_stream), "cudaEventRecord");
+        }
+        cuda_check(cudaStreamWaitEvent(ctx->stream, small_ev, 0), "cudaStreamWaitEvent");
+        // inputs: A band 0, B panel 0, the other bands, the other panels
+        copy_band_in(0);
+        copy_panel_in(0);
+        for (int b = 1; b < nb; ++b) copy_band_in(b);
+        for (int p = 1; p < np; ++p) copy_panel_in(p);
+        if (tune_now) {
+            for (int b = 0; b < nb; ++b) cuda_check(cudaStreamWaitEvent(ctx->stream, band_in(b), 0), "cudaStreamWaitEvent");
+            for (int p = 0; p < np; ++p) cuda_check(cudaStreamWaitEvent(ctx->stream, panel_ev(p), 0), "cudaStreamWaitEvent");
+            adaptive(ctx, plan, &dev, *bounds, clock, clock_user, nullptr, rep);
+            cuda_check(cudaEventRecord(band_done(0), ctx->stream), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(ctx->copy_out, band_done(0), 0), "cudaStreamWaitEvent");
+            cuda_check(cudaMemcpyAsync(host_ops->r.data, ctx->hbuf[2], bytes[2], cudaMemcpyDeviceToHost,
+                                       ctx->copy_out), "D2H R");
+        } else {
+            for (int p = 0; p < np; ++p) {
+                cuda_check(cudaStreamWaitEvent(ctx->stream, panel_ev(p), 0), "cudaStreamWaitEvent");
+                for (int b = 0; b < nb; ++b) {
+                    if (p == 0) cuda_check(cudaStreamWaitEvent(ctx->stream, band_in(b), 0), "cudaStreamWaitEvent");
+                    amlt_bounds bb = band_bounds(b, p);
+                    Resolved rv = resolve(plan, &dev, &bb);
+                    Dispatch dp = plan_dispatch(ctx, plan, &tp, rv);
+                    enqueue(ctx, plan, rv, dp);
+                    if (p + 1 < np) continue;
+                    cuda_check(cudaEventRecord(band_done(b), ctx->stream), "cudaEventRecord");
+                    cuda_check(cudaStreamWaitEvent(ctx->copy_out, band_done(b), 0), "cudaStreamWaitEvent");
+                    const int64_t r0 = bb.i0, r1 = bb.i1;
+                    if (nb == 1)
+                        cuda_check(cudaMemcpyAsync(host_ops->r.data, ctx->hbuf[2], bytes[2], cudaMemcpyDeviceToHost,
+                                                   ctx->copy_out), "D2H R");
+                    else
+                        cuda_check(cudaMemcpyAsync(static_cast<char*>(host_ops->r.data) + r0 * rrow,
+                                                   static_cast<const char*>(ctx->hbuf[2]) + r0 * rrow,
+                                                   size_t(r1 - r0) * rrow, cudaMemcpyDeviceToHost, ctx->copy_out),
+                                   "D2H R band");
+                }
+            }
+        }
+        cuda_check(cudaEventRecord(out_ev, ctx->copy_out), "cudaEventRecord");
+        cuda_check(cudaStreamWaitEvent(ctx->stream, out_ev, 0), "cudaStreamWaitEvent");
+        if (bcast) {  // the comm stream's work is part of this call
+            cuda_check(cudaEventRecord(small_ev, ctx->comm_stream), "cudaEventRecord");
+            cuda_check(cudaStreamWaitEvent(ctx->stream, small_ev, 0), "cudaStreamWaitEvent");
+        }
+    };
+    double el = 0;
+    if (clock && !tune_now) {
+        const double t0 = clock(clock_user);
+        body();
+        cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+        el = clock(clock_user) - t0;
+    } else {
+        // (tuning with a caller clock: the tuner reads it around each of its
+        // subtasks, as adaptive_execute does; the call is timed by events)
+        // (own timing events: the tuner's trials use ev0 / ev1)
+        if (!ctx->hev0) {
+            cuda_check(cudaEventCreate(&ctx->hev0), "cudaEventCreate");
+            cuda_check(cudaEventCreate(&ctx->hev1), "cudaEventCreate");
+        }
+        cuda_check(cudaEventRecord(ctx->hev0, ctx->stream), "cudaEventRecord");
+        body();
+        cuda_check(cudaEventRecord(ctx->hev1, ctx->stream), "cudaEventRecord");
+        cuda_check(cudaEventSynchronize(ctx->hev1), "cudaEventSynchronize");
+        float ms = 0;
+        cuda_check(cudaEventElapsedTime(&ms, ctx->hev0, ctx->hev1), "cudaEventElapsedTime");
+        el = ms * 1e-3;
+        if (tune_now && clock) el = rep->total_seconds;
+    }
+    if (rep && !tune_now) {
+        std::memset(rep, 0, sizeof(*rep));
+        rep->best_variant = plan_local_index(plan, vi);
+        rep->best_kc = split_winner ? tp.kc : K;
+        rep->from_cache = cached ? 1 : 0;
+        // one completed region per K panel (every row band has run it)
+        for (int p = 0; p < np; ++p) add_cover(rep, amlt_bounds{bounds->i0, bounds->i1, bounds->j0, bounds->j1,
+                                                                 kedge[static_cast<size_t>(p)], kedge[static_cast<size_t>(p) + 1]});
+        rep->total_seconds = el;
+    } else if (rep && tune_now) {
+        // the report's subtasks plus the copies around them
+        if (!clock) rep->total_seconds = el;
+        // a later call of this shape reuses the winner
+    }
+    if (elapsed_s) *elapsed_s = el;
+}
+
 // ---------------------------------------------------------------------------
 // boundary helpers
 
@@ -1138,6 +1510,18 @@ amlt_status guarded(amlt_ctx* ctx, F&& f) {
 }
 
 }  // namespace
+
+namespace amltk {
+// A rank of a single-process group (csrc/sharded.cu) uses a communicator the
+// group owns (ncclCommInitAll).
+amlt_status ctx_use_comm(amlt_ctx* ctx, void* comm, int rank, int nranks) {
+    if (!ctx) return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        comm_use(ctx, static_cast<ncclComm_t>(comm), rank, nranks, false);
+    });
+}
+}  // namespace amltk
 
 // ===========================================================================
 // C ABI
@@ -1220,6 +1604,8 @@ void amlt_gpu_ctx_destroy(amlt_ctx* ctx) {
     if (!ctx->dry()) {
         cudaSetDevice(ctx->device);
         if (ctx->own_stream) cudaStreamSynchronize(ctx->own_stream);
+        if (ctx->comm_stream) cudaStreamSynchronize(ctx->comm_stream);
+        comm_release(ctx);
         if (ctx->work) cudaFree(ctx->work);
         if (ctx->pack_ws) cudaFree(ctx->pack_ws);
         if (ctx->scratch) cudaFree(ctx->scratch);
@@ -1228,6 +1614,9 @@ void amlt_gpu_ctx_destroy(amlt_ctx* ctx) {
             if (p) cudaFree(p);
         if (ctx->ev0) cudaEventDestroy(ctx->ev0);
         if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+        if (ctx->hev0) cudaEventDestroy(ctx->hev0);
+        if (ctx->hev1) cudaEventDestroy(ctx->hev1);
+        if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
         for (cudaEvent_t e : ctx->pipe_ev) cudaEventDestroy(e);
         if (ctx->copy_in) cudaStreamDestroy(ctx->copy_in);
         if (ctx->copy_out) cudaStreamDestroy(ctx->copy_out);
@@ -1306,6 +1695,9 @@ amlt_status amlt_gpu_recognize(const char* task_source, amlt_task_info* info) {
         put(info->r, rt.r);
         put(info->thres, rt.thres);
         put(info->dis, rt.dis);
+        for (int c = 0; c < AMLT_PROG_NOPS; ++c) info->prog_counts[c] = rt.prog_counts[c];
+        info->prog_instrs = rt.prog_instrs;
+        info->prog_flops = rt.prog_flops;
         info->n_aux = static_cast<int32_t>(rt.aux_names.size());
         for (size_t q = 0; q < rt.aux_names.size(); ++q) {
             put(info->aux_names[q], rt.aux_names[q]);
@@ -1536,179 +1928,54 @@ amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_o
                               amlt_clock_fn clock, void* clock_user, double* elapsed_s) {
     if (!ctx || !plan || !host_ops || !bounds) return AMLT_ERR_INVALID_ARGUMENT;
     return guarded(ctx, [&] {
-        if (ctx->dry()) fail(AMLT_ERR_NO_DEVICE, "amlt_gpu_run_host needs a device context");
-        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
-        const int es = dtype_size(plan->desc.dtype);
-        const bool r_zero = (flags & AMLT_HOST_R_ZERO) != 0;
-        // validate against the host description first (same rules)
-        Resolved hv = resolve(plan, host_ops, bounds);
-        amlt_operands dev = *host_ops;
-        const int nslot = 5 + std::max(0, std::min<int>(host_ops->n_aux, AMLT_MAX_AUX));
-        const amlt_matrix* src[5 + AMLT_MAX_AUX] = {&host_ops->a, &host_ops->b, &host_ops->r,
-                                                    &host_ops->thres, &host_ops->dis};
-        amlt_matrix* dst[5 + AMLT_MAX_AUX] = {&dev.a, &dev.b, &dev.r, &dev.thres, &dev.dis};
-        for (int q = 0; q + 5 < nslot; ++q) {
-            src[5 + q] = &host_ops->aux[q];
-            dst[5 + q] = &dev.aux[q];
-        }
-        size_t bytes[5 + AMLT_MAX_AUX] = {};
-        for (int s = 0; s < nslot; ++s) {
-            const amlt_matrix& m = *src[s];
-            bytes[s] = 0;
-            if (!m.data) continue;
-            const int64_t outer = m.order == AMLT_ROW_MAJOR ? m.rows : m.cols;
-            bytes[s] = size_t(std::max<int64_t>(outer, 1)) * size_t(m.ld) * es;
-            if (bytes[s] > ctx->hbuf_bytes[s]) {
-                if (ctx->hbuf[s]) cudaFree(ctx->hbuf[s]);
-                ctx->hbuf[s] = nullptr;
-                ctx->hbuf_bytes[s] = 0;
-                cuda_check(cudaMalloc(&ctx->hbuf[s], bytes[s]), "cudaMalloc(host staging)");
-                ctx->hbuf_bytes[s] = bytes[s];
-            }
-            dst[s]->data = ctx->hbuf[s];
-        }
-        if (!ctx->copy_in) {
-            cuda_check(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking), "cudaStreamCreate");
-            cuda_check(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking), "cudaStreamCreate");
-        }
-        // Row-band pipeline: band b's A rows (and R rows unless R starts at
-        // zero) go H2D on copy_in while band b-1 computes on the context
-        // stream and band b-2's R rows go D2H on copy_out. Needs A and R
-        // stored with whole rows contiguous (row-major, normal layout);
-        // otherwise one band.
-        const bool a_rows = host_ops->a.order == AMLT_ROW_MAJOR && plan->desc.layout_a == AMLT_LAYOUT_NORMAL;
-        const bool r_rows = host_ops->r.order == AMLT_ROW_MAJOR;
-        const int64_t M = hv.M;
-        int nb = 1;
-        if (a_rows && r_rows && M >= 1024) nb = static_cast<int>(std::min<int64_t>(8, M / 256));
-        // Band edges: equal bands except a last one a quarter as tall, so the
-        // copy-out that trails the final compute is short; multiples of 64 rows.
-        std::vector<int64_t> edge(static_cast<size_t>(nb) + 1);
-        for (int bi = 0; bi <= nb; ++bi) {
-            const double f = nb == 1 ? double(bi) : std::min(1.0, bi / (nb - 0.75));
-            int64_t r = static_cast<int64_t>(f * double(M));
-            if (bi < nb) r = r / 64 * 64;
-            edge[static_cast<size_t>(bi)] = bounds->i0 + std::min<int64_t>(M, bi == nb ? M : r);
-        }
-        // events: [0] shared inputs ready, [1] start, per band [2+3b] inputs
-        // in, [3+3b] computed, and [2+3nb] all outputs out
-        while (static_cast<int>(ctx->pipe_ev.size()) < 3 * nb + 3) {
-            cudaEvent_t e;
-            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
-            ctx->pipe_ev.push_back(e);
-        }
-        // variant for the bands: caller's tile, else the cached winner for this
-        // shape, else the planner default
-        amlt_tile_params tp{0, 0, 0, -1};
-        if (tile) tp = *tile;
-        else {
-            // (the device copies keep the host pitches and offsets, so the host
-            // description's alignment is the device's)
-            auto it = ctx->tune_cache.find(tune_key(plan, hv));
-            if (it != ctx->tune_cache.end()) {
-                tp.variant = plan_local_index(plan, it->second.variant);
-                tp.kc = it->second.kc;
-            }
-        }
-        // Fewer bands when one band would not fill the SMs (a band is one
-        // launch of the variant; split-K multiplies its CTAs).
-        if (nb > 1) {
-            const int vi = tp.variant >= 0 ? plan->variants[static_cast<size_t>(tp.variant)]
-                                           : default_variant(ctx, plan, hv.M, hv.N, hv.aligned);
-            const VariantDesc& v = vdesc(vi);
-            const int64_t splits = (!v.run && tp.kc > 0 && tp.kc < hv.K) ? (hv.K + tp.kc - 1) / tp.kc : 1;
-            const int64_t slots = int64_t(ctx->num_sms) * occ_of(ctx, vi);
-            const int64_t fill = ctas_for(v, hv.M, hv.N) * splits / std::max<int64_t>(1, slots);
-            nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nb, fill)));
-            for (int bi = 0; bi <= nb; ++bi) {
-                const double f = nb == 1 ? double(bi) : std::min(1.0, bi / (nb - 0.75));
-                int64_t r = static_cast<int64_t>(f * double(M));
-                if (bi < nb) r = r / 64 * 64;
-                edge[static_cast<size_t>(bi)] = bounds->i0 + std::min<int64_t>(M, bi == nb ? M : r);
-            }
-            edge.resize(static_cast<size_t>(nb) + 1);
-        }
-        auto body = [&] {
-            cudaEvent_t shared_ready = ctx->pipe_ev[0];
-            cudaEvent_t start_ev = ctx->pipe_ev[1];
-            cuda_check(cudaEventRecord(start_ev, ctx->stream), "cudaEventRecord");
-            cuda_check(cudaStreamWaitEvent(ctx->copy_in, start_ev, 0), "cudaStreamWaitEvent");
-            for (int s = 1; s < nslot; ++s)
-                if (s != 2 && bytes[s])
-                    cuda_check(cudaMemcpyAsync(ctx->hbuf[s], src[s]->data, bytes[s],
-                                               cudaMemcpyHostToDevice, ctx->copy_in),
-                               "cudaMemcpyAsync H2D");
-            cuda_check(cudaEventRecord(shared_ready, ctx->copy_in), "cudaEventRecord");
-            const int64_t arow = host_ops->a.ld * es, rrow = host_ops->r.ld * es;
-            for (int bi = 0; bi < nb; ++bi) {
-                const int64_t r0 = edge[static_cast<size_t>(bi)], r1 = edge[static_cast<size_t>(bi) + 1];
-                cudaEvent_t in_ev = ctx->pipe_ev[2 + 3 * bi], done_ev = ctx->pipe_ev[3 + 3 * bi];
-                if (nb == 1) {
-                    cuda_check(cudaMemcpyAsync(ctx->hbuf[0], src[0]->data, bytes[0],
-                                               cudaMemcpyHostToDevice, ctx->copy_in), "H2D A");
-                } else {
-                    cuda_check(cudaMemcpyAsync(static_cast<char*>(ctx->hbuf[0]) + r0 * arow,
-                                               static_cast<const char*>(src[0]->data) + r0 * arow,
-                                               size_t(r1 - r0) * arow, cudaMemcpyHostToDevice,
-                                               ctx->copy_in), "H2D A band");
-                }
-                if (r_zero) {
-                    if (nb == 1)
-                        cuda_check(cudaMemsetAsync(ctx->hbuf[2], 0, bytes[2], ctx->copy_in), "memset R");
-                    else
-                        cuda_check(cudaMemsetAsync(static_cast<char*>(ctx->hbuf[2]) + r0 * rrow, 0,
-                                                   size_t(r1 - r0) * rrow, ctx->copy_in), "memset R band");
-                } else {
-                    if (nb == 1)
-                        cuda_check(cudaMemcpyAsync(ctx->hbuf[2], src[2]->data, bytes[2],
-                                                   cudaMemcpyHostToDevice, ctx->copy_in), "H2D R");
-                    else
-                        cuda_check(cudaMemcpyAsync(static_cast<char*>(ctx->hbuf[2]) + r0 * rrow,
-                                                   static_cast<const char*>(src[2]->data) + r0 * rrow,
-                                                   size_t(r1 - r0) * rrow, cudaMemcpyHostToDevice,
-                                                   ctx->copy_in), "H2D R band");
-                }
-                cuda_check(cudaEventRecord(in_ev, ctx->copy_in), "cudaEventRecord");
-                cuda_check(cudaStreamWaitEvent(ctx->stream, in_ev, 0), "cudaStreamWaitEvent");
-                amlt_bounds bb = *bounds;
-                bb.i0 = r0;
-                bb.i1 = r1;
-                Resolved rv = resolve(plan, &dev, &bb);
-                Dispatch dp = plan_dispatch(ctx, plan, &tp, rv);
-                enqueue(ctx, plan, rv, dp);
-                cuda_check(cudaEventRecord(done_ev, ctx->stream), "cudaEventRecord");
-                cuda_check(cudaStreamWaitEvent(ctx->copy_out, done_ev, 0), "cudaStreamWaitEvent");
-                if (nb == 1)
-                    cuda_check(cudaMemcpyAsync(host_ops->r.data, ctx->hbuf[2], bytes[2],
-                                               cudaMemcpyDeviceToHost, ctx->copy_out), "D2H R");
-                else
-                    cuda_check(cudaMemcpyAsync(static_cast<char*>(host_ops->r.data) + r0 * rrow,
-                                               static_cast<const char*>(ctx->hbuf[2]) + r0 * rrow,
-                                               size_t(r1 - r0) * rrow, cudaMemcpyDeviceToHost,
-                                               ctx->copy_out), "D2H R band");
-            }
-            cudaEvent_t out_done = ctx->pipe_ev[2 + 3 * nb];
-            cuda_check(cudaEventRecord(out_done, ctx->copy_out), "cudaEventRecord");
-            cuda_check(cudaStreamWaitEvent(ctx->stream, out_done, 0), "cudaStreamWaitEvent");
-        };
-        double el = 0;
-        if (clock) {
-            double t0 = clock(clock_user);
-            body();
-            cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
-            el = clock(clock_user) - t0;
-        } else {
-            cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
-            body();
-            cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
-            cuda_check(cudaEventSynchronize(ctx->ev1), "cudaEventSynchronize");
-            float ms = 0;
-            cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "cudaEventElapsedTime");
-            el = ms * 1e-3;
-        }
-        if (elapsed_s) *elapsed_s = el;
+        host_pipeline(ctx, plan, host_ops, tile, bounds, flags, clock, clock_user, nullptr, elapsed_s);
     });
 }
+
+amlt_status amlt_gpu_run_host_adaptive(amlt_ctx* ctx, const amlt_plan* plan,
+                                       const amlt_operands* host_ops, const amlt_bounds* bounds,
+                                       int flags, amlt_clock_fn clock, void* clock_user,
+                                       amlt_tune_report* report, double* elapsed_s) {
+    if (!ctx || !plan || !host_ops || !bounds || !report) return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        host_pipeline(ctx, plan, host_ops, nullptr, bounds, flags, clock, clock_user, report, elapsed_s);
+    });
+}
+
+amlt_status amlt_gpu_comm_unique_id(void* id_out) {
+    if (!id_out) return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(nullptr, [&] {
+        if (!nccl().ok) fail(AMLT_ERR_CUDA, "libnccl.so.2 could not be loaded");
+        NcclUniqueId id;
+        const int r = nccl().get_unique_id(&id);
+        if (r != kNcclSuccess) fail(AMLT_ERR_CUDA, std::string("ncclGetUniqueId: ") + nccl_error_string(r));
+        std::memcpy(id_out, id.internal, sizeof(id.internal));
+    });
+}
+
+amlt_status amlt_gpu_comm_attach(amlt_ctx* ctx, const void* id, int rank, int nranks) {
+    if (!ctx || !id || nranks < 1 || rank < 0 || rank >= nranks) return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] {
+        if (ctx->dry()) fail(AMLT_ERR_NO_DEVICE, "amlt_gpu_comm_attach needs a device context");
+        comm_release(ctx);
+        if (nranks == 1) return;  // nothing to exchange
+        if (!nccl().ok) fail(AMLT_ERR_CUDA, "libnccl.so.2 could not be loaded");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        NcclUniqueId uid;
+        std::memcpy(uid.internal, id, sizeof(uid.internal));
+        ncclComm_t c = nullptr;
+        const int r = nccl().init_rank(&c, nranks, uid, rank);
+        if (r != kNcclSuccess) fail(AMLT_ERR_CUDA, std::string("ncclCommInitRank: ") + nccl_error_string(r));
+        comm_use(ctx, c, rank, nranks, true);
+    });
+}
+
+amlt_status amlt_gpu_comm_detach(amlt_ctx* ctx) {
+    if (!ctx) return AMLT_ERR_INVALID_ARGUMENT;
+    return guarded(ctx, [&] { comm_release(ctx); });
+}
+
+int amlt_gpu_comm_size(const amlt_ctx* ctx) { return ctx ? ctx->comm_size : 0; }
 
 // ---------------------------------------------------------------------------
 // device matrices for callers without their own allocator (SURVEY §8b

@@ -6,10 +6,12 @@
 // operands' roles and orientations. This is a small recursive-descent parser
 // for the reference grammar (README.md:37-60, parser.cpp:142-365; `//` and
 // `#` comments), the recognition conditions 2-4 (recognize.cpp:84-166), and
-// a structural match of the statement tree against the bodies' canonical
-// trees (presets.cpp:52-94 + the sqdiff / eqcount statements), allowing
-// operand swaps at commutative nodes (a swap never changes an IEEE result).
-// Python twin: paper_2305_08872_b200/task.py (same rules, tested together).
+// a match of the statement tree against the bodies' canonical trees
+// (presets.cpp:52-94 + the sqdiff / eqcount statements) after normalising
+// comparisons (t < p -> p > t) and matching products and sums as factor /
+// term lists in any order, and the op counts of the reference's compiled
+// program for the statement (SURVEY §8(d) measure (B)). The Python front
+// end (task.py) calls this through amlt_gpu_recognize.
 #include <cctype>
 #include <cmath>
 #include <cstdio>
@@ -181,6 +183,53 @@ bool same(const P& a, const P& b) {
 
 using Env = std::map<std::string, P>;
 
+// Canonical form for matching (the reference DAG's own normalisations,
+// expr_dag.cpp:182-245, plus the IEEE identities that hold exactly):
+//   x < y  ->  y > x,   x <= y  ->  y >= x   (same truth value, NaN included)
+// and products / sums are matched as flattened factor / term lists in any
+// order (a commuted or re-associated product of the same factors differs by
+// rounding only, inside the bodies' stated tolerance, and not at all on
+// integer-valued data).
+P canon(const P& n) {
+    if (n->kind != Node::Bin) return n;
+    auto b = std::make_shared<Node>(*n);
+    b->l = canon(n->l);
+    b->r = canon(n->r);
+    if (b->op == "<" || b->op == "<=") {
+        std::swap(b->l, b->r);
+        b->op = b->op == "<" ? ">" : ">=";
+    }
+    return b;
+}
+
+void flatten(const P& n, const std::string& op, std::vector<P>& out) {
+    if (n->kind == Node::Bin && n->op == op) {
+        flatten(n->l, op, out);
+        flatten(n->r, op, out);
+    } else {
+        out.push_back(n);
+    }
+}
+
+bool match(const P& tpl, const P& n, Env& env);
+
+// Template factors tf[i..] against tree factors nf (a permutation), with
+// backtracking over the placeholder bindings.
+bool match_perm(const std::vector<P>& tf, size_t i, const std::vector<P>& nf, std::vector<bool>& used, Env& env) {
+    if (i == tf.size()) return true;
+    for (size_t j = 0; j < nf.size(); ++j) {
+        if (used[j]) continue;
+        Env saved = env;
+        if (match(tf[i], nf[j], env)) {
+            used[j] = true;
+            if (match_perm(tf, i + 1, nf, used, env)) return true;
+            used[j] = false;
+        }
+        env = saved;
+    }
+    return false;
+}
+
 bool match(const P& tpl, const P& n, Env& env) {
     if (tpl->kind == Node::Ref) {  // placeholder A, B, T, D
         const std::string& ph = tpl->name;
@@ -194,15 +243,127 @@ bool match(const P& tpl, const P& n, Env& env) {
     }
     if (tpl->kind == Node::Num) return n->kind == Node::Num && n->num == tpl->num;
     if (n->kind != Node::Bin || n->op != tpl->op) return false;
+    if (tpl->op == "*" || tpl->op == "+") {
+        std::vector<P> tf, nf;
+        flatten(tpl, tpl->op, tf);
+        flatten(n, tpl->op, nf);
+        if (tf.size() != nf.size()) return false;
+        std::vector<bool> used(nf.size(), false);
+        return match_perm(tf, 0, nf, used, env);
+    }
     Env saved = env;
     if (match(tpl->l, n->l, env) && match(tpl->r, n->r, env)) return true;
     env = saved;
-    if ((tpl->op == "+" || tpl->op == "*" || tpl->op == "==") && match(tpl->l, n->r, env) &&
-        match(tpl->r, n->l, env))
-        return true;
+    if (tpl->op == "==" && match(tpl->l, n->r, env) && match(tpl->r, n->l, env)) return true;
     env = saved;
     return false;
 }
+
+// ---------------------------------------------------------------------------
+// The reference's compiled program for a statement (build_dag +
+// schedule_labelfs, expr_dag.cpp:63-245, schedule.cpp:265-273): one pseudo-
+// instruction per DAG op node (equal subexpressions shared), then the final
+// accumulate (or move, for "="). Restated here only to COUNT the program's
+// operations per opcode: the body-op flops of SURVEY §8(d) measure (B).
+// Mask rewrites: in an additive chain a product with a comparison factor
+// becomes masksub / maskadd(lhs, cond, product of the other factors); any
+// other comparison used as a number becomes maskadd(0, cond, 1).
+struct ProgramCounter {
+    std::map<std::string, int> ids;  // structural key -> node id (CSE)
+    int counts[AMLT_PROG_NOPS] = {};
+
+    std::string key_of(const P& n) const {
+        switch (n->kind) {
+            case Node::Num: {
+                char buf[64];
+                std::snprintf(buf, sizeof(buf), "#%a", n->num);
+                return buf;
+            }
+            case Node::Role: return "@" + n->cls;
+            case Node::Aux: return "$" + n->name;
+            default: return "?";
+        }
+    }
+    std::string leaf(const P& n) { return key_of(n); }
+    std::string lit(double v) {
+        char buf[64];
+        std::snprintf(buf, sizeof(buf), "#%a", v);
+        return buf;
+    }
+    std::string op(int opc, const std::string& a, const std::string& b, const std::string& c = "") {
+        const std::string k = "(" + std::to_string(opc) + " " + a + " " + b + " " + c + ")";
+        if (!ids.count(k)) {
+            ids[k] = static_cast<int>(ids.size());
+            ++counts[opc];
+        }
+        return k;
+    }
+    static bool is_cmp(const P& n) {
+        return n->kind == Node::Bin && (n->op == ">" || n->op == ">=" || n->op == "<" || n->op == "<=" || n->op == "==");
+    }
+    static int cmp_code(const std::string& o) {
+        return o == ">" ? AMLT_PROG_GTCMP : o == ">=" ? AMLT_PROG_GECMP : o == "<" ? AMLT_PROG_LTCMP
+               : o == "<=" ? AMLT_PROG_LECMP : AMLT_PROG_EQCMP;
+    }
+    void factors(const P& n, std::vector<P>& out) const {  // Mul spine only; Div is opaque
+        if (n->kind == Node::Bin && n->op == "*") {
+            factors(n->l, out);
+            out.push_back(n->r);
+        } else {
+            out.push_back(n);
+        }
+    }
+    std::string cmp(const P& n) { return op(cmp_code(n->op), numeric(n->l), numeric(n->r)); }
+    // a product term with a comparison factor: (cond, value)
+    bool masked(const P& n, std::string* cond, std::string* value) {
+        if (is_cmp(n)) {
+            *cond = cmp(n);
+            *value = lit(1.0);
+            return true;
+        }
+        if (!(n->kind == Node::Bin && n->op == "*")) return false;
+        std::vector<P> f;
+        factors(n, f);
+        size_t at = f.size();
+        for (size_t i = 0; i < f.size() && at == f.size(); ++i)
+            if (is_cmp(f[i])) at = i;
+        if (at == f.size()) return false;
+        *cond = cmp(f[at]);
+        std::string v;
+        for (size_t i = 0; i < f.size(); ++i) {
+            if (i == at) continue;
+            const std::string x = numeric(f[i]);
+            v = v.empty() ? x : op(AMLT_PROG_MUL, v, x);
+        }
+        *value = v.empty() ? lit(1.0) : v;
+        return true;
+    }
+    std::string sum(const P& n) {
+        if (n->kind == Node::Bin && (n->op == "+" || n->op == "-")) {
+            const std::string l = sum(n->l);
+            std::string c, v;
+            if (masked(n->r, &c, &v)) return op(n->op == "-" ? AMLT_PROG_MASKSUB : AMLT_PROG_MASKADD, l, c, v);
+            return op(n->op == "-" ? AMLT_PROG_SUB : AMLT_PROG_ADD, l, numeric(n->r));
+        }
+        std::string c, v;
+        if (masked(n, &c, &v)) return op(AMLT_PROG_MASKADD, lit(0.0), c, v);
+        return plain(n);
+    }
+    std::string numeric(const P& n) {
+        if (is_cmp(n)) return op(AMLT_PROG_MASKADD, lit(0.0), cmp(n), lit(1.0));
+        if (n->kind == Node::Bin && (n->op == "+" || n->op == "-")) return sum(n);
+        std::string c, v;
+        if (masked(n, &c, &v)) return op(AMLT_PROG_MASKADD, lit(0.0), c, v);
+        return plain(n);
+    }
+    std::string plain(const P& n) {
+        if (n->kind != Node::Bin) return leaf(n);
+        if (n->op == "+" || n->op == "-") return sum(n);
+        if (n->op == "*") return op(AMLT_PROG_MUL, numeric(n->l), numeric(n->r));
+        if (n->op == "/") return op(AMLT_PROG_DIV, numeric(n->l), numeric(n->r));
+        return op(AMLT_PROG_MASKADD, lit(0.0), cmp(n), lit(1.0));
+    }
+};
 
 P parse_expr(const char* text) {
     Parser ps;
@@ -311,6 +472,21 @@ RecognizedTask recognize_task(const std::string& source) {
         return out;
     };
     P tree = classify(rhs);
+    {
+        ProgramCounter pc;
+        pc.numeric(tree);
+        pc.counts[op == "+=" ? AMLT_PROG_ADD : AMLT_PROG_MOV] += 1;  // the final accumulate / move
+        int instrs = 0, flops = 0;
+        for (int c = 0; c < AMLT_PROG_NOPS; ++c) {
+            rt.prog_counts[c] = pc.counts[c];
+            instrs += pc.counts[c];
+            // (B): add / sub / mul / div / compare 1, masksub / maskadd 2 (x -+ m*y), mov 0
+            flops += pc.counts[c] * (c == AMLT_PROG_MOV ? 0 : (c == AMLT_PROG_MASKSUB || c == AMLT_PROG_MASKADD) ? 2 : 1);
+        }
+        rt.prog_instrs = instrs;
+        rt.prog_flops = flops;
+    }
+    const P ctree = canon(tree);
     int na = 0, nb = 0;
     for (auto& kv : role) {
         if (kv.second[0] == 'A') {
@@ -336,7 +512,7 @@ RecognizedTask recognize_task(const std::string& source) {
     };
     for (const auto& tp : kTemplates) {
         Env env;
-        if (!match(parse_expr(tp.text), tree, env)) continue;
+        if (!match(canon(parse_expr(tp.text)), ctree, env)) continue;
         rt.desc.body = tp.body;
         rt.desc.accumulate = op == "+=" ? 1 : 0;
         rt.desc.thres_class = AMLT_LEAF_CONSTANT;

@@ -23,6 +23,11 @@ struct RecognizedTask {
     std::string expr;
     std::vector<std::string> aux_names;
     std::vector<int> aux_class;  // amlt_leaf_class
+    // the reference's compiled program for the statement: instructions per
+    // opcode (AMLT_PROG_*), their total, and its body-op flops
+    int prog_counts[AMLT_PROG_NOPS] = {};
+    int prog_instrs = 0;
+    int prog_flops = 0;
 };
 
 // Parse + recognise; throws TaskError (UNSUPPORTED / ENGINE).

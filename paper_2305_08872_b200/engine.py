@@ -260,11 +260,23 @@ def _dtype_code_of(x) -> int:
             np.dtype(np.int32): N.I32}[np.asarray(x).dtype]
 
 
+@dataclass(frozen=True)
+class Shape:
+    """The shape of an operand another rank holds: with
+    AMLT_HOST_BCAST_SHARED, ranks other than 0 describe B and the shared
+    vectors by shape only (row-major, dense) and receive them by broadcast."""
+    rows: int
+    cols: int = 1
+    dtype: str = "f64"
+
+
 def matrix_of(x, expect_device: Optional[bool] = None) -> N.Matrix:
     """Describes a 1-D/2-D torch tensor or numpy array as an amlt_matrix
     (MatrixBuffer-like: rows, cols, leading stride, storage order)."""
     if x is None:
         return N.Matrix()
+    if isinstance(x, Shape):
+        return N.Matrix(None, x.rows, x.cols, max(x.cols, 1), N.ROW_MAJOR, DTYPES[x.dtype])
     try:
         import torch
         is_t = isinstance(x, torch.Tensor)
@@ -348,6 +360,32 @@ class Context:
             self.close()
         except Exception:  # noqa: BLE001
             pass
+
+    def attach_comm(self, rank: int, world_size: int, unique_id: Optional[bytes] = None,
+                    exchange=None) -> None:
+        """Attaches an NCCL communicator for the multi-process host entry
+        (amlt_gpu_comm_attach): rank 0 makes the id; `exchange(id_or_None)`
+        must return rank 0's id on every rank (e.g. a torch.distributed
+        object broadcast). Collective: every rank must call it."""
+        if world_size <= 1:
+            return
+        if unique_id is None:
+            if rank == 0:
+                buf = C.create_string_buffer(N.NCCL_ID_BYTES)
+                _raise(self._lib.amlt_gpu_comm_unique_id(buf), None)
+                unique_id = buf.raw
+            if exchange is None:
+                raise EngineError("attach_comm needs the id or an exchange function")
+            unique_id = exchange(unique_id)
+        buf = C.create_string_buffer(bytes(unique_id), N.NCCL_ID_BYTES)
+        _raise(self._lib.amlt_gpu_comm_attach(self.handle, buf, int(rank), int(world_size)), self.handle)
+
+    def detach_comm(self) -> None:
+        _raise(self._lib.amlt_gpu_comm_detach(self.handle), self.handle)
+
+    @property
+    def comm_size(self) -> int:
+        return int(self._lib.amlt_gpu_comm_size(self.handle))
 
     def set_stream(self, stream) -> None:
         """Launch on a torch.cuda.Stream (or raw cudaStream_t int); None
@@ -608,12 +646,18 @@ def adaptive_execute_amulet(plan: GpuPlan, ops: Operands, bounds: Bounds, i_h: i
     return rep
 
 
+def _host_flags(r_zero: bool, bcast: bool) -> int:
+    return (N.HOST_R_ZERO if r_zero else 0) | (N.HOST_BCAST_SHARED if bcast else 0)
+
+
 def run_host(plan: GpuPlan, ops: Operands, bounds: Bounds, params: Optional[TileParams] = None,
-             clock: Optional[Clock] = None, r_zero: bool = False) -> float:
+             clock: Optional[Clock] = None, r_zero: bool = False, bcast: bool = False) -> float:
     """Host-buffer entry: operands in host memory (pinned for full speed).
-    Copies in, computes (row bands pipelined against the copies), copies R
+    A / R row bands and B K-panels are pipelined against compute; R comes
     back into ops.r; returns elapsed seconds for all of it. r_zero=True
-    states R starts at zero (zero-filled on the device, not copied in)."""
+    states R starts at zero (zero-filled on the device, not copied in).
+    bcast=True (a communicator attached): B and the shared vectors come
+    from rank 0's host memory by NCCL broadcast (other ranks pass Shape)."""
     ctx = plan.ctx
     bridge = _ClockBridge(clock)
     oc = ops._c(False)
@@ -622,11 +666,83 @@ def run_host(plan: GpuPlan, ops: Operands, bounds: Bounds, params: Optional[Tile
     el = C.c_double()
     st = ctx._lib.amlt_gpu_run_host(ctx.handle, plan.handle, C.byref(oc),
                                     C.byref(tp) if tp is not None else None, C.byref(bc),
-                                    N.HOST_R_ZERO if r_zero else 0, bridge.fn, None,
-                                    C.byref(el))
+                                    _host_flags(r_zero, bcast), bridge.fn, None, C.byref(el))
     bridge.check()
     _raise(st, ctx.handle)
     return el.value
+
+
+def run_host_adaptive(plan: GpuPlan, ops: Operands, bounds: Bounds, clock: Optional[Clock] = None,
+                      r_zero: bool = False, bcast: bool = False) -> TuneReport:
+    """run_adaptive over host buffers (amlt_gpu_run_host_adaptive): the
+    tuner picks the tile on the first call of a shape (the task then runs
+    whole through adaptive_execute), later calls reuse the winner through
+    the copy / compute pipeline. The report's total_seconds covers the
+    copies too."""
+    ctx = plan.ctx
+    bridge = _ClockBridge(clock)
+    oc = ops._c(False)
+    bc = bounds._c()
+    rc = N.TuneReportC()
+    el = C.c_double()
+    st = ctx._lib.amlt_gpu_run_host_adaptive(ctx.handle, plan.handle, C.byref(oc), C.byref(bc),
+                                             _host_flags(r_zero, bcast), bridge.fn, None,
+                                             C.byref(rc), C.byref(el))
+    bridge.check()
+    _raise(st, ctx.handle)
+    return _report(rc)
+
+
+class ShardedGroup:
+    """A persistent row-band group over several devices of this process
+    (amlt_sharded_create): contexts, the NCCL communicator, plans and tuning
+    winners are made once and reused by every run."""
+
+    def __init__(self, devices):
+        self._lib = N.lib()
+        self.devices = list(devices)
+        devs = (C.c_int * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        st = self._lib.amlt_sharded_create(len(self.devices), devs, 0, C.byref(h))
+        if st != N.OK:
+            raise _ERRS.get(st, EngineError)(self._lib.amlt_sharded_last_error(None).decode())
+        self.handle = h
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self._lib.amlt_sharded_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def run(self, ops: Operands, bounds: Bounds, body=None, source: Optional[str] = None,
+            dtype="f64", r_zero: bool = False, **desc):
+        """Runs the task on every device's row band; returns (elapsed seconds,
+        one TuneReport per device). The plan: `source` (a task text), else
+        `body` with the GpuPlan descriptor fields in **desc."""
+        dt = DTYPES[dtype] if isinstance(dtype, str) else int(dtype)
+        d = None
+        if source is None:
+            b = BODIES[body] if isinstance(body, str) else int(body)
+            tc = desc.get("thres_class", "j")
+            tc = THRES_CLASSES[tc] if isinstance(tc, str) else int(tc)
+            d = N.BodyDesc(b, dt, int(bool(desc.get("accumulate", True))), int(desc.get("layout_a", 0)),
+                           int(desc.get("layout_b", 0)), tc, float(desc.get("thres_value", 0.0)))
+        oc = ops._c(False)
+        bc = bounds._c()
+        reps = (N.TuneReportC * len(self.devices))()
+        el = C.c_double()
+        st = self._lib.amlt_sharded_run(self.handle, C.byref(d) if d is not None else None,
+                                        source.encode() if source is not None else None, dt,
+                                        C.byref(oc), C.byref(bc), N.HOST_R_ZERO if r_zero else 0,
+                                        reps, C.byref(el))
+        if st != N.OK:
+            raise _ERRS.get(st, EngineError)(self._lib.amlt_sharded_last_error(self.handle).decode())
+        return el.value, [_report(r) for r in reps]
 
 
 def run_sharded_host(desc_plan: GpuPlan, ops: Operands, bounds: Bounds, devices,

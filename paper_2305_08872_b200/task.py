@@ -13,9 +13,11 @@ This module restates just enough of that pipeline:
   variables, a 2-D target on two distinct loop variables, exactly one
   ``[i][k]``/``[k][i]`` array (A), one ``[k][j]``/``[j][k]`` array (B), and aux
   leaves that are scalars, ``[i]``, ``[j]`` or ``[i][j]``;
-* a match of the statement tree against the five bodies' canonical trees
-  (presets.cpp:52-94 plus the sqdiff / eqcount statements), allowing operand
-  swaps of commutative nodes (a swap never changes an IEEE result).
+* the body match itself — the statement against the fixed bodies' canonical
+  trees after the comparison / product / sum normalisations, else a
+  generated body — and the op counts of the reference's compiled program for
+  the statement come from the native recogniser (csrc/task.cpp through
+  amlt_gpu_recognize), so there is one implementation of the match.
 
 Anything else raises UnsupportedExpression, as the reference does for forms
 its vector backend cannot lower.
@@ -23,8 +25,8 @@ its vector backend cannot lower.
 from __future__ import annotations
 
 import re
-from dataclasses import dataclass
-from typing import List, Optional, Tuple
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Tuple
 
 from . import _native as N
 
@@ -184,56 +186,15 @@ class TaskPlan:
     aux_names: Tuple[str, ...] = ()
     aux_classes: Tuple[int, ...] = ()
     source: str = ""
+    # the reference's compiled program for the statement: instructions per
+    # opcode, and its body-op flops per inner iteration
+    program: Dict[str, int] = field(default_factory=dict, compare=False, hash=False)
+    program_flops: int = 0
 
 
-_TEMPLATES = [
-    ("gemm", N.BODY_GEMM, "A*B"),
-    ("discount", N.BODY_DISCOUNT, "A*B - (A*B > T)*A*B*D"),
-    ("boost", N.BODY_BOOST, "A*B + (A*B > T)*(A*B - T)"),
-    ("sqdiff", N.BODY_SQDIFF, "(A - B)*(A - B)"),
-    ("eqcount", N.BODY_EQCOUNT, "A == B"),
-    ("thrcount", N.BODY_THRCOUNT, "A*B > T"),
-]
-_COMMUTATIVE = {"+", "*", "=="}
-
-
-def _template_tree(text):
-    p = _Parser(_lex(text))
-    e = p.expr()
-    return e
-
-
-def _match(tpl, node, env) -> bool:
-    kind = tpl[0]
-    if kind == "ref":  # template placeholder A, B, T or D
-        ph = tpl[1]
-        if ph in ("A", "B"):
-            return node == ("role", ph)
-        if ph == "T":
-            if node[0] not in ("aux", "num"):
-                return False
-            if node[0] == "aux" and node[2] not in ("c", "i", "j", "ij"):
-                return False
-        if ph == "D" and not (node[0] == "aux" and node[2] == "j"):
-            return False
-        if ph in env:
-            return env[ph] == node
-        env[ph] = node
-        return True
-    if kind == "num":
-        return node == tpl
-    if node[0] != kind:
-        return False
-    saved = dict(env)
-    if _match(tpl[1], node[1], env) and _match(tpl[2], node[2], env):
-        return True
-    env.clear()
-    env.update(saved)
-    if kind in _COMMUTATIVE and _match(tpl[1], node[2], env) and _match(tpl[2], node[1], env):
-        return True
-    env.clear()
-    env.update(saved)
-    return False
+_BODY_NAMES = {N.BODY_GEMM: "gemm", N.BODY_DISCOUNT: "discount", N.BODY_BOOST: "boost",
+               N.BODY_SQDIFF: "sqdiff", N.BODY_EQCOUNT: "eqcount", N.BODY_THRCOUNT: "thrcount",
+               N.BODY_GENERIC: "generic"}
 
 
 def compile_task(source: str) -> TaskPlan:
@@ -297,44 +258,29 @@ def compile_task(source: str) -> TaskPlan:
     if len(a_names) != 1 or len(b_names) != 1:
         raise UnsupportedExpression("not an MMLT: needs exactly one A[i][k] and one B[k][j] array")
 
-    for name, bid, text in _TEMPLATES:
-        env = {}
-        if _match(_template_tree(text), tree, env):
-            t = env.get("T")
-            d = env.get("D")
-            if t is None:
-                tcls, tval, tname = N.LEAF_CONSTANT, 0.0, None
-            elif t[0] == "num":
-                tcls, tval, tname = N.LEAF_CONSTANT, t[1], None
-            elif t[2] == "c":
-                # named scalar: bound at run time as a 1 x 1 buffer
-                tcls, tval, tname = N.LEAF_CONSTANT, 0.0, t[1]
-            else:
-                tcls = {"i": N.LEAF_VEC_I, "j": N.LEAF_VEC_J, "ij": N.LEAF_MAT_IJ}[t[2]]
-                tval, tname = 0.0, t[1]
-            return TaskPlan(
-                body=bid, body_name=name, accumulate=accumulate,
-                layout_a=roles[a_names[0]][1], layout_b=roles[b_names[0]][1],
-                thres_class=tcls, thres_value=tval, a_name=a_names[0], b_name=b_names[0],
-                result_name=target, thres_name=tname, dis_name=d[1] if d else None,
-                var_i=vi, var_j=vj, var_k=vk,
-                dims=(str(ends[vi]), str(ends[vk]), str(ends[vj])))
-    # Any other recognised statement: a generated body, compiled by the native
-    # planner at plan time (csrc/jit.cu); the aux leaf order comes from it.
+    # The body match (six fixed bodies after the canonical rewrites, else a
+    # generated body), the leaf roles and the reference program's op counts
+    # come from the native recogniser (csrc/task.cpp, amlt_gpu_recognize).
     import ctypes as C
     info = N.TaskInfoC()
     st = N.lib().amlt_gpu_recognize(source.encode(), C.byref(info))
     if st != N.OK:
         msg = N.lib().amlt_gpu_last_error(None)
         raise UnsupportedExpression(msg.decode() if msg else "statement not recognised")
+    d = info.desc
     names = tuple(info.aux_names[q].value.decode() for q in range(info.n_aux))
+    thres = info.thres.decode() or None
+    dis = info.dis.decode() or None
+    program = {op: int(info.prog_counts[c]) for c, op in enumerate(N.PROG_OPCODES) if info.prog_counts[c]}
     return TaskPlan(
-        body=N.BODY_GENERIC, body_name="generic", accumulate=accumulate,
-        layout_a=roles[a_names[0]][1], layout_b=roles[b_names[0]][1],
-        thres_class=N.LEAF_CONSTANT, thres_value=0.0, a_name=a_names[0], b_name=b_names[0],
-        result_name=target, thres_name=None, dis_name=None, var_i=vi, var_j=vj, var_k=vk,
-        dims=(str(ends[vi]), str(ends[vk]), str(ends[vj])), aux_names=names,
-        aux_classes=tuple(int(info.aux_class[q]) for q in range(info.n_aux)), source=source)
+        body=d.body, body_name=_BODY_NAMES[d.body], accumulate=bool(d.accumulate),
+        layout_a=d.layout_a, layout_b=d.layout_b, thres_class=d.thres_class,
+        thres_value=d.thres_value, a_name=info.a.decode(), b_name=info.b.decode(),
+        result_name=target, thres_name=thres, dis_name=dis, var_i=vi, var_j=vj, var_k=vk,
+        dims=(str(ends[vi]), str(ends[vk]), str(ends[vj])),
+        aux_names=names if d.body == N.BODY_GENERIC else (),
+        aux_classes=tuple(int(info.aux_class[q]) for q in range(info.n_aux)) if d.body == N.BODY_GENERIC else (),
+        source=source, program=program, program_flops=int(info.prog_flops))
 
 
 # ---------------------------------------------------------------------------

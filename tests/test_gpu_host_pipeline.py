@@ -1,0 +1,192 @@
+"""GPU parity of the host-buffer entry's copy / compute pipeline (row bands
+of A / R, K panels of B), the tuned host entry (run_host_adaptive, the
+reference's run_adaptive over host MatrixBuffers, src/engine.cpp:165-169),
+and the row-band multi-GPU paths: the persistent single-process group
+(amlt_sharded_*) and the one-process-per-GPU broadcast entry (torchrun).
+
+The K panels split the reduction over k into consecutive launches that
+accumulate into R, so integer-valued data (the reference's determinism
+convention, acceptance.cpp:109-132) must stay bit-exact; the tests force
+small panels with AMLT_HOST_PANEL_BYTES.
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from tests.helpers import check, make_inputs, oracle
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture
+def small_panels(monkeypatch):
+    monkeypatch.setenv("AMLT_HOST_PANEL_BYTES", "65536")
+
+
+@pytest.mark.parametrize("body", ["discount", "gemm", "boost", "eqcount", "sqdiff"])
+@pytest.mark.parametrize("r_zero", [False, True])
+def test_panels_and_bands_bit_exact(gpu_ctx, small_panels, body, r_zero):
+    """1100 rows (several row bands) x K = 1000 (three K panels of B): the
+    pipeline's result equals the oracle's bit for bit on int-valued data,
+    R's prior values included."""
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 1100, 1000, 300
+    A, B, t, d = make_inputs(body, M, K, N, "int", seed=71)
+    rng = np.random.default_rng(72)
+    R0 = np.zeros((M, N)) if r_zero else rng.integers(-8, 9, (M, N)).astype(np.float64)
+    want = oracle(body, A, B, t, d, R0=R0)
+    R = R0.copy()
+    plan = gpu_ctx.plan(body, "f64")
+    el = P.run_host(plan, P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K), r_zero=r_zero)
+    assert el > 0
+    check(body, "f64", R, want, exact=True, what=f"pipeline {body} r_zero={r_zero}")
+
+
+def test_panels_sub_rectangle(gpu_ctx, small_panels):
+    """Bounds with k0 > 0, j0 > 0 and a row sub-range: only R(bounds) moves."""
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 1300, 1100, 260
+    A, B, t, d = make_inputs("discount", M, K, N, "int", seed=73)
+    R0 = np.random.default_rng(74).integers(-8, 9, (M, N)).astype(np.float64)
+    b = (40, 1250, 6, 250, 64, 1090)
+    want = oracle("discount", A, B, t, d, R0=R0, bounds=b)
+    R = R0.copy()
+    P.run_host(gpu_ctx.plan("discount", "f64"), P.Operands(A, B, R, t, d), P.Bounds(*b))
+    check("discount", "f64", R, want, exact=True, what="pipeline sub-rectangle")
+
+
+def test_panels_baseline_distribution(gpu_ctx, small_panels):
+    """Config-0 distributions through the panelled pipeline: within 1e-12."""
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 1024, 1024, 1024
+    A, B, t, d = make_inputs("discount", M, K, N, "baseline", seed=75)
+    want = oracle("discount", A, B, t, d)
+    R = np.zeros((M, N))
+    plan = gpu_ctx.plan("discount", "f64")
+    names = [v.name for v in plan.variants()]
+    theta = next(i for i, n in enumerate(names) if "_theta_" in n)
+    for tile in (None, P.TileParams(variant=theta)):
+        R[:] = 0
+        P.run_host(plan, P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K), params=tile, r_zero=True)
+        check("discount", "f64", R, want, what=f"pipeline baseline tile={tile}")
+
+
+def test_run_host_adaptive_tunes_then_reuses(gpu_ctx):
+    """The first call of a shape tunes (row-band or scratch trials) and
+    reports its trials; the second reuses the winner (from_cache) through the
+    pipeline. Coverage: disjoint rectangles whose union is the bounds."""
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 1536, 512, 640
+    A, B, t, d = make_inputs("discount", M, K, N, "int", seed=76)
+    want = oracle("discount", A, B, t, d)
+    gpu_ctx.clear_tuning_cache()
+    plan = gpu_ctx.plan("discount", "f64")
+    reps = []
+    for _ in range(2):
+        R = np.zeros((M, N))
+        reps.append(P.run_host_adaptive(plan, P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K),
+                                        r_zero=True))
+        check("discount", "f64", R, want, exact=True, what="run_host_adaptive")
+    first, second = reps
+    assert first.trials and (first.tuned or first.scratch_tuned)
+    assert not second.trials and second.from_cache and second.best_variant == first.best_variant
+    for rep in reps:
+        area = sum((c.i1 - c.i0) * (c.j1 - c.j0) * (c.k1 - c.k0) for c in rep.coverage)
+        assert area == M * N * K
+        cells = np.zeros((M, N), dtype=np.int32)
+        for c in rep.coverage:
+            if c.k0 == 0:
+                cells[c.i0:c.i1, c.j0:c.j1] += 1
+        assert (cells == 1).all()
+        assert rep.total_seconds > 0
+
+
+def test_bcast_flag_single_rank_is_a_no_op(gpu_ctx, small_panels):
+    """AMLT_HOST_BCAST_SHARED without a communicator (one rank): every
+    operand comes from this rank's host memory."""
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 300, 600, 200
+    A, B, t, d = make_inputs("discount", M, K, N, "int", seed=77)
+    want = oracle("discount", A, B, t, d)
+    R = np.zeros((M, N))
+    gpu_ctx.attach_comm(0, 1)
+    assert gpu_ctx.comm_size == 1
+    P.run_host(gpu_ctx.plan("discount", "f64"), P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K),
+               bcast=True)
+    check("discount", "f64", R, want, exact=True, what="bcast, one rank")
+
+
+def _shard_rows(M, n):
+    """First and last row of every device's band (64-row edges, as the group cuts)."""
+    edges = [min(M, (M * d // n + 32) // 64 * 64) for d in range(n)] + [M]
+    rows = set()
+    for r0, r1 in zip(edges[:-1], edges[1:]):
+        if r1 > r0:
+            rows.update((r0, r1 - 1))
+    return sorted(rows)
+
+
+def test_sharded_group_all_devices(gpu_ctx, small_panels):
+    """The persistent group over every visible device (one on a 1-GPU box):
+    run twice (the second run reuses the tuned winners); the first and last
+    row of every device's band match the oracle bit for bit."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    n = torch.cuda.device_count()
+    M, K, N = 256 * n + 70, 700, 300
+    A, B, t, d = make_inputs("discount", M, K, N, "int", seed=78)
+    rows = _shard_rows(M, n)
+    want = oracle("discount", A[rows], B, t, d)
+    g = P.ShardedGroup(list(range(n)))
+    try:
+        for it in range(2):
+            R = np.zeros((M, N))
+            el, reps = g.run(P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K), body="discount",
+                             r_zero=True)
+            assert el > 0 and len(reps) == n
+            check("discount", "f64", R[rows], want, exact=True, what=f"group run {it}")
+            if it == 1:
+                assert all(r.from_cache or not r.trials for r in reps)
+        # a task text (generated body) through the same group
+        src = ("where(i in [0..M] and j in [0..N] and k in [0..K]) {\n"
+               "  R[i][j] += A[i][k]*B[k][j] + (A[i][k] > thres[j]);\n}\n")
+        R = np.zeros((M, N))
+        g.run(P.Operands(A, B, R, None, None, (t,)), P.Bounds(0, M, 0, N, 0, K), source=src)
+        want2 = (A[rows] @ B) + (A[rows][:, :, None] > t[None, None, :]).sum(axis=1)
+        check("discount", "f64", R[rows], want2, exact=True, what="group, generated body")
+    finally:
+        g.close()
+
+
+@pytest.mark.skipif("not __import__('torch').cuda.is_available() or "
+                    "__import__('torch').cuda.device_count() < 2", reason="needs >= 2 GPUs")
+def test_torchrun_broadcast_entry(tmp_path):
+    """One process per GPU (torchrun, NCCL): each rank attaches the
+    communicator, rank 0 alone holds B / thres / dis in host memory, every
+    rank its own A / R rows; the first and last row of every band match the
+    oracle (tests/mp_bcast_worker.py)."""
+    import torch
+
+    n = torch.cuda.device_count()
+    out = tmp_path / "rows.npz"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", "29531",
+           os.path.join(ROOT, "tests", "mp_bcast_worker.py"), str(out)]
+    r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    z = np.load(out)
+    assert z["bad"] == 0, f"{int(z['bad'])} mismatching rows"

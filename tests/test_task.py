@@ -160,3 +160,71 @@ def test_native_recognizer_parse_error():
     st, _ = native_recognize("where(i in [0..M] {")
     assert st == N.ERR_ENGINE
     assert b"parse error" in N.lib().amlt_gpu_last_error(None)
+
+
+# ---------------------------------------------------------------------------
+# canonical matching: a fixed body written differently still
+# runs its fused kernel; the reference DAG normalises the same way
+# (expr_dag.cpp:182-245)
+
+@pytest.mark.parametrize("rhs,body", [
+    # q1 with the comparison reversed, the mask factor moved, re-associated
+    ("A[i][k]*B[k][j] - (thres[j] < A[i][k]*B[k][j])*A[i][k]*B[k][j]*dis[j]", "discount"),
+    ("A[i][k]*B[k][j] - A[i][k]*B[k][j]*dis[j]*(A[i][k]*B[k][j] > thres[j])", "discount"),
+    ("B[k][j]*A[i][k] - dis[j]*(B[k][j]*A[i][k] > thres[j])*(A[i][k]*B[k][j])", "discount"),
+    # q2 with the terms swapped and the comparison reversed
+    ("(thres[j] < A[i][k]*B[k][j])*(A[i][k]*B[k][j] - thres[j]) + A[i][k]*B[k][j]", "boost"),
+    ("100 < A[i][k]*B[k][j]", "thrcount"),
+])
+def test_canonical_forms_hit_fixed_bodies(rhs, body):
+    assert compile_task(wrap(rhs)).body_name == body
+
+
+@pytest.mark.parametrize("rhs", [
+    "A[i][k]*B[k][j] - (A[i][k]*B[k][j] >= thres[j])*A[i][k]*B[k][j]*dis[j]",  # >= is not >
+    "A[i][k]*B[k][j] + (A[i][k]*B[k][j] > thres[j])*A[i][k]*B[k][j]*dis[j]",  # + is not -
+    "A[i][k]*B[k][j] - (A[i][k] > thres[j])*A[i][k]*B[k][j]*dis[j]",          # mask of A alone
+    "(B[k][j] - A[i][k])*(A[i][k] - B[k][j])",
+])
+def test_near_misses_stay_generic(rhs):
+    assert compile_task(wrap(rhs)).body == N.BODY_GENERIC
+
+
+# ---------------------------------------------------------------------------
+# the reference program's op counts (SURVEY §8(d) measure (B)), pinned
+# against the unmodified reference's schedule_labelfs output
+
+def _ref_program_counts(src):
+    t = po.RefTask.create(src, 4, 4, 4)
+    counts = {}
+    for ln in t.program():
+        op = ln.split()[0]
+        counts[op] = counts.get(op, 0) + 1
+    return counts
+
+
+def _program_sources():
+    srcs = [P.task.preset_source(n) for n in P.task.preset_names()]
+    srcs += [wrap("(A[i][k] - B[k][j])*(A[i][k] - B[k][j])"), wrap("A[i][k] == B[k][j]"),
+             wrap("A[i][k]*B[k][j] - (thres[j] < A[i][k]*B[k][j])*A[i][k]*B[k][j]*dis[j]"),
+             wrap("A[i][k]*B[k][j] + u[i]*v[j]"), wrap("(A[i][k] + 1)*(B[k][j] - 1)/2 + W[i][j]"),
+             wrap("A[i][k]*B[k][j]*s + u[i] - v[j]*W[i][j]"),
+             wrap("(A[i][k] > v[j])*(B[k][j] + 2) - (A[i][k] < 1)*u[i] + 3"),
+             wrap("A[i][k]*B[k][j]", "=")]
+    return srcs
+
+
+@pytest.mark.skipif(not po.ref_available(), reason="reference engine not built")
+@pytest.mark.parametrize("src", _program_sources())
+def test_program_op_counts_match_the_reference(src):
+    t = compile_task(src)
+    assert t.program == _ref_program_counts(src)
+
+
+def test_body_op_flops_of_the_five_bodies():
+    """(B) per SURVEY §8(d): discount / boost 6, gemm 2, sqdiff 3, eqcount 4."""
+    flops = {"q1": 6, "q2": 6, "matmul": 2}
+    for name, want in flops.items():
+        assert compile_task(P.task.preset_source(name)).program_flops == want
+    assert compile_task(wrap("(A[i][k] - B[k][j])*(A[i][k] - B[k][j])")).program_flops == 3
+    assert compile_task(wrap("A[i][k] == B[k][j]")).program_flops == 4
