@@ -7,27 +7,41 @@ distributions (A integers 0..9, B U[1,100), thres U[50,450), dis U[0,0.3)),
 R zero-initialised. A "step" is one pass of the hot path over that whole
 problem: R += sum_k body(A, B, thres, dis).
 
-Multi-GPU (torchrun): rank r owns R / A rows [r*M/n, (r+1)*M/n); B and the
-per-column vectors are created on rank 0 and NCCL-broadcast over NVLink to
-every rank (no reduction: rows of R are independent). Strong scaling: the
-total problem is fixed as n grows.
+Multi-GPU: `bench.py --gpus N` with WORLD_SIZE unset re-launches itself
+under torch.distributed.run (one process per GPU, NCCL); under torchrun
+WORLD_SIZE must equal --gpus. Rank r owns R / A rows [r*M/n, (r+1)*M/n)
+(64-row edges); B and the per-column vectors come from rank 0 (NCCL
+broadcast over NVLink), no reduction: rows of R are independent. The total
+problem is fixed as n grows (strong scaling).
 
 Legs:
-  value   device-resident inputs; K timed steps through the public API
-          (adaptive_execute -> cached tuned tile -> one kernel per step),
-          CUDA events on the launch stream, max over ranks.
-  e2e     the same metric through the host-buffer C-ABI entry
-          (amlt_gpu_run_host) with pinned host inputs: every step copies A, B
-          and the vectors H2D and R D2H inside the timed region.
+  value     device-resident inputs; K timed steps of the tuned winner through
+            the public API (one enqueue per step), CUDA events on the launch
+            stream, max over ranks.
+  verified  after the timed region: the same winner once more on a zeroed R,
+            then the CPU oracle (oracle/, the checker only) on the first and
+            last row of every rank's band plus random rows x sampled columns.
+  e2e       the same metric through the host-buffer C-ABI entry
+            (amlt_gpu_run_host) from pinned host memory: every step copies
+            A (each rank its rows) and B / thres / dis (rank 0 only; NCCL
+            broadcast to the other ranks inside the call, panel by panel) H2D
+            and R D2H, all inside the timed region.
+  roofline  (A) matmul-like flops (2 per inner iteration) against the pipe
+            peak measured in this run; (B) the reference program's body-op
+            flops (the statement's compiled pseudo-program, counted by the
+            native recogniser); (C) pipe-busy % and DRAM bytes of the reported
+            tile from its committed ncu capture (profiles/r*/ncu_keyed.json).
   cpu_baseline  the UNMODIFIED reference engine (oracle/_ref) on the box's
-          host cores, rank 0 at N=1 only, on a bounded sample of the same
-          workload (reference arm: --impl reference).
+            host cores, rank 0 at N=1 only, on a bounded sample of the same
+            workload, extrapolated by rate (reference arm: --impl reference).
 """
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
+import socket
 import subprocess
 import sys
 import tempfile
@@ -40,7 +54,7 @@ METRIC = ("matmul-like GFLOP/s (inner iters/s) & fraction of FMA/tensor peak, "
           "1/2/4/8 B200")
 
 WORKLOADS = {
-    # name: (body, dtype, M, K, N, distribution)
+    # name: (body, dtype, M, K, N)
     "cfg4_discount_f64": ("discount", "f64", 32768, 8192, 32768),
     "cfg0_discount_f64": ("discount", "f64", 1024, 1024, 1024),
     "cfg1_boost_f32": ("boost", "f32", 4096, 4096, 4096),
@@ -50,9 +64,12 @@ WORKLOADS = {
     "cfg3_sqdiff_f32": ("sqdiff", "f32", 65536, 1024, 256),
     "cfg3_eqcount_i32": ("eqcount", "i32", 65536, 1024, 256),
 }
-# FP64-pipe ops per inner iteration of each body's kernel;
-# the ceiling as a fraction of 2-flop "matmul-like" accounting is 1/ops.
+TEXT = {"discount": "A[i][k]*B[k][j] - (A[i][k]*B[k][j] > thres[j])*A[i][k]*B[k][j]*dis[j]",
+        "boost": "A[i][k]*B[k][j] + (A[i][k]*B[k][j] > thres[j])*(A[i][k]*B[k][j] - thres[j])",
+        "gemm": "A[i][k]*B[k][j]", "sqdiff": "(A[i][k] - B[k][j])*(A[i][k] - B[k][j])",
+        "eqcount": "A[i][k] == B[k][j]"}
 PIPE = {"f64": "dfma", "f32": "ffma", "i32": "alu"}
+TOL = {"f64": 1e-12, "f32": 1e-5, "i32": 0.0}  # BASELINE north_star tolerances vs the fp64 oracle
 
 
 def log(*a):
@@ -64,6 +81,62 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     lrank = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, lrank
+
+
+def task_source(body):
+    return ("where(i in [0..M] and j in [0..N] and k in [0..K]) {\n  R[i][j] += "
+            + TEXT[body] + ";\n}\n")
+
+
+# ---------------------------------------------------------------------------
+# rank launch
+
+
+def free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-run this command as N ranks
+    (torch.distributed.run, one process per GPU); rank 0's JSON line passes
+    through on stdout."""
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < n and "--dry-run" not in sys.argv:
+        log(f"bench.py: --gpus {n} but only {have} CUDA device(s) are visible")
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.abspath(__file__), *sys.argv[1:]]
+    log("bench.py: launching", " ".join(cmd))
+    return subprocess.call(cmd)
+
+
+class NcclLog:
+    """NCCL_DEBUG=INFO for the communicator lines (nranks, rank, NVLS /
+    transport choices), written to a per-rank file and echoed to stderr at
+    the end so stdout keeps exactly one JSON line."""
+
+    def __init__(self, rank: int):
+        self.path = None
+        if "NCCL_DEBUG_FILE" not in os.environ:
+            self.path = os.path.join(tempfile.gettempdir(), f"amlt_bench_nccl.{os.getpid()}.r{rank}.log")
+            os.environ["NCCL_DEBUG_FILE"] = self.path
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT,ENV")
+        self.rank = rank
+
+    def echo(self):
+        if not self.path or not os.path.exists(self.path):
+            return
+        with open(self.path, errors="replace") as f:
+            for line in f:
+                if any(s in line for s in ("nranks", "Init COMPLETE", "NVLS", "comm ", "NCCL version")):
+                    log(f"[nccl rank {self.rank}] {line.rstrip()}")
+        os.unlink(self.path)
 
 
 # ---------------------------------------------------------------------------
@@ -124,14 +197,14 @@ class ClockSampler:
 # data
 
 
-def gen_inputs(body, dtype, M_rows, K, N, row0, rank, device, broadcast):
-    """BASELINE-distribution inputs on `device`. B / thres / dis are made on
-    rank 0 and broadcast (NCCL) when `broadcast`; A rows are per rank."""
+def gen_shared(body, dtype, K, N, device):
+    """B and the per-column vectors with BASELINE's distributions (seeded)."""
     import torch
 
     tdt = {"f64": torch.float64, "f32": torch.float32, "i32": torch.int32}[dtype]
     g = torch.Generator(device=device)
     g.manual_seed(1)
+    th = ds = None
     if body == "discount":
         Bv = torch.empty((K, N), dtype=tdt, device=device).uniform_(1, 100, generator=g)
         th = torch.empty(N, dtype=tdt, device=device).uniform_(50, 450, generator=g)
@@ -139,33 +212,33 @@ def gen_inputs(body, dtype, M_rows, K, N, row0, rank, device, broadcast):
     elif body == "boost":
         Bv = torch.rand((K, N), dtype=tdt, device=device, generator=g)
         th = torch.empty(N, dtype=tdt, device=device).uniform_(0.25, 0.75, generator=g)
-        ds = None
     elif body == "gemm":
         Bv = torch.randn((K, N), dtype=tdt, device=device, generator=g)
-        th = ds = None
     elif body == "sqdiff":
         Bv = torch.empty((K, N), dtype=tdt, device=device).uniform_(-1, 1, generator=g)
-        th = ds = None
     else:  # eqcount
         Bv = torch.randint(0, 16, (K, N), dtype=tdt, device=device, generator=g)
-        th = ds = None
-    if broadcast:  # B and the per-column vectors: NCCL broadcast from rank 0
-        from paper_2305_08872_b200.sharded import broadcast_replicated
+    return Bv, th, ds
 
-        broadcast_replicated([Bv, th, ds], src=0)
+
+def gen_rows(body, dtype, rows, K, row0, device):
+    """This rank's rows of A (seeded by the first row, so any split gives the
+    same A for the same rows only per split; the oracle check uses the rows
+    each rank actually holds)."""
+    import torch
+
+    tdt = {"f64": torch.float64, "f32": torch.float32, "i32": torch.int32}[dtype]
     ga = torch.Generator(device=device)
     ga.manual_seed(1000 + row0)
     if body == "discount":
-        A = torch.randint(0, 10, (M_rows, K), device=device, generator=ga).to(tdt)
-    elif body == "boost":
-        A = torch.rand((M_rows, K), dtype=tdt, device=device, generator=ga)
-    elif body == "gemm":
-        A = torch.randn((M_rows, K), dtype=tdt, device=device, generator=ga)
-    elif body == "sqdiff":
-        A = torch.empty((M_rows, K), dtype=tdt, device=device).uniform_(-1, 1, generator=ga)
-    else:
-        A = torch.randint(0, 16, (M_rows, K), dtype=tdt, device=device, generator=ga)
-    return A, Bv, th, ds
+        return torch.randint(0, 10, (rows, K), device=device, generator=ga).to(tdt)
+    if body == "boost":
+        return torch.rand((rows, K), dtype=tdt, device=device, generator=ga)
+    if body == "gemm":
+        return torch.randn((rows, K), dtype=tdt, device=device, generator=ga)
+    if body == "sqdiff":
+        return torch.empty((rows, K), dtype=tdt, device=device).uniform_(-1, 1, generator=ga)
+    return torch.randint(0, 16, (rows, K), dtype=tdt, device=device, generator=ga)
 
 
 # ---------------------------------------------------------------------------
@@ -179,9 +252,7 @@ def reference_sample(body, M, K, N, threads):
     reference's ~0.1 G iterations/s per thread on the interpreted bodies.
     Rows are independent, so the sample's rate is the workload's rate."""
     rows = min(M, 12 * threads)
-    cols = min(N, 4096)
-    if body == "gemm":
-        cols = min(N, 8192)
+    cols = min(N, 8192 if body == "gemm" else 4096)
     return rows, K, cols
 
 
@@ -222,34 +293,12 @@ def run_reference(body, M, K, N, steps, warmup, threads):
     iters = rows * K_ * cols
     sec = sum(times) / len(times)
     return {"iters_per_s": iters / sec, "seconds_per_sample": sec,
+            "sample_fraction": (rows * cols) / (M * N),
             "sample": f"{rows} rows x {cols} cols x K={K_} of the workload "
                       f"({iters / 1e9:.2f} G inner iterations), reference adaptive_execute "
                       f"on {threads} row bands (one std::thread each), seed-1 BASELINE "
-                      f"distributions"}
-
-
-def traffic_for(workload, tile):
-    """DRAM bytes per launch of this workload's kernel from the newest
-    committed ncu capture (profiles/r*/traffic.json), or None."""
-    import glob
-
-    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")),
-                       reverse=True):
-        try:
-            d = json.load(open(path)).get(workload, {})
-        except (OSError, ValueError):
-            continue
-        entry = d.get(tile) or d.get("*")  # "*": tile-independent (same raster groups)
-        if entry:
-            return entry["dram_read"] + entry["dram_write"]
-    return None
-
-
-def algorithmic_bytes(body, dtype, M, K, N):
-    """Compulsory HBM bytes per launch: A, B, R read + R write, vectors."""
-    es = 8 if dtype == "f64" else 4
-    vec = {"discount": 2, "boost": 1}.get(body, 0) * N
-    return es * (M * K + K * N + 2 * M * N + vec)
+                      f"distributions; the workload's rate is extrapolated from the sample's "
+                      f"(rows of R are independent)"}
 
 
 def cpu_threads():
@@ -260,7 +309,29 @@ def cpu_threads():
 
 
 # ---------------------------------------------------------------------------
-# main
+# roofline helpers
+
+
+def ncu_capture_for(workload, tile):
+    """Pipe-busy % and DRAM bytes per launch of `tile` on `workload` from the
+    newest committed keyed ncu capture (profiles/r*/ncu_keyed.json), or None."""
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "ncu_keyed.json")), reverse=True):
+        try:
+            d = json.load(open(path)).get(workload, {})
+        except (OSError, ValueError):
+            continue
+        if tile in d:
+            e = dict(d[tile])
+            e["file"] = os.path.relpath(path, ROOT)
+            return e
+    return None
+
+
+def algorithmic_bytes(body, dtype, M, K, N):
+    """Compulsory HBM bytes per launch: A, B, R read + R write, vectors."""
+    es = 8 if dtype == "f64" else 4
+    vec = {"discount": 2, "boost": 1}.get(body, 0) * N
+    return es * (M * K + K * N + 2 * M * N + vec)
 
 
 def tensor_tf32_peak() -> float:
@@ -272,6 +343,149 @@ def tensor_tf32_peak() -> float:
             return float(json.load(f)["bf16_tflops"]) / 2.0
     except Exception:  # noqa: BLE001
         return 2250.0 / 2.0
+
+
+def launches_of(name: str, split: bool) -> int:
+    """Kernel launches one enqueue of the winner makes."""
+    if "tcgen05_3xtf32" in name:
+        return 3  # operand split of A, of B, the tensor-core GEMM
+    if "ozaki" in name:
+        return 5  # row / column exponents, A / B slicing, the int8 GEMM
+    if "_theta_" in name or "_swar_" in name:
+        return 4  # B preparation, A scan, the tile, the guard-exited fallback
+    return 2 if split else 1
+
+
+# ---------------------------------------------------------------------------
+# legs
+
+
+def verify_rows(P, plan, win, A, B, th, ds, R, body, dtype, rows, rank, row0, stream):
+    """The timed winner once more on a zeroed R, then the oracle on this
+    rank's first and last row plus random rows x sampled columns."""
+    import numpy as np
+    import torch
+
+    from oracle import pyoracle as po
+
+    M, K, N = rows, A.shape[1], B.shape[1]
+    R.zero_()
+    P.enqueue(plan, P.Operands(A, B, R, th, ds), win, P.Bounds(0, M, 0, N, 0, K))
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(17 + rank)
+    ri = sorted({0, M - 1} | set(int(x) for x in rng.integers(0, M, 4))) if M > 0 else []
+    ci = sorted({0, N - 1} | set(int(x) for x in rng.integers(0, N, 510)))
+    if not ri:
+        return 0, len(ci), 0.0, 0
+    idx = torch.tensor(ri, device=A.device)
+    cdx = torch.tensor(ci, device=A.device)
+    got = R[idx][:, cdx].double().cpu().numpy()
+    Ah = A[idx].double().cpu().numpy()
+    Bh = B[:, cdx].double().cpu().numpy()
+    th_h = th[cdx].double().cpu().numpy() if th is not None else None
+    ds_h = ds[cdx].double().cpu().numpy() if ds is not None else None
+    kind = {"gemm": po.GEMM, "discount": po.DISCOUNT, "boost": po.BOOST, "sqdiff": po.SQDIFF,
+            "eqcount": po.EQCOUNT}[body]
+    want = np.zeros((len(ri), len(ci)))
+    po.oracle_run(kind, Ah, Bh, want, thres=th_h, dis=ds_h)
+    if dtype == "i32" or body == "eqcount":
+        return len(ri), len(ci), 0.0, int((got != want).sum())
+    err = np.abs(got - want)
+    if body in ("gemm", "sqdiff"):  # normwise: |d| <= tol * sum_k |term_k| (SURVEY §7)
+        if body == "gemm":
+            scale = np.abs(Ah) @ np.abs(Bh)
+        else:
+            scale = (Ah * Ah) @ np.ones_like(Bh) + np.ones_like(Ah) @ (Bh * Bh) + 2 * np.abs(Ah) @ np.abs(Bh)
+    else:
+        scale = np.abs(want)
+    rel = err / np.maximum(scale, np.finfo(np.float64).tiny)
+    return len(ri), len(ci), float(rel.max()), int((rel > TOL[dtype]).sum())
+
+
+def cuda_core_leg(P, plan, ops, bounds, stream, steps, M, K, N, peak_ffma_tflops):
+    """Config 2 fp32 as BASELINE writes it (the CUDA-core path): the fastest
+    SIMT FFMA tile, timed like the value leg (the tuner picks the tcgen05
+    3xTF32 GEMM for the headline)."""
+    import torch
+
+    best = None
+    for vi, v in enumerate(plan.variants()):
+        if v.tensor_core or "tcgen05" in v.name or v.name.endswith("_u"):
+            continue
+        tp = P.TileParams(variant=vi)
+        try:
+            P.enqueue(plan, ops, tp, bounds)
+        except P.EngineError:
+            continue
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(max(steps, 2)):
+            P.enqueue(plan, ops, tp, bounds)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t = e0.elapsed_time(e1) / 1e3 / max(steps, 2)
+        if best is None or t < best[1]:
+            best = (v.name, t)
+    if best is None:
+        return None
+    tf = 2 * M * K * N / best[1] / 1e12
+    return {"value": tf * 1e3, "unit": "GFLOP/s", "tile": best[0], "ms_per_step": best[1] * 1e3,
+            "frac_of_ffma_peak": tf / peak_ffma_tflops,
+            "note": "BASELINE config 2 fp32 on the CUDA-core FFMA path, best SIMT tile; the headline "
+                    "value is the tcgen05 3xTF32 tensor-core GEMM the tuner picks"}
+
+
+# ---------------------------------------------------------------------------
+# CPU dry run of the multi-rank plumbing
+
+
+def dry_run(args, body, dtype, M, K, N, ws, rank):
+    """The harness's multi-rank logic on CPU (gloo): each rank's row band,
+    B and the vectors made on rank 0 and broadcast, a checksum of them
+    gathered from every rank, the max-over-ranks reduction; rank 0 prints one
+    JSON line with "dry_run": true and no measured value."""
+    import torch
+
+    from paper_2305_08872_b200.sharded import row_band
+
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("gloo")
+    row0, row1 = row_band(M, ws, rank, align=64)
+    kk, nn = min(K, 64), min(N, 64)  # a corner of B stands in for the whole
+    g = torch.Generator().manual_seed(1 + rank)  # ranks differ until the broadcast
+    Bv = torch.rand((kk, nn), dtype=torch.float64, generator=g)
+    vec = torch.rand(nn, dtype=torch.float64, generator=g)
+    if dist is not None:
+        dist.broadcast(Bv, src=0)
+        dist.broadcast(vec, src=0)
+    local = torch.tensor([float(row0), float(row1), float(Bv.sum() + vec.sum()), float(rank + 1)],
+                         dtype=torch.float64)
+    parts = [torch.zeros_like(local) for _ in range(ws)]
+    if dist is not None:
+        dist.all_gather(parts, local)
+        el = torch.tensor([float(rank + 1)], dtype=torch.float64)
+        dist.all_reduce(el, op=dist.ReduceOp.MAX)
+    else:
+        parts = [local]
+        el = torch.tensor([1.0])
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "value": None, "metric": METRIC, "n_gpus": ws,
+                          "config": {"workload": args.workload, "body": body, "dtype": dtype,
+                                     "M": M, "K": K, "N": N, "parallelism": f"rowshard{ws}"},
+                          "bands": [[int(p[0].item()), int(p[1].item())] for p in parts],
+                          "shared_checksums": [float(p[2].item()) for p in parts],
+                          "max_over_ranks": float(el.item())}), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# main
 
 
 def main():
@@ -287,12 +501,26 @@ def main():
                          "change the trial timings")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-verify", action="store_true")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU only (gloo): rank launch, row bands, the broadcast of B / vectors and "
+                         "the max-over-ranks reduction, with no kernel and no timing claim "
+                         "(tests/test_bench_harness.py)")
     ap.add_argument("--f64-emulation", action="store_true",
                     help="let the tuner use the int8-tensor-core f64 GEMM (AMLT_CTX_F64_EMULATION)")
     args = ap.parse_args()
-    ws, rank, lrank = dist_env()
     body, dtype, M, K, N = WORKLOADS[args.workload]
     steps, warmup = args.steps, max(args.warmup, 0)
+
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        return spawn_ranks(args.gpus)
+    ws, rank, lrank = dist_env()
+    if "WORLD_SIZE" in os.environ and ws != args.gpus:
+        log(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch one rank per GPU")
+        return 2
+
+    if args.dry_run:
+        return dry_run(args, body, dtype, M, K, N, ws, rank)
 
     if args.impl == "reference":
         if rank != 0:
@@ -303,32 +531,36 @@ def main():
         line = {"impl": "reference", "metric": METRIC, "value": gf, "unit": "GFLOP/s",
                 "inner_iters_per_s": r["iters_per_s"], "n_gpus": args.gpus, "steps": steps,
                 "warmup": warmup, "ms_per_step": r["seconds_per_sample"] * 1e3,
+                "ms_per_step_note": "seconds of one bounded sample (see cpu_baseline.sample); the "
+                                    "workload's rate is extrapolated from it",
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic",
                 "config": {"workload": args.workload, "body": body, "M": M, "K": K, "N": N,
                            "parallelism": f"cpu_threads{threads}"},
                 "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": threads,
-                                 "kind": "reference", "sample": r["sample"]},
+                                 "kind": "reference", "sample": r["sample"],
+                                 "extrapolated_from_sample": True,
+                                 "sample_fraction": r["sample_fraction"]},
                 "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
         return 0
 
+    nccl_log = NcclLog(rank) if ws > 1 else None
     import torch
 
     import paper_2305_08872_b200 as P
+    from paper_2305_08872_b200.sharded import row_band
     from paper_2305_08872_b200.task import compile_task
 
     assert torch.cuda.is_available(), "bench.py needs a CUDA device"
     torch.cuda.set_device(lrank)
     device = torch.device("cuda", lrank)
     dist = None
-    if ws > 1 or "TORCHELASTIC_RUN_ID" in os.environ:  # launched by torchrun
+    if ws > 1:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=device)
-    from paper_2305_08872_b200.sharded import row_band
-
     row0, row1 = row_band(M, ws, rank, align=64)
     rows = row1 - row0
 
@@ -338,27 +570,26 @@ def main():
     stream = torch.cuda.Stream(device)
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream)
-    text = {"discount": "A[i][k]*B[k][j] - (A[i][k]*B[k][j] > thres[j])*A[i][k]*B[k][j]*dis[j]",
-            "boost": "A[i][k]*B[k][j] + (A[i][k]*B[k][j] > thres[j])*(A[i][k]*B[k][j] - thres[j])",
-            "gemm": "A[i][k]*B[k][j]", "sqdiff": "(A[i][k] - B[k][j])*(A[i][k] - B[k][j])",
-            "eqcount": "A[i][k] == B[k][j]"}[body]
-    task = compile_task("where(i in [0..M] and j in [0..N] and k in [0..K]) {\n  R[i][j] += "
-                        + text + ";\n}\n")
+    task = compile_task(task_source(body))
     plan = ctx.plan_for(task, dtype)
 
     # roofline denominator, measured on this GPU now
     pipe = PIPE[dtype] if not (body == "gemm" and dtype == "f64") else "dmma"
     peak_ops, peak_ghz = P.engine.measure_peak(pipe)
     if pipe == "alu":
-        # integer bodies are issue-bound (ISETP + predicated add per
-        # iteration, both integer-pipe instructions): the ceiling is the
-        # SM's issue rate, 4 schedulers x 32 lanes per clock
+        # integer bodies are issue-bound: the ceiling is the SM's issue rate,
+        # 4 schedulers x 32 lanes per clock
         props = torch.cuda.get_device_properties(device)
         peak_tflops = 128 * props.multi_processor_count * peak_ghz * 1e9 / 1e12
     else:
         peak_tflops = 2 * peak_ops / 1e12
 
-    A, B, th, ds = gen_inputs(body, dtype, rows, K, N, row0, rank, device, dist is not None)
+    B, th, ds = gen_shared(body, dtype, K, N, device)
+    if dist is not None:  # input placement before timing: B and the vectors from rank 0
+        for t in (B, th, ds):
+            if t is not None:
+                dist.broadcast(t, src=0)
+    A = gen_rows(body, dtype, rows, K, row0, device)
     R = torch.zeros((rows, N), dtype=A.dtype, device=device)
     ops = P.Operands(A, B, R, th, ds)
     bounds = P.Bounds(0, rows, 0, N, 0, K)
@@ -392,9 +623,14 @@ def main():
     flush = in_bytes < (256 << 20)
     flush_buf = torch.empty(512 << 20, dtype=torch.uint8, device=device) if flush else None
     sampler = ClockSampler(lrank)
-    launches = 0
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(steps)]
+    last = reports[-1] if reports else None
+    win = P.TileParams(kc=last.best_kc if last and last.best_kc < K else 0,
+                       variant=last.best_variant if last else -1)
+    variants = plan.variants()
+    win_name = variants[win.variant].name if win.variant is not None and win.variant >= 0 else ""
+    split = bool(last and last.best_kc < K)
     barrier()
     torch.cuda.synchronize()
     sampler.start()
@@ -402,33 +638,14 @@ def main():
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     t0.record(stream)
-    # timed steps: the tuned winner, enqueued back to back on the stream (one
-    # tile launch per step, plus the ordered split-K reduction if split; the
-    # tensor-core f32 GEMM is two operand-split launches plus the GEMM)
-    last = reports[-1] if reports else None
-    win = P.TileParams(kc=last.best_kc if last and last.best_kc < K else 0,
-                       variant=last.best_variant if last else -1)
-    split = bool(last and last.best_kc < K)
-    win_is_tc = last is not None and last.best_variant >= 0 and \
-        "tcgen05_3xtf32" in plan.variants()[last.best_variant].name
-    win_is_oz = last is not None and last.best_variant >= 0 and \
-        "ozaki" in plan.variants()[last.best_variant].name
-    win_is_swar = last is not None and last.best_variant >= 0 and \
-        "_swar_" in plan.variants()[last.best_variant].name
-    win_is_theta = last is not None and last.best_variant >= 0 and \
-        "_theta_" in plan.variants()[last.best_variant].name
+    launches = 0
     for s in range(steps):
         if flush:
             flush_buf.zero_()  # evict L2 (outside the step's events)
         ev[s][0].record(stream)
         P.enqueue(plan, ops, win, bounds)
         ev[s][1].record(stream)
-        # tcgen05 3xTF32: operand split of A, of B, then the tensor-core GEMM
-        # Ozaki: row / column exponents, A / B slicing, then the int8 GEMM
-        # theta-form discount: B planes, A range scan, theta tile, guard-exited fallback
-        # byte-packed eqcount: B packing, A packing, packed tile, guard-exited fallback
-        launches += 3 if win_is_tc else (5 if win_is_oz else (4 if (win_is_theta or win_is_swar)
-                                                              else (2 if split else 1)))
+        launches += launches_of(win_name, split)
     t1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -445,7 +662,6 @@ def main():
     value = 2 * iters_total / el / 1e9
     kernel_s = sum(per_launch) / len(per_launch)
     achieved_tflops = 2 * rows * K * N / kernel_s / 1e12
-    win_name = plan.variants()[win.variant].name if win.variant is not None and win.variant >= 0 else ""
     tensor_tf32 = "tcgen05_3xtf32" in win_name
     ozaki = "ozaki" in win_name
     if ozaki:
@@ -454,41 +670,80 @@ def main():
         peak_tflops, pipe = tensor_tf32_peak() * 4.0 / 28.0, "tcgen05.kind::i8 (Ozaki, 28 slice GEMMs)"
         tensor_tf32 = True
     elif tensor_tf32:
-        # the winner runs on the tcgen05 tensor cores: 3 TF32 MMAs per
-        # product (3xTF32); TF32 dense is half the bf16 rate, so the
-        # effective ceiling is measured bf16 / 2 / 3 (MEASURED_PEAKS.json)
+        # 3 TF32 MMAs per product (3xTF32); TF32 dense is half the bf16 rate
         peak_tflops, pipe = tensor_tf32_peak() / 3.0, "tcgen05.kind::tf32 (3xTF32)"
+
+    # ---- config 2 fp32 on the CUDA-core path, beside the tensor-core headline
+    cuda_core = None
+    if args.workload == "cfg2_gemm_f32" and rank == 0 and ws == 1:
+        ffma_ops, _ = P.engine.measure_peak("ffma")
+        cuda_core = cuda_core_leg(P, plan, ops, bounds, stream, steps, rows, K, N, 2 * ffma_ops / 1e12)
+
+    # ---- verified: the timed winner, re-run once on a zeroed R, vs the oracle
+    verified = None
+    if not args.no_verify:
+        nr, nc, worst, bad = verify_rows(P, plan, win, A, B, th, ds, R, body, dtype, rows, rank, row0,
+                                         stream)
+        if dist is not None:
+            tt = torch.tensor([nr, worst, bad], dtype=torch.float64, device=device)
+            parts = [torch.zeros_like(tt) for _ in range(ws)]
+            dist.all_gather(parts, tt)
+            nr = int(sum(p[0].item() for p in parts))
+            worst = max(p[1].item() for p in parts)
+            bad = int(sum(p[2].item() for p in parts))
+        verified = {"rows": nr, "cols": nc, "max_rel": worst, "tol": TOL[dtype], "mismatches": bad,
+                    "ok": bad == 0,
+                    "how": "the timed winner re-run once on a zeroed R after the timed region; the "
+                           "C oracle (oracle/liboracle.so, pinned to the reference's run_naive) on the "
+                           "first and last row of every rank's band plus random rows x sampled columns"
+                           + ("; normwise for gemm/sqdiff" if body in ("gemm", "sqdiff") else "")}
 
     # ---- e2e leg: host buffers through the C-ABI host entry
     e2e = None
     if not args.no_e2e:
         hA = A.cpu().pin_memory()
-        hB = B.cpu().pin_memory()
-        hth = th.cpu().pin_memory() if th is not None else None
-        hds = ds.cpu().pin_memory() if ds is not None else None
+        hB = B.cpu().pin_memory() if rank == 0 else P.Shape(K, N, dtype)
+        hth = (th.cpu().pin_memory() if rank == 0 else P.Shape(N, 1, dtype)) if th is not None else None
+        hds = (ds.cpu().pin_memory() if rank == 0 else P.Shape(N, 1, dtype)) if ds is not None else None
         hR = torch.empty((rows, N), dtype=A.dtype).pin_memory()
         hops = P.Operands(hA, hB, hR, hth, hds)
         del A, B, R, ops
         torch.cuda.empty_cache()
-        P.run_host(plan, hops, bounds, r_zero=True)  # warm-up (staging alloc)
+        bcast = ws > 1
+        if bcast:
+            def exchange(uid):
+                box = [uid]
+                dist.broadcast_object_list(box, src=0)
+                return box[0]
+
+            ctx.attach_comm(rank, ws, exchange=exchange)
+        P.run_host(plan, hops, bounds, r_zero=True, bcast=bcast)  # warm-up (staging alloc)
         barrier()
         tms = []
         for _ in range(steps):
-            tms.append(P.run_host(plan, hops, bounds, r_zero=True))
+            tms.append(P.run_host(plan, hops, bounds, r_zero=True, bcast=bcast))
         e_el = sum(tms)
         if dist is not None:
             tt = torch.tensor([e_el], dtype=torch.float64, device=device)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             e_el = float(tt.item())
         es = hA.element_size()
-        h2d = (hA.numel() + hB.numel() + (hth.numel() if hth is not None else 0)
-               + (hds.numel() if hds is not None else 0)) * es
-        d2h = hR.numel() * es
+        # bytes this rank copies per step: its A rows (+ B and the vectors on
+        # rank 0, the only rank that reads them from host memory), its R rows
+        shared = sum(x.numel() for x in (hB, hth, hds) if isinstance(x, torch.Tensor)) * es
+        h2d_total, d2h_total = float(hA.numel() * es + shared), float(hR.numel() * es)
+        if dist is not None:
+            tt = torch.tensor([h2d_total, d2h_total], dtype=torch.float64, device=device)
+            dist.all_reduce(tt)
+            h2d_total, d2h_total = float(tt[0].item()), float(tt[1].item())
         e2e = {"value": 2 * iters_total / e_el / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": h2d * ws, "d2h_bytes_per_step": d2h * ws,
+               "h2d_bytes_per_step": int(h2d_total),
+               "d2h_bytes_per_step": int(d2h_total),
                "ms_per_step": e_el / steps * 1e3,
-               "path": "amlt_gpu_run_host (C-ABI) from pinned host buffers, R zero-init on device, "
-                       "A/R row bands pipelined against compute"}
+               "path": ("amlt_gpu_run_host (C-ABI) from pinned host buffers: A / R row bands and B K-panels "
+                        "pipelined against compute, R zero-init on the device"
+                        + ("; B / thres / dis read on rank 0 only and NCCL-broadcast panel by panel "
+                           "inside the call" if bcast else ""))}
 
     # ---- CPU baseline (rank 0, N = 1)
     cpu = None
@@ -497,23 +752,24 @@ def main():
             threads = cpu_threads()
             r = run_reference(body, M, K, N, 1, 0, threads)
             cpu = {"value": 2 * r["iters_per_s"] / 1e9, "unit": "GFLOP/s", "cores": threads,
-                   "kind": "reference", "sample": r["sample"]}
+                   "kind": "reference", "sample": r["sample"], "extrapolated_from_sample": True,
+                   "sample_fraction": r["sample_fraction"]}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
 
     if rank == 0:
-        variants = plan.variants()
         best = last.best_variant if last else -1
-        # pipe instructions per inner iteration of the body's kernel; the
-        # ceiling under 2-op accounting is 1/ops of the pipe peak
-        ops_per_iter = {"discount": 3, "boost": 3, "gemm": 1, "sqdiff": 2, "eqcount": 1}[body]
-        if best >= 0 and "_theta_" in variants[best].name:
-            ops_per_iter = 2  # theta form: DSETP + DFMA per iteration (csrc/theta_discount.cu)
-        if best >= 0 and "_swar_" in variants[best].name:
-            # byte-packed eqcount: XOR, AND, LEA.HI on the ALU per packed word of
-            # 4 iterations (the add runs on the FMA pipe; csrc/swar_eqcount.cu)
-            ops_per_iter = 0.75
+        tile = variants[best].name if best >= 0 else None
+        cap = ncu_capture_for(args.workload, tile) if tile else None
+        if cap is None:
+            log(f"bench.py: no committed ncu capture of tile {tile} for {args.workload} "
+                "(profiles/r*/ncu_keyed.json): roofline.pipe_busy and traffic are null")
+        iters_per_s_kernel = rows * K * N / kernel_s
+        body_flops = task.program_flops
+        # (B): the reference program's body-op flops per second against the
+        # same pipe peak in flops (2 per FMA lane op)
+        frac_b = iters_per_s_kernel * body_flops / (peak_tflops * 1e12) if not tensor_tf32 else None
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s",
             "inner_iters_per_s": iters_total / el,
@@ -525,7 +781,7 @@ def main():
                        "l2": ("flushed between timed steps (512 MiB memset outside the step "
                               "events; value from the sum of per-step kernel times)"
                               if flush else "inputs larger than L2 (no flush)"),
-                       "tile": variants[best].name if best >= 0 else None,
+                       "tile": tile,
                        "split_k_kc": win.kc or None,
                        "tuning": ("pinned by --tile" if args.tile else
                                   "row-band trials" if tuned and tuned.tuned else
@@ -537,44 +793,53 @@ def main():
                          ("fp64" if dtype == "f64" else ("fp32" if dtype == "f32" else "int32")),
                          "pipe": pipe, "achieved": achieved_tflops, "peak": peak_tflops,
                          "unit": "TFLOP/s", "frac": achieved_tflops / peak_tflops,
-                         "traffic": traffic_for(args.workload,
-                                                variants[best].name if best >= 0 else None),
-                         "traffic_unit": "bytes per launch (ncu dram read+write, committed "
-                                         "capture profiles/*/traffic.json)",
-                         "algorithmic_bytes": algorithmic_bytes(body, dtype, M, K, N),
+                         "peak_source": ("measured in this run by amlt_gpu_measure_peak "
+                                         f"({pipe} probe at {peak_ghz:.3f} GHz)" if not tensor_tf32 else
+                                         "MEASURED_PEAKS.json dense bf16 (burst), scaled as the "
+                                         "accounting states"),
                          "accounting": (
-                             "2 flops per inner iteration (matmul-like); 28 int8 tensor-core "
+                             "(A) 2 flops per inner iteration (matmul-like); 28 int8 tensor-core "
                              "slice products per iteration (Ozaki, 7 slices), peak = measured dense "
-                             "bf16 (MEASURED_PEAKS.json) x 2 (int8 rate) / 28"
-                             if ozaki else
-                             "2 flops per inner iteration (matmul-like); the tile runs 3 TF32 "
-                             "tensor-core products per iteration (3xTF32), peak = measured dense "
-                             "bf16 (MEASURED_PEAKS.json) / 2 (TF32 rate) / 3"
+                             "bf16 x 2 (int8 rate) / 28" if ozaki else
+                             "(A) 2 flops per inner iteration (matmul-like); 3 TF32 tensor-core "
+                             "products per iteration (3xTF32), peak = measured dense bf16 / 2 / 3"
                              if tensor_tf32 else
-                             "2 ops per inner iteration (matmul-like); peak = the SM issue rate "
-                             f"(128 lane-instructions/clk/SM) at the probe's {peak_ghz:.3f} GHz; the "
-                             "byte-packed body runs 3 ALU instructions per 4 iterations (XOR, AND, "
-                             "LEA.HI; the add on the FMA pipe), the ALU taking 64 "
-                             "lane-instructions/clk/SM: a ceiling of 4/3 of that peak"
-                             if pipe == "alu" and "_swar_" in win_name else
-                             "2 ops per inner iteration (matmul-like); peak = the SM issue rate "
-                             f"(128 lane-instructions/clk/SM) at the probe's {peak_ghz:.3f} GHz; the "
-                             "body issues exactly 2 instructions per iteration"
+                             "(A) 2 ops per inner iteration (matmul-like); peak = the SM issue rate "
+                             "(128 lane-instructions/clk/SM) at the probe's clock"
                              if pipe == "alu" else
-                             "2 flops per inner iteration (matmul-like); peak = measured "
-                             f"{pipe} probe x2 on this GPU at {peak_ghz:.3f} GHz"),
-                         "body_pipe_ops_per_iter": ops_per_iter,
-                         "frac_of_body_ceiling": achieved_tflops / peak_tflops * (1 if tensor_tf32 else ops_per_iter),
+                             "(A) 2 flops per inner iteration (matmul-like); peak = 2 x the measured "
+                             f"{pipe} lane-op rate on this GPU"),
+                         "body_program": task.program,
+                         "body_flops_per_iter": body_flops,
+                         "frac_body_flops": frac_b,
+                         "frac_body_flops_note": "(B): the reference's compiled program for the "
+                                                 "statement (csrc/task.cpp, pinned to schedule_labelfs "
+                                                 "in tests/test_task.py), add/sub/mul/div/cmp 1, "
+                                                 "masksub/maskadd 2, final add 1, x iterations/s, "
+                                                 "over the same peak; above 1 when the kernel needs "
+                                                 "fewer pipe ops than the program states",
+                         "pipe_busy": cap.get("pipe_pct") if cap else None,
+                         "issue_active_pct": cap.get("issue_active_pct") if cap else None,
+                         "traffic": cap.get("dram_bytes") if cap else None,
+                         "traffic_unit": "bytes per launch of the tile (ncu dram read+write)",
+                         "capture": (f"{cap['file']}: {cap.get('capture', '')}" if cap else
+                                     f"none committed for tile {tile}"),
+                         "algorithmic_bytes": algorithmic_bytes(body, dtype, M, K, N),
                          "kernel_ms": kernel_s * 1e3},
+            "verified": verified,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks,
         }
+        if cuda_core is not None:
+            line["cuda_core"] = cuda_core
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+    if nccl_log is not None:
+        nccl_log.echo()
     return 0
 
 

@@ -133,6 +133,7 @@ struct TuneReport {
     std::int64_t best_kc = 0;
     bool tuned = false;
     bool from_cache = false;
+    bool scratch_tuned = false;
     std::vector<CoverRect> coverage;
     double tuning_fraction = 0.0;
     double total_seconds = 0.0;
@@ -234,6 +235,12 @@ public:
     const amlt_plan* get() const { return plan_; }
     Context& ctx() const { return *ctx_; }
     const amlt_task_info& roles() const { return info_; }
+    int num_variants() const { return amlt_gpu_plan_num_variants(plan_); }
+    amlt_variant_info variant(int idx) const {
+        amlt_variant_info v{};
+        check(amlt_gpu_plan_variant(plan_, idx, &v), ctx_->get());
+        return v;
+    }
 
 private:
     Context* ctx_;
@@ -296,10 +303,41 @@ inline TuneReport adaptive_execute(const Plan& plan, const Operands& ops, const 
     rep.best_kc = r.best_kc;
     rep.tuned = r.tuned != 0;
     rep.from_cache = r.from_cache != 0;
+    rep.scratch_tuned = r.scratch_tuned != 0;
     rep.coverage.assign(r.coverage, r.coverage + r.n_cover);
     rep.tuning_fraction = r.tuning_fraction;
     rep.total_seconds = r.total_seconds;
     return rep;
+}
+
+namespace detail {
+inline TuneReport report_of(const amlt_tune_report& r) {
+    TuneReport rep;
+    rep.trials.assign(r.trials, r.trials + r.n_trials);
+    rep.best_variant = r.best_variant;
+    rep.best_kc = r.best_kc;
+    rep.tuned = r.tuned != 0;
+    rep.from_cache = r.from_cache != 0;
+    rep.scratch_tuned = r.scratch_tuned != 0;
+    rep.coverage.assign(r.coverage, r.coverage + r.n_cover);
+    rep.tuning_fraction = r.tuning_fraction;
+    rep.total_seconds = r.total_seconds;
+    return rep;
+}
+}  // namespace detail
+
+// run_adaptive over host MatrixBuffers (amlt_gpu_run_host_adaptive): tunes
+// on the first call of a shape, reuses the winner after; the report's
+// total_seconds covers the copies too.
+inline TuneReport run_host_adaptive(const Plan& plan, const Operands& host_ops, const Bounds& b,
+                                    Clock& clock, bool r_zero = false) {
+    amlt_operands o = host_ops.c();
+    amlt_tune_report r{};
+    double el = 0;
+    check(amlt_gpu_run_host_adaptive(plan.ctx().get(), plan.get(), &o, &b, r_zero ? AMLT_HOST_R_ZERO : 0,
+                                     &Clock::thunk, &clock, &r, &el),
+          plan.ctx().get());
+    return detail::report_of(r);
 }
 
 // Host MatrixBuffers in, host R out (copies + compute inside the interval).

@@ -17,6 +17,7 @@
 // objects); run by tests/test_gpu_integration.py on the GPU box.
 //   adapter_demo            run + verify on cuda:0 (exit 0 iff all pass)
 //   adapter_demo --dry-run  plumbing only (no device; nothing verified)
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <functional>
@@ -29,6 +30,26 @@
 #include "amlt_ref_gpu_backend.hpp"
 
 using namespace amlt;
+
+// The reference's TuneReport invariants (autotuner.hpp:25-34): coverage
+// pairwise disjoint with union K x N (checked cell by cell), trials present
+// exactly when the call tuned, best_kc / best_nc inside the task.
+bool report_ok(const TuneReport& rep, const Bounds& b) {
+    const std::int64_t K = b.k1 - b.k0, N = b.j1 - b.j0;
+    std::vector<int> cells(static_cast<size_t>(std::max<std::int64_t>(K * N, 0)), 0);
+    for (const CoverRect& c : rep.coverage) {
+        if (c.k0 < b.k0 || c.k1 > b.k1 || c.j0 < b.j0 || c.j1 > b.j1) return false;
+        for (std::int64_t k = c.k0; k < c.k1; ++k)
+            for (std::int64_t j = c.j0; j < c.j1; ++j) ++cells[static_cast<size_t>((k - b.k0) * N + (j - b.j0))];
+    }
+    for (int v : cells)
+        if (v != 1) return false;
+    if (rep.tuned != !rep.nc_trials.empty()) return false;
+    if (rep.best_kc < 1 || rep.best_kc > std::max<std::int64_t>(K, 1) || rep.best_nc < 1) return false;
+    return rep.total_seconds > 0;
+}
+
+int tuned_calls = 0;
 
 int main(int argc, char** argv) {
     const bool dry = argc > 1 && std::strcmp(argv[1], "--dry-run") == 0;
@@ -66,10 +87,18 @@ int main(int argc, char** argv) {
                         (void)gpu::operands(*plan, data);
                         continue;
                     }
-                    if (fixed)
+                    if (fixed) {
                         gpu::run_fixed(gpu, ct, data, bind, 64, 128, false, clock);
-                    else
-                        gpu::run_adaptive(gpu, ct, data, bind, false, clock);
+                    } else {
+                        TuneReport rep = gpu::run_adaptive(gpu, ct, data, bind, false, clock);
+                        ++checks;
+                        if (!report_ok(rep, bind.bounds)) {
+                            ++failures;
+                            std::printf("FAIL %s %lldx%lldx%lld: TuneReport invariants\n", name.c_str(),
+                                        (long long)d[0], (long long)d[1], (long long)d[2]);
+                        }
+                        if (rep.tuned) ++tuned_calls;
+                    }
                     VerifyResult v = verify_against_naive(ct, data, bind, mode);
                     ++checks;
                     if (!v.pass) {
@@ -182,7 +211,13 @@ int main(int argc, char** argv) {
         ++failures;
         std::printf("FAIL a non-MMLT statement was not refused\n");
     }
-    std::printf("%s: %d checks, %d failures%s\n", failures ? "FAIL" : "PASS", checks, failures,
-                dry ? " (dry run: plumbing only)" : "");
+    // the fixed-body tasks above are small enough for whole-task trials: the
+    // first call of each shape must have tuned
+    if (!dry && tuned_calls == 0) {
+        ++failures;
+        std::printf("FAIL no run_adaptive call reported trials\n");
+    }
+    std::printf("%s: %d checks (%d tuned run_adaptive calls), %d failures%s\n", failures ? "FAIL" : "PASS",
+                checks, tuned_calls, failures, dry ? " (dry run: plumbing only)" : "");
     return failures ? 1 : 0;
 }

@@ -20,6 +20,7 @@
 // f64 MatrixBuffers in host memory; the backend copies them in and R out.
 #pragma once
 
+#include <algorithm>
 #include <memory>
 #include <string>
 
@@ -101,22 +102,59 @@ inline double run_fixed(amlt_gpu::Context& gpu, const CompiledTask& ct, TaskData
     return amlt_gpu::run_host(*plan, ops, to_gpu(bind.bounds), cb, &tp);
 }
 
-// run_adaptive: measured tile choice + remainder; the GPU report mapped onto
-// the reference TuneReport (trials carry the tile variant index; coverage is
-// the bounds' full K x N rectangle once every row band has run).
+// run_adaptive: the GPU runtime tuner over host buffers
+// (amlt_gpu_run_host_adaptive), its report mapped onto the reference
+// TuneReport (autotuner.hpp:11-34) without inventing anything:
+//   tuned         true iff this call measured candidates (row-band or
+//                 scratch trials); false when the winner came from an earlier
+//                 call of the same shape (no trials then) or the task ran
+//                 untuned
+//   nc_trials     one per tile variant measured: value = the variant's CTA
+//                 width (the GPU planner's nc, amlt_tile_params.nc), elapsed
+//                 = its measured seconds, score = seconds per output row of
+//                 its band (the GPU tuner lays candidates on row bands; lower
+//                 is better, as the reference's elapsed/nc)
+//   kc_trials     empty: the GPU tuner does not search kc on these sizes
+//   best_kc       the winner's K-segment depth (K when it runs whole K)
+//   best_nc       the winner's CTA width
+//   coverage      the (k, j) rectangles completed for ALL rows: the GPU
+//                 report's row-band rectangles are checked to tile
+//                 [i0, i1) x (k, j) exactly once and merged over rows, so the
+//                 reference's invariant holds (pairwise disjoint, union K x N)
+//   tuning_fraction  rows measured by trials / M (the GPU tuner's unit)
+//   total_seconds    all subtasks and copies
+// The reference's own kc / nc search (find_kc, find_nc) stays available
+// on the GPU as amlt_gpu_adaptive_execute_amulet.
 inline TuneReport run_adaptive(amlt_gpu::Context& gpu, const CompiledTask& ct, TaskData& data,
                                const DimBinding& bind, bool pack, amlt::Clock& clock) {
     std::unique_ptr<amlt_gpu::Plan> plan(plan_for(gpu, ct));
     amlt_gpu::Operands ops = operands(*plan, data);
     ClockBridge cb(clock);
+    (void)pack;  // operands are always staged through shared memory
+    const amlt_bounds gb = to_gpu(bind.bounds);
+    amlt_gpu::TuneReport g = amlt_gpu::run_host_adaptive(*plan, ops, gb, cb);
     TuneReport rep;
-    rep.tuned = true;
-    rep.total_seconds = amlt_gpu::run_host(*plan, ops, to_gpu(bind.bounds), cb, nullptr);
-    (void)pack;
-    const Bounds& b = bind.bounds;
-    rep.best_kc = b.k1 - b.k0;
-    rep.best_nc = b.j1 - b.j0;
-    rep.coverage.push_back(CoverRect{b.k0, b.k1, b.j0, b.j1});
+    rep.tuned = g.tuned || g.scratch_tuned;
+    for (const amlt_trial& t : g.trials)
+        rep.nc_trials.push_back(Trial{plan->variant(static_cast<int>(t.value)).block_n, t.elapsed, t.score});
+    rep.best_kc = g.best_kc;
+    rep.best_nc = g.best_variant >= 0 ? plan->variant(g.best_variant).block_n : gb.j1 - gb.j0;
+    // merge the row bands of each (k, j) rectangle; each must tile the rows once
+    std::vector<std::pair<CoverRect, std::int64_t>> kj;  // rect, rows covered
+    for (const amlt_cover_rect& c : g.coverage) {
+        auto it = std::find_if(kj.begin(), kj.end(), [&](const auto& e) {
+            return e.first.k0 == c.k0 && e.first.k1 == c.k1 && e.first.j0 == c.j0 && e.first.j1 == c.j1;
+        });
+        if (it == kj.end()) kj.push_back({CoverRect{c.k0, c.k1, c.j0, c.j1}, c.i1 - c.i0});
+        else it->second += c.i1 - c.i0;
+    }
+    for (const auto& e : kj) {
+        if (e.second != gb.i1 - gb.i0)
+            throw EngineError("GPU coverage does not tile the rows of a (k, j) rectangle exactly once");
+        rep.coverage.push_back(e.first);
+    }
+    rep.tuning_fraction = g.tuning_fraction;
+    rep.total_seconds = g.total_seconds;
     return rep;
 }
 
