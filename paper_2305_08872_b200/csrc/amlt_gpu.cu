@@ -133,6 +133,7 @@ struct amlt_ctx {
     struct Winner {
         int variant;
         int64_t kc;
+        double row_seconds = 0.0;  // measured seconds per output row (0: unknown)
     };
     // keyed by (body, dtype, M, N, K, operands staging-aligned, variant family):
     // a winner only serves calls its variant can run
@@ -529,8 +530,9 @@ Dispatch plan_dispatch(const amlt_ctx* ctx, const amlt_plan* plan, const amlt_ti
     Dispatch dp;
     dp.variant = choose_variant(ctx, plan, tile, rv);
     dp.kslice = rv.K;
-    if (tile && tile->kc > 0 && tile->kc < rv.K && !vdesc(dp.variant).run) {
-        // (variants with their own staging run the whole K range)
+    if (tile && tile->kc > 0 && tile->kc < rv.K && (!vdesc(dp.variant).run || vdesc(dp.variant).splittable)) {
+        // (variants with their own staging run the whole K range unless they
+        // take K segments)
         // Segment starts stay multiples of 32 elements so every segment's
         // operand rows keep the 16-byte alignment the staged copies need.
         const int64_t kc = (tile->kc + 31) / 32 * 32;
@@ -668,11 +670,27 @@ void enqueue_compute(amlt_ctx* ctx, const amlt_plan* plan, Resolved& rv, const D
         return;
     }
     const VariantDesc& v = vdesc(dp.variant);
-    if (v.run) {  // own staging (tcgen05 3xTF32 GEMM): operand pre-pass + tensor-core GEMM
+    if (v.run) {  // own staging (tensor-core GEMMs, theta-form discount, packed eqcount)
         ensure_tc_ws(ctx, v, kp);
         const bool ready = bprep_ready(ctx, v, kp);
-        cuda_check(v.run(kp, ctx->tc_ws, ready, ctx->stream), "tensor-core GEMM launch");
+        kp.splits = 1;
+        kp.kslice = rv.K;
+        kp.work = nullptr;
+        if (dp.splits > 1 && v.splittable) {
+            kp.splits = dp.splits;
+            kp.kslice = dp.kslice;
+            ensure_work(ctx, size_t(dp.splits) * size_t(rv.M) * size_t(rv.N) * dtype_size(plan->desc.dtype));
+            kp.work = ctx->work;
+        }
+        cuda_check(v.run(kp, ctx->tc_ws, ready, ctx->stream), "own-staging variant launch");
         if (!ready) bprep_mark(ctx, v, kp);
+        if (kp.splits > 1) {
+            const int64_t total = rv.M * rv.N;
+            const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
+            cuda_check(launch_helper_any(plan->aux->reduce, plan->aux->reduce_func, kp, dim3(blocks),
+                                         ctx->stream),
+                       "split-K reduce launch");
+        }
         return;
     }
     kp.tiles_m = static_cast<int32_t>((rv.M + v.bm - 1) / v.bm);
@@ -800,8 +818,9 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
         const int occ = occ_of(ctx, v);
         const int64_t ctas = ctas_for(vd, whole.M, whole.N);
         const int64_t slots = int64_t(ctx->num_sms) * occ;
-        // split-K forms for small outputs (variants with their own staging run whole K)
-        if (!vd.run && ctas < 2 * slots && whole.K >= 512) {
+        // split-K forms for small outputs (variants with their own staging run
+        // whole K unless they take K segments)
+        if ((!vd.run || vd.splittable) && ctas < 2 * slots && whole.K >= 512) {
             for (int64_t splits : {int64_t(2), (2 * slots + ctas - 1) / ctas}) {
                 splits = std::min<int64_t>(splits, whole.K / 128);
                 if (splits < 2) continue;
@@ -844,7 +863,7 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
     }
     rep->scratch_tuned = 1;
     ctx->tune_cache[tune_key(plan, whole)] =
-        amlt_ctx::Winner{best.variant, best.kc};
+        amlt_ctx::Winner{best.variant, best.kc, best_t / double(std::max<int64_t>(whole.M, 1))};
 }
 
 void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, const amlt_bounds& b,
@@ -987,7 +1006,7 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
     rep->best_variant = plan_local_index(plan, best);
     rep->best_kc = whole.K;
     rep->tuning_fraction = double(cur - b.i0) / double(whole.M);
-    ctx->tune_cache[key] = amlt_ctx::Winner{best, 0};
+    ctx->tune_cache[key] = amlt_ctx::Winner{best, 0, best_score};
     if (cur < b.i1) run_rect(amlt_bounds{cur, b.i1, b.j0, b.j1, b.k0, b.k1}, best, 0);
 }
 
@@ -1183,7 +1202,7 @@ bool slot_replicated(const amlt_plan* plan, int s) {
 std::vector<int64_t> band_edges(int64_t lo, int64_t n, int nb, int64_t align, bool short_last) {
     std::vector<int64_t> e(static_cast<size_t>(nb) + 1);
     for (int b = 0; b <= nb; ++b) {
-        double f = nb == 1 ? double(b) : (short_last ? std::min(1.0, b / (nb - 0.75)) : double(b) / nb);
+        double f = nb == 1 ? double(b) : (short_last ? std::min(1.0, b / (nb - 0.875)) : double(b) / nb);
         int64_t r = static_cast<int64_t>(f * double(n));
         if (b < nb) r = r / align * align;
         e[static_cast<size_t>(b)] = lo + std::min<int64_t>(n, b == nb ? n : r);
@@ -1252,13 +1271,15 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
     amlt_tile_params tp{0, 0, 0, -1};
     const auto key = tune_key(plan, hv);
     bool cached = false;
-    if (tile) {
-        tp = *tile;
-    } else {
+    double row_seconds = 0.0;
+    {
         auto it = ctx->tune_cache.find(key);
-        if (it != ctx->tune_cache.end()) {
+        if (tile) {
+            tp = *tile;
+        } else if (it != ctx->tune_cache.end()) {
             tp.variant = plan_local_index(plan, it->second.variant);
             tp.kc = it->second.kc;
+            row_seconds = it->second.row_seconds;
             cached = true;
         }
     }
@@ -1290,18 +1311,40 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
                                                 : default_variant(ctx, plan, M, N, hv.aligned))
                              : -1;
     if (nb > 1) {
-        // fewer bands when one band would not fill the SMs (split-K multiplies CTAs)
+        // fewer bands when a band would be short: every band boundary drains
+        // the GPU (up to one wave of CTAs idles), so each band keeps >= 16
+        // waves (split-K multiplies CTAs)
         const VariantDesc& v = vdesc(vi);
-        const int64_t splits = (!v.run && split_winner) ? (K + tp.kc - 1) / tp.kc : 1;
+        const int64_t splits = ((!v.run || v.splittable) && split_winner) ? (K + tp.kc - 1) / tp.kc : 1;
         const int64_t slots = int64_t(ctx->num_sms) * occ_of(ctx, vi);
         const int64_t fill = ctas_for(v, M, N) * splits / std::max<int64_t>(1, slots);
-        nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nb, fill)));
+        nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nb, fill / 16)));
     }
-    // Bands: equal but for a last one a quarter as tall, so the copy-out that
-    // trails the final compute is short; 64-row multiples. Panels: equal,
-    // edges on multiples of 64 k (16-byte aligned operand offsets).
-    const std::vector<int64_t> redge = band_edges(bounds->i0, M, nb, 64, true);
+    // Panels: equal, edges on multiples of 64 k (16-byte aligned operand
+    // offsets). Only the first row band runs panel by panel, as B arrives;
+    // it is tall enough that its compute covers the rest of B's transfer
+    // (from the winner's measured seconds per row, assuming ~40 GB/s host
+    // copies, more with a broadcast behind them), between 1/8 and 1/2 of the
+    // rows. The other bands run whole K (one launch each, no extra R
+    // traffic); the last one is an eighth as tall as the others, so the
+    // copy-out that trails the final compute is short. 64-row multiples.
     const std::vector<int64_t> kedge = band_edges(bounds->k0, K, np, 64, false);
+    std::vector<int64_t> redge;
+    if (nb == 1) {
+        redge = {bounds->i0, bounds->i1};
+    } else {
+        int64_t rows0 = M / nb;
+        if (np > 1 && row_seconds > 0.0) {
+            const double b_bytes = double(K) * double(host_ops->b.ld) * es;
+            const double t_b = b_bytes / 40e9 * (bcast ? 1.25 : 1.0);
+            rows0 = static_cast<int64_t>(std::ceil(1.3 * t_b / row_seconds));
+        }
+        rows0 = std::min<int64_t>(std::max<int64_t>(rows0, M / 8), M / 2) / 64 * 64;
+        rows0 = std::max<int64_t>(rows0, std::min<int64_t>(M, 64));
+        redge.push_back(bounds->i0);
+        const std::vector<int64_t> rest = band_edges(bounds->i0 + rows0, M - rows0, nb - 1, 64, true);
+        redge.insert(redge.end(), rest.begin(), rest.end());
+    }
 
     // events: [0] start, [1] replicated operands ready, [2..2+nb) band inputs,
     // [2+nb..2+nb+np) panels ready, [2+nb+np..2+2nb+np) bands done, [last] out
@@ -1378,8 +1421,20 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
         return bb;
     };
 
+    // AMLT_HOST_TRACE=1: timing events at the stage boundaries, printed to
+    // stderr after the call (pipeline diagnostics; off by default)
+    const bool trace = std::getenv("AMLT_HOST_TRACE") != nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    auto mark = [&](const std::string& what, cudaStream_t s) {
+        if (!trace) return;
+        cudaEvent_t e;
+        cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+        cuda_check(cudaEventRecord(e, s), "cudaEventRecord");
+        marks.emplace_back(what, e);
+    };
     auto body = [&] {
         cuda_check(cudaEventRecord(start_ev, ctx->stream), "cudaEventRecord");
+        mark("start", ctx->stream);
         cuda_check(cudaStreamWaitEvent(ctx->copy_in, start_ev, 0), "cudaStreamWaitEvent");
         if (bcast) cuda_check(cudaStreamWaitEvent(ctx->comm_stream, start_ev, 0), "cudaStreamWaitEvent");
         // replicated operands other than B (thresholds, vectors, [i] / [i][j]
@@ -1397,11 +1452,16 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
             cuda_check(cudaEventRecord(small_ev, ctx->comm_stream), "cudaEventRecord");
         }
         cuda_check(cudaStreamWaitEvent(ctx->stream, small_ev, 0), "cudaStreamWaitEvent");
-        // inputs: A band 0, B panel 0, the other bands, the other panels
+        // inputs: A band 0, the B panels (band 0 consumes them as they land),
+        // then the other A bands
         copy_band_in(0);
+        mark("A band 0 in", ctx->copy_in);
         copy_panel_in(0);
-        for (int b = 1; b < nb; ++b) copy_band_in(b);
+        mark("B panel 0 in", bcast ? ctx->comm_stream : ctx->copy_in);
         for (int p = 1; p < np; ++p) copy_panel_in(p);
+        mark("B panels in", bcast ? ctx->comm_stream : ctx->copy_in);
+        for (int b = 1; b < nb; ++b) copy_band_in(b);
+        mark("A bands in", ctx->copy_in);
         if (tune_now) {
             for (int b = 0; b < nb; ++b) cuda_check(cudaStreamWaitEvent(ctx->stream, band_in(b), 0), "cudaStreamWaitEvent");
             for (int p = 0; p < np; ++p) cuda_check(cudaStreamWaitEvent(ctx->stream, panel_ev(p), 0), "cudaStreamWaitEvent");
@@ -1411,15 +1471,29 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
             cuda_check(cudaMemcpyAsync(host_ops->r.data, ctx->hbuf[2], bytes[2], cudaMemcpyDeviceToHost,
                                        ctx->copy_out), "D2H R");
         } else {
-            for (int p = 0; p < np; ++p) {
-                cuda_check(cudaStreamWaitEvent(ctx->stream, panel_ev(p), 0), "cudaStreamWaitEvent");
-                for (int b = 0; b < nb; ++b) {
-                    if (p == 0) cuda_check(cudaStreamWaitEvent(ctx->stream, band_in(b), 0), "cudaStreamWaitEvent");
-                    amlt_bounds bb = band_bounds(b, p);
+            for (int b = 0; b < nb; ++b) {
+                cuda_check(cudaStreamWaitEvent(ctx->stream, band_in(b), 0), "cudaStreamWaitEvent");
+                // band 0 panel by panel as B lands; the others whole K
+                const int parts = b == 0 ? np : 1;
+                amlt_bounds bb{};
+                for (int p = 0; p < parts; ++p) {
+                    bb = band_bounds(b, p);
+                    if (b > 0) {
+                        bb.k0 = bounds->k0;
+                        bb.k1 = bounds->k1;
+                    } else {
+                        cuda_check(cudaStreamWaitEvent(ctx->stream, panel_ev(p), 0), "cudaStreamWaitEvent");
+                    }
+                    if (b == 0 && p == 0) mark("compute begins", ctx->stream);
                     Resolved rv = resolve(plan, &dev, &bb);
                     Dispatch dp = plan_dispatch(ctx, plan, &tp, rv);
                     enqueue(ctx, plan, rv, dp);
-                    if (p + 1 < np) continue;
+                }
+                if (b == 0)  // (every panel has landed once band 0 is done)
+                    for (int p = 0; p < np; ++p)
+                        cuda_check(cudaStreamWaitEvent(ctx->stream, panel_ev(p), 0), "cudaStreamWaitEvent");
+                mark("band " + std::to_string(b) + " computed", ctx->stream);
+                {
                     cuda_check(cudaEventRecord(band_done(b), ctx->stream), "cudaEventRecord");
                     cuda_check(cudaStreamWaitEvent(ctx->copy_out, band_done(b), 0), "cudaStreamWaitEvent");
                     const int64_t r0 = bb.i0, r1 = bb.i1;
@@ -1434,6 +1508,7 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
                 }
             }
         }
+        mark("R out", ctx->copy_out);
         cuda_check(cudaEventRecord(out_ev, ctx->copy_out), "cudaEventRecord");
         cuda_check(cudaStreamWaitEvent(ctx->stream, out_ev, 0), "cudaStreamWaitEvent");
         if (bcast) {  // the comm stream's work is part of this call
@@ -1464,14 +1539,29 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
         el = ms * 1e-3;
         if (tune_now && clock) el = rep->total_seconds;
     }
+    if (trace && !marks.empty()) {
+        cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
+        std::fprintf(stderr, "[amlt host pipeline] nb=%d np=%d M=%lld N=%lld K=%lld bcast=%d\n", nb, np,
+                     (long long)M, (long long)N, (long long)K, bcast ? 1 : 0);
+        for (auto& m : marks) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, marks.front().second, m.second);
+            std::fprintf(stderr, "[amlt host pipeline]   %8.2f ms  %s\n", ms, m.first.c_str());
+        }
+        for (auto& m : marks) cudaEventDestroy(m.second);
+    }
     if (rep && !tune_now) {
         std::memset(rep, 0, sizeof(*rep));
         rep->best_variant = plan_local_index(plan, vi);
         rep->best_kc = split_winner ? tp.kc : K;
         rep->from_cache = cached ? 1 : 0;
-        // one completed region per K panel (every row band has run it)
-        for (int p = 0; p < np; ++p) add_cover(rep, amlt_bounds{bounds->i0, bounds->i1, bounds->j0, bounds->j1,
-                                                                 kedge[static_cast<size_t>(p)], kedge[static_cast<size_t>(p) + 1]});
+        // completed regions: band 0 per K panel, the other bands whole K
+        for (int p = 0; p < np; ++p)
+            add_cover(rep, amlt_bounds{redge[0], redge[1], bounds->j0, bounds->j1, kedge[static_cast<size_t>(p)],
+                                       kedge[static_cast<size_t>(p) + 1]});
+        for (int b = 1; b < nb; ++b)
+            add_cover(rep, amlt_bounds{redge[static_cast<size_t>(b)], redge[static_cast<size_t>(b) + 1], bounds->j0,
+                                       bounds->j1, bounds->k0, bounds->k1});
         rep->total_seconds = el;
     } else if (rep && tune_now) {
         // the report's subtasks plus the copies around them

@@ -302,11 +302,13 @@ cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
         if (!encode(&ma, p.A, 2, ad, as, ab, Cfg::SWZ) || !encode(&mb, planes, 3, bd, bs, bb))
             return cudaErrorInvalidValue;
     }
+    // K segments (split-K): partials into p.work, reduced by the caller
+    const int splits = p.splits > 1 && p.work ? p.splits : 1;
     KParams q = p;
     q.guard = g;
-    q.splits = 1;
-    q.kslice = p.K;
-    q.work = nullptr;
+    q.splits = splits;
+    q.kslice = splits > 1 ? p.kslice : p.K;
+    q.work = splits > 1 ? p.work : nullptr;
     q.tiles_m = static_cast<int32_t>((p.M + Cfg::BM - 1) / Cfg::BM);
     q.tiles_n = static_cast<int32_t>((p.N + Cfg::BN - 1) / Cfg::BN);
     // raster groups of ~512 rows, as for the ordinary tiles (2304-row groups
@@ -314,7 +316,8 @@ cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
     q.group_m = std::min(64, std::max(8, 512 / Cfg::BM));
     auto kt = &mmlt_tile_kernel<Body, double, TM, TN, WR, WC, BK, ST, LOAD, MINB>;
     if ((e = smem_attr_once(reinterpret_cast<const void*>(kt), Cfg::SMEM_BYTES)) != cudaSuccess) return e;
-    kt<<<static_cast<unsigned>(int64_t(q.tiles_m) * q.tiles_n), Cfg::THREADS, Cfg::SMEM_BYTES, s>>>(q, ma, mb);
+    kt<<<dim3(static_cast<unsigned>(int64_t(q.tiles_m) * q.tiles_n), static_cast<unsigned>(splits)), Cfg::THREADS,
+         Cfg::SMEM_BYTES, s>>>(q, ma, mb);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
     // fallback: the ordinary discount tile over the raw operands
@@ -335,7 +338,8 @@ cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
     auto kf = &mmlt_tile_kernel<BodyDiscountFallback, double, FB_TM, FB_TN, FB_WR, FB_WC, FB_BK, FB_ST, LOAD_TMA,
                                 FB_MINB>;
     if ((e = smem_attr_once(reinterpret_cast<const void*>(kf), FbCfg::SMEM_BYTES)) != cudaSuccess) return e;
-    kf<<<static_cast<unsigned>(int64_t(f.tiles_m) * f.tiles_n), FbCfg::THREADS, FbCfg::SMEM_BYTES, s>>>(f, fa, fb);
+    kf<<<dim3(static_cast<unsigned>(int64_t(f.tiles_m) * f.tiles_n), static_cast<unsigned>(splits)), FbCfg::THREADS,
+         FbCfg::SMEM_BYTES, s>>>(f, fa, fb);
     return cudaGetLastError();
 }
 
@@ -369,6 +373,7 @@ void add_theta(Registry& reg, const char* name) {
     v.run = &th::run<Body, TM, TN, WR, WC, BK, ST, MINB, LOAD>;
     v.prep_b = &th::prep_b;
     v.prep_id = 3;  // (theta, x0, x1) planes of B, shared by every theta tile
+    v.splittable = true;
     reg.variants.push_back(v);
 }
 

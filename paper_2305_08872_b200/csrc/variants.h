@@ -46,6 +46,9 @@ struct VariantDesc {
     cudaError_t (*run)(const KParams&, void* ws, bool b_ready, cudaStream_t) = nullptr;
     cudaError_t (*prep_b)(const KParams&, void* ws, cudaStream_t) = nullptr;
     int prep_id = 0;
+    // run() variants that accept K segments (KParams splits / kslice / work,
+    // partials reduced in segment order afterwards like the tile variants)
+    bool splittable = false;
 };
 
 // Per (body, dtype) helpers that are not tile variants.

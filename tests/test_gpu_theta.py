@@ -198,3 +198,56 @@ def test_theta_skipped_when_planes_do_not_fit():
     rows = [0, 777, M - 1]
     want = oracle("discount", A[rows].cpu().numpy(), B.cpu().numpy(), t.cpu().numpy(), d.cpu().numpy())
     check("discount", "f64", R[rows].cpu().numpy(), want, what="fallback tiles under memory pressure")
+
+
+@pytest.mark.parametrize("kc", [128, 320, 512])
+def test_theta_split_k_bit_exact(gpu_ctx, kc):
+    """K segments for the theta tiles: partials per segment,
+    reduced in segment order; exact on data whose products and sums are
+    exact (A integers 0..9, integer B and thresholds, dis a multiple of 1/4),
+    including a K tail, a prior-valued R and a sub-rectangle."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    rng = np.random.default_rng(kc)
+    M, K, N = 300, 1000, 260
+    A = rng.integers(0, 10, (M, K)).astype(np.float64)
+    B = rng.integers(1, 100, (K, N)).astype(np.float64)
+    t = rng.integers(50, 450, N).astype(np.float64)
+    d = rng.integers(0, 2, N) * 0.25
+    R0 = rng.integers(-8, 9, (M, N)).astype(np.float64)
+    plan = gpu_ctx.plan("discount", "f64")
+    b = (5, 290, 2, 258, 64, 1000)
+    want = oracle("discount", A, B, t, d, R0=R0, bounds=b)
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
+    for vi, name in theta_variants(plan):
+        R = dev(R0)
+        log = P.ExecLog(capacity=8)
+        P.run_subtask(plan, P.Operands(dev(A), dev(B), R, dev(t), dev(d)), P.TileParams(kc=kc, variant=vi),
+                      P.Bounds(*b), log=log)
+        assert log.records[0].splits == (936 + (kc + 31) // 32 * 32 - 1) // ((kc + 31) // 32 * 32)
+        check("discount", "f64", R.cpu().numpy(), want, exact=True, what=f"{name} kc={kc}")
+
+
+def test_config0_tunes_theta_with_k_segments(gpu_ctx):
+    """Config 0 (1024^3): the tuner's candidates include the theta tiles with
+    K segments, and whatever wins is within 1e-12 of the oracle."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+    from tests.helpers import make_inputs
+
+    M = K = N = 1024
+    A, B, t, d = make_inputs("discount", M, K, N, "baseline", seed=81)
+    want = oracle("discount", A, B, t, d)
+    plan = gpu_ctx.plan("discount", "f64")
+    gpu_ctx.clear_tuning_cache()
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
+    R = dev(np.zeros((M, N)))
+    rep = P.adaptive_execute(plan, P.Operands(dev(A), dev(B), R, dev(t), dev(d)), P.Bounds(0, M, 0, N, 0, K))
+    names = [v.name for v in plan.variants()]
+    tried = {(names[tr.value], tr.rows) for tr in rep.trials}
+    assert any("_theta_" in n for n, _ in tried)
+    assert rep.scratch_tuned and len(rep.trials) > len({n for n, _ in tried})  # split-K forms tried too
+    check("discount", "f64", R.cpu().numpy(), want, what="config 0 tuned")
