@@ -499,6 +499,7 @@ def main():
                     help="skip the tuner and run this tile variant (name from plan.variants()); "
                          "used to pin the tuned winner under ncu, whose serialised launches "
                          "change the trial timings")
+    ap.add_argument("--kc", type=int, default=0, help="with --tile: the K-segment depth (split-K)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
@@ -603,9 +604,9 @@ def main():
 
         vi = [v.name for v in plan.variants()].index(args.tile)
         for _ in range(warmup):
-            P.run_subtask(plan, ops, P.TileParams(variant=vi), bounds)
-        reports.append(SimpleNamespace(best_variant=vi, best_kc=K, tuned=False, scratch_tuned=False,
-                                       trials=[]))
+            P.run_subtask(plan, ops, P.TileParams(kc=args.kc, variant=vi), bounds)
+        reports.append(SimpleNamespace(best_variant=vi, best_kc=args.kc if 0 < args.kc < K else K, tuned=False,
+                                       scratch_tuned=False, trials=[]))
     else:
         for _ in range(warmup):
             reports.append(P.adaptive_execute(plan, ops, bounds))

@@ -1311,14 +1311,23 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
                                                 : default_variant(ctx, plan, M, N, hv.aligned))
                              : -1;
     if (nb > 1) {
-        // fewer bands when a band would be short: every band boundary drains
-        // the GPU (up to one wave of CTAs idles), so each band keeps >= 16
-        // waves (split-K multiplies CTAs)
+        // Band count: every band boundary drains the GPU (up to a wave of CTAs
+        // idles), while more bands hide more of the A / R transfers. With the
+        // winner's measured seconds per row, minimise boundaries x wave time +
+        // exposed copy (~ copy time / bands): nb = sqrt(copy x waves /
+        // compute); without it, as many bands as full waves allow. At most 8,
+        // at least one wave each (split-K multiplies CTAs).
         const VariantDesc& v = vdesc(vi);
         const int64_t splits = ((!v.run || v.splittable) && split_winner) ? (K + tp.kc - 1) / tp.kc : 1;
         const int64_t slots = int64_t(ctx->num_sms) * occ_of(ctx, vi);
         const int64_t fill = ctas_for(v, M, N) * splits / std::max<int64_t>(1, slots);
-        nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nb, fill / 16)));
+        int64_t want = fill;
+        if (row_seconds > 0.0) {
+            const double copy_s = (double(bytes[0]) + double(bytes[2]) * (r_zero ? 1.0 : 2.0)) / 40e9;
+            const double compute_s = row_seconds * double(M);
+            want = static_cast<int64_t>(std::lround(std::sqrt(copy_s * double(std::max<int64_t>(fill, 1)) / compute_s)));
+        }
+        nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({int64_t(nb), fill, want})));
     }
     // Panels: equal, edges on multiples of 64 k (16-byte aligned operand
     // offsets). Only the first row band runs panel by panel, as B arrives;

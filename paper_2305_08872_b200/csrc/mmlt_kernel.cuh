@@ -388,6 +388,17 @@ struct BodyPlanes<Body, decltype(void(Body::BPLANES))> {
     static constexpr int n = Body::BPLANES;
 };
 
+// Bodies whose inner step runs row-outer (the row's a is the shared operand
+// of consecutive instructions) instead of the default column-outer order.
+template <class Body, class = void>
+struct RowOuter {
+    static constexpr bool value = false;
+};
+template <class Body>
+struct RowOuter<Body, decltype(void(Body::ROW_OUTER))> {
+    static constexpr bool value = Body::ROW_OUTER;
+};
+
 // Bodies that run only when Body::guard(p) holds (checked once per CTA).
 template <class Body, class = void>
 struct BodyGuard {
@@ -740,15 +751,29 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
                             for (int e = 0; e < VN; ++e) bx[pl - 1][q * VN + e] = V16<T>::get(xv, e);
                         }
                     }
-#pragma unroll
-                    for (int c = 0; c < TN; ++c) {
+                    if constexpr (RowOuter<Body>::value) {
 #pragma unroll
                         for (int r = 0; r < TM; ++r) {
                             const T a = V16<T>::get(av[r], v);
-                            if constexpr (Body::TWO_LEVEL)
-                                STEP(part[r][c], a, c, COL(r, c));
-                            else
-                                STEP(acc[r][c], a, c, COL(r, c));
+#pragma unroll
+                            for (int c = 0; c < TN; ++c) {
+                                if constexpr (Body::TWO_LEVEL)
+                                    STEP(part[r][c], a, c, COL(r, c));
+                                else
+                                    STEP(acc[r][c], a, c, COL(r, c));
+                            }
+                        }
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < TN; ++c) {
+#pragma unroll
+                            for (int r = 0; r < TM; ++r) {
+                                const T a = V16<T>::get(av[r], v);
+                                if constexpr (Body::TWO_LEVEL)
+                                    STEP(part[r][c], a, c, COL(r, c));
+                                else
+                                    STEP(acc[r][c], a, c, COL(r, c));
+                            }
                         }
                     }
                 }

@@ -70,8 +70,10 @@ __device__ __forceinline__ bool safe(const KParams& p) {
     return hi <= 1020 && lo >= -1020;
 }
 
-struct BodyTheta {
+template <bool ROWS>
+struct BodyThetaT {
     using Acc = double;
+    static constexpr bool ROW_OUTER = ROWS;
     static constexpr int NACC = 1;
     static constexpr bool TWO_LEVEL = false;
     static constexpr int BPLANES = 3;
@@ -84,6 +86,8 @@ struct BodyTheta {
     }
     __device__ static __forceinline__ double finish(const double* acc, const Col&, int64_t) { return acc[0]; }
 };
+using BodyTheta = BodyThetaT<false>;
+using BodyThetaRows = BodyThetaT<true>;
 
 // The ordinary discount tile kernel, run only when the theta form is not
 // applicable to this call's operands.
@@ -393,6 +397,11 @@ void register_theta_discount(Registry& reg) {
     // bounds this body, profiles/r01/thetabench.txt); kept as a tuner
     // candidate and to keep the lane-grid path exercised.
     add_theta<8, 4, 3, 4, 16, 2, 1, LOAD_TMA | LOAD_LR4>(reg, "theta_t8x4_l4x8_w3x4");
+    // 16 warps per SM (4 per scheduler) with 6 rows per thread. Measured at
+    // 8192^3 (tools/quick_perf.py, r02): 99.8 ms against 98.8 for the 12-warp
+    // 8 x 4 tile; 5 x 4 (101.4), 6 x 4 BK = 8 (100.1) and row-outer inner
+    // order (104.7) were slower and are not kept.
+    add_theta<6, 4, 16, 1, 16, 2, 1>(reg, "theta_t6x4_w16x1");
 }
 
 }  // namespace amltk
