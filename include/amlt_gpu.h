@@ -210,7 +210,7 @@ typedef struct {
  * time the subtask. */
 typedef double (*amlt_clock_fn)(void* user);
 
-#define AMLT_MAX_TRIALS 32
+#define AMLT_MAX_TRIALS 128
 #define AMLT_MAX_COVER 64
 
 typedef struct {
@@ -242,8 +242,14 @@ typedef struct {
                               (trials rows == M), then the task ran once    */
     int32_t n_cover;
     amlt_cover_rect coverage[AMLT_MAX_COVER]; /* disjoint, union = bounds   */
-    double tuning_fraction;                   /* tuned rows / M             */
-    double total_seconds;                     /* sum over all subtasks      */
+    double tuning_fraction;                   /* rows of R produced by trial
+                                                 bands / M (scratch trials
+                                                 produce none: 0)          */
+    double total_seconds;                     /* sum over all subtasks,
+                                                 scratch trials included   */
+    double tuning_seconds;                    /* of which whole-task trials on
+                                                 the scratch R (work redone
+                                                 for the real R afterwards) */
 } amlt_tune_report;
 
 typedef struct amlt_ctx amlt_ctx;

@@ -137,6 +137,7 @@ struct TuneReport {
     std::vector<CoverRect> coverage;
     double tuning_fraction = 0.0;
     double total_seconds = 0.0;
+    double tuning_seconds = 0.0;  // scratch (whole-task) trials, included in total_seconds
 };
 
 // A MatrixBuffer-like view (device memory for run_subtask / adaptive_execute,
@@ -307,6 +308,7 @@ inline TuneReport adaptive_execute(const Plan& plan, const Operands& ops, const 
     rep.coverage.assign(r.coverage, r.coverage + r.n_cover);
     rep.tuning_fraction = r.tuning_fraction;
     rep.total_seconds = r.total_seconds;
+    rep.tuning_seconds = r.tuning_seconds;
     return rep;
 }
 
@@ -322,6 +324,7 @@ inline TuneReport report_of(const amlt_tune_report& r) {
     rep.coverage.assign(r.coverage, r.coverage + r.n_cover);
     rep.tuning_fraction = r.tuning_fraction;
     rep.total_seconds = r.total_seconds;
+    rep.tuning_seconds = r.tuning_seconds;
     return rep;
 }
 }  // namespace detail

@@ -29,7 +29,7 @@ LAYOUT_NORMAL, LAYOUT_TRANSPOSED = 0, 1
 LEAF_CONSTANT, LEAF_VEC_I, LEAF_VEC_J, LEAF_MAT_IJ = range(4)
 CTX_DRY_RUN = 1
 CTX_F64_EMULATION = 2
-MAX_TRIALS = 32
+MAX_TRIALS = 128
 MAX_COVER = 64
 
 
@@ -92,7 +92,7 @@ class TuneReportC(C.Structure):
                 ("best_variant", C.c_int32), ("best_kc", C.c_int64), ("tuned", C.c_int32),
                 ("from_cache", C.c_int32), ("scratch_tuned", C.c_int32), ("n_cover", C.c_int32),
                 ("coverage", CoverRectC * MAX_COVER), ("tuning_fraction", C.c_double),
-                ("total_seconds", C.c_double)]
+                ("total_seconds", C.c_double), ("tuning_seconds", C.c_double)]
 
 
 MAX_REF_TRIALS = 64

@@ -821,12 +821,18 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
         // split-K forms for small outputs (variants with their own staging run
         // whole K unless they take K segments)
         if ((!vd.run || vd.splittable) && ctas < 2 * slots && whole.K >= 512) {
-            for (int64_t splits : {int64_t(2), (2 * slots + ctas - 1) / ctas}) {
+            // K segments: 2, 3, 4, 6, 8 and the count that fills two waves;
+            // each segment at least 128 deep. (Waves come out fractional for
+            // most counts on 148 SMs; the measurement picks.)
+            std::vector<int64_t> kcs;
+            for (int64_t splits : {int64_t(2), int64_t(3), int64_t(4), int64_t(6), int64_t(8),
+                                   (2 * slots + ctas - 1) / ctas}) {
                 splits = std::min<int64_t>(splits, whole.K / 128);
                 if (splits < 2) continue;
                 const int64_t kc = ((whole.K + splits - 1) / splits + 31) / 32 * 32;
-                if (trials.back().kc != kc) trials.push_back({v, kc});
+                if (std::find(kcs.begin(), kcs.end(), kc) == kcs.end()) kcs.push_back(kc);
             }
+            for (int64_t kc : kcs) trials.push_back({v, kc});
         }
     }
     Resolved rs = resolve(plan, ops, &b);
@@ -856,6 +862,9 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
             t.elapsed = el;
             t.score = el / double(whole.M);
         }
+        // the trial's work is repeated for the real R: charged to the call
+        rep->tuning_seconds += el;
+        rep->total_seconds += el;
         if (best.variant < 0 || el < best_t) {
             best_t = el;
             best = c;

@@ -224,6 +224,7 @@ class TuneReport:
     coverage: List[CoverRect] = field(default_factory=list)
     tuning_fraction: float = 0.0
     total_seconds: float = 0.0
+    tuning_seconds: float = 0.0  # whole-task trials on the scratch R (included in total_seconds)
 
 
 @dataclass
@@ -566,6 +567,7 @@ def _report(rc: N.TuneReportC) -> TuneReport:
                     for c in rc.coverage[:rc.n_cover]]
     rep.tuning_fraction = rc.tuning_fraction
     rep.total_seconds = rc.total_seconds
+    rep.tuning_seconds = rc.tuning_seconds
     return rep
 
 

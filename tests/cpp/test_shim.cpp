@@ -25,7 +25,7 @@ int main() {
     CHECK(plan.roles().desc.body == AMLT_BODY_DISCOUNT);
     CHECK(std::string(plan.roles().thres) == "thres" && std::string(plan.roles().dis) == "dis");
 
-    const std::int64_t M = 65536, K = 64, N = 1024;
+    const std::int64_t M = 131072, K = 64, N = 1024;
     // dry-run: buffers are described, never touched
     std::vector<double> tiny(16);
     auto mat = [&](std::int64_t r, std::int64_t c) {
@@ -49,7 +49,7 @@ int main() {
     CHECK(el == 0.5 && fc.consumed() == 1);
 
     // tuner: scripted intervals -> argmin(score) wins, rows covered once
-    FakeClock tc({0.9, 0.2, 0.7, 0.8, 0.6, 0.4, 0.95, 0.85, 0.75, 0.65, 0.55, 0.45, 0.35, 0.99});
+    FakeClock tc({0.9, 0.2, 0.7, 0.8, 0.6, 0.4, 0.95, 0.85, 0.75, 0.65, 0.55, 0.45, 0.35, 0.99, 0.3, 0.25, 0.97, 0.96});
     ExecLog log;
     TuneReport rep = adaptive_execute(plan, ops, Bounds{0, M, 0, N, 0, K}, false, tc, &log);
     CHECK(rep.tuned && rep.trials.size() >= 2);

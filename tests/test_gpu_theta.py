@@ -152,7 +152,13 @@ def test_nonfinite_a_in_theta_form(gpu_ctx):
     """inf / NaN in A stay on the theta path; on IntValued data the result must
     equal the ordinary kernel's exactly, inf signs and NaN positions included
     (both evaluate p * (p > t ? c1 : 1); the finite entries also equal the
-    oracle)."""
+    oracle).
+
+    Stated divergence: for a term whose product is infinite the
+    fused kernels accumulate the IEEE value p * c (+-inf, or NaN for 0 * inf),
+    while the reference's mask arithmetic ((m*A)*B)*dis multiplies 0 or 1 by
+    inf and yields NaN. Every such output is non-finite on both sides, at the
+    same positions; the values (+-inf vs NaN) may differ."""
     rng = np.random.default_rng(9)
     M, K, N = 40, 64, 34
     A, B = int_valued(rng, (M, K)), int_valued(rng, (K, N))
@@ -162,6 +168,8 @@ def test_nonfinite_a_in_theta_form(gpu_ctx):
     plan = gpu_ctx.plan("discount", "f64")
     base = run(gpu_ctx, A, B, t, d, ordinary(plan))
     fin = np.isfinite(base)
+    np.testing.assert_array_equal(fin, np.isfinite(want))  # non-finite at the same positions
+    assert (~fin).any()
     np.testing.assert_array_equal(base[fin], want[fin])
     for vi, name in theta_variants(plan):
         got = run(gpu_ctx, A, B, t, d, vi)
@@ -251,3 +259,25 @@ def test_config0_tunes_theta_with_k_segments(gpu_ctx):
     assert any("_theta_" in n for n, _ in tried)
     assert rep.scratch_tuned and len(rep.trials) > len({n for n, _ in tried})  # split-K forms tried too
     check("discount", "f64", R.cpu().numpy(), want, what="config 0 tuned")
+
+
+def test_scratch_trials_are_charged(gpu_ctx):
+    """Whole-task trials on the scratch R are work the real task repeats: the
+    report charges them (tuning_seconds, inside total_seconds) and counts no
+    output rows for them (tuning_fraction 0)."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+    from tests.helpers import make_inputs
+
+    M = K = N = 512
+    A, B, t, d = make_inputs("discount", M, K, N, "baseline", seed=82)
+    plan = gpu_ctx.plan("discount", "f64")
+    gpu_ctx.clear_tuning_cache()
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
+    R = dev(np.zeros((M, N)))
+    rep = P.adaptive_execute(plan, P.Operands(dev(A), dev(B), R, dev(t), dev(d)), P.Bounds(0, M, 0, N, 0, K))
+    assert rep.scratch_tuned and rep.tuning_fraction == 0.0
+    trials = sum(tr.elapsed for tr in rep.trials)
+    assert rep.tuning_seconds == pytest.approx(trials, rel=1e-9)
+    assert rep.total_seconds > rep.tuning_seconds

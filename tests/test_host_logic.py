@@ -85,7 +85,7 @@ def test_run_subtask_reads_clock_exactly_twice(dry_ctx):
                       clock=clk)
 
 
-def tuned_call(ctx, deltas, M=65536, K=64, N=1024):
+def tuned_call(ctx, deltas, M=131072, K=64, N=1024):
     plan = ctx.plan("discount", "f64")
     ctx.clear_tuning_cache()
     clk = P.FakeClock(deltas)
@@ -113,7 +113,7 @@ def test_tuner_picks_argmin_score_and_covers_once(dry_ctx):
         want = rep.trials[int(np.argmin(scores))].value  # ties keep the earlier
         assert rep.best_variant == want
         # exactly-once coverage of the rows, full N and K each
-        cover = np.zeros(65536, dtype=np.int32)
+        cover = np.zeros(131072, dtype=np.int32)
         for c in rep.coverage:
             assert (c.j0, c.j1, c.k0, c.k1) == (0, 1024, 0, 64)
             cover[c.i0:c.i1] += 1
@@ -136,7 +136,7 @@ def test_tuner_cache_reused_on_second_call(dry_ctx):
     plan, rep, clk, log = tuned_call(dry_ctx, [0.5, 0.1] + [0.9] * 14)
     clk2 = P.FakeClock([0.3])
     log2 = P.ExecLog()
-    rep2 = P.adaptive_execute(plan, big_ops(65536, 64, 1024), P.Bounds(0, 65536, 0, 1024, 0, 64),
+    rep2 = P.adaptive_execute(plan, big_ops(131072, 64, 1024), P.Bounds(0, 131072, 0, 1024, 0, 64),
                               clock=clk2, log=log2)
     assert rep2.from_cache and not rep2.tuned
     assert rep2.best_variant == rep.best_variant
