@@ -502,6 +502,9 @@ const char* amlt_gpu_sharded_last_error(void);
  * task text (generated bodies included). reports: NULL or n entries, one per
  * device. *elapsed_s: wall time of the whole run. */
 typedef struct amlt_sharded amlt_sharded;
+/* ctx_flags AMLT_CTX_DRY_RUN: a group of device-less contexts (no NCCL);
+ * runs plan and validate every band's operands and report each band's
+ * rectangle (absolute rows) as its coverage, without computing. */
 amlt_status amlt_sharded_create(int n_devices, const int* devices, int ctx_flags, amlt_sharded** out);
 void amlt_sharded_destroy(amlt_sharded* group);
 amlt_status amlt_sharded_run(amlt_sharded* group, const amlt_body_desc* desc, const char* task_source,

@@ -32,6 +32,7 @@ amlt_status ctx_use_comm(amlt_ctx* ctx, void* comm, int rank, int nranks);
 using namespace amltk;
 
 struct amlt_sharded {
+    bool dry = false;  // AMLT_CTX_DRY_RUN: contexts without devices; runs validate and plan only
     std::vector<int> devices;
     std::vector<amlt_ctx*> ctx;
     std::vector<ncclComm_t> comms;
@@ -182,10 +183,20 @@ amlt_status group_run(amlt_sharded* g, const amlt_body_desc* desc, const char* s
                 amlt_tune_report local;
                 amlt_tune_report* rep = reports ? &reports[d] : &local;
                 std::memset(rep, 0, sizeof(*rep));
-                // every rank takes part in the broadcasts, an empty band too
-                st[static_cast<size_t>(d)] = amlt_gpu_run_host_adaptive(
-                    g->ctx[static_cast<size_t>(d)], plans[static_cast<size_t>(d)], &o, &bb,
-                    flags | (n > 1 ? AMLT_HOST_BCAST_SHARED : 0), nullptr, nullptr, rep, nullptr);
+                if (g->dry) {
+                    // plan and validate the band's operands (no device): one
+                    // subtask over the band, its rectangle reported
+                    st[static_cast<size_t>(d)] = amlt_gpu_run_subtask(
+                        g->ctx[static_cast<size_t>(d)], plans[static_cast<size_t>(d)], &o, nullptr, &bb, nullptr,
+                        nullptr, nullptr, nullptr);
+                    rep->n_cover = 1;
+                    rep->coverage[0] = amlt_cover_rect{r0, r1, bb.k0, bb.k1, bb.j0, bb.j1};
+                } else {
+                    // every rank takes part in the broadcasts, an empty band too
+                    st[static_cast<size_t>(d)] = amlt_gpu_run_host_adaptive(
+                        g->ctx[static_cast<size_t>(d)], plans[static_cast<size_t>(d)], &o, &bb,
+                        flags | (n > 1 ? AMLT_HOST_BCAST_SHARED : 0), nullptr, nullptr, rep, nullptr);
+                }
                 if (st[static_cast<size_t>(d)] != AMLT_OK)
                     msg[static_cast<size_t>(d)] = amlt_gpu_last_error(g->ctx[static_cast<size_t>(d)]);
             });
@@ -217,7 +228,7 @@ amlt_status amlt_sharded_create(int n, const int* devices, int ctx_flags, amlt_s
     *out = nullptr;
     auto g = std::make_unique<amlt_sharded>();
     try {
-        if (ctx_flags & AMLT_CTX_DRY_RUN) throw Fail(AMLT_ERR_NO_DEVICE, "a sharded group needs devices");
+        g->dry = (ctx_flags & AMLT_CTX_DRY_RUN) != 0;
         g->devices.assign(devices, devices + n);
         for (int d = 0; d < n; ++d) {
             amlt_ctx* c = nullptr;
@@ -225,7 +236,7 @@ amlt_status amlt_sharded_create(int n, const int* devices, int ctx_flags, amlt_s
             if (st != AMLT_OK) throw Fail(st, amlt_gpu_last_error(nullptr));
             g->ctx.push_back(c);
         }
-        if (n > 1) {
+        if (n > 1 && !g->dry) {
             if (!nccl().ok) throw Fail(AMLT_ERR_CUDA, "libnccl.so.2 could not be loaded");
             g->comms.assign(static_cast<size_t>(n), nullptr);
             const int r = nccl().init_all(g->comms.data(), n, devices);
@@ -251,7 +262,7 @@ void amlt_sharded_destroy(amlt_sharded* g) {
         for (amlt_plan* p : kv.second)
             if (p) amlt_gpu_plan_destroy(p);
     for (size_t d = 0; d < g->ctx.size(); ++d) {
-        if (d < g->comms.size()) amlt_gpu_comm_detach(g->ctx[d]);  // (not owned by the context)
+        if (d < g->comms.size() && g->comms[d]) amlt_gpu_comm_detach(g->ctx[d]);  // (not owned by the context)
         amlt_gpu_ctx_destroy(g->ctx[d]);
     }
     for (size_t d = 0; d < g->comms.size(); ++d)

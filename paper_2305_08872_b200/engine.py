@@ -700,12 +700,14 @@ class ShardedGroup:
     (amlt_sharded_create): contexts, the NCCL communicator, plans and tuning
     winners are made once and reused by every run."""
 
-    def __init__(self, devices):
+    def __init__(self, devices, dry_run: bool = False):
         self._lib = N.lib()
         self.devices = list(devices)
+        self.dry_run = dry_run
         devs = (C.c_int * len(self.devices))(*self.devices)
         h = C.c_void_p()
-        st = self._lib.amlt_sharded_create(len(self.devices), devs, 0, C.byref(h))
+        st = self._lib.amlt_sharded_create(len(self.devices), devs, N.CTX_DRY_RUN if dry_run else 0,
+                                           C.byref(h))
         if st != N.OK:
             raise _ERRS.get(st, EngineError)(self._lib.amlt_sharded_last_error(None).decode())
         self.handle = h

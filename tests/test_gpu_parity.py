@@ -636,3 +636,43 @@ def test_tuning_cache_across_layouts_alignment_and_threshold_forms(gpu_ctx):
         wi[i] = oracle("discount", A[i:i + 1], B, np.full(N, ti[i]), d)[0]
     check("discount", "f64", R.cpu().numpy(), wi, exact=True, what="thres[i] after cached thres[j]")
     assert rep.best_variant >= 0
+
+
+@pytest.mark.parametrize("dtype,variant", [("f64", None), ("f32", None), ("f32", "cuda_core")])
+def test_config2_full_size_sampled_rows(gpu_ctx, dtype, variant):
+    """BASELINE config 2 at its full 8192^3 shape (plain GEMM, A and B
+    N(0,1)): the tuned winner (DMMA for f64, the tcgen05 3xTF32 GEMM for
+    f32) and, for f32, the fastest CUDA-core FFMA tile as the config is
+    written; the oracle on the first / last rows plus random rows x sampled
+    columns, normwise (|d| <= tol * sum_k |a b|)."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    M = K = N = 8192
+    td = {"f64": torch.float64, "f32": torch.float32}[dtype]
+    g = torch.Generator(device="cuda").manual_seed(21)
+    A = torch.randn((M, K), device="cuda", dtype=td, generator=g)
+    B = torch.randn((K, N), device="cuda", dtype=td, generator=g)
+    R = torch.zeros((M, N), device="cuda", dtype=td)
+    plan = gpu_ctx.plan("gemm", dtype)
+    ops = P.Operands(A, B, R, None, None)
+    bounds = P.Bounds(0, M, 0, N, 0, K)
+    names = [v.name for v in plan.variants()]
+    if variant == "cuda_core":
+        vi = names.index("gemm_f32_64x128_t8x4_w8x1")
+        P.run_subtask(plan, ops, P.TileParams(variant=vi), bounds)
+        used = names[vi]
+    else:
+        rep = P.adaptive_execute(plan, ops, bounds)
+        used = names[rep.best_variant]
+        assert ("dmma" in used) if dtype == "f64" else ("tcgen05" in used)
+    rows = sorted({0, M - 1, M // 2} | set(int(x) for x in np.random.default_rng(6).integers(0, M, 9)))
+    cols = sorted({0, N - 1} | set(int(x) for x in np.random.default_rng(7).integers(0, N, 300)))
+    idx = torch.tensor(rows, device="cuda")
+    cdx = torch.tensor(cols, device="cuda")
+    got = R[idx][:, cdx].double().cpu().numpy()
+    Ah = A[idx].double().cpu().numpy()
+    Bh = B[:, cdx].double().cpu().numpy()
+    want = oracle("gemm", Ah, Bh)
+    check("gemm", dtype, got, want, A=Ah, B=Bh, what=f"config 2 {dtype} {used}")

@@ -287,3 +287,34 @@ def test_run_naive_validates_like_run_subtask(dry_ctx):
         P.run_naive(plan, ops, P.Bounds(0, 16, 0, 16, 0, 16))
     with pytest.raises(P.EngineError):
         P.run_naive(plan, big_ops(16, 16, 16), P.Bounds(0, 16, 0, 17, 0, 16))
+
+
+def test_sharded_group_dry_run_bands_and_plans():
+    """The persistent row-band group (amlt_sharded_*) on CPU: dry-run
+    contexts plan and validate each device's band; bands are 64-row aligned
+    and tile [i0, i1) exactly once (the same cut as bench.py's row_band);
+    a second run of the group reuses its plans; bad operands fail loudly."""
+    from paper_2305_08872_b200.sharded import row_band
+
+    g = P.ShardedGroup([0, 1, 2, 3, 4, 5, 6, 7], dry_run=True)
+    try:
+        for M in (32768, 1000, 70):
+            ops = big_ops(M, 64, 256)
+            for _ in range(2):
+                _, reps = g.run(ops, P.Bounds(0, M, 0, 256, 0, 64), body="discount")
+                edges = [(r.coverage[0].i0, r.coverage[0].i1) for r in reps]
+                assert edges == [row_band(M, 8, d, align=64) for d in range(8)]
+                assert edges[0][0] == 0 and edges[-1][1] == M
+                assert all(a1 == b0 for (_, a1), (b0, _) in zip(edges, edges[1:]))
+        # a generated body through the same group
+        src = ("where(i in [0..M] and j in [0..N] and k in [0..K]) {\n"
+               "  R[i][j] += A[i][k]*B[k][j] + u[i]*v[j];\n}\n")
+        M = 512
+        ops = P.Operands(np.empty((M, 64)), np.empty((64, 256)), np.empty((M, 256)), None, None,
+                         (np.empty(M), np.empty(256)))
+        g.run(ops, P.Bounds(0, M, 0, 256, 0, 64), source=src)
+        with pytest.raises(P.MissingBinding):  # dis missing
+            g.run(P.Operands(np.empty((M, 64)), np.empty((64, 256)), np.empty((M, 256)), np.empty(256)),
+                  P.Bounds(0, M, 0, 256, 0, 64), body="discount")
+    finally:
+        g.close()
