@@ -275,7 +275,10 @@ void amlt_gpu_ctx_destroy(amlt_ctx* ctx);
  * ctx == NULL). Never NULL. */
 const char* amlt_gpu_last_error(const amlt_ctx* ctx);
 /* Launch on the caller's CUDA stream (cudaStream_t as void*); NULL restores
- * the context's own stream. */
+ * the context's own stream. The own stream is a blocking stream: ordered
+ * with the legacy default stream (work the caller queued there before a call
+ * is complete when the call's kernels start). Callers producing operands on
+ * any other stream pass that stream here. */
 amlt_status amlt_gpu_set_stream(amlt_ctx* ctx, void* stream);
 /* Forget tuning winners cached by amlt_gpu_adaptive_execute. */
 void amlt_gpu_clear_tuning_cache(amlt_ctx* ctx);

@@ -1669,7 +1669,11 @@ amlt_status amlt_gpu_ctx_create(int device, int flags, amlt_ctx** out) {
                                          std::to_string(prop.minor) +
                                          "; this build targets sm_100a (B200) only");
         ctx->num_sms = prop.multiProcessorCount;
-        cuda_check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        // The context's own stream is a BLOCKING stream: it is ordered with
+        // the legacy default stream, where callers without a stream of their
+        // own (PyTorch's default) produce the operands. (A non-blocking one
+        // let a kernel start before the caller's zero-fill of R had run.)
+        cuda_check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamDefault), "cudaStreamCreate");
         ctx->stream = ctx->own_stream;
         cuda_check(cudaEventCreate(&ctx->ev0), "cudaEventCreate");
         cuda_check(cudaEventCreate(&ctx->ev1), "cudaEventCreate");

@@ -660,7 +660,7 @@ def test_config2_full_size_sampled_rows(gpu_ctx, dtype, variant):
     bounds = P.Bounds(0, M, 0, N, 0, K)
     names = [v.name for v in plan.variants()]
     if variant == "cuda_core":
-        vi = names.index("gemm_f32_64x128_t8x4_w8x1")
+        vi = names.index("gemm_f32_64x128_t8x4_w8x1")  # the cuda_core leg of bench.py
         P.run_subtask(plan, ops, P.TileParams(variant=vi), bounds)
         used = names[vi]
     else:
@@ -676,3 +676,22 @@ def test_config2_full_size_sampled_rows(gpu_ctx, dtype, variant):
     Bh = B[:, cdx].double().cpu().numpy()
     want = oracle("gemm", Ah, Bh)
     check("gemm", dtype, got, want, A=Ah, B=Bh, what=f"config 2 {dtype} {used}")
+
+
+def test_context_stream_is_ordered_after_the_default_stream(gpu_ctx):
+    """Operands made by PyTorch on its default stream (here a 1 GiB zero-fill
+    of R queued right before the call) must be complete when the context's
+    own stream runs the kernel: the own stream is a blocking stream. With a
+    non-blocking one the zero-fill could land after the kernel (R all zero)."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 8192, 16, 16384
+    A = torch.ones((M, K), device="cuda", dtype=torch.float64)
+    B = torch.ones((K, N), device="cuda", dtype=torch.float64)
+    plan = gpu_ctx.plan("gemm", "f64")
+    for _ in range(3):
+        R = torch.zeros((M, N), device="cuda", dtype=torch.float64)  # 1 GiB fill on the default stream
+        P.run_subtask(plan, P.Operands(A, B, R, None, None), P.TileParams(), P.Bounds(0, M, 0, N, 0, K))
+        assert bool((R == K).all())
