@@ -592,13 +592,19 @@ void prep_b_untimed(amlt_ctx* ctx, const VariantDesc& v, const KParams& kp) {
     if (!v.prep_b || ctx->dry()) return;
     ensure_tc_ws(ctx, v, kp);
     if (bprep_ready(ctx, v, kp)) return;
-    cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
-    cuda_check(v.prep_b(kp, ctx->tc_ws, ctx->stream), "tensor-core operand preparation");
-    cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
-    cuda_check(cudaEventSynchronize(ctx->ev1), "cudaEventSynchronize");
-    float ms = 0;
-    cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "cudaEventElapsedTime");
-    bprep_mark(ctx, v, kp, ms * 1e-3);
+    // timed twice, the faster kept: a first run can pay one-off costs (cold
+    // instruction cache, first use of the kernel) that no later call pays
+    float best = 0;
+    for (int rep = 0; rep < 2; ++rep) {
+        cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
+        cuda_check(v.prep_b(kp, ctx->tc_ws, ctx->stream), "tensor-core operand preparation");
+        cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
+        cuda_check(cudaEventSynchronize(ctx->ev1), "cudaEventSynchronize");
+        float ms = 0;
+        cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "cudaEventElapsedTime");
+        best = rep == 0 ? ms : std::min(best, ms);
+    }
+    bprep_mark(ctx, v, kp, best * 1e-3);
 }
 // The preparation cost a trial of variant v leaves out (0 without one).
 double prep_seconds(const amlt_ctx* ctx, const VariantDesc& v) {
@@ -847,12 +853,20 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
         Dispatch dp = plan_dispatch(ctx, plan, &tp, rs);
         if (!rs.packed()) prep_b_untimed(ctx, vdesc(dp.variant), rs.kp);
         else ensure_tc_ws(ctx, vdesc(dp.variant), rs.kp);
-        cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
-        enqueue(ctx, plan, rs, dp);
-        cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
-        cuda_check(cudaEventSynchronize(ctx->ev1), "cudaEventSynchronize");
-        float ms = 0;
-        cuda_check(cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1), "cudaEventElapsedTime");
+        // two runs, the faster scored: the first can pay one-off costs (cold
+        // instruction cache, first launch of the kernel) the cached winner
+        // never pays again; both are charged to the call
+        float ms = 0, ms_sum = 0;
+        for (int rep = 0; rep < 2; ++rep) {
+            cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
+            enqueue(ctx, plan, rs, dp);
+            cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
+            cuda_check(cudaEventSynchronize(ctx->ev1), "cudaEventSynchronize");
+            float one = 0;
+            cuda_check(cudaEventElapsedTime(&one, ctx->ev0, ctx->ev1), "cudaEventElapsedTime");
+            ms = rep == 0 ? one : std::min(ms, one);
+            ms_sum += one;
+        }
         // the whole task: its B preparation is part of every call
         const double el = ms * 1e-3 + (rs.packed() ? 0.0 : prep_seconds(ctx, vdesc(dp.variant)));
         if (rep->n_trials < AMLT_MAX_TRIALS) {
@@ -862,9 +876,10 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
             t.elapsed = el;
             t.score = el / double(whole.M);
         }
-        // the trial's work is repeated for the real R: charged to the call
-        rep->tuning_seconds += el;
-        rep->total_seconds += el;
+        // the trials' work is repeated for the real R: charged to the call
+        const double spent = ms_sum * 1e-3 + (rs.packed() ? 0.0 : prep_seconds(ctx, vdesc(dp.variant)));
+        rep->tuning_seconds += spent;
+        rep->total_seconds += spent;
         if (best.variant < 0 || el < best_t) {
             best_t = el;
             best = c;
