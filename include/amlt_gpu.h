@@ -458,6 +458,7 @@ amlt_status amlt_gpu_run_host_adaptive(amlt_ctx* ctx, const amlt_plan* plan,
  * AMLT_HOST_BCAST_SHARED: rank 0 makes an id (AMLT_NCCL_ID_BYTES opaque
  * bytes), the caller hands it to every rank by its own means, and every rank
  * attaches it to its context (collective: blocks until all ranks attach).
+ * One rank is valid: the broadcasts are then no-ops (the path is the same).
  * NCCL (libnccl.so.2) is loaded at run time. */
 #define AMLT_NCCL_ID_BYTES 128
 amlt_status amlt_gpu_comm_unique_id(void* id_out);

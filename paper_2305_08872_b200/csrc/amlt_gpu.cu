@@ -1242,7 +1242,7 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
     const amlt_body_desc& d = plan->desc;
     const int es = dtype_size(d.dtype);
     const bool r_zero = (flags & AMLT_HOST_R_ZERO) != 0;
-    const bool bcast = (flags & AMLT_HOST_BCAST_SHARED) != 0 && ctx->comm && ctx->comm_size > 1;
+    const bool bcast = (flags & AMLT_HOST_BCAST_SHARED) != 0 && ctx->comm;
     const bool root = !bcast || ctx->comm_rank == 0;
     const int nslot = host_ncopies(host_ops);
 
@@ -2085,7 +2085,8 @@ amlt_status amlt_gpu_comm_attach(amlt_ctx* ctx, const void* id, int rank, int nr
     return guarded(ctx, [&] {
         if (ctx->dry()) fail(AMLT_ERR_NO_DEVICE, "amlt_gpu_comm_attach needs a device context");
         comm_release(ctx);
-        if (nranks == 1) return;  // nothing to exchange
+        // (a one-rank communicator is made too: its broadcasts are no-ops, but
+        // the whole broadcast path runs, which is how one GPU tests it)
         if (!nccl().ok) fail(AMLT_ERR_CUDA, "libnccl.so.2 could not be loaded");
         cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
         NcclUniqueId uid;

@@ -367,9 +367,10 @@ class Context:
         """Attaches an NCCL communicator for the multi-process host entry
         (amlt_gpu_comm_attach): rank 0 makes the id; `exchange(id_or_None)`
         must return rank 0's id on every rank (e.g. a torch.distributed
-        object broadcast). Collective: every rank must call it."""
-        if world_size <= 1:
-            return
+        object broadcast). Collective: every rank must call it. A one-rank
+        communicator is valid (its broadcasts are no-ops)."""
+        if world_size <= 1 and unique_id is None and exchange is None:
+            exchange = lambda uid: uid  # noqa: E731  (rank 0 is the only rank)
         if unique_id is None:
             if rank == 0:
                 buf = C.create_string_buffer(N.NCCL_ID_BYTES)

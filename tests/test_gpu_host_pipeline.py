@@ -112,20 +112,46 @@ def test_run_host_adaptive_tunes_then_reuses(gpu_ctx):
         assert rep.total_seconds > 0
 
 
-def test_bcast_flag_single_rank_is_a_no_op(gpu_ctx, small_panels):
-    """AMLT_HOST_BCAST_SHARED without a communicator (one rank): every
-    operand comes from this rank's host memory."""
+def test_bcast_flag_without_communicator(gpu_ctx, small_panels):
+    """AMLT_HOST_BCAST_SHARED without a communicator: every operand comes
+    from this rank's host memory."""
     import paper_2305_08872_b200 as P
 
     M, K, N = 300, 600, 200
     A, B, t, d = make_inputs("discount", M, K, N, "int", seed=77)
     want = oracle("discount", A, B, t, d)
     R = np.zeros((M, N))
-    gpu_ctx.attach_comm(0, 1)
     assert gpu_ctx.comm_size == 1
     P.run_host(gpu_ctx.plan("discount", "f64"), P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K),
                bcast=True)
-    check("discount", "f64", R, want, exact=True, what="bcast, one rank")
+    check("discount", "f64", R, want, exact=True, what="bcast, no communicator")
+
+
+@pytest.mark.parametrize("body", ["discount", "gemm"])
+def test_broadcast_path_on_a_one_rank_communicator(small_panels, body):
+    """The NCCL broadcast path of the host pipeline on one GPU: a real
+    one-rank communicator (amlt_gpu_comm_unique_id / _attach), so every
+    ncclBroadcast, group and stream / event hand-off of the multi-rank path
+    runs (the broadcasts themselves are no-ops). B in several K panels; two
+    calls (the first tunes); bit-exact."""
+    import paper_2305_08872_b200 as P
+
+    ctx = P.Context(0)
+    try:
+        ctx.attach_comm(0, 1)
+        assert ctx.comm_size == 1
+        M, K, N = 1100, 1000, 300
+        A, B, t, d = make_inputs(body, M, K, N, "int", seed=80)
+        want = oracle(body, A, B, t, d)
+        plan = ctx.plan(body, "f64")
+        for _ in range(2):
+            R = np.zeros((M, N))
+            P.run_host_adaptive(plan, P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K), r_zero=True,
+                                bcast=True)
+            check(body, "f64", R, want, exact=True, what=f"one-rank broadcast path {body}")
+        ctx.detach_comm()
+    finally:
+        ctx.close()
 
 
 def _shard_rows(M, n):
