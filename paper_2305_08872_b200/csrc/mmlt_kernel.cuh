@@ -145,6 +145,15 @@ __device__ __forceinline__ T ldg_elem(const void* base, int64_t idx) {
     return __ldg(static_cast<const T*>(base) + idx);
 }
 
+template <typename T>
+struct IsF32 {
+    static constexpr bool value = false;
+};
+template <>
+struct IsF32<float> {
+    static constexpr bool value = true;
+};
+
 // Counting bodies: acc += (x CMP y), as SETP + predicated add — two issue
 // slots (nvcc's own lowering of `acc += cond ? 1 : 0` is a speculative add
 // plus a predicated move, three).
@@ -199,6 +208,15 @@ struct BodyGemm {
     __device__ static Col col(const KParams&, int64_t) { return {}; }
     __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col&) {
         acc[0] = fma_rn(a, b, acc[0]);
+    }
+    // fp32: two columns per FFMA2 (half the issue slots, the same FMA-pipe work)
+    static constexpr bool PAIRED = IsF32<T>::value;
+    __device__ static __forceinline__ void step2(Acc* acc0, Acc* acc1, T a, T b0, T b1, const Col&, const Col&) {
+        asm("{\n .reg .b64 x, y, s;\n"
+            " mov.b64 x, {%2, %2};\n mov.b64 y, {%3, %4};\n mov.b64 s, {%0, %1};\n"
+            " fma.rn.f32x2 s, x, y, s;\n mov.b64 {%0, %1}, s;\n}\n"
+            : "+f"(acc0[0]), "+f"(acc1[0])
+            : "f"(a), "f"(b0), "f"(b1));
     }
     __device__ static __forceinline__ T finish(const Acc* acc, const Col&, int64_t) { return acc[0]; }
 };
@@ -273,19 +291,33 @@ struct BodyBoost {
         T s = acc[0] - static_cast<T>(kcount) * c.t;  // sum of (a*b - t)
         return acc[0] + T(0.5) * (s + acc[1]);
     }
+    // (A two-column fp32 form, FFMA2 + FFMA2 + FADD2, needs |u| as a sign
+    // mask: two LOP3 per pair on the ALU. Measured 17.8 against 19.9 TFLOP/s
+    // at 4096^3, so boost keeps the one-column step with its free |.|.)
 };
 
-// SQDIFF — `R += (A - B)*(A - B)`: FADD + FFMA per iteration.
+// SQDIFF — `R += (A - B)*(A - B)`: FADD + FFMA per iteration; in fp32 two
+// columns at a time as FADD2 + FFMA2 (sm_100's two-wide fp32 instructions:
+// the same FMA-pipe work in half the issue slots).
 template <typename T>
 struct BodySqdiff {
     using Acc = T;
     static constexpr int NACC = 1;
     static constexpr bool TWO_LEVEL = sizeof(T) == 4;
+    static constexpr bool PAIRED = IsF32<T>::value;
     struct Col {};
     __device__ static Col col(const KParams&, int64_t) { return {}; }
     __device__ static __forceinline__ void step(Acc* acc, T a, T b, const Col&) {
         T d = a - b;
         acc[0] = fma_rn(d, d, acc[0]);
+    }
+    // columns c and c+1 of one row: acc0 / acc1
+    __device__ static __forceinline__ void step2(Acc* acc0, Acc* acc1, T a, T b0, T b1, const Col&, const Col&) {
+        asm("{\n .reg .b64 x, y, s, d;\n"
+            " mov.b64 x, {%2, %2};\n mov.b64 y, {%3, %4};\n mov.b64 s, {%0, %1};\n"
+            " sub.rn.f32x2 d, x, y;\n fma.rn.f32x2 s, d, d, s;\n mov.b64 {%0, %1}, s;\n}\n"
+            : "+f"(acc0[0]), "+f"(acc1[0])
+            : "f"(a), "f"(b0), "f"(b1));
     }
     __device__ static __forceinline__ T finish(const Acc* acc, const Col&, int64_t) { return acc[0]; }
 };
@@ -386,6 +418,16 @@ struct BodyPlanes {
 template <class Body>
 struct BodyPlanes<Body, decltype(void(Body::BPLANES))> {
     static constexpr int n = Body::BPLANES;
+};
+
+// Bodies with a two-column step (Body::step2, e.g. fp32 FFMA2 forms).
+template <class Body, class = void>
+struct Paired {
+    static constexpr bool value = false;
+};
+template <class Body>
+struct Paired<Body, decltype(void(Body::PAIRED))> {
+    static constexpr bool value = Body::PAIRED;
 };
 
 // Bodies whose inner step runs row-outer (the row's a is the shared operand
@@ -761,6 +803,18 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
                                     STEP(part[r][c], a, c, COL(r, c));
                                 else
                                     STEP(acc[r][c], a, c, COL(r, c));
+                            }
+                        }
+                    } else if constexpr (Paired<Body>::value && NPL == 1 && TN % 2 == 0) {
+#pragma unroll
+                        for (int c = 0; c < TN; c += 2) {
+#pragma unroll
+                            for (int r = 0; r < TM; ++r) {
+                                const T a = V16<T>::get(av[r], v);
+                                if constexpr (Body::TWO_LEVEL)
+                                    Body::step2(part[r][c], part[r][c + 1], a, b[c], b[c + 1], COL(r, c), COL(r, c + 1));
+                                else
+                                    Body::step2(acc[r][c], acc[r][c + 1], a, b[c], b[c + 1], COL(r, c), COL(r, c + 1));
                             }
                         }
                     } else {
