@@ -827,12 +827,22 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
         // split-K forms for small outputs (variants with their own staging run
         // whole K unless they take K segments)
         if ((!vd.run || vd.splittable) && ctas < 2 * slots && whole.K >= 512) {
-            // K segments: 2, 3, 4, 6, 8 and the count that fills two waves;
-            // each segment at least 128 deep. (Waves come out fractional for
-            // most counts on 148 SMs; the measurement picks.)
+            // K segments: 2, 3, 4, 6, 8, the count that fills two waves, and
+            // the two counts (up to 16) whose CTAs come closest to whole waves
+            // on this GPU (e.g. 88 tiles x 5 = 2.97 waves of 148); each
+            // segment at least 128 deep. The measurement picks.
+            std::vector<int64_t> counts = {2, 3, 4, 6, 8, (2 * slots + ctas - 1) / ctas};
+            {
+                std::vector<std::pair<double, int64_t>> eff;
+                for (int64_t sp = 2; sp <= std::min<int64_t>(16, whole.K / 128); ++sp) {
+                    const double waves = double(ctas * sp) / double(slots);
+                    eff.push_back({-waves / std::ceil(waves), sp});
+                }
+                std::sort(eff.begin(), eff.end());
+                for (size_t q = 0; q < eff.size() && q < 2; ++q) counts.push_back(eff[q].second);
+            }
             std::vector<int64_t> kcs;
-            for (int64_t splits : {int64_t(2), int64_t(3), int64_t(4), int64_t(6), int64_t(8),
-                                   (2 * slots + ctas - 1) / ctas}) {
+            for (int64_t splits : counts) {
                 splits = std::min<int64_t>(splits, whole.K / 128);
                 if (splits < 2) continue;
                 const int64_t kc = ((whole.K + splits - 1) / splits + 31) / 32 * 32;
