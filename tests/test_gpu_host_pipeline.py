@@ -216,3 +216,48 @@ def test_torchrun_broadcast_entry(tmp_path):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     z = np.load(out)
     assert z["bad"] == 0, f"{int(z['bad'])} mismatching rows"
+
+
+@pytest.mark.parametrize("case", range(24))
+def test_random_pipeline_cases_bit_exact(gpu_ctx, small_panels, case):
+    """Randomised sweep of the host pipeline: shapes large enough for several
+    row bands, B cut into K panels (small panels forced), a bounds
+    sub-rectangle of a prior-valued (or zero, with AMLT_HOST_R_ZERO) R, every
+    fixed body / dtype, transposed or col-major operands (which fall back to
+    one band / one panel), run_host or run_host_adaptive; int-valued data, so
+    bit-exact against the oracle, R outside the bounds untouched."""
+    import paper_2305_08872_b200 as P
+    from tests.helpers import NP_DT
+
+    bodies = [("gemm", "f64"), ("gemm", "f32"), ("discount", "f64"), ("boost", "f64"), ("boost", "f32"),
+              ("sqdiff", "f32"), ("eqcount", "i32"), ("thrcount", "f64")]
+    rng = np.random.default_rng(7000 + case)
+    body, dtype = bodies[case % len(bodies)]
+    M, K, N = int(rng.integers(1024, 2600)), int(rng.integers(300, 1300)), int(rng.integers(64, 420))
+    i0, j0, k0 = int(rng.integers(0, 200)), int(rng.integers(0, 40)), int(rng.integers(0, 100))
+    i1, j1, k1 = int(rng.integers(M - 200, M + 1)), int(rng.integers(N - 30, N + 1)), int(rng.integers(K - 80, K + 1))
+    at = bool(rng.random() < 0.2)
+    bcm = bool(rng.random() < 0.2)
+    r_zero = bool(rng.random() < 0.4)
+    A, B, t, d = make_inputs(body, M, K, N, "int", seed=7100 + case)
+    R0 = np.zeros((M, N)) if r_zero else rng.integers(-50, 50, (M, N)).astype(np.float64)
+    b = (i0, i1, j0, j1, k0, k1)
+    if r_zero:  # R starts at zero: only the bounds rows are zero-filled, so the bounds cover whole rows
+        b = (i0, i1, 0, N, k0, k1)
+    want = oracle(body, A, B, t, d, R0=R0, bounds=b)
+    npd = NP_DT[dtype]
+    Ab = np.ascontiguousarray(A.T if at else A).astype(npd)
+    Bb = (np.asfortranarray(B) if bcm else np.ascontiguousarray(B)).astype(npd)
+    R = R0.astype(npd).copy()
+    plan = gpu_ctx.plan(body, dtype, layout_a=int(at))
+    ops = P.Operands(Ab, Bb, R, None if t is None else t.astype(npd), None if d is None else d.astype(npd))
+    if case % 3 == 0:
+        gpu_ctx.clear_tuning_cache()
+        P.run_host_adaptive(plan, ops, P.Bounds(*b), r_zero=r_zero)
+    else:
+        P.run_host(plan, ops, P.Bounds(*b), r_zero=r_zero)
+    got = R.astype(np.float64)
+    bad = np.argwhere(got != want)
+    assert bad.size == 0, (f"case {case}: {body}/{dtype} {M}x{K}x{N} bounds {b} at={at} bcm={bcm} "
+                           f"r_zero={r_zero}: {len(bad)} mismatches, first {tuple(bad[0])} got "
+                           f"{got[tuple(bad[0])]} want {want[tuple(bad[0])]}")
