@@ -384,12 +384,24 @@ def verify_rows(P, plan, win, A, B, th, ds, R, body, dtype, rows, rank, row0, st
     Bh = B[:, cdx].double().cpu().numpy()
     th_h = th[cdx].double().cpu().numpy() if th is not None else None
     ds_h = ds[cdx].double().cpu().numpy() if ds is not None else None
+    return (len(ri), len(ci)) + check_rows(got, Ah, Bh, th_h, ds_h, body, dtype)
+
+
+def check_rows(got, Ah, Bh, th_h, ds_h, body, dtype):
+    """(max relative error, mismatches) of sampled R rows x columns against
+    the C oracle on the same rows of A and columns of B / thres / dis."""
+    import numpy as np
+
+    from oracle import pyoracle as po
+
     kind = {"gemm": po.GEMM, "discount": po.DISCOUNT, "boost": po.BOOST, "sqdiff": po.SQDIFF,
             "eqcount": po.EQCOUNT}[body]
+    ri = range(got.shape[0])
+    ci = range(got.shape[1])
     want = np.zeros((len(ri), len(ci)))
     po.oracle_run(kind, Ah, Bh, want, thres=th_h, dis=ds_h)
     if dtype == "i32" or body == "eqcount":
-        return len(ri), len(ci), 0.0, int((got != want).sum())
+        return 0.0, int((got != want).sum())
     err = np.abs(got - want)
     if body in ("gemm", "sqdiff"):  # normwise: |d| <= tol * sum_k |term_k| (SURVEY §7)
         if body == "gemm":
@@ -399,7 +411,7 @@ def verify_rows(P, plan, win, A, B, th, ds, R, body, dtype, rows, rank, row0, st
     else:
         scale = np.abs(want)
     rel = err / np.maximum(scale, np.finfo(np.float64).tiny)
-    return len(ri), len(ci), float(rel.max()), int((rel > TOL[dtype]).sum())
+    return float(rel.max()), int((rel > TOL[dtype]).sum())
 
 
 def cuda_core_leg(P, plan, ops, bounds, stream, steps, M, K, N, peak_ffma_tflops):
@@ -548,6 +560,7 @@ def main():
         return 0
 
     nccl_log = NcclLog(rank) if ws > 1 else None
+    import numpy as np
     import torch
 
     import paper_2305_08872_b200 as P
@@ -708,6 +721,14 @@ def main():
         hds = (ds.cpu().pin_memory() if rank == 0 else P.Shape(N, 1, dtype)) if ds is not None else None
         hR = torch.empty((rows, N), dtype=A.dtype).pin_memory()
         hops = P.Operands(hA, hB, hR, hth, hds)
+        # columns kept for checking the e2e result afterwards (every rank)
+        rng = np.random.default_rng(29 + rank)
+        e_ci = sorted({0, N - 1} | set(int(x) for x in rng.integers(0, N, 254)))
+        e_ri = sorted({0, rows - 1} | set(int(x) for x in rng.integers(0, rows, 6))) if rows > 0 else []
+        cdx = torch.tensor(e_ci, device=B.device)
+        e_B = B[:, cdx].double().cpu().numpy()
+        e_th = th[cdx].double().cpu().numpy() if th is not None else None
+        e_ds = ds[cdx].double().cpu().numpy() if ds is not None else None
         del A, B, R, ops
         torch.cuda.empty_cache()
         bcast = ws > 1
@@ -730,6 +751,7 @@ def main():
             log("bench.py: e2e leg failed:", e2e_error)
             tms = [float("inf")]
         e_el = sum(tms)
+        layout = ctx.last_host_layout() if not e2e_error else {}
         if dist is not None:
             tt = torch.tensor([e_el], dtype=torch.float64, device=device)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -747,12 +769,32 @@ def main():
                "h2d_bytes_per_step": int(h2d_total),
                "d2h_bytes_per_step": int(d2h_total),
                "ms_per_step": e_el / steps * 1e3,
-               "path": ("amlt_gpu_run_host (C-ABI) from pinned host buffers: A / R row bands and B K-panels "
-                        "pipelined against compute, R zero-init on the device"
+               "path": ("amlt_gpu_run_host (C-ABI) from pinned host buffers: B in K panels and A in row "
+                        "bands H2D, pipelined against compute; band 0 computed panel by panel as B lands "
+                        "(its R zero-filled on the device, D2H afterwards); "
+                        + ("the other rows in one launch whose epilogue writes R straight into the pinned "
+                           "host buffer (zero-copy)" if layout.get("zero_copy_r") else
+                           "the other row bands whole-K, each R band D2H as soon as it is done")
                         + ("; B / thres / dis read on rank 0 only and NCCL-broadcast panel by panel "
-                           "inside the call" if bcast else ""))}
+                           "inside the call" if bcast else "")),
+               "layout": layout}
         if e2e_error:
             e2e["error"] = e2e_error
+        elif not args.no_verify:
+            # the last timed step's R, as it landed in host memory
+            worst, bad = check_rows(hR[e_ri][:, e_ci].double().numpy(), hA[e_ri].double().numpy(), e_B, e_th,
+                                    e_ds, body, dtype) if e_ri else (0.0, 0)
+            nr = len(e_ri)
+            if dist is not None:
+                tt = torch.tensor([nr, worst, bad], dtype=torch.float64, device=device)
+                parts = [torch.zeros_like(tt) for _ in range(ws)]
+                dist.all_gather(parts, tt)
+                nr = int(sum(p[0].item() for p in parts))
+                worst = max(p[1].item() for p in parts)
+                bad = int(sum(p[2].item() for p in parts))
+            e2e["verified"] = {"rows": nr, "cols": len(e_ci), "max_rel": worst, "mismatches": bad, "ok": bad == 0,
+                               "how": "the last timed step's R in host memory, sampled rows x columns, "
+                                      "against the C oracle"}
 
     # ---- CPU baseline (rank 0, N = 1)
     cpu = None

@@ -467,6 +467,14 @@ amlt_status amlt_gpu_comm_detach(amlt_ctx* ctx);
 /* Ranks of the attached communicator (1 when none). */
 int amlt_gpu_comm_size(const amlt_ctx* ctx);
 
+/* How the last amlt_gpu_run_host(_adaptive) call on ctx ran (diagnostics,
+ * e.g. for a bench line): out[0] row bands, [1] K panels of B, [2] 1 when the
+ * rows after band 0 wrote R straight into mapped host memory (zero-copy),
+ * [3] rows of band 0, [4] k depth of the first panel, [5] 1 when B came by
+ * broadcast, [6] 1 when the call tuned (whole task, no pipeline). */
+#define AMLT_HOST_LAYOUT_FIELDS 7
+amlt_status amlt_gpu_last_host_layout(const amlt_ctx* ctx, int64_t* out);
+
 /* Row-band multi-GPU execution of one task from a single process (the
  * reference engine's process model). Device d of n owns rows
  * [i0 + M d/n, i0 + M (d+1)/n) of A and R; B and the per-column vectors are

@@ -143,9 +143,11 @@ EXPORTS = [
     "amlt_gpu_run_sharded_source", "amlt_gpu_matrix_alloc", "amlt_gpu_matrix_free",
     "amlt_gpu_matrix_upload", "amlt_gpu_matrix_download", "amlt_gpu_run_host_adaptive",
     "amlt_gpu_comm_unique_id", "amlt_gpu_comm_attach", "amlt_gpu_comm_detach", "amlt_gpu_comm_size",
+    "amlt_gpu_last_host_layout",
     "amlt_sharded_create", "amlt_sharded_destroy", "amlt_sharded_run", "amlt_sharded_size",
     "amlt_sharded_last_error",
 ]
+HOST_LAYOUT_FIELDS = 7
 HOST_R_ZERO = 1
 HOST_BCAST_SHARED = 2
 NCCL_ID_BYTES = 128
@@ -198,6 +200,7 @@ def lib():
     L.amlt_gpu_comm_attach.argtypes = [P, C.c_void_p, C.c_int, C.c_int]
     L.amlt_gpu_comm_detach.argtypes = [P]
     L.amlt_gpu_comm_size.argtypes = [P]
+    L.amlt_gpu_last_host_layout.argtypes = [P, C.POINTER(C.c_int64)]
     L.amlt_sharded_create.argtypes = [C.c_int, C.POINTER(C.c_int), C.c_int, C.POINTER(P)]
     L.amlt_sharded_destroy.argtypes = [P]
     L.amlt_sharded_destroy.restype = None

@@ -116,6 +116,8 @@ struct amlt_ctx {
     size_t tc_ws_bytes = 0;
     // B's preparation in tc_ws, valid within one C-ABI call (call_gen)
     uint64_t call_gen = 0;
+    // layout of the last host-pipeline call (amlt_gpu_last_host_layout)
+    int64_t host_layout[AMLT_HOST_LAYOUT_FIELDS] = {};
     struct BPrep {
         const void* B = nullptr;
         int64_t ldb = 0, K = 0, N = 0;
@@ -981,10 +983,11 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
         int v;
         int64_t kc = 0;
         if (it != ctx->tune_cache.end()) {
-            // a winner measured on an earlier call with the same shape
+            // a winner measured on an earlier call with the same shape (or
+            // by this call's scratch trials just above: not from the cache)
             v = it->second.variant;
             kc = it->second.kc;
-            rep->from_cache = 1;
+            rep->from_cache = rep->scratch_tuned ? 0 : 1;
         } else if (!plan->desc.accumulate) {
             // "=" runs the per-element assign kernel; any staging-compatible variant
             v = default_variant(ctx, plan, whole.M, whole.N, whole.aligned);
@@ -1269,35 +1272,15 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
     }
     Resolved hv = resolve(plan, &hview, bounds);
 
-    // device staging, one buffer per operand (same pitch and offsets as the host's)
-    amlt_operands dev = hview;
-    amlt_matrix* dslot[5 + AMLT_MAX_AUX] = {&dev.a, &dev.b, &dev.r, &dev.thres, &dev.dis};
-    for (int q = 0; q + 5 < nslot; ++q) dslot[5 + q] = &dev.aux[q];
+    // each operand's host extent: (outer - 1) whole pitches plus one inner run
+    // (a view into a larger host buffer never reads past its own end)
     size_t bytes[5 + AMLT_MAX_AUX] = {};
     for (int s = 0; s < nslot; ++s) {
         const amlt_matrix& m = *hslot[s];
         if (!m.data) continue;
-        // the buffer's extent: (outer - 1) whole pitches plus one inner run
-        // (a view into a larger host buffer never reads past its own end)
         const int64_t outer = m.order == AMLT_ROW_MAJOR ? m.rows : m.cols;
         const int64_t inner = m.order == AMLT_ROW_MAJOR ? m.cols : m.rows;
         bytes[s] = outer > 0 && inner > 0 ? (size_t(outer - 1) * size_t(m.ld) + size_t(inner)) * es : 0;
-        if (!bytes[s]) {
-            dslot[s]->data = ctx->hbuf[s] ? ctx->hbuf[s] : reinterpret_cast<void*>(uintptr_t(256));
-            continue;
-        }
-        if (bytes[s] > ctx->hbuf_bytes[s]) {
-            if (ctx->hbuf[s]) cudaFree(ctx->hbuf[s]);
-            ctx->hbuf[s] = nullptr;
-            ctx->hbuf_bytes[s] = 0;
-            cuda_check(cudaMalloc(&ctx->hbuf[s], bytes[s]), "cudaMalloc(host staging)");
-            ctx->hbuf_bytes[s] = bytes[s];
-        }
-        dslot[s]->data = ctx->hbuf[s];
-    }
-    if (!ctx->copy_in) {
-        cuda_check(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking), "cudaStreamCreate");
-        cuda_check(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking), "cudaStreamCreate");
     }
 
     // the variant: the caller's tile, else the winner cached for this shape,
@@ -1319,16 +1302,39 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
     }
     const bool tune_now = rep && !tile && !cached;
     const int64_t M = hv.M, N = hv.N, K = hv.K;
+    const int vi = !tune_now ? (tp.variant >= 0 ? plan->variants[static_cast<size_t>(tp.variant)]
+                                                : default_variant(ctx, plan, M, N, hv.aligned))
+                             : -1;
 
     // row bands of A / R (A rows k-contiguous, R row-major)
     const bool a_rows = (d.layout_a == AMLT_LAYOUT_NORMAL && host_ops->a.order == AMLT_ROW_MAJOR);
     const bool r_rows = host_ops->r.order == AMLT_ROW_MAJOR;
-    int nb = 1;
-    if (!tune_now && a_rows && r_rows && M >= 1024) nb = static_cast<int>(std::min<int64_t>(8, M / 256));
     // K panels of B (B's k rows contiguous)
     const bool b_kouter = (d.layout_b == AMLT_LAYOUT_NORMAL && host_ops->b.order == AMLT_ROW_MAJOR) ||
                           (d.layout_b == AMLT_LAYOUT_TRANSPOSED && host_ops->b.order == AMLT_COL_MAJOR);
     const bool split_winner = tp.kc > 0 && tp.kc < K;
+    const bool banded = !tune_now && a_rows && r_rows && M >= 1024;
+
+    // Result straight to the host: when R is pinned host memory the device
+    // can address (cudaHostAlloc / cudaHostRegister, mapped), the rows after
+    // band 0 run as ONE launch whose epilogue stores R into host memory over
+    // PCIe (and, without R_ZERO, reads it from there): each R element crosses
+    // the bus once, as the D2H copy would have, with no copy-out stage, no
+    // staging buffer and no band boundaries after band 0. Needs a variant
+    // whose epilogue does plain global stores and honours KParams::r_zero,
+    // whole-K launches, and no packing of R. AMLT_HOST_NO_ZEROCOPY=1 keeps
+    // the staged pipeline (diagnostics).
+    void* r_mapped = nullptr;
+    if (banded && d.accumulate && vi >= 0 && vdesc(vi).r_overwrite && !split_winner &&
+        !std::getenv("AMLT_HOST_NO_ZEROCOPY")) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, host_ops->r.data) == cudaSuccess) {
+            if (at.type == cudaMemoryTypeHost && at.devicePointer) r_mapped = at.devicePointer;
+        } else {
+            (void)cudaGetLastError();  // unregistered pageable memory: staged pipeline
+        }
+    }
+
     // (the panel count depends only on what every rank of a broadcast shares,
     // so all ranks issue the same sequence of collectives)
     // Panels of at least 256 MiB of B (AMLT_HOST_PANEL_BYTES overrides; tests
@@ -1341,41 +1347,44 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
         np = static_cast<int>(std::max(1.0, std::min({8.0, std::floor(b_bytes / panel_bytes),
                                                       std::floor(double(K) / 256.0)})));
     }
-    const int vi = !tune_now ? (tp.variant >= 0 ? plan->variants[static_cast<size_t>(tp.variant)]
-                                                : default_variant(ctx, plan, M, N, hv.aligned))
-                             : -1;
-    if (nb > 1) {
-        // Band count: every band boundary drains the GPU (up to a wave of CTAs
-        // idles), while more bands hide more of the A / R transfers. With the
-        // winner's measured seconds per row, minimise boundaries x wave time +
-        // exposed copy (~ copy time / bands): nb = sqrt(copy x waves /
-        // compute); without it, as many bands as full waves allow. At most 8,
-        // at least one wave each (split-K multiplies CTAs).
-        const VariantDesc& v = vdesc(vi);
-        const int64_t splits = ((!v.run || v.splittable) && split_winner) ? (K + tp.kc - 1) / tp.kc : 1;
-        const int64_t slots = int64_t(ctx->num_sms) * occ_of(ctx, vi);
-        const int64_t fill = ctas_for(v, M, N) * splits / std::max<int64_t>(1, slots);
-        int64_t want = fill;
-        if (row_seconds > 0.0) {
-            const double copy_s = (double(bytes[0]) + double(bytes[2]) * (r_zero ? 1.0 : 2.0)) / 40e9;
-            const double compute_s = row_seconds * double(M);
-            want = static_cast<int64_t>(std::lround(std::sqrt(copy_s * double(std::max<int64_t>(fill, 1)) / compute_s)));
-        }
-        nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({int64_t(nb), fill, want})));
-    }
-    // Panels: equal, edges on multiples of 64 k (16-byte aligned operand
-    // offsets). Only the first row band runs panel by panel, as B arrives;
-    // it is tall enough that its compute covers the rest of B's transfer
-    // (from the winner's measured seconds per row, assuming ~40 GB/s host
-    // copies, more with a broadcast behind them), between 1/8 and 1/2 of the
-    // rows. The other bands run whole K (one launch each, no extra R
-    // traffic); the last one is an eighth as tall as the others, so the
-    // copy-out that trails the final compute is short. 64-row multiples.
-    const std::vector<int64_t> kedge = band_edges(bounds->k0, K, np, 64, false);
+    // Bands: only the first runs panel by panel, as B arrives; it is tall
+    // enough that its compute covers the rest of B's transfer (from the
+    // winner's measured seconds per row, assuming ~40 GB/s host copies, more
+    // with a broadcast behind them), between 1/8 and 1/2 of the rows. The
+    // other bands run whole K (one launch each, no extra R traffic); the last
+    // one is an eighth as tall as the others, so the copy-out that trails the
+    // final compute is short. 64-row multiples.
+    int nb = 1;
     std::vector<int64_t> redge;
-    if (nb == 1) {
-        redge = {bounds->i0, bounds->i1};
-    } else {
+    auto layout = [&](bool zero_copy) {
+        nb = banded ? static_cast<int>(std::min<int64_t>(8, M / 256)) : 1;
+        if (nb > 1 && zero_copy) {
+            nb = 2;  // band 0 (as B lands), then every other row in one launch
+        } else if (nb > 1) {
+            // Band count: every band boundary drains the GPU (up to a wave of
+            // CTAs idles), while more bands hide more of the A / R transfers.
+            // With the winner's measured seconds per row, minimise boundaries
+            // x wave time + exposed copy (~ copy time / bands): nb = sqrt(copy
+            // x waves / compute); without it, as many bands as full waves
+            // allow. At most 8, at least one wave each (split-K multiplies CTAs).
+            const VariantDesc& v = vdesc(vi);
+            const int64_t splits = ((!v.run || v.splittable) && split_winner) ? (K + tp.kc - 1) / tp.kc : 1;
+            const int64_t slots = int64_t(ctx->num_sms) * occ_of(ctx, vi);
+            const int64_t fill = ctas_for(v, M, N) * splits / std::max<int64_t>(1, slots);
+            int64_t want = fill;
+            if (row_seconds > 0.0) {
+                const double copy_s = (double(bytes[0]) + double(bytes[2]) * (r_zero ? 1.0 : 2.0)) / 40e9;
+                const double compute_s = row_seconds * double(M);
+                want = static_cast<int64_t>(
+                    std::lround(std::sqrt(copy_s * double(std::max<int64_t>(fill, 1)) / compute_s)));
+            }
+            nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({int64_t(nb), fill, want})));
+        }
+        redge.clear();
+        if (nb == 1) {
+            redge = {bounds->i0, bounds->i1};
+            return;
+        }
         int64_t rows0 = M / nb;
         if (np > 1 && row_seconds > 0.0) {
             const double b_bytes = double(K) * double(host_ops->b.ld) * es;
@@ -1387,11 +1396,82 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
         redge.push_back(bounds->i0);
         const std::vector<int64_t> rest = band_edges(bounds->i0 + rows0, M - rows0, nb - 1, 64, true);
         redge.insert(redge.end(), rest.begin(), rest.end());
+    };
+    layout(r_mapped != nullptr);
+    if (r_mapped) {
+        // the zero-copy band must run unpacked, as one whole-K launch of a
+        // variant that honours r_zero (else: the staged pipeline)
+        amlt_operands probe = hview;
+        probe.r.data = r_mapped;
+        amlt_bounds bb = *bounds;
+        bb.i0 = nb > 1 ? redge[1] : bounds->i1;
+        const Resolved rv = resolve(plan, &probe, &bb);
+        const Dispatch dp = plan_dispatch(ctx, plan, &tp, rv);
+        if (nb < 2 || rv.packed() || dp.splits > 1 || !vdesc(dp.variant).r_overwrite) {
+            r_mapped = nullptr;
+            layout(false);
+        }
+    }
+    const bool zc = r_mapped != nullptr;
+
+    // A of band 0 arrives K panel by K panel with B (a 2-D copy per panel)
+    // when its rows are k-contiguous, so compute waits for one panel of each.
+    const bool a0_panels = np > 1 && a_rows;
+    // Panels: edges on multiples of 64 k (16-byte aligned operand offsets).
+    // With the winner's seconds per row, band 0 computes rho times faster
+    // than a k row of B (and of its A) crosses the bus; the first panel is
+    // then rho times thinner than the others (at most 4x), so compute starts
+    // sooner and the second panel still lands before the first is done.
+    std::vector<int64_t> kedge = band_edges(bounds->k0, K, np, 64, false);
+    if (np > 1 && row_seconds > 0.0) {
+        const double rows0 = double(redge[1] - redge[0]);
+        const double comp_k = rows0 * row_seconds / double(K);
+        const double xfer_k =
+            (double(host_ops->b.ld) * es * (bcast ? 1.25 : 1.0) + (a0_panels ? rows0 * es : 0.0)) / 40e9;
+        const double rho = std::min(4.0, comp_k / xfer_k);
+        const int64_t s0 = static_cast<int64_t>(double(K) / np / std::max(1.0, rho)) / 64 * 64;
+        if (s0 >= 64 && s0 < kedge[1] - kedge[0]) {
+            const std::vector<int64_t> rest = band_edges(bounds->k0 + s0, K - s0, np - 1, 64, false);
+            kedge.assign(1, bounds->k0);
+            kedge.insert(kedge.end(), rest.begin(), rest.end());
+        }
+    }
+
+    // device staging, one buffer per operand (same pitch and offsets as the
+    // host's); with the result going straight to the host, R is staged for
+    // band 0's rows only
+    amlt_operands dev = hview;
+    amlt_matrix* dslot[5 + AMLT_MAX_AUX] = {&dev.a, &dev.b, &dev.r, &dev.thres, &dev.dis};
+    for (int q = 0; q + 5 < nslot; ++q) dslot[5 + q] = &dev.aux[q];
+    const int64_t arow = host_ops->a.ld * es, rrow = host_ops->r.ld * es;
+    for (int s = 0; s < nslot; ++s) {
+        if (!hslot[s]->data) continue;
+        size_t need = bytes[s];
+        if (s == 2 && zc) need = std::min(need, size_t(redge[1]) * size_t(rrow));
+        if (!need) {
+            dslot[s]->data = ctx->hbuf[s] ? ctx->hbuf[s] : reinterpret_cast<void*>(uintptr_t(256));
+            continue;
+        }
+        if (need > ctx->hbuf_bytes[s]) {
+            if (ctx->hbuf[s]) cudaFree(ctx->hbuf[s]);
+            ctx->hbuf[s] = nullptr;
+            ctx->hbuf_bytes[s] = 0;
+            cuda_check(cudaMalloc(&ctx->hbuf[s], need), "cudaMalloc(host staging)");
+            ctx->hbuf_bytes[s] = need;
+        }
+        dslot[s]->data = ctx->hbuf[s];
+    }
+    amlt_operands dev_zc = dev;  // bands after the first, R in host memory
+    if (zc) dev_zc.r.data = r_mapped;
+    if (!ctx->copy_in) {
+        cuda_check(cudaStreamCreateWithFlags(&ctx->copy_in, cudaStreamNonBlocking), "cudaStreamCreate");
+        cuda_check(cudaStreamCreateWithFlags(&ctx->copy_out, cudaStreamNonBlocking), "cudaStreamCreate");
     }
 
     // events: [0] start, [1] replicated operands ready, [2..2+nb) band inputs,
-    // [2+nb..2+nb+np) panels ready, [2+nb+np..2+2nb+np) bands done, [last] out
-    const int nev = 3 + 2 * nb + np;
+    // [2+nb..2+nb+np) panels ready, [2+nb+np..2+2nb+np) bands done,
+    // [2+2nb+np..2+2nb+2np) band 0's A panels, [last] out
+    const int nev = 3 + 2 * nb + 2 * np;
     while (static_cast<int>(ctx->pipe_ev.size()) < nev) {
         cudaEvent_t e;
         cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
@@ -1402,8 +1482,8 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
     auto band_in = [&](int b) { return ev[2 + b]; };
     auto panel_ev = [&](int p) { return ev[2 + nb + p]; };
     auto band_done = [&](int b) { return ev[2 + nb + np + b]; };
+    auto a0_ev = [&](int p) { return ev[2 + 2 * nb + np + p]; };
 
-    const int64_t arow = host_ops->a.ld * es, rrow = host_ops->r.ld * es;
     const int64_t brow = host_ops->b.ld * es;  // one k row of B (b_kouter)
     // k rows [k0, k1) of B, relative to the buffer (the bounds' k0 is an offset into it)
     auto b_span = [&](int64_t k0, int64_t k1, size_t* off, size_t* len) {
@@ -1421,27 +1501,46 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
     auto bcast_bytes = [&](void* buf, size_t n) {
         if (n) nccl_check(nccl().bcast(buf, buf, n, kNcclUint8, 0, ctx->comm, ctx->comm_stream), "ncclBroadcast");
     };
+    // band b's A rows (unless they come panel by panel) and R rows (staged
+    // bands only: zeroed, or copied in)
     auto copy_band_in = [&](int b) {
         const int64_t r0 = redge[static_cast<size_t>(b)], r1 = redge[static_cast<size_t>(b) + 1];
+        const bool with_a = !(b == 0 && a0_panels);
+        const bool with_r = !(zc && b > 0);
         if (nb == 1) {
-            h2d(ctx->hbuf[0], host_ops->a.data, bytes[0], ctx->copy_in, "H2D A");
+            if (with_a) h2d(ctx->hbuf[0], host_ops->a.data, bytes[0], ctx->copy_in, "H2D A");
             if (r_zero) cuda_check(cudaMemsetAsync(ctx->hbuf[2], 0, bytes[2], ctx->copy_in), "memset R");
             else h2d(ctx->hbuf[2], host_ops->r.data, bytes[2], ctx->copy_in, "H2D R");
         } else {
-            h2d(static_cast<char*>(ctx->hbuf[0]) + r0 * arow, static_cast<const char*>(host_ops->a.data) + r0 * arow,
-                size_t(r1 - r0) * arow, ctx->copy_in, "H2D A band");
-            if (r_zero)
-                cuda_check(cudaMemsetAsync(static_cast<char*>(ctx->hbuf[2]) + r0 * rrow, 0, size_t(r1 - r0) * rrow,
-                                           ctx->copy_in), "memset R band");
-            else
-                h2d(static_cast<char*>(ctx->hbuf[2]) + r0 * rrow, static_cast<const char*>(host_ops->r.data) + r0 * rrow,
-                    size_t(r1 - r0) * rrow, ctx->copy_in, "H2D R band");
+            if (with_r) {
+                if (r_zero)
+                    cuda_check(cudaMemsetAsync(static_cast<char*>(ctx->hbuf[2]) + r0 * rrow, 0, size_t(r1 - r0) * rrow,
+                                               ctx->copy_in), "memset R band");
+                else
+                    h2d(static_cast<char*>(ctx->hbuf[2]) + r0 * rrow,
+                        static_cast<const char*>(host_ops->r.data) + r0 * rrow, size_t(r1 - r0) * rrow, ctx->copy_in,
+                        "H2D R band");
+            }
+            if (with_a)
+                h2d(static_cast<char*>(ctx->hbuf[0]) + r0 * arow, static_cast<const char*>(host_ops->a.data) + r0 * arow,
+                    size_t(r1 - r0) * arow, ctx->copy_in, "H2D A band");
         }
         cuda_check(cudaEventRecord(band_in(b), ctx->copy_in), "cudaEventRecord");
     };
     auto copy_panel_in = [&](int p) {
+        const int64_t k0 = kedge[static_cast<size_t>(p)], k1 = kedge[static_cast<size_t>(p) + 1];
+        if (a0_panels) {  // band 0's A, k columns [k0, k1)
+            const size_t off = size_t(redge[0]) * size_t(arow) + size_t(k0) * es;
+            if (k1 > k0 && redge[1] > redge[0])
+                cuda_check(cudaMemcpy2DAsync(static_cast<char*>(ctx->hbuf[0]) + off, size_t(arow),
+                                             static_cast<const char*>(host_ops->a.data) + off, size_t(arow),
+                                             size_t(k1 - k0) * es, size_t(redge[1] - redge[0]),
+                                             cudaMemcpyHostToDevice, ctx->copy_in),
+                           "H2D A panel");
+            cuda_check(cudaEventRecord(a0_ev(p), ctx->copy_in), "cudaEventRecord");
+        }
         size_t off, len;
-        b_span(kedge[static_cast<size_t>(p)], kedge[static_cast<size_t>(p) + 1], &off, &len);
+        b_span(k0, k1, &off, &len);
         if (root) h2d(static_cast<char*>(ctx->hbuf[1]) + off, static_cast<const char*>(host_ops->b.data) + off, len,
                       ctx->copy_in, "H2D B panel");
         if (bcast) {
@@ -1495,19 +1594,22 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
             cuda_check(cudaEventRecord(small_ev, ctx->comm_stream), "cudaEventRecord");
         }
         cuda_check(cudaStreamWaitEvent(ctx->stream, small_ev, 0), "cudaStreamWaitEvent");
-        // inputs: A band 0, the B panels (band 0 consumes them as they land),
-        // then the other A bands
+        // inputs: band 0 (R, and A unless it comes with the panels), the B
+        // panels (band 0 consumes them as they land), then the other A bands
         copy_band_in(0);
-        mark("A band 0 in", ctx->copy_in);
+        mark("band 0 in", ctx->copy_in);
         copy_panel_in(0);
-        mark("B panel 0 in", bcast ? ctx->comm_stream : ctx->copy_in);
+        mark("panel 0 in", bcast ? ctx->comm_stream : ctx->copy_in);
         for (int p = 1; p < np; ++p) copy_panel_in(p);
-        mark("B panels in", bcast ? ctx->comm_stream : ctx->copy_in);
+        mark("panels in", bcast ? ctx->comm_stream : ctx->copy_in);
         for (int b = 1; b < nb; ++b) copy_band_in(b);
-        mark("A bands in", ctx->copy_in);
+        mark("bands in", ctx->copy_in);
         if (tune_now) {
             for (int b = 0; b < nb; ++b) cuda_check(cudaStreamWaitEvent(ctx->stream, band_in(b), 0), "cudaStreamWaitEvent");
-            for (int p = 0; p < np; ++p) cuda_check(cudaStreamWaitEvent(ctx->stream, panel_ev(p), 0), "cudaStreamWaitEvent");
+            for (int p = 0; p < np; ++p) {
+                cuda_check(cudaStreamWaitEvent(ctx->stream, panel_ev(p), 0), "cudaStreamWaitEvent");
+                if (a0_panels) cuda_check(cudaStreamWaitEvent(ctx->stream, a0_ev(p), 0), "cudaStreamWaitEvent");
+            }
             adaptive(ctx, plan, &dev, *bounds, clock, clock_user, nullptr, rep);
             cuda_check(cudaEventRecord(band_done(0), ctx->stream), "cudaEventRecord");
             cuda_check(cudaStreamWaitEvent(ctx->copy_out, band_done(0), 0), "cudaStreamWaitEvent");
@@ -1519,6 +1621,8 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
                 // band 0 panel by panel as B lands; the others whole K
                 const int parts = b == 0 ? np : 1;
                 amlt_bounds bb{};
+                KParams whole_k{};  // band 0's preparation of B, as one whole-K preparation
+                const VariantDesc* prepped = nullptr;
                 for (int p = 0; p < parts; ++p) {
                     bb = band_bounds(b, p);
                     if (b > 0) {
@@ -1526,29 +1630,48 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
                         bb.k1 = bounds->k1;
                     } else {
                         cuda_check(cudaStreamWaitEvent(ctx->stream, panel_ev(p), 0), "cudaStreamWaitEvent");
+                        if (a0_panels) cuda_check(cudaStreamWaitEvent(ctx->stream, a0_ev(p), 0), "cudaStreamWaitEvent");
                     }
                     if (b == 0 && p == 0) mark("compute begins", ctx->stream);
-                    Resolved rv = resolve(plan, &dev, &bb);
+                    const bool to_host = zc && b > 0;
+                    Resolved rv = resolve(plan, to_host ? &dev_zc : &dev, &bb);
+                    if (to_host) rv.kp.r_zero = r_zero ? 1 : 0;
                     Dispatch dp = plan_dispatch(ctx, plan, &tp, rv);
+                    const VariantDesc& v = vdesc(dp.variant);
+                    if (b == 0 && np > 1 && d.accumulate && v.run && v.prep_b && v.prep_panels && !rv.packed() &&
+                        rv.M > 0 && rv.N > 0 && rv.K > 0) {
+                        // B prepared panel by panel into one whole-K
+                        // preparation, which the later bands reuse as is
+                        rv.kp.plane_k0 = bb.k0 - bounds->k0;
+                        rv.kp.plane_kdim = K;
+                        ensure_tc_ws(ctx, v, rv.kp);
+                        cuda_check(v.prep_b(rv.kp, ctx->tc_ws, ctx->stream), "B preparation (panel)");
+                        bprep_mark(ctx, v, rv.kp);
+                        if (p == 0) {
+                            whole_k = rv.kp;
+                            whole_k.K = K;
+                            prepped = &v;
+                        }
+                    }
                     enqueue(ctx, plan, rv, dp);
                 }
+                if (prepped) bprep_mark(ctx, *prepped, whole_k);
                 if (b == 0)  // (every panel has landed once band 0 is done)
                     for (int p = 0; p < np; ++p)
                         cuda_check(cudaStreamWaitEvent(ctx->stream, panel_ev(p), 0), "cudaStreamWaitEvent");
                 mark("band " + std::to_string(b) + " computed", ctx->stream);
-                {
-                    cuda_check(cudaEventRecord(band_done(b), ctx->stream), "cudaEventRecord");
-                    cuda_check(cudaStreamWaitEvent(ctx->copy_out, band_done(b), 0), "cudaStreamWaitEvent");
-                    const int64_t r0 = bb.i0, r1 = bb.i1;
-                    if (nb == 1)
-                        cuda_check(cudaMemcpyAsync(host_ops->r.data, ctx->hbuf[2], bytes[2], cudaMemcpyDeviceToHost,
-                                                   ctx->copy_out), "D2H R");
-                    else
-                        cuda_check(cudaMemcpyAsync(static_cast<char*>(host_ops->r.data) + r0 * rrow,
-                                                   static_cast<const char*>(ctx->hbuf[2]) + r0 * rrow,
-                                                   size_t(r1 - r0) * rrow, cudaMemcpyDeviceToHost, ctx->copy_out),
-                                   "D2H R band");
-                }
+                cuda_check(cudaEventRecord(band_done(b), ctx->stream), "cudaEventRecord");
+                if (zc && b > 0) continue;  // its rows are in host memory already
+                cuda_check(cudaStreamWaitEvent(ctx->copy_out, band_done(b), 0), "cudaStreamWaitEvent");
+                const int64_t r0 = bb.i0, r1 = bb.i1;
+                if (nb == 1)
+                    cuda_check(cudaMemcpyAsync(host_ops->r.data, ctx->hbuf[2], bytes[2], cudaMemcpyDeviceToHost,
+                                               ctx->copy_out), "D2H R");
+                else
+                    cuda_check(cudaMemcpyAsync(static_cast<char*>(host_ops->r.data) + r0 * rrow,
+                                               static_cast<const char*>(ctx->hbuf[2]) + r0 * rrow,
+                                               size_t(r1 - r0) * rrow, cudaMemcpyDeviceToHost, ctx->copy_out),
+                               "D2H R band");
             }
         }
         mark("R out", ctx->copy_out);
@@ -1584,14 +1707,25 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
     }
     if (trace && !marks.empty()) {
         cuda_check(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
-        std::fprintf(stderr, "[amlt host pipeline] nb=%d np=%d M=%lld N=%lld K=%lld bcast=%d\n", nb, np,
-                     (long long)M, (long long)N, (long long)K, bcast ? 1 : 0);
+        std::fprintf(stderr, "[amlt host pipeline] nb=%d np=%d M=%lld N=%lld K=%lld bcast=%d zero-copy R=%d "
+                             "rows0=%lld k-panel0=%lld\n", nb, np, (long long)M, (long long)N, (long long)K,
+                     bcast ? 1 : 0, zc ? 1 : 0, (long long)(redge[1] - redge[0]), (long long)(kedge[1] - kedge[0]));
         for (auto& m : marks) {
             float ms = 0;
             cudaEventElapsedTime(&ms, marks.front().second, m.second);
             std::fprintf(stderr, "[amlt host pipeline]   %8.2f ms  %s\n", ms, m.first.c_str());
         }
         for (auto& m : marks) cudaEventDestroy(m.second);
+    }
+    {
+        int64_t* L = ctx->host_layout;
+        L[0] = nb;
+        L[1] = np;
+        L[2] = zc ? 1 : 0;
+        L[3] = redge[1] - redge[0];
+        L[4] = kedge[1] - kedge[0];
+        L[5] = bcast ? 1 : 0;
+        L[6] = tune_now ? 1 : 0;
     }
     if (rep && !tune_now) {
         std::memset(rep, 0, sizeof(*rep));
@@ -2114,6 +2248,12 @@ amlt_status amlt_gpu_comm_detach(amlt_ctx* ctx) {
 }
 
 int amlt_gpu_comm_size(const amlt_ctx* ctx) { return ctx ? ctx->comm_size : 0; }
+
+amlt_status amlt_gpu_last_host_layout(const amlt_ctx* ctx, int64_t* out) {
+    if (!ctx || !out) return AMLT_ERR_INVALID_ARGUMENT;
+    std::memcpy(out, ctx->host_layout, sizeof(ctx->host_layout));
+    return AMLT_OK;
+}
 
 // ---------------------------------------------------------------------------
 // device matrices for callers without their own allocator (SURVEY §8b

@@ -141,13 +141,13 @@ __global__ void __launch_bounds__(32 * WARPS_M * WARPS_N, MINB) dmma_gemm_kernel
             } else {
                 double* dst = Rg + gi * p.ldr + gj;
                 if (p.r_vec_ok && gj + 2 <= p.N) {
-                    double2 o = *reinterpret_cast<const double2*>(dst);
+                    double2 o = p.r_zero ? make_double2(0.0, 0.0) : *reinterpret_cast<const double2*>(dst);
                     o.x += acc[a][b][0];
                     o.y += acc[a][b][1];
                     *reinterpret_cast<double2*>(dst) = o;
                 } else {
-                    if (gj < p.N) dst[0] += acc[a][b][0];
-                    if (gj + 1 < p.N) dst[1] += acc[a][b][1];
+                    if (gj < p.N) dst[0] = (p.r_zero ? 0.0 : dst[0]) + acc[a][b][0];
+                    if (gj + 1 < p.N) dst[1] = (p.r_zero ? 0.0 : dst[1]) + acc[a][b][1];
                 }
             }
         }
@@ -180,6 +180,7 @@ void add_dmma(Registry& reg, const char* name) {
     v.minb = MINB;
     v.vec = true;
     v.tc = true;
+    v.r_overwrite = true;
     v.name = name;
     v.func = reinterpret_cast<const void*>(&dmma_gemm_kernel<WTM, WTN, WARPS_M, WARPS_N, BK, STAGES, MINB>);
     v.launch = &launch_dmma<WTM, WTN, WARPS_M, WARPS_N, BK, STAGES, MINB>;

@@ -384,6 +384,7 @@ const JitBody& jit_body(const RecognizedTask& rt, int dtype, bool load) {
             v.minb = minb_of(sh, tout);
             v.vec = (sh.load & kTma) != 0;
             v.tout = tout;
+            v.r_overwrite = true;  // the tile kernel, compiled by NVRTC
             C.names.push_back(std::string(sh.name) + (tout ? "_ti" : ""));
             v.name = C.names.back().c_str();
             v.func = nullptr;

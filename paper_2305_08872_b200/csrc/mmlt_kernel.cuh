@@ -81,6 +81,14 @@ struct KParams {
     // Guarded variants (theta-form discount and its fallback): operand range
     // statistics the kernels read to decide which of the two runs.
     const int* guard;
+    // R starts at zero: the epilogue writes 0 + value and never reads R (a
+    // result written straight to mapped host memory needs no memset there)
+    int32_t r_zero;
+    // Variants with a prepared copy of B (VariantDesc::prep_panels): this
+    // launch's k rows start at row plane_k0 of a preparation plane_kdim rows
+    // deep (0: the preparation is exactly this launch's K range).
+    int64_t plane_k0;
+    int64_t plane_kdim;
 };
 
 // --------------------------------------------------------------------------
@@ -912,7 +920,14 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
             } else {
                 T* dst = Rg + gi * p.ldr + gj0;
                 if (p.r_vec_ok && gj0 + VN <= p.N) {
-                    Vec o = *reinterpret_cast<const Vec*>(dst);
+                    Vec o;
+                    if (p.r_zero) {
+                        T* op = reinterpret_cast<T*>(&o);
+#pragma unroll
+                        for (int e = 0; e < VN; ++e) op[e] = T(0);
+                    } else {
+                        o = *reinterpret_cast<const Vec*>(dst);
+                    }
                     T* op = reinterpret_cast<T*>(&o);
 #pragma unroll
                     for (int e = 0; e < VN; ++e) op[e] = op[e] + val[e];
@@ -920,7 +935,7 @@ __global__ void __launch_bounds__(32 * WR * WC, MINB)
                 } else {
 #pragma unroll
                     for (int e = 0; e < VN; ++e)
-                        if (gj0 + e < p.N) dst[e] = dst[e] + val[e];
+                        if (gj0 + e < p.N) dst[e] = (p.r_zero ? T(0) : dst[e]) + val[e];
                 }
             }
         }
@@ -941,7 +956,7 @@ __global__ void mmlt_splitk_reduce(const KParams p) {
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t i = idx / p.N;
         const int64_t j = idx - i * p.N;
-        T v = R[i * p.ldr + j];
+        T v = p.r_zero ? T(0) : R[i * p.ldr + j];
         for (int s = 0; s < p.splits; ++s) v = v + W[static_cast<int64_t>(s) * total + idx];
         R[i * p.ldr + j] = v;
     }

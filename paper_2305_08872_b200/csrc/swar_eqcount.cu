@@ -314,6 +314,7 @@ void add_swar(Registry& reg, const char* name) {
     v.launch = &sw::no_tile_launch;
     v.ws_bytes = &sw::ws_bytes;
     v.run = &sw::run<TM, TN, WR, WC, BK, ST, MINB>;
+    v.r_overwrite = true;  // packed and fallback launches are both the tile kernel
     v.prep_b = &sw::prep_b;
     v.prep_id = 6;  // 7-bit byte-packed B
     reg.variants.push_back(v);

@@ -154,8 +154,11 @@ __device__ __forceinline__ void block_max(int (&v)[NS], int* g, int first) {
     }
 }
 
-// Planes (theta, x0, x1), each K x npad doubles, plus the B-side statistics.
-__global__ void __launch_bounds__(256) prep_kernel(const KParams p, double* planes, int64_t npad, int* g) {
+// Planes (theta, x0, x1), each kdim x npad doubles, plus the B-side
+// statistics; this launch fills rows [plane_k0, plane_k0 + K) (planes points
+// at row plane_k0 of the first plane).
+__global__ void __launch_bounds__(256) prep_kernel(const KParams p, double* planes, int64_t npad, int64_t pstride,
+                                                   int* g) {
     const double* B = static_cast<const double*>(p.B);
     const double* T = static_cast<const double*>(p.thres);
     const double* D = static_cast<const double*>(p.dis);
@@ -198,8 +201,8 @@ __global__ void __launch_bounds__(256) prep_kernel(const KParams p, double* plan
             }
         }
         planes[idx] = theta;
-        planes[plane + idx] = x0;
-        planes[2 * plane + idx] = x1;
+        planes[pstride + idx] = x0;
+        planes[2 * pstride + idx] = x1;
     }
     block_max<5>(st, g, G_BAD);
 }
@@ -224,16 +227,27 @@ __global__ void __launch_bounds__(256) a_stats_kernel(const KParams p, int* g) {
 
 int64_t npad_of(int64_t N) { return (N + 1) / 2 * 2; }  // 16-byte plane rows (TMA)
 
-size_t ws_bytes(const KParams& p) { return HEADER + size_t(3) * size_t(p.K) * size_t(npad_of(p.N)) * 8; }
+// K rows of the preparation (panel-wise preparations: the whole K range)
+int64_t kdim_of(const KParams& p) { return p.plane_kdim > 0 ? p.plane_kdim : p.K; }
 
+size_t ws_bytes(const KParams& p) { return HEADER + size_t(3) * size_t(kdim_of(p)) * size_t(npad_of(p.N)) * 8; }
+
+// B planes of k rows [plane_k0, plane_k0 + K). The statistics restart with
+// the first panel (plane_k0 == 0) and accumulate over the later ones: a
+// launch on panel p checks ranges over panels 0..p, a superset of its own.
 cudaError_t prep_b(const KParams& p, void* ws, cudaStream_t s) {
     int* g = static_cast<int*>(ws);
-    cudaError_t e = cudaMemsetAsync(g, 0, G_AMAX * sizeof(int), s);
-    if (e != cudaSuccess) return e;
+    if (p.plane_k0 + p.K > kdim_of(p)) return cudaErrorInvalidValue;
+    if (p.plane_k0 == 0) {
+        const cudaError_t e = cudaMemsetAsync(g, 0, G_AMAX * sizeof(int), s);
+        if (e != cudaSuccess) return e;
+    }
     const int64_t npad = npad_of(p.N);
     const int64_t total = p.K * npad;
+    const int64_t pstride = kdim_of(p) * npad;
     const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-    prep_kernel<<<blocks, 256, 0, s>>>(p, reinterpret_cast<double*>(static_cast<char*>(ws) + HEADER), npad, g);
+    prep_kernel<<<blocks, 256, 0, s>>>(
+        p, reinterpret_cast<double*>(static_cast<char*>(ws) + HEADER) + p.plane_k0 * npad, npad, pstride, g);
     return cudaGetLastError();
 }
 
@@ -283,8 +297,8 @@ template <class Body, int TM, int TN, int WR, int WC, int BK, int ST, int MINB, 
 cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
     using Cfg = MmltTile<Body, double, TM, TN, WR, WC, BK, ST, LOAD, MINB>;
     int* g = static_cast<int*>(ws);
-    const double* planes = reinterpret_cast<const double*>(static_cast<char*>(ws) + HEADER);
     const int64_t npad = npad_of(p.N);
+    const double* planes = reinterpret_cast<const double*>(static_cast<char*>(ws) + HEADER) + p.plane_k0 * npad;
     cudaError_t e;
     if (!b_ready && (e = prep_b(p, ws, s)) != cudaSuccess) return e;
     if ((e = cudaMemsetAsync(g + G_AMAX, 0, 2 * sizeof(int), s)) != cudaSuccess) return e;
@@ -301,7 +315,7 @@ cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
         const cuuint64_t as[1] = {cuuint64_t(p.lda) * 8};
         const cuuint32_t ab[2] = {cuuint32_t(BK), cuuint32_t(Cfg::BM)};
         const cuuint64_t bd[3] = {cuuint64_t(p.N), cuuint64_t(p.K), 3};
-        const cuuint64_t bs[2] = {cuuint64_t(npad) * 8, cuuint64_t(p.K) * cuuint64_t(npad) * 8};
+        const cuuint64_t bs[2] = {cuuint64_t(npad) * 8, cuuint64_t(kdim_of(p)) * cuuint64_t(npad) * 8};
         const cuuint32_t bb[3] = {cuuint32_t(Cfg::BN), cuuint32_t(BK), 3};
         if (!encode(&ma, p.A, 2, ad, as, ab, Cfg::SWZ) || !encode(&mb, planes, 3, bd, bs, bb))
             return cudaErrorInvalidValue;
@@ -378,6 +392,8 @@ void add_theta(Registry& reg, const char* name) {
     v.prep_b = &th::prep_b;
     v.prep_id = 3;  // (theta, x0, x1) planes of B, shared by every theta tile
     v.splittable = true;
+    v.prep_panels = true;
+    v.r_overwrite = true;  // the tile kernel's epilogue (theta and fallback)
     reg.variants.push_back(v);
 }
 

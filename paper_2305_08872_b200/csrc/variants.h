@@ -49,6 +49,12 @@ struct VariantDesc {
     // run() variants that accept K segments (KParams splits / kslice / work,
     // partials reduced in segment order afterwards like the tile variants)
     bool splittable = false;
+    // the epilogue honours KParams::r_zero and stores R with plain global
+    // loads / stores (R may be mapped host memory)
+    bool r_overwrite = false;
+    // prep_b / run honour KParams::plane_k0 / plane_kdim: B can be prepared
+    // K panel by K panel into one whole-K preparation as the panels land
+    bool prep_panels = false;
 };
 
 // Per (body, dtype) helpers that are not tile variants.
@@ -143,6 +149,7 @@ void add_variant(Registry& reg, int body, int dtype, const char* name) {
         v.minb = MINB;
         v.vec = (LOAD & LOAD_TMA) != 0;
         v.tout = (LOAD & LOAD_TOUT) != 0;
+        v.r_overwrite = true;
         v.name = name;
         v.func = reinterpret_cast<const void*>(
             &mmlt_tile_kernel<Body, T, TM, TN, WR, WC, BK, STAGES, LOAD, MINB>);

@@ -389,6 +389,14 @@ class Context:
     def comm_size(self) -> int:
         return int(self._lib.amlt_gpu_comm_size(self.handle))
 
+    def last_host_layout(self) -> dict:
+        """How the last run_host / run_host_adaptive call on this context ran
+        (amlt_gpu_last_host_layout)."""
+        out = (C.c_int64 * N.HOST_LAYOUT_FIELDS)()
+        _raise(self._lib.amlt_gpu_last_host_layout(self.handle, out), self.handle)
+        keys = ("bands", "k_panels", "zero_copy_r", "band0_rows", "k_panel0", "bcast", "tuned")
+        return {k: int(v) for k, v in zip(keys, out)}
+
     def set_stream(self, stream) -> None:
         """Launch on a torch.cuda.Stream (or raw cudaStream_t int); None
         restores the context's own stream."""

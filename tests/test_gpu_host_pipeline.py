@@ -154,6 +154,99 @@ def test_broadcast_path_on_a_one_rank_communicator(small_panels, body):
         ctx.close()
 
 
+def _pinned(x):
+    """A page-locked (cudaHostAlloc, device-mapped) copy of a numpy array."""
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+
+
+@pytest.mark.parametrize("body", ["discount", "gemm", "boost", "eqcount", "sqdiff"])
+@pytest.mark.parametrize("r_zero", [False, True])
+def test_zero_copy_result_bit_exact(gpu_ctx, small_panels, body, r_zero):
+    """R in pinned host memory: the rows after band 0 run as one launch whose
+    epilogue stores R straight into host memory (and reads R's prior values
+    from there without R_ZERO); band 0 goes through the staged panels.
+    Bit-exact against the oracle, and the trace shows the zero-copy layout."""
+    import paper_2305_08872_b200 as P
+    from tests.helpers import NP_DT
+
+    dtype = {"eqcount": "i32", "sqdiff": "f32"}.get(body, "f64")
+    npd = NP_DT[dtype]
+    M, K, N = 1300, 1000, 300
+    A, B, t, d = make_inputs(body, M, K, N, "int", seed=91)
+    rng = np.random.default_rng(92)
+    R0 = np.zeros((M, N)) if r_zero else rng.integers(-8, 9, (M, N)).astype(np.float64)
+    want = oracle(body, A, B, t, d, R0=R0)
+    R = _pinned(R0.astype(npd))
+    ops = P.Operands(_pinned(A.astype(npd)), _pinned(B.astype(npd)), R,
+                     None if t is None else t.astype(npd), None if d is None else d.astype(npd))
+    plan = gpu_ctx.plan(body, dtype)
+    P.run_host(plan, ops, P.Bounds(0, M, 0, N, 0, K), r_zero=r_zero)
+    lay = gpu_ctx.last_host_layout()
+    assert lay["zero_copy_r"] == 1 and lay["bands"] == 2 and lay["k_panels"] > 1, lay
+    check(body, dtype, R.numpy().astype(np.float64), want, exact=True, what=f"zero-copy {body} r_zero={r_zero}")
+
+
+def test_zero_copy_sub_rectangle_and_tuned_theta(gpu_ctx, small_panels):
+    """Zero-copy R with a bounds sub-rectangle (k0, j0 > 0, a row range): R
+    outside the bounds, in host memory, is never touched. Then the tuned
+    path: run_host_adaptive tunes (staged, whole task), the second call runs
+    the cached winner (theta form forced through TileParams too) with B
+    prepared panel by panel into one whole-K preparation."""
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 1400, 1100, 260
+    A, B, t, d = make_inputs("discount", M, K, N, "int", seed=93)
+    R0 = np.random.default_rng(94).integers(-8, 9, (M, N)).astype(np.float64)
+    b = (40, 1350, 6, 250, 64, 1090)
+    want = oracle("discount", A, B, t, d, R0=R0, bounds=b)
+    plan = gpu_ctx.plan("discount", "f64")
+    R = _pinned(R0)
+    P.run_host(plan, P.Operands(A, B, R, t, d), P.Bounds(*b))
+    assert gpu_ctx.last_host_layout()["zero_copy_r"] == 1
+    check("discount", "f64", R.numpy(), want, exact=True, what="zero-copy sub-rectangle")
+
+    theta = next(i for i, v in enumerate(plan.variants()) if "_theta_" in v.name)
+    want0 = oracle("discount", A, B, t, d)
+    R = _pinned(np.zeros((M, N)))
+    P.run_host(plan, P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K), params=P.TileParams(variant=theta),
+               r_zero=True)
+    assert gpu_ctx.last_host_layout()["zero_copy_r"] == 1
+    check("discount", "f64", R.numpy(), want0, exact=True, what="zero-copy theta")
+    gpu_ctx.clear_tuning_cache()
+    for it in range(2):
+        R = _pinned(np.zeros((M, N)))
+        rep = P.run_host_adaptive(plan, P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K), r_zero=True)
+        check("discount", "f64", R.numpy(), want0, exact=True, what=f"run_host_adaptive zero-copy call {it}")
+        assert rep.from_cache == (it == 1)
+        lay = gpu_ctx.last_host_layout()
+        # (a split-K winner keeps the staged pipeline: zero-copy needs one whole-K launch)
+        zc = 0 if it == 0 else int(rep.best_kc == K)
+        assert (lay["tuned"], lay["zero_copy_r"]) == (int(it == 0), zc), (lay, rep.best_kc)
+
+
+def test_pageable_or_disabled_zero_copy_stays_staged(gpu_ctx, small_panels, monkeypatch):
+    """Pageable R (numpy) and AMLT_HOST_NO_ZEROCOPY=1 keep the staged
+    pipeline (R bands copied out); same results."""
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 1300, 700, 200
+    A, B, t, d = make_inputs("discount", M, K, N, "int", seed=95)
+    want = oracle("discount", A, B, t, d)
+    plan = gpu_ctx.plan("discount", "f64")
+    R = np.zeros((M, N))
+    P.run_host(plan, P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K), r_zero=True)
+    lay = gpu_ctx.last_host_layout()
+    assert lay["zero_copy_r"] == 0 and lay["k_panels"] > 1, lay
+    check("discount", "f64", R, want, exact=True, what="pageable R")
+    monkeypatch.setenv("AMLT_HOST_NO_ZEROCOPY", "1")
+    Rp = _pinned(np.zeros((M, N)))
+    P.run_host(plan, P.Operands(A, B, Rp, t, d), P.Bounds(0, M, 0, N, 0, K), r_zero=True)
+    assert gpu_ctx.last_host_layout()["zero_copy_r"] == 0
+    check("discount", "f64", Rp.numpy(), want, exact=True, what="zero-copy disabled")
+
+
 def _shard_rows(M, n):
     """First and last row of every device's band (64-row edges, as the group cuts)."""
     edges = [min(M, (M * d // n + 32) // 64 * 64) for d in range(n)] + [M]
@@ -249,6 +342,8 @@ def test_random_pipeline_cases_bit_exact(gpu_ctx, small_panels, case):
     Ab = np.ascontiguousarray(A.T if at else A).astype(npd)
     Bb = (np.asfortranarray(B) if bcm else np.ascontiguousarray(B)).astype(npd)
     R = R0.astype(npd).copy()
+    if case % 2 == 1:  # pinned R: the zero-copy result path where it applies
+        R = _pinned(R)
     plan = gpu_ctx.plan(body, dtype, layout_a=int(at))
     ops = P.Operands(Ab, Bb, R, None if t is None else t.astype(npd), None if d is None else d.astype(npd))
     if case % 3 == 0:
@@ -256,7 +351,7 @@ def test_random_pipeline_cases_bit_exact(gpu_ctx, small_panels, case):
         P.run_host_adaptive(plan, ops, P.Bounds(*b), r_zero=r_zero)
     else:
         P.run_host(plan, ops, P.Bounds(*b), r_zero=r_zero)
-    got = R.astype(np.float64)
+    got = (R if isinstance(R, np.ndarray) else R.numpy()).astype(np.float64)
     bad = np.argwhere(got != want)
     assert bad.size == 0, (f"case {case}: {body}/{dtype} {M}x{K}x{N} bounds {b} at={at} bcm={bcm} "
                            f"r_zero={r_zero}: {len(bad)} mismatches, first {tuple(bad[0])} got "
