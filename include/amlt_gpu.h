@@ -428,16 +428,24 @@ amlt_status amlt_gpu_adaptive_execute_amulet(amlt_ctx* ctx, const amlt_plan* pla
 /* Host-buffer entry (the reference's callers hold host MatrixBuffers:
  * run_fixed / run_adaptive, src/engine.cpp:165-175): operands' `data` are
  * HOST pointers (pinned for full copy bandwidth). A copy / compute pipeline:
- * A (and R, unless AMLT_HOST_R_ZERO) in row bands and B in K panels go H2D on
- * a copy stream; compute starts once the first band and the first panel
- * are resident and runs panel by panel over the bands (the kernels
- * accumulate into R); each R band goes back D2H on a second copy stream as
- * soon as its last panel is done. B is cut into K panels when its k rows are
- * contiguous (B[k][j] row-major, B[j][k] col-major), the winner is not
- * split-K and the statement accumulates. The tile: `tile` if given, else the
- * winner cached by an earlier tuning of the same shape, else the planner
- * default. *elapsed_s covers all copies and compute (the clock, if any, is
- * read exactly twice around all of it). */
+ * B in K panels and A in row bands go H2D on a copy stream; the first row
+ * band is computed panel by panel as B lands (band 0's A arrives with each
+ * panel), its R zero-filled (AMLT_HOST_R_ZERO) or copied in on the device and
+ * copied back D2H when done. The other rows:
+ *  - R in pinned, device-mapped host memory (cudaHostAlloc / cudaHostRegister)
+ *    and a winner whose epilogue allows it: launches whose epilogue writes R
+ *    straight into the host buffer (zero-copy; prior values read from there
+ *    unless AMLT_HOST_R_ZERO), one launch for all these rows unless the A
+ *    copies dominate (then a few row bands). R outside the bounds is never
+ *    touched.
+ *  - otherwise: whole-K row bands, each R band D2H on a second copy stream as
+ *    soon as it is done (R bands zero-filled or copied in like band 0).
+ * B is cut into K panels when its k rows are contiguous (B[k][j] row-major,
+ * B[j][k] col-major), the winner is not split-K and the statement
+ * accumulates. The tile: `tile` if given, else the winner cached by an
+ * earlier tuning of the same shape, else the planner default. *elapsed_s
+ * covers all copies and compute (the clock, if any, is read exactly twice
+ * around all of it). amlt_gpu_last_host_layout reports the layout used. */
 amlt_status amlt_gpu_run_host(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* host_ops,
                               const amlt_tile_params* tile, const amlt_bounds* bounds, int flags,
                               amlt_clock_fn clock, void* clock_user, double* elapsed_s);

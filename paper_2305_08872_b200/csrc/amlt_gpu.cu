@@ -1321,12 +1321,11 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
     // PCIe (and, without R_ZERO, reads it from there): each R element crosses
     // the bus once, as the D2H copy would have, with no copy-out stage, no
     // staging buffer and no band boundaries after band 0. Needs a variant
-    // whose epilogue does plain global stores and honours KParams::r_zero,
-    // whole-K launches, and no packing of R. AMLT_HOST_NO_ZEROCOPY=1 keeps
-    // the staged pipeline (diagnostics).
+    // whose epilogue (and split-K reduce) does plain global stores and
+    // honours KParams::r_zero, whole-K launches, and no packing of R.
+    // AMLT_HOST_NO_ZEROCOPY=1 keeps the staged pipeline (diagnostics).
     void* r_mapped = nullptr;
-    if (banded && d.accumulate && vi >= 0 && vdesc(vi).r_overwrite && !split_winner &&
-        !std::getenv("AMLT_HOST_NO_ZEROCOPY")) {
+    if (banded && d.accumulate && vi >= 0 && vdesc(vi).r_overwrite && !std::getenv("AMLT_HOST_NO_ZEROCOPY")) {
         cudaPointerAttributes at{};
         if (cudaPointerGetAttributes(&at, host_ops->r.data) == cudaSuccess) {
             if (at.type == cudaMemoryTypeHost && at.devicePointer) r_mapped = at.devicePointer;
@@ -1337,11 +1336,11 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
 
     // (the panel count depends only on what every rank of a broadcast shares,
     // so all ranks issue the same sequence of collectives)
-    // Panels of at least 256 MiB of B (AMLT_HOST_PANEL_BYTES overrides; tests
+    // Panels of at least 4 MiB of B (AMLT_HOST_PANEL_BYTES overrides; tests
     // use it to cut small tasks) and 256 k, at most 8.
     int np = 1;
     if (b_kouter && d.accumulate) {
-        double panel_bytes = double(256 << 20);
+        double panel_bytes = double(4 << 20);
         if (const char* e = std::getenv("AMLT_HOST_PANEL_BYTES")) panel_bytes = std::max(1.0, std::atof(e));
         const double b_bytes = double(K) * double(host_ops->b.ld) * es;
         np = static_cast<int>(std::max(1.0, std::min({8.0, std::floor(b_bytes / panel_bytes),
@@ -1358,56 +1357,70 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
     std::vector<int64_t> redge;
     auto layout = [&](bool zero_copy) {
         nb = banded ? static_cast<int>(std::min<int64_t>(8, M / 256)) : 1;
-        if (nb > 1 && zero_copy) {
-            nb = 2;  // band 0 (as B lands), then every other row in one launch
-        } else if (nb > 1) {
-            // Band count: every band boundary drains the GPU (up to a wave of
-            // CTAs idles), while more bands hide more of the A / R transfers.
-            // With the winner's measured seconds per row, minimise boundaries
-            // x wave time + exposed copy (~ copy time / bands): nb = sqrt(copy
-            // x waves / compute); without it, as many bands as full waves
-            // allow. At most 8, at least one wave each (split-K multiplies CTAs).
-            const VariantDesc& v = vdesc(vi);
-            const int64_t splits = ((!v.run || v.splittable) && split_winner) ? (K + tp.kc - 1) / tp.kc : 1;
-            const int64_t slots = int64_t(ctx->num_sms) * occ_of(ctx, vi);
-            const int64_t fill = ctas_for(v, M, N) * splits / std::max<int64_t>(1, slots);
-            int64_t want = fill;
-            if (row_seconds > 0.0) {
-                const double copy_s = (double(bytes[0]) + double(bytes[2]) * (r_zero ? 1.0 : 2.0)) / 40e9;
-                const double compute_s = row_seconds * double(M);
-                want = static_cast<int64_t>(
-                    std::lround(std::sqrt(copy_s * double(std::max<int64_t>(fill, 1)) / compute_s)));
-            }
-            nb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({int64_t(nb), fill, want})));
-        }
         redge.clear();
         if (nb == 1) {
             redge = {bounds->i0, bounds->i1};
             return;
         }
-        int64_t rows0 = M / nb;
-        if (np > 1 && row_seconds > 0.0) {
-            const double b_bytes = double(K) * double(host_ops->b.ld) * es;
-            const double t_b = b_bytes / 40e9 * (bcast ? 1.25 : 1.0);
-            rows0 = static_cast<int64_t>(std::ceil(1.3 * t_b / row_seconds));
+        const double t_b = double(K) * double(host_ops->b.ld) * es / 40e9 * (bcast ? 1.25 : 1.0);
+        const double t_a = double(bytes[0]) / 40e9;
+        // band 0's rows: with a measured rate, tall enough that its compute
+        // covers B's transfer (K panels) or, zero-copy, B's and all of A's
+        // (the later rows then never wait); between M/8 and M/2
+        auto rows0_of = [&](int bands) {
+            int64_t r = M / bands;
+            if (row_seconds > 0.0 && (zero_copy || np > 1))
+                r = static_cast<int64_t>(std::ceil(1.3 * (t_b + (zero_copy ? t_a : 0.0)) / row_seconds));
+            r = std::min<int64_t>(std::max<int64_t>(r, M / 8), M / 2) / 64 * 64;
+            return std::max<int64_t>(r, std::min<int64_t>(M, 64));
+        };
+        {
+            // Band count: every band boundary drains the GPU (up to a wave of
+            // CTAs idles), while more bands hide more of the A / R transfers.
+            // With the winner's measured seconds per row, minimise boundaries
+            // x wave time + exposed copy (~ copy time / bands): nb = sqrt(copy
+            // x waves / compute); without it, as many bands as full waves
+            // allow. At most 8, at least one wave each (split-K multiplies
+            // CTAs). Zero-copy: only A is copied; when band 0's compute covers
+            // every copy, or without a measured rate, the other rows run as
+            // one launch (at least 2 bands: band 0 is staged).
+            const VariantDesc& v = vdesc(vi);
+            const int64_t splits = ((!v.run || v.splittable) && split_winner) ? (K + tp.kc - 1) / tp.kc : 1;
+            const int64_t slots = int64_t(ctx->num_sms) * occ_of(ctx, vi);
+            const int64_t fill = ctas_for(v, M, N) * splits / std::max<int64_t>(1, slots);
+            int64_t want = zero_copy ? 2 : fill;
+            if (row_seconds > 0.0) {
+                const double compute_s = row_seconds * double(M);
+                const double copy_s = zero_copy ? t_a : (double(bytes[0]) + double(bytes[2]) * (r_zero ? 1.0 : 2.0)) / 40e9;
+                want = static_cast<int64_t>(std::lround(std::sqrt(copy_s * double(std::max<int64_t>(fill, 1)) / compute_s)));
+                if (zero_copy && double(rows0_of(2)) * row_seconds >= t_b + t_a) want = 2;
+            }
+            nb = static_cast<int>(std::max<int64_t>(zero_copy ? 2 : 1, std::min<int64_t>({int64_t(nb), fill, want})));
         }
-        rows0 = std::min<int64_t>(std::max<int64_t>(rows0, M / 8), M / 2) / 64 * 64;
-        rows0 = std::max<int64_t>(rows0, std::min<int64_t>(M, 64));
+        if (nb == 1) {
+            redge = {bounds->i0, bounds->i1};
+            return;
+        }
+        const int64_t rows0 = rows0_of(nb);
         redge.push_back(bounds->i0);
         const std::vector<int64_t> rest = band_edges(bounds->i0 + rows0, M - rows0, nb - 1, 64, true);
         redge.insert(redge.end(), rest.begin(), rest.end());
     };
     layout(r_mapped != nullptr);
     if (r_mapped) {
-        // the zero-copy band must run unpacked, as one whole-K launch of a
-        // variant that honours r_zero (else: the staged pipeline)
+        // every zero-copy band must run unpacked, on a variant whose epilogue
+        // (and split-K reduce) honours r_zero (else: the staged pipeline)
         amlt_operands probe = hview;
         probe.r.data = r_mapped;
-        amlt_bounds bb = *bounds;
-        bb.i0 = nb > 1 ? redge[1] : bounds->i1;
-        const Resolved rv = resolve(plan, &probe, &bb);
-        const Dispatch dp = plan_dispatch(ctx, plan, &tp, rv);
-        if (nb < 2 || rv.packed() || dp.splits > 1 || !vdesc(dp.variant).r_overwrite) {
+        bool ok = nb >= 2;
+        for (int b = 1; ok && b < nb; ++b) {
+            amlt_bounds bb = *bounds;
+            bb.i0 = redge[static_cast<size_t>(b)];
+            bb.i1 = redge[static_cast<size_t>(b) + 1];
+            const Resolved rv = resolve(plan, &probe, &bb);
+            ok = !rv.packed() && vdesc(plan_dispatch(ctx, plan, &tp, rv).variant).r_overwrite;
+        }
+        if (!ok) {
             r_mapped = nullptr;
             layout(false);
         }
