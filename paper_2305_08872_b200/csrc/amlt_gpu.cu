@@ -1430,23 +1430,39 @@ void host_pipeline(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ho
     // A of band 0 arrives K panel by K panel with B (a 2-D copy per panel)
     // when its rows are k-contiguous, so compute waits for one panel of each.
     const bool a0_panels = np > 1 && a_rows;
-    // Panels: edges on multiples of 64 k (16-byte aligned operand offsets).
-    // With the winner's seconds per row, band 0 computes rho times faster
-    // than a k row of B (and of its A) crosses the bus; the first panel is
-    // then rho times thinner than the others (at most 4x), so compute starts
-    // sooner and the second panel still lands before the first is done.
+    // Panels: edges on multiples of 64 k (16-byte aligned operand offsets),
+    // growing geometrically by g: compute starts after the first (thin)
+    // panel's copy, and panel p+1 (g times deeper) still lands before panel
+    // p is done as long as band 0 computes a k row at least g times faster
+    // than one crosses the bus (rho, from the winner's seconds per row;
+    // g = rho, at most 1.5). With a broadcast every rank must cut B the same
+    // way whatever its rows or tuning, so the edges depend on K and np only:
+    // g = 1.25, which band 0's height (its compute covers 1.3x the copies)
+    // sustains.
     std::vector<int64_t> kedge = band_edges(bounds->k0, K, np, 64, false);
-    if (np > 1 && row_seconds > 0.0) {
-        const double rows0 = double(redge[1] - redge[0]);
-        const double comp_k = rows0 * row_seconds / double(K);
-        const double xfer_k =
-            (double(host_ops->b.ld) * es * (bcast ? 1.25 : 1.0) + (a0_panels ? rows0 * es : 0.0)) / 40e9;
-        const double rho = std::min(4.0, comp_k / xfer_k);
-        const int64_t s0 = static_cast<int64_t>(double(K) / np / std::max(1.0, rho)) / 64 * 64;
-        if (s0 >= 64 && s0 < kedge[1] - kedge[0]) {
-            const std::vector<int64_t> rest = band_edges(bounds->k0 + s0, K - s0, np - 1, 64, false);
-            kedge.assign(1, bounds->k0);
-            kedge.insert(kedge.end(), rest.begin(), rest.end());
+    if (np > 1) {
+        double g = bcast ? 1.25 : 1.0;
+        if (!bcast && row_seconds > 0.0) {
+            const double rows0 = double(redge[1] - redge[0]);
+            const double comp_k = rows0 * row_seconds / double(K);
+            const double xfer_k = (double(host_ops->b.ld) * es + (a0_panels ? rows0 * es : 0.0)) / 40e9;
+            g = std::min(1.5, std::max(1.0, comp_k / xfer_k));
+        }
+        if (g > 1.0) {
+            double total = 0.0, w = 1.0;
+            for (int p = 0; p < np; ++p, w *= g) total += w;
+            std::vector<int64_t> e(1, bounds->k0);
+            double cum = 0.0;
+            w = 1.0;
+            for (int p = 0; p + 1 < np; ++p, w *= g) {
+                cum += w;
+                int64_t k = static_cast<int64_t>(std::llround(double(K) * cum / total / 64.0)) * 64;
+                k = std::max(k, e.back() - bounds->k0 + 64);
+                if (k >= K) break;
+                e.push_back(bounds->k0 + k);
+            }
+            e.push_back(bounds->k0 + K);
+            if (static_cast<int>(e.size()) == np + 1) kedge = e;  // (else keep equal panels)
         }
     }
 

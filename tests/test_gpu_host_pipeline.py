@@ -149,6 +149,9 @@ def test_broadcast_path_on_a_one_rank_communicator(small_panels, body):
             P.run_host_adaptive(plan, P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K), r_zero=True,
                                 bcast=True)
             check(body, "f64", R, want, exact=True, what=f"one-rank broadcast path {body}")
+        lay = ctx.last_host_layout()
+        # every rank cuts B the same way: geometric panels from K and the panel count alone
+        assert lay["bcast"] == 1 and lay["k_panels"] > 1 and lay["k_panel0"] < K // lay["k_panels"], lay
         ctx.detach_comm()
     finally:
         ctx.close()
