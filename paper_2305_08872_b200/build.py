@@ -5,6 +5,10 @@ run in parallel, then one link. Incremental: an object is rebuilt when its
 source or any header under csrc/ or include/ is newer.
 
     python -m paper_2305_08872_b200.build [--force] [-j N]
+
+AMLT_PTXAS_<UNIT>=<flag> (e.g. AMLT_PTXAS_THETA_DISCOUNT=-O1) passes one
+extra ptxas flag to one unit (scheduling experiments; touch the source so it
+is rebuilt).
 """
 from __future__ import annotations
 
@@ -94,7 +98,8 @@ def build(force: bool = False, jobs: int | None = None, verbose: bool = False) -
 
     def run(job):
         src, out, defs = job
-        cmd = [exe, *ARCH, *NVCC_FLAGS, *defs, "-c", src, "-o", out]
+        extra = os.environ.get("AMLT_PTXAS_" + os.path.splitext(os.path.basename(src))[0].upper(), "")
+        cmd = [exe, *ARCH, *NVCC_FLAGS, *defs, *(["-Xptxas", extra] if extra else []), "-c", src, "-o", out]
         r = subprocess.run(cmd, capture_output=True, text=True)
         logs[out] = r.stdout + r.stderr
         if r.returncode != 0:
