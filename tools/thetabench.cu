@@ -246,6 +246,26 @@ __global__ void __launch_bounds__(384, 1) kern(double* out, const double* in, lo
                         acc[r][c] = __uint_as_float(hi(la[r])) > __uint_as_float(hi(lth[c])) ? lx1[c] : acc[r][c];
                 return;
             }
+            if constexpr (FORM >= 27 && FORM <= 30) {
+                // exact compare split between the FP64 pipe (DSETP) and the
+                // ALU (signed 64-bit compare of the raw bits: exact for a
+                // with the sign bit clear): the first NI columns on the ALU
+                // (27: 4 of 4, 28: 1 of 4, 29: 2 of 4, 30: 1 of 4 rows-major)
+                constexpr int NI = FORM == 27 ? 4 : FORM == 29 ? 2 : 1;
+#pragma unroll
+                for (int c = 0; c < TN; ++c)
+#pragma unroll
+                    for (int r = 0; r < TM; ++r) {
+                        bool m;
+                        const bool alu = FORM == 30 ? (r % 4 == 0) : (c < NI);
+                        if (alu)
+                            m = __double_as_longlong(la[r]) > __double_as_longlong(lth[c]);
+                        else
+                            m = la[r] > lth[c];
+                        acc[r][c] = __fma_rn(la[r], m ? lx1[c] : lx0[c], acc[r][c]);
+                    }
+                return;
+            }
             if constexpr (FORM == 12) {
 #pragma unroll
                 for (int c = 0; c < TN; ++c)
@@ -398,6 +418,10 @@ int main() {
         run<15>(sms, blk, "15 smem-fed, DFMA only", out, in, cyc);
         run<25>(sms, blk, "25 theta form, PTX block per column", out, in, cyc);
         run<26>(sms, blk, "26 theta form, PTX block per row", out, in, cyc);
+        run<27>(sms, blk, "27 int64 compare (ALU) for every product", out, in, cyc);
+        run<28>(sms, blk, "28 int64 compare for 1 column of 4", out, in, cyc);
+        run<29>(sms, blk, "29 int64 compare for 2 columns of 4", out, in, cyc);
+        run<30>(sms, blk, "30 int64 compare for 2 rows of 8", out, in, cyc);
         if (getenv("ALLFORMS")) {
         run<18>(sms, blk, "18 P3: ISETP hi + DFMA x0 + @P DFMA d", out, in, cyc);
         run<19>(sms, blk, "19 P3 grouped per column (PTX)", out, in, cyc);
