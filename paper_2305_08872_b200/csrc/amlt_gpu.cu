@@ -919,9 +919,11 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
         if (v.vec == whole.aligned && (!v.tc || whole.aligned)) cands.push_back(idx);
     }
     // Band height per candidate: `waves` full waves of CTAs across all SMs
-    // (4 when the rows allow it, so partial-wave tails weigh little in the
-    // score; otherwise 1).
-    // The bands must fit in a quarter of the rows (4-wave, then 1-wave bands).
+    // (8 when the rows allow it, else 4, so partial-wave tails weigh little
+    // in the score; otherwise 1). At config 4's shape 4-wave bands ranked the
+    // 96 x 128 theta tile 0.6% ahead of the 48 x 128 one, which is 1.3%
+    // faster over whole launches (tools/theta_variants.py).
+    // The bands must fit in a quarter of the rows (8-, 4-, then 1-wave bands).
     // Tasks small enough are better measured whole on a scratch R (below);
     // for larger ones with many candidates, 1-wave bands may take up to 40%
     // of the rows (their rows are real output, computed by the candidate
@@ -931,9 +933,9 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
     std::vector<int64_t> band(cands.size());
     int64_t need = 0;
     int64_t cap = whole.M / 4;
-    for (int attempt = 0; attempt < (scratch_ok ? 2 : 3); ++attempt) {
-        const int waves = attempt == 0 ? 4 : 1;
-        cap = attempt < 2 ? whole.M / 4 : whole.M * 2 / 5;
+    for (int attempt = 0; attempt < (scratch_ok ? 3 : 4); ++attempt) {
+        const int waves = attempt == 0 ? 8 : attempt == 1 ? 4 : 1;
+        cap = attempt < 3 ? whole.M / 4 : whole.M * 2 / 5;
         need = 0;
         for (size_t c = 0; c < cands.size(); ++c) {
             const VariantDesc& v = vdesc(cands[c]);

@@ -9,6 +9,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2305_08872_b200 as P  # noqa: E402
 
 M = K = N = int(os.environ.get("SIZE", "8192"))
+if os.environ.get("MKN"):  # e.g. MKN=8192,8192,32768
+    M, K, N = (int(x) for x in os.environ["MKN"].split(","))
 ctx = P.Context(0)
 g = torch.Generator(device="cuda").manual_seed(1)
 A = torch.rand((M, K), device="cuda", dtype=torch.float64, generator=g)
