@@ -282,6 +282,10 @@ def test_sharded_group_all_devices(gpu_ctx, small_panels):
             check("discount", "f64", R[rows], want, exact=True, what=f"group run {it}")
             if it == 1:
                 assert all(r.from_cache or not r.trials for r in reps)
+        # R pinned: every device's band writes its rows straight into it (zero-copy)
+        R = _pinned(np.zeros((M, N)))
+        el, reps = g.run(P.Operands(A, B, R, t, d), P.Bounds(0, M, 0, N, 0, K), body="discount", r_zero=True)
+        check("discount", "f64", R.numpy()[rows], want, exact=True, what="group run, pinned R")
         # a task text (generated body) through the same group
         src = ("where(i in [0..M] and j in [0..N] and k in [0..K]) {\n"
                "  R[i][j] += A[i][k]*B[k][j] + (A[i][k] > thres[j]);\n}\n")
