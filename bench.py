@@ -770,7 +770,8 @@ def main():
                "d2h_bytes_per_step": int(d2h_total),
                "ms_per_step": e_el / steps * 1e3,
                "path": ("amlt_gpu_run_host (C-ABI) from pinned host buffers: B in K panels and A in row "
-                        "bands H2D, pipelined against compute; band 0 computed panel by panel as B lands "
+                        "bands H2D (each rank its own A rows), pipelined against compute; band 0 computed "
+                        "panel by panel as B lands "
                         "(its R zero-filled on the device, D2H afterwards); "
                         + ("the other rows in one launch whose epilogue writes R straight into the pinned "
                            "host buffer (zero-copy)" if layout.get("zero_copy_r") else
@@ -780,11 +781,15 @@ def main():
                "layout": layout}
         if e2e_error:
             e2e["error"] = e2e_error
-        elif not args.no_verify:
-            # the last timed step's R, as it landed in host memory
-            worst, bad = check_rows(hR[e_ri][:, e_ci].double().numpy(), hA[e_ri].double().numpy(), e_B, e_th,
-                                    e_ds, body, dtype) if e_ri else (0.0, 0)
-            nr = len(e_ri)
+        if not args.no_verify:
+            # the last timed step's R, as it landed in host memory (every rank
+            # joins the gather below, a failed one with no rows checked)
+            if e2e_error or not e_ri:
+                worst, bad, nr = 0.0, 0, 0
+            else:
+                worst, bad = check_rows(hR[e_ri][:, e_ci].double().numpy(), hA[e_ri].double().numpy(), e_B,
+                                        e_th, e_ds, body, dtype)
+                nr = len(e_ri)
             if dist is not None:
                 tt = torch.tensor([nr, worst, bad], dtype=torch.float64, device=device)
                 parts = [torch.zeros_like(tt) for _ in range(ws)]
