@@ -830,6 +830,8 @@ def main():
             "metric": METRIC, "value": value, "unit": "GFLOP/s",
             "inner_iters_per_s": iters_total / el,
             "n_gpus": ws, "steps": steps, "warmup": warmup, "ms_per_step": el / steps * 1e3,
+            "step_ms_rank0": {"best": min(per_launch) * 1e3, "median": sorted(per_launch)[len(per_launch) // 2] * 1e3,
+                              "worst": max(per_launch) * 1e3, "n": len(per_launch)},
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": dtype, "data": "synthetic",
             "config": {"workload": args.workload, "body": body, "M": M, "K": K, "N": N,
