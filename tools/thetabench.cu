@@ -47,6 +47,10 @@ __global__ void __launch_bounds__(384, 1) kern(double* out, const double* in, lo
     for (int i = t; i < 8 * 128; i += blockDim.x) sTh[i] = __halves2half2(__double2half(in[64 + (i & 63)]), __double2half(in[64 + ((i + 1) & 63)]));
     __syncthreads();
     const int lane = t & 31, warp = t >> 5;
+    // runtime 2 and -1 (in[0] is 0): keeps ptxas from strength-reducing the
+    // IMAD-based forms into shifts and adds on the ALU
+    const unsigned k2 = static_cast<unsigned>(in[0] + 2.0);
+    const int kneg = -static_cast<int>(in[0] + 1.0);
     const long long c0 = clock64();
     if constexpr (FORM >= 8) {
         // smem-fed: 8: row outer, loads then compute per k; 9: loads for the next
@@ -266,6 +270,48 @@ __global__ void __launch_bounds__(384, 1) kern(double* out, const double* in, lo
                     }
                 return;
             }
+            if constexpr (FORM >= 31 && FORM <= 37) {
+                // per-column forms (F: DSETP + 2 FSEL; X: ISETP on the high
+                // words + 2 FSEL; Y: integer compare of the high words on the
+                // FMA pipe, mask by IMAD.HI, select by 2 IMAD; I: DADD
+                // theta - a, mask from its sign by IMAD.HI, select by 2 IMAD).
+                // Y and X need a >= 0 with zero low words; I is general.
+                auto kind = [](int c) {
+                    if (FORM == 31) return c == 3 ? 'Y' : 'F';
+                    if (FORM == 32) return c == 3 ? 'Y' : c == 2 ? 'X' : 'F';
+                    if (FORM == 33) return 'Y';
+                    if (FORM == 34) return 'I';
+                    if (FORM == 35) return c == 3 ? 'I' : 'F';
+                    if (FORM == 36) return c >= 2 ? 'I' : 'F';
+                    return c == 3 ? 'Y' : c == 1 ? 'I' : 'F';
+                };
+#pragma unroll
+                for (int c = 0; c < TN; ++c) {
+                    const unsigned x0h = hi(lx0[c]), x0l = lo(lx0[c]);
+                    const unsigned dh = hi(lx1[c]) - x0h, dl = lo(lx1[c]) - x0l;
+#pragma unroll
+                    for (int r = 0; r < TM; ++r) {
+                        const char kd = kind(c);
+                        if (kd == 'F') {
+                            acc[r][c] = __fma_rn(la[r], la[r] > lth[c] ? lx1[c] : lx0[c], acc[r][c]);
+                        } else if (kd == 'X') {
+                            const bool m = static_cast<int>(hi(la[r])) > static_cast<int>(hi(lth[c]));
+                            acc[r][c] = __fma_rn(la[r], m ? lx1[c] : lx0[c], acc[r][c]);
+                        } else {
+                            unsigned m;
+                            if (kd == 'Y') {
+                                const int d = static_cast<int>(hi(la[r])) * kneg + static_cast<int>(hi(lth[c]));
+                                m = __umulhi(static_cast<unsigned>(d), k2);
+                            } else {
+                                m = __umulhi(hi(__dsub_rn(lth[c], la[r])), k2);
+                            }
+                            const double s = __hiloint2double(static_cast<int>(m * dh + x0h), static_cast<int>(m * dl + x0l));
+                            acc[r][c] = __fma_rn(la[r], s, acc[r][c]);
+                        }
+                    }
+                }
+                return;
+            }
             if constexpr (FORM == 12) {
 #pragma unroll
                 for (int c = 0; c < TN; ++c)
@@ -422,6 +468,13 @@ int main() {
         run<28>(sms, blk, "28 int64 compare for 1 column of 4", out, in, cyc);
         run<29>(sms, blk, "29 int64 compare for 2 columns of 4", out, in, cyc);
         run<30>(sms, blk, "30 int64 compare for 2 rows of 8", out, in, cyc);
+        run<31>(sms, blk, "31 col 3 Y (IMAD compare + IMAD select)", out, in, cyc);
+        run<32>(sms, blk, "32 col 2 X (ISETP), col 3 Y", out, in, cyc);
+        run<33>(sms, blk, "33 all Y", out, in, cyc);
+        run<34>(sms, blk, "34 all I (DADD sign + IMAD select)", out, in, cyc);
+        run<35>(sms, blk, "35 col 3 I", out, in, cyc);
+        run<36>(sms, blk, "36 cols 2-3 I", out, in, cyc);
+        run<37>(sms, blk, "37 col 1 I, col 3 Y", out, in, cyc);
         if (getenv("ALLFORMS")) {
         run<18>(sms, blk, "18 P3: ISETP hi + DFMA x0 + @P DFMA d", out, in, cyc);
         run<19>(sms, blk, "19 P3 grouped per column (PTX)", out, in, cyc);
