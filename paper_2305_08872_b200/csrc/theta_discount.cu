@@ -154,78 +154,118 @@ __device__ __forceinline__ void block_max(int (&v)[NS], int* g, int first) {
     }
 }
 
+// Units of the preparation and the A scan are (row, 4 * blockDim-column
+// chunk) pairs: one integer division per unit, not a 64-bit division per
+// element.
+__device__ __forceinline__ void unit_of(int64_t u, int64_t per_row, int64_t cols, int64_t& row, int64_t& c0,
+                                        int64_t& c1) {
+    const int64_t chunk = 4 * static_cast<int64_t>(blockDim.x);
+    row = u / per_row;
+    c0 = (u - row * per_row) * chunk;
+    c1 = c0 + chunk < cols ? c0 + chunk : cols;
+}
+
 // Planes (theta, x0, x1), each kdim x npad doubles, plus the B-side
-// statistics; this launch fills rows [plane_k0, plane_k0 + K) (planes points
-// at row plane_k0 of the first plane).
-__global__ void __launch_bounds__(256) prep_kernel(const KParams p, double* planes, int64_t npad, int64_t pstride,
-                                                   int* g) {
+// statistics, over blocks [0, nb) of the launch; this launch fills rows
+// [plane_k0, plane_k0 + K) (planes points at row plane_k0 of the first
+// plane).
+__device__ __forceinline__ void prep_part(const KParams& p, double* planes, int64_t npad, int64_t pstride, int* g,
+                                          int bid, int nb) {
     const double* B = static_cast<const double*>(p.B);
     const double* T = static_cast<const double*>(p.thres);
     const double* D = static_cast<const double*>(p.dis);
-    const int64_t plane = p.K * npad;
     int st[5] = {0, 0, 0, 0, 0};  // bad, bmax, bmin, cmax, cmin
-    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < plane;
-         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t k = idx / npad;
-        const int64_t j = idx - k * npad;
-        double theta = 0.0, x0 = 0.0, x1 = 0.0;
-        if (j < p.N) {
-            const double b = B[k * p.ldb + j];
-            const double t = T ? T[j * p.t_sj] : p.tconst;
-            const double c1 = __dsub_rn(1.0, D[j * p.d_sj]);
-            if (!isfinite(b) || !isfinite(t) || !isfinite(c1)) {
-                st[0] = 1;
-            } else {
-                if (k == 0 && c1 != 0.0) {
-                    const int e = expo(c1);
-                    st[3] = max(st[3], EB + e);
-                    st[4] = max(st[4], EB - e);
-                }
-                if (b == 0.0) {
-                    x0 = x1 = b;
+    const int64_t per_row = (npad + 4 * blockDim.x - 1) / (4 * blockDim.x);
+    for (int64_t u = bid; u < p.K * per_row; u += nb) {
+        int64_t k, j0, j1;
+        unit_of(u, per_row, npad, k, j0, j1);
+        for (int64_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+            double theta = 0.0, x0 = 0.0, x1 = 0.0;
+            if (j < p.N) {
+                const double b = B[k * p.ldb + j];
+                const double t = T ? T[j * p.t_sj] : p.tconst;
+                const double c1 = __dsub_rn(1.0, D[j * p.d_sj]);
+                if (!isfinite(b) || !isfinite(t) || !isfinite(c1)) {
+                    st[0] = 1;
                 } else {
-                    const int e = expo(b);
-                    st[1] = max(st[1], EB + e);
-                    st[2] = max(st[2], EB - e);
-                    theta = theta_of(b, t);
-                    const double bc = __dmul_rn(b, c1);
-                    if (c1 != 0.0 && !(fabs(bc) >= DBL_MIN && fabs(bc) <= DBL_MAX)) st[0] = 1;
-                    if (b > 0) {
-                        x0 = b;
-                        x1 = bc;
+                    if (k == 0 && c1 != 0.0) {
+                        const int e = expo(c1);
+                        st[3] = max(st[3], EB + e);
+                        st[4] = max(st[4], EB - e);
+                    }
+                    if (b == 0.0) {
+                        x0 = x1 = b;
                     } else {
-                        x0 = bc;
-                        x1 = b;
+                        const int e = expo(b);
+                        st[1] = max(st[1], EB + e);
+                        st[2] = max(st[2], EB - e);
+                        theta = theta_of(b, t);
+                        const double bc = __dmul_rn(b, c1);
+                        if (c1 != 0.0 && !(fabs(bc) >= DBL_MIN && fabs(bc) <= DBL_MAX)) st[0] = 1;
+                        if (b > 0) {
+                            x0 = b;
+                            x1 = bc;
+                        } else {
+                            x0 = bc;
+                            x1 = b;
+                        }
                     }
                 }
             }
+            const int64_t idx = k * npad + j;
+            planes[idx] = theta;
+            planes[pstride + idx] = x0;
+            planes[2 * pstride + idx] = x1;
         }
-        planes[idx] = theta;
-        planes[pstride + idx] = x0;
-        planes[2 * pstride + idx] = x1;
     }
     block_max<5>(st, g, G_BAD);
 }
 
-// A-side statistics of this run's rows (finite nonzero entries only).
-__global__ void __launch_bounds__(256) a_stats_kernel(const KParams p, int* g) {
+// A-side statistics of this run's rows (finite nonzero entries only), over
+// blocks [0, nb).
+__device__ __forceinline__ void a_stats_part(const KParams& p, int* g, int bid, int nb) {
     const double* A = static_cast<const double*>(p.A);
-    const int64_t total = p.M * p.K;
     int st[2] = {0, 0};
-    for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-         idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t i = idx / p.K;
-        const double a = A[i * p.lda + (idx - i * p.K)];
-        if (a != 0.0 && isfinite(a)) {
-            const int e = expo(a);
-            st[0] = max(st[0], EB + e);
-            st[1] = max(st[1], EB - e);
+    const int64_t per_row = (p.K + 4 * blockDim.x - 1) / (4 * blockDim.x);
+    for (int64_t u = bid; u < p.M * per_row; u += nb) {
+        int64_t i, k0, k1;
+        unit_of(u, per_row, p.K, i, k0, k1);
+        for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+            const double a = A[i * p.lda + k];
+            if (a != 0.0 && isfinite(a)) {
+                const int e = expo(a);
+                st[0] = max(st[0], EB + e);
+                st[1] = max(st[1], EB - e);
+            }
         }
     }
     block_max<2>(st, g, G_AMAX);
 }
 
+// The preparation alone (panel-wise preparations; blocks [0, grid)) ...
+__global__ void __launch_bounds__(256) prep_kernel(const KParams p, double* planes, int64_t npad, int64_t pstride,
+                                                   int* g) {
+    prep_part(p, planes, npad, pstride, g, blockIdx.x, gridDim.x);
+}
+
+// ... and, per call, the A scan, with the preparation of B in the same
+// launch when it is not ready (blocks [0, nbp) prepare B, the rest scan A).
+__global__ void __launch_bounds__(256) prep_stats_kernel(const KParams p, double* planes, int64_t npad,
+                                                         int64_t pstride, int* g, int nbp) {
+    if (static_cast<int>(blockIdx.x) < nbp)
+        prep_part(p, planes, npad, pstride, g, blockIdx.x, nbp);
+    else
+        a_stats_part(p, g, blockIdx.x - nbp, gridDim.x - nbp);
+}
+
 int64_t npad_of(int64_t N) { return (N + 1) / 2 * 2; }  // 16-byte plane rows (TMA)
+
+// blocks of 256 threads for the preparation / the A scan: one per unit, at
+// most 16 per SM
+int prep_blocks(const KParams& p) {
+    return static_cast<int>(std::min<int64_t>(p.K * ((npad_of(p.N) + 1023) / 1024), 148 * 16));
+}
+int a_stats_blocks(const KParams& p) { return static_cast<int>(std::min<int64_t>(p.M * ((p.K + 1023) / 1024), 148 * 8)); }
 
 // K rows of the preparation (panel-wise preparations: the whole K range)
 int64_t kdim_of(const KParams& p) { return p.plane_kdim > 0 ? p.plane_kdim : p.K; }
@@ -243,10 +283,8 @@ cudaError_t prep_b(const KParams& p, void* ws, cudaStream_t s) {
         if (e != cudaSuccess) return e;
     }
     const int64_t npad = npad_of(p.N);
-    const int64_t total = p.K * npad;
     const int64_t pstride = kdim_of(p) * npad;
-    const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 16));
-    prep_kernel<<<blocks, 256, 0, s>>>(
+    prep_kernel<<<prep_blocks(p), 256, 0, s>>>(
         p, reinterpret_cast<double*>(static_cast<char*>(ws) + HEADER) + p.plane_k0 * npad, npad, pstride, g);
     return cudaGetLastError();
 }
@@ -300,12 +338,18 @@ cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
     const int64_t npad = npad_of(p.N);
     const double* planes = reinterpret_cast<const double*>(static_cast<char*>(ws) + HEADER) + p.plane_k0 * npad;
     cudaError_t e;
-    if (!b_ready && (e = prep_b(p, ws, s)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(g + G_AMAX, 0, 2 * sizeof(int), s)) != cudaSuccess) return e;
+    // one reset and one launch: the B preparation (when not ready) and the
+    // scan of this call's A rows side by side (the B-side statistics restart
+    // with the first panel, plane_k0 == 0, and accumulate over later ones)
     {
-        const int64_t total = p.M * p.K;
-        const int blocks = static_cast<int>(std::min<int64_t>((total + 255) / 256, 148 * 8));
-        a_stats_kernel<<<blocks, 256, 0, s>>>(p, g);
+        if (!b_ready && p.plane_k0 + p.K > kdim_of(p)) return cudaErrorInvalidValue;
+        const bool reset_b = !b_ready && p.plane_k0 == 0;
+        if ((e = cudaMemsetAsync(reset_b ? g : g + G_AMAX, 0, (reset_b ? G_COUNT : 2) * sizeof(int), s)) !=
+            cudaSuccess)
+            return e;
+        const int nbp = b_ready ? 0 : prep_blocks(p);
+        prep_stats_kernel<<<nbp + a_stats_blocks(p), 256, 0, s>>>(
+            p, const_cast<double*>(planes), npad, kdim_of(p) * npad, g, nbp);
         if ((e = cudaGetLastError()) != cudaSuccess) return e;
     }
     // theta kernel: A box BK x BM; B planes box BN x BK x 3
