@@ -519,6 +519,10 @@ def main():
                     help="CPU only (gloo): rank launch, row bands, the broadcast of B / vectors and "
                          "the max-over-ranks reduction, with no kernel and no timing claim "
                          "(tests/test_bench_harness.py)")
+    ap.add_argument("--proxy-band", type=int, default=0, metavar="N",
+                    help="one GPU: time only rank 0's row band of an N-way split (what each rank "
+                         "of an N-GPU run computes), B / vectors copied by this rank; the line is "
+                         "labelled 'proxy' and is not a multi-GPU measurement")
     ap.add_argument("--f64-emulation", action="store_true",
                     help="let the tuner use the int8-tensor-core f64 GEMM (AMLT_CTX_F64_EMULATION)")
     args = ap.parse_args()
@@ -575,8 +579,14 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=device)
-    row0, row1 = row_band(M, ws, rank, align=64)
+    proxy = args.proxy_band if args.proxy_band > 1 else 0
+    if proxy and ws > 1:
+        log("bench.py: --proxy-band is a one-GPU measurement; do not launch it under torchrun")
+        return 2
+    row0, row1 = row_band(M, proxy or ws, rank, align=64)
     rows = row1 - row0
+    if proxy:
+        M = rows  # the work of this step: rank 0's band
 
     ctx = P.Context(lrank, f64_emulation=args.f64_emulation)
     # one explicit (non-default) stream for torch and the kernels alike, so the
@@ -892,6 +902,14 @@ def main():
         }
         if cuda_core is not None:
             line["cuda_core"] = cuda_core
+        if proxy:
+            line["proxy"] = {"of_gpus": proxy, "band_rows": rows, "full_M": WORKLOADS[args.workload][2],
+                             "note": "rank 0's row band of an N-way split timed alone on one GPU: every "
+                                     "value here is that band's rate (M in config = the band's rows); "
+                                     "the e2e leg copies B / vectors H2D itself (rank 0's share of an "
+                                     "N-GPU run, without its NCCL broadcast); not a multi-GPU "
+                                     "measurement"}
+            line["config"]["parallelism"] = f"proxy_band_of_{proxy}"
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
