@@ -536,6 +536,11 @@ def main():
         log(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; launch one rank per GPU")
         return 2
 
+    proxy = args.proxy_band if args.proxy_band > 1 else 0
+    if proxy and (ws > 1 or args.gpus > 1):
+        log("bench.py: --proxy-band is a one-GPU measurement; run it with --gpus 1 outside torchrun")
+        return 2
+
     if args.dry_run:
         return dry_run(args, body, dtype, M, K, N, ws, rank)
 
@@ -579,10 +584,6 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=device)
-    proxy = args.proxy_band if args.proxy_band > 1 else 0
-    if proxy and ws > 1:
-        log("bench.py: --proxy-band is a one-GPU measurement; do not launch it under torchrun")
-        return 2
     row0, row1 = row_band(M, proxy or ws, rank, align=64)
     rows = row1 - row0
     if proxy:

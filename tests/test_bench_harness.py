@@ -54,3 +54,11 @@ def test_single_rank_dry_run():
     assert r.returncode == 0, r.stderr[-2000:]
     out = json.loads(r.stdout.strip())
     assert out["n_gpus"] == 1 and out["bands"] == [[0, out["config"]["M"]]]
+
+
+def test_proxy_band_refuses_multi_rank():
+    """--proxy-band times one rank's band on ONE GPU; under torchrun or with
+    --gpus > 1 it is refused before any work (bench.py)."""
+    r = run_bench("--gpus", "2", "--proxy-band", "8", "--dry-run",
+                  env={"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode == 2 and "proxy-band" in r.stderr
