@@ -351,8 +351,12 @@ def launches_of(name: str, split: bool) -> int:
         return 3  # operand split of A, of B, the tensor-core GEMM
     if "ozaki" in name:
         return 5  # row / column exponents, A / B slicing, the int8 GEMM
-    if "_theta_" in name or "_swar_" in name:
-        return 4  # B preparation, A scan, the tile, the guard-exited fallback
+    if "_theta_" in name:
+        # B preparation and A scan in one launch, the tile, the guard-exited
+        # fallback (+ the ordered split-K reduce)
+        return 3 + (1 if split else 0)
+    if "_swar_" in name:
+        return 4  # B packing, A packing, the tile, the guard-exited fallback
     return 2 if split else 1
 
 
