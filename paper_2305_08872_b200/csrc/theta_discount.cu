@@ -460,7 +460,9 @@ void register_theta_discount(Registry& reg) {
     // 16 warps per SM (4 per scheduler) with 6 rows per thread. Measured at
     // 8192^3 (tools/quick_perf.py, r02): 99.8 ms against 98.8 for the 12-warp
     // 8 x 4 tile; 5 x 4 (101.4), 6 x 4 BK = 8 (100.1) and row-outer inner
-    // order (104.7) were slower and are not kept.
+    // order (104.7) were slower and are not kept; so was (r02) a 20-warp
+    // 4 x 4 tile on the lane grid in 64 x 32 CTAs, five per SM (118.6 ms:
+    // 96 registers with small spills, and a third more loads per product).
     add_theta<6, 4, 16, 1, 16, 2, 1>(reg, "theta_t6x4_w16x1");
 }
 
