@@ -35,6 +35,7 @@
 #include <math_constants.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <mutex>
 #include <set>
 #include <utility>
@@ -373,9 +374,13 @@ cudaError_t run(const KParams& p, void* ws, bool b_ready, cudaStream_t s) {
     q.work = splits > 1 ? p.work : nullptr;
     q.tiles_m = static_cast<int32_t>((p.M + Cfg::BM - 1) / Cfg::BM);
     q.tiles_n = static_cast<int32_t>((p.N + Cfg::BN - 1) / Cfg::BN);
-    // raster groups of ~512 rows, as for the ordinary tiles (2304-row groups
-    // measured 690 GB of DRAM reads per config-4 launch against 632 GB)
-    q.group_m = std::min(64, std::max(8, 512 / Cfg::BM));
+    // raster groups of (resident CTAs / 8) row tiles, so one wave covers a
+    // group's rows x about 8 column panels: DRAM reads of 4096 rows of config
+    // 4 fall from 92.6 GB (512-row groups) to 56.9 GB at the same speed
+    // (tools/raster_probe.sh; 960 / 3552-row groups read 66.3 / 68.2 GB)
+    q.group_m = std::min(64, std::max(8, 148 * MINB / 8));
+    if (const char* gr = getenv("AMLT_THETA_GROUP_ROWS"))  // raster experiments (tools/raster_probe.sh)
+        q.group_m = std::max(1, atoi(gr) / Cfg::BM);
     auto kt = &mmlt_tile_kernel<Body, double, TM, TN, WR, WC, BK, ST, LOAD, MINB>;
     if ((e = smem_attr_once(reinterpret_cast<const void*>(kt), Cfg::SMEM_BYTES)) != cudaSuccess) return e;
     kt<<<dim3(static_cast<unsigned>(int64_t(q.tiles_m) * q.tiles_n), static_cast<unsigned>(splits)), Cfg::THREADS,
