@@ -263,10 +263,13 @@ int64_t npad_of(int64_t N) { return (N + 1) / 2 * 2; }  // 16-byte plane rows (T
 
 // blocks of 256 threads for the preparation / the A scan: one per unit, at
 // most 16 per SM
+// (at least one: an empty range still launches a valid grid)
 int prep_blocks(const KParams& p) {
-    return static_cast<int>(std::min<int64_t>(p.K * ((npad_of(p.N) + 1023) / 1024), 148 * 16));
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(p.K * ((npad_of(p.N) + 1023) / 1024), 148 * 16)));
 }
-int a_stats_blocks(const KParams& p) { return static_cast<int>(std::min<int64_t>(p.M * ((p.K + 1023) / 1024), 148 * 8)); }
+int a_stats_blocks(const KParams& p) {
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(p.M * ((p.K + 1023) / 1024), 148 * 8)));
+}
 
 // K rows of the preparation (panel-wise preparations: the whole K range)
 int64_t kdim_of(const KParams& p) { return p.plane_kdim > 0 ? p.plane_kdim : p.K; }
