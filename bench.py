@@ -301,6 +301,16 @@ def run_reference(body, M, K, N, steps, warmup, threads):
                       f"(rows of R are independent)"}
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -566,7 +576,7 @@ def main():
                 "cpu_baseline": {"value": gf, "unit": "GFLOP/s", "cores": threads,
                                  "kind": "reference", "sample": r["sample"],
                                  "extrapolated_from_sample": True,
-                                 "sample_fraction": r["sample_fraction"]},
+                                 "sample_fraction": r["sample_fraction"], "cpu_model": cpu_model()},
                 "e2e": {"value": gf, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
         print(json.dumps(line), flush=True)
@@ -822,9 +832,13 @@ def main():
         try:
             threads = cpu_threads()
             r = run_reference(body, M, K, N, 1, 0, threads)
+            # the reference's own single-threaded mode (run_adaptive) beside it
+            r1 = run_reference(body, M, K, N, 1, 0, 1) if threads > 1 else r
             cpu = {"value": 2 * r["iters_per_s"] / 1e9, "unit": "GFLOP/s", "cores": threads,
                    "kind": "reference", "sample": r["sample"], "extrapolated_from_sample": True,
-                   "sample_fraction": r["sample_fraction"]}
+                   "sample_fraction": r["sample_fraction"], "cpu_model": cpu_model(),
+                   "value_1thread": 2 * r1["iters_per_s"] / 1e9,
+                   "sample_1thread": r1["sample"]}
         except Exception as e:  # noqa: BLE001
             cpu = {"value": None, "unit": "GFLOP/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {e}"}
