@@ -768,11 +768,14 @@ def main():
 
             ctx.attach_comm(rank, ws, exchange=exchange)
         tms = []
+        # --tile pins the e2e leg's tile too (else: the winner the value leg's
+        # warm-up tuned and cached for this shape)
+        e2e_tp = win if args.tile else None
         try:
-            P.run_host(plan, hops, bounds, r_zero=True, bcast=bcast)  # warm-up (staging alloc)
+            P.run_host(plan, hops, bounds, params=e2e_tp, r_zero=True, bcast=bcast)  # warm-up (staging alloc)
             barrier()
             for _ in range(steps):
-                tms.append(P.run_host(plan, hops, bounds, r_zero=True, bcast=bcast))
+                tms.append(P.run_host(plan, hops, bounds, params=e2e_tp, r_zero=True, bcast=bcast))
         except P.EngineError as e:  # reported in the line, not fatal to the value leg
             e2e_error = f"rank {rank}: {e}"
             log("bench.py: e2e leg failed:", e2e_error)
