@@ -959,8 +959,16 @@ __global__ void mmlt_splitk_reduce(const KParams p) {
     const int64_t per_row = (p.N + chunk - 1) / chunk;
     const int64_t units = p.M * per_row;
     for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const int64_t i = u / per_row;
-        const int64_t j0 = (u - i * per_row) * chunk;
+        int64_t i, j0;
+        if (u <= 0xffffffffLL && per_row <= 0xffffffffLL) {  // a 32-bit division (the common case)
+            const unsigned uu = static_cast<unsigned>(u), pr = static_cast<unsigned>(per_row);
+            const unsigned i32 = uu / pr;
+            i = i32;
+            j0 = int64_t(uu - i32 * pr) * chunk;
+        } else {
+            i = u / per_row;
+            j0 = (u - i * per_row) * chunk;
+        }
         const int64_t j1 = j0 + chunk < p.N ? j0 + chunk : p.N;
         const T* w = W + i * p.N;
         T* r = R + i * p.ldr;

@@ -111,18 +111,22 @@ __device__ __forceinline__ bool pred(double x, double b, double t) {
 }
 // max{x : pred(x)}: pred is true-then-false over [-inf, +inf] (finite t,
 // finite nonzero b), pred(-inf) holds and pred(+inf) does not.
+// The walk steps over the ordered keys (one integer add per step instead of
+// nextafter's special-case handling; -0 and +0 are adjacent keys with equal
+// pred, so the maximum found is the same double up to the sign of a zero,
+// which no compare a > theta can tell apart).
 __device__ double theta_of(double b, double t) {
     double x = __ddiv_rn(t, b);
     if (x != x) x = 0.0;
+    long long kx = okey(x);
 #pragma unroll 1
     for (int i = 0; i < 8; ++i) {
-        if (!pred(x, b, t)) {
-            x = nextafter(x, -CUDART_INF);
+        if (!pred(odec(kx), b, t)) {
+            --kx;
             continue;
         }
-        const double up = nextafter(x, CUDART_INF);
-        if (!pred(up, b, t)) return x;
-        x = up;
+        if (!pred(odec(kx + 1), b, t)) return odec(kx);
+        ++kx;
     }
     long long lo = okey(-CUDART_INF), hi = okey(CUDART_INF);
 #pragma unroll 1
@@ -161,8 +165,15 @@ __device__ __forceinline__ void block_max(int (&v)[NS], int* g, int first) {
 __device__ __forceinline__ void unit_of(int64_t u, int64_t per_row, int64_t cols, int64_t& row, int64_t& c0,
                                         int64_t& c1) {
     const int64_t chunk = 4 * static_cast<int64_t>(blockDim.x);
-    row = u / per_row;
-    c0 = (u - row * per_row) * chunk;
+    if (u <= 0xffffffffLL && per_row <= 0xffffffffLL) {  // a 32-bit division (the common case)
+        const unsigned uu = static_cast<unsigned>(u), pr = static_cast<unsigned>(per_row);
+        const unsigned r32 = uu / pr;
+        row = r32;
+        c0 = int64_t(uu - r32 * pr) * chunk;
+    } else {
+        row = u / per_row;
+        c0 = (u - row * per_row) * chunk;
+    }
     c1 = c0 + chunk < cols ? c0 + chunk : cols;
 }
 
@@ -231,8 +242,15 @@ __device__ __forceinline__ void a_stats_part(const KParams& p, int* g, int bid, 
     for (int64_t u = bid; u < p.M * per_row; u += nb) {
         int64_t i, k0, k1;
         unit_of(u, per_row, p.K, i, k0, k1);
-        for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-            const double a = A[i * p.lda + k];
+        double av[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // four loads in flight per thread
+            const int64_t k = k0 + threadIdx.x + int64_t(q) * blockDim.x;
+            av[q] = k < k1 ? __ldg(A + i * p.lda + k) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double a = av[q];
             if (a != 0.0 && isfinite(a)) {
                 const int e = expo(a);
                 st[0] = max(st[0], EB + e);
