@@ -344,6 +344,22 @@ def algorithmic_bytes(body, dtype, M, K, N):
     return es * (M * K + K * N + 2 * M * N + vec)
 
 
+def hbm_peak_gbs():
+    """MEASURED_PEAKS.json's copy bandwidth (driver-written), or None."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+def cap_rows(cap, workload):
+    """Rows of R the keyed capture's launch covered: the whole workload at
+    N=1 (tools/capture_keyed.sh); a rank's band scales the traffic by its
+    share of the rows."""
+    return cap.get("rows") or WORKLOADS[workload][2]
+
+
 def tensor_tf32_peak() -> float:
     """Dense TF32 tensor-core TFLOP/s: the driver-measured dense bf16 figure
     (MEASURED_PEAKS.json, burst) halved (TF32 runs at half the bf16 rate on
@@ -914,6 +930,13 @@ def main():
                          "issue_active_pct": cap.get("issue_active_pct") if cap else None,
                          "traffic": cap.get("dram_bytes") if cap else None,
                          "traffic_unit": "bytes per launch of the tile (ncu dram read+write)",
+                         # achieved HBM rate: the capture's DRAM bytes over this run's kernel time,
+                         # against MEASURED_PEAKS.json's copy bandwidth (north_star's HBM GB/s)
+                         "hbm_gbps": (cap["dram_bytes"] * (rows / cap_rows(cap, args.workload)) / kernel_s / 1e9
+                                      if cap and cap.get("dram_bytes") else None),
+                         "hbm_frac": (cap["dram_bytes"] * (rows / cap_rows(cap, args.workload)) / kernel_s / 1e9
+                                      / hbm_peak_gbs() if cap and cap.get("dram_bytes") and hbm_peak_gbs()
+                                      else None),
                          "capture": (f"{cap['file']}: {cap.get('capture', '')}" if cap else
                                      f"none committed for tile {tile}"),
                          "algorithmic_bytes": algorithmic_bytes(body, dtype, M, K, N),
