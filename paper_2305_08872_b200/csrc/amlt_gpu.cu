@@ -441,10 +441,12 @@ int choose_variant(const amlt_ctx* ctx, const amlt_plan* plan, const amlt_tile_p
         if (tile->variant >= (int)plan->variants.size())
             fail(AMLT_ERR_INVALID_ARGUMENT, "tile variant index out of range");
         int idx = plan->variants[static_cast<size_t>(tile->variant)];
-        if (vdesc(idx).vec && !rv.aligned)
+        // (an empty rectangle runs nothing: no operand requirement applies)
+        const bool empty = rv.M == 0 || rv.N == 0 || rv.K == 0;
+        if (vdesc(idx).vec && !rv.aligned && !empty)
             fail(AMLT_ERR_INVALID_ARGUMENT,
                  "variant needs 16-byte aligned operands with vector-multiple strides");
-        if (vdesc(idx).max_k && rv.K > vdesc(idx).max_k)
+        if (vdesc(idx).max_k && rv.K > vdesc(idx).max_k && !empty)
             fail(AMLT_ERR_INVALID_ARGUMENT, std::string("variant accepts K <= ") +
                                                 std::to_string(vdesc(idx).max_k));
         return idx;
@@ -940,7 +942,9 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
         for (size_t c = 0; c < cands.size(); ++c) {
             const VariantDesc& v = vdesc(cands[c]);
             const int occ = occ_of(ctx, cands[c]);
-            const int64_t tiles_n = (whole.N + v.bn - 1) / v.bn;
+            // (an empty N leaves no tiles: one-row bands; the task is then
+            // not tunable and runs through the untuned path below)
+            const int64_t tiles_n = std::max<int64_t>(1, (whole.N + v.bn - 1) / v.bn);
             const int64_t want_ctas = int64_t(waves) * ctx->num_sms * occ;
             const int64_t tiles_m = std::max<int64_t>(1, (want_ctas + tiles_n - 1) / tiles_n);
             band[c] = tiles_m * v.bm;
@@ -956,7 +960,7 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
     // band trials: its readings are the AMULET contract's scores.
     const bool prefer_scratch = scratch_ok && !clock && !ctx->dry();
     const bool tunable = !prefer_scratch && plan->desc.accumulate && !cands.empty() && whole.K > 0 &&
-                         whole.N > 0 && need <= cap && ctx->tune_cache.find(key) == ctx->tune_cache.end();
+                         whole.N > 0 && whole.M > 0 && need <= cap && ctx->tune_cache.find(key) == ctx->tune_cache.end();
 
     auto run_rect = [&](const amlt_bounds& rb, int variant, int64_t kc) {
         amlt_tile_params tp{kc, 0, 0, plan_local_index(plan, variant)};

@@ -695,3 +695,40 @@ def test_context_stream_is_ordered_after_the_default_stream(gpu_ctx):
         R = torch.zeros((M, N), device="cuda", dtype=torch.float64)  # 1 GiB fill on the default stream
         P.run_subtask(plan, P.Operands(A, B, R, None, None), P.TileParams(), P.Bounds(0, M, 0, N, 0, K))
         assert bool((R == K).all())
+
+
+@pytest.mark.parametrize("body,dtype", [("discount", "f64"), ("gemm", "f64"), ("eqcount", "i32"),
+                                        ("boost", "f32"), ("gemm", "f32")])
+def test_empty_bounds_leave_r_untouched(gpu_ctx, body, dtype):
+    """Empty rectangles (no rows, no columns, or an empty k range) through
+    every entry and every tile variant: R keeps its prior value exactly
+    (tiled_executor.cpp:9-77 does nothing for an empty range), nothing is
+    launched with a zero grid."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 70, 96, 128  # aligned: every variant (TMA ones included) runs the non-empty cases
+    A, B, t, d = make_inputs(body, M, K, N, "int", seed=4)
+    R0 = np.random.default_rng(4).integers(-8, 9, (M, N)).astype(np.float64)
+    plan = gpu_ctx.plan(body, dtype)
+    ops = lambda R: P.Operands(dev(A, dtype), dev(B, dtype), R, dev(t, dtype), dev(d, dtype))  # noqa: E731
+    # (j0 = 7 / k0 = 31 offsets leave the operand views unaligned: an empty
+    # rectangle must not care)
+    empties = [P.Bounds(5, 5, 0, N, 0, K), P.Bounds(0, M, 7, 7, 0, K), P.Bounds(0, M, 0, N, 31, 31),
+               P.Bounds(0, 0, 0, 0, 0, 0)]
+    for b in empties:
+        for vi, v in enumerate(plan.variants()):
+            R = dev(R0, dtype)
+            P.run_subtask(plan, ops(R), P.TileParams(variant=vi), b)
+            assert np.array_equal(R.cpu().numpy().astype(np.float64), R0), (v.name, b)
+        R = dev(R0, dtype)
+        P.adaptive_execute(plan, ops(R), b)
+        assert np.array_equal(R.cpu().numpy().astype(np.float64), R0), ("adaptive", b)
+        hR = torch.from_numpy(R0.astype(NP_DT[dtype])).pin_memory()
+        hops = P.Operands(*(torch.from_numpy(np.ascontiguousarray(x).astype(NP_DT[dtype])).pin_memory()
+                            if x is not None else None for x in (A, B)), hR,
+                          *(torch.from_numpy(x.astype(NP_DT[dtype])).pin_memory() if x is not None else None
+                            for x in (t, d)))
+        P.run_host(plan, hops, b)
+        assert np.array_equal(hR.numpy().astype(np.float64), R0), ("run_host", b)

@@ -318,3 +318,18 @@ def test_sharded_group_dry_run_bands_and_plans():
                   P.Bounds(0, M, 0, 256, 0, 64), body="discount")
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("bounds", [(0, 70, 7, 7, 0, 96), (5, 5, 0, 128, 0, 96), (0, 70, 0, 128, 31, 31),
+                                    (0, 0, 0, 0, 0, 0)])
+def test_adaptive_on_an_empty_rectangle(dry_ctx, bounds):
+    """An empty rectangle takes the untuned path (autotuner.cpp:112-122):
+    no trials, tuned = false, its one coverage rectangle; the band sizing
+    must not divide by its zero column-tile count (it did: SIGFPE)."""
+    plan = dry_ctx.plan("discount", "f64")
+    M, K, N = 70, 96, 128
+    ops = P.Operands(np.zeros((M, K)), np.zeros((K, N)), np.zeros((M, N)), np.zeros(N), np.zeros(N))
+    rep = P.adaptive_execute(plan, ops, P.Bounds(*bounds))
+    i0, i1, j0, j1, k0, k1 = bounds
+    assert not rep.tuned and not rep.trials
+    assert [(c.i0, c.i1, c.j0, c.j1, c.k0, c.k1) for c in rep.coverage] == [bounds]
