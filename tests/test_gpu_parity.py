@@ -732,3 +732,46 @@ def test_empty_bounds_leave_r_untouched(gpu_ctx, body, dtype):
                             for x in (t, d)))
         P.run_host(plan, hops, b)
         assert np.array_equal(hR.numpy().astype(np.float64), R0), ("run_host", b)
+
+
+@pytest.mark.parametrize("stmt", ["+= A[i][k]*B[k][j] + u[i]*v[j] - (A[i][k] > s)*W[i][j]/4",
+                                  "= A[i][k]*B[k][j] - (A[i][k]*B[k][j] > thres[j])*A[i][k]*B[k][j]*dis[j]",
+                                  "+= A[i][k]*B[k][j]"])
+def test_empty_bounds_generated_assign_naive_host(gpu_ctx, stmt):
+    """Empty rectangles through a generated (NVRTC) body, an "=" statement
+    (last k wins), the per-element executor and the tuned host entry: R
+    keeps its prior value (R[j][j]-style views with unaligned offsets
+    included)."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    head = "where(i in [0..M] and j in [0..N] and k in [0..K]) {\n  R[i][j] "
+    plan = gpu_ctx.plan_source(head + stmt + ";\n}\n", "f64")
+    M, K, N = 40, 48, 64
+    rng = np.random.default_rng(9)
+    R0 = rng.integers(-8, 9, (M, N)).astype(np.float64)
+    names = plan.aux_names
+    aux_shape = {"u": (M,), "v": (N,), "s": (1, 1), "W": (M, N)}
+    named = {"thres": rng.integers(-8, 9, N).astype(np.float64), "dis": rng.integers(-8, 9, N).astype(np.float64)}
+    A = rng.integers(-8, 9, (M, K)).astype(np.float64)
+    B = rng.integers(-8, 9, (K, N)).astype(np.float64)
+
+    def operands(R, place):
+        aux = tuple(place(rng.integers(-8, 9, aux_shape[n]).astype(np.float64)) for n in names)
+        thres = place(named["thres"]) if "thres" in stmt else None
+        dis = place(named["dis"]) if "dis" in stmt else None
+        return P.Operands(place(A), place(B), R, thres, dis, aux=aux)
+
+    to_dev = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda()  # noqa: E731
+    to_host = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
+    for b in (P.Bounds(3, 3, 0, N, 0, K), P.Bounds(0, M, 5, 5, 0, K), P.Bounds(0, M, 0, N, 7, 7)):
+        R = to_dev(R0)
+        P.adaptive_execute(plan, operands(R, to_dev), b)
+        P.run_naive(plan, operands(R, to_dev), b)
+        for vi in range(len(plan.variants())):
+            P.run_subtask(plan, operands(R, to_dev), P.TileParams(variant=vi), b)
+        assert np.array_equal(R.cpu().numpy(), R0), (stmt, b)
+        hR = to_host(R0)
+        P.run_host_adaptive(plan, operands(hR, to_host), b)
+        assert np.array_equal(hR.numpy(), R0), ("host", stmt, b)
