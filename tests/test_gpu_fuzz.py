@@ -209,3 +209,72 @@ def test_random_real_data_within_tolerance(gpu_ctx, case):
                       P.Bounds(0, M, 0, N, 0, K))
     check(body, dtype, R.cpu().numpy(), want, A=A, B=B,
           what=f"case {case} {body}/{dtype} {M}x{K}x{N} mode {mode}")
+
+
+@pytest.mark.parametrize("case", range(36))
+def test_random_degenerate_and_banded(gpu_ctx, case):
+    """Bounds that may be empty in any dimension or a single row / column /
+    k, and tall tasks (M >= 1024) that take the host pipeline's row bands
+    (pinned R: zero-copy; pageable R: staged), through every entry; bit-exact
+    on IntValued data, R outside the bounds untouched."""
+    import torch
+
+    import paper_2305_08872_b200 as P
+
+    rng = np.random.default_rng(7000 + case)
+    body, dtype = [("discount", "f64"), ("gemm", "f64"), ("eqcount", "i32"), ("boost", "f32"),
+                   ("sqdiff", "f32"), ("gemm", "f32")][case % 6]
+    tall = case % 3 == 0
+    M = int(rng.integers(1024, 1600)) if tall else int(rng.integers(1, 120))
+    K, N = int(rng.integers(1, 300)), int(rng.integers(1, 200))
+
+    def extent(n):
+        a = int(rng.integers(0, n + 1))
+        kind = rng.integers(0, 4)
+        b = a if kind == 0 else min(n, a + 1) if kind == 1 else int(rng.integers(a, n + 1))
+        return a, b
+
+    (i0, i1), (j0, j1), (k0, k1) = extent(M), extent(N), extent(K)
+    if tall:
+        i0, i1 = 0, M  # the whole tall band (the banded pipeline needs M >= 1024 rows)
+    A = rng.integers(-8, 9, (M, K)).astype(np.float64)
+    B = rng.integers(-8, 9, (K, N)).astype(np.float64)
+    if body == "eqcount":
+        A, B = np.abs(A) % 5, np.abs(B) % 5
+    thres = rng.integers(-8, 9, N).astype(np.float64) if body in ("discount", "boost") else None
+    dis = rng.integers(-8, 9, N).astype(np.float64) if body == "discount" else None
+    R0 = rng.integers(-50, 50, (M, N)).astype(np.float64)
+    b = (i0, i1, j0, j1, k0, k1)
+    want = oracle(body, A, B, thres, dis, R0=R0, bounds=b)
+    npd = NP_DT[dtype]
+    plan = gpu_ctx.plan(body, dtype)
+    mode = int(rng.integers(0, 6))
+    host = mode >= 4 or tall and mode >= 2
+    if host:
+        pinned = mode != 5
+        cv = (lambda x: None if x is None else torch.from_numpy(x.astype(npd)).pin_memory()) if pinned else \
+            (lambda x: None if x is None else torch.from_numpy(x.astype(npd)))
+        R = cv(R0)
+        ops = P.Operands(cv(A), cv(B), R, cv(thres), cv(dis))
+        if mode % 2:
+            P.run_host_adaptive(plan, ops, P.Bounds(*b))
+        else:
+            P.run_host(plan, ops, P.Bounds(*b))
+        got = R.numpy().astype(np.float64)
+    else:
+        dv = lambda x: None if x is None else torch.from_numpy(x.astype(npd)).cuda()  # noqa: E731
+        R = dv(R0)
+        ops = P.Operands(dv(A), dv(B), R, dv(thres), dv(dis))
+        if mode == 0:
+            P.adaptive_execute(plan, ops, P.Bounds(*b))
+        elif mode == 1:
+            P.run_naive(plan, ops, P.Bounds(*b))
+        elif mode == 2:
+            P.run_subtask(plan, ops, P.TileParams(kc=int(rng.integers(1, 200))), P.Bounds(*b))
+        else:
+            P.run_subtask(plan, ops, P.TileParams(), P.Bounds(*b))
+        got = R.cpu().numpy().astype(np.float64)
+    bad = np.argwhere(got != want)
+    assert bad.size == 0, (f"case {case}: {body}/{dtype} {M}x{K}x{N} bounds {b} mode={mode}: "
+                           f"{len(bad)} mismatches, first {tuple(bad[0])} got {got[tuple(bad[0])]} "
+                           f"want {want[tuple(bad[0])]}")
