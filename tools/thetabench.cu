@@ -21,6 +21,8 @@ __device__ __forceinline__ unsigned lo(double x) { return static_cast<unsigned>(
 template <int FORM>
 __global__ void __launch_bounds__(384, 1) kern(double* out, const double* in, long long* cyc) {
     double a[TM], th[TN], x0[TN], x1[TN], acc[TM][TN];
+    double acc2[TM][TN] = {};
+    int cnt[TM][TN] = {};
     float ahf[TM], thf[TN];
     const int t = threadIdx.x;
 #pragma unroll
@@ -312,6 +314,34 @@ __global__ void __launch_bounds__(384, 1) kern(double* out, const double* in, lo
                 }
                 return;
             }
+            if constexpr (FORM == 38) {
+                // boost in theta form: acc += a * (m ? 2b : b) (2b = b with the
+                // exponent + 1: only the high word is selected) and a count of
+                // masked products (R = acc - count * t afterwards)
+#pragma unroll
+                for (int c = 0; c < TN; ++c)
+#pragma unroll
+                    for (int r = 0; r < TM; ++r) {
+                        const bool m = la[r] > lth[c];
+                        const double s = __hiloint2double(static_cast<int>(m ? hi(lx1[c]) : hi(lx0[c])),
+                                                          static_cast<int>(lo(lx0[c])));
+                        acc[r][c] = __fma_rn(la[r], s, acc[r][c]);
+                        cnt[r][c] += m ? 1 : 0;
+                    }
+                return;
+            }
+            if constexpr (FORM == 39) {
+                // boost as shipped (|u| form): acc0 += a b, u = a b - t, acc1 += |u|
+#pragma unroll
+                for (int c = 0; c < TN; ++c)
+#pragma unroll
+                    for (int r = 0; r < TM; ++r) {
+                        acc[r][c] = __fma_rn(la[r], lx0[c], acc[r][c]);
+                        const double u = __fma_rn(la[r], lx0[c], -lth[c]);
+                        acc2[r][c] = __dadd_rn(acc2[r][c], fabs(u));
+                    }
+                return;
+            }
             if constexpr (FORM == 12) {
 #pragma unroll
                 for (int c = 0; c < TN; ++c)
@@ -420,7 +450,7 @@ __global__ void __launch_bounds__(384, 1) kern(double* out, const double* in, lo
 #pragma unroll
     for (int r = 0; r < TM; ++r)
 #pragma unroll
-        for (int c = 0; c < TN; ++c) s += acc[r][c];
+        for (int c = 0; c < TN; ++c) s += acc[r][c] + acc2[r][c] + cnt[r][c];
     if (s == 1234.5) out[t] = s;
     if (t == 0) cyc[blockIdx.x] = c1 - c0;
 }
@@ -475,6 +505,8 @@ int main() {
         run<35>(sms, blk, "35 col 3 I", out, in, cyc);
         run<36>(sms, blk, "36 cols 2-3 I", out, in, cyc);
         run<37>(sms, blk, "37 col 1 I, col 3 Y", out, in, cyc);
+        run<38>(sms, blk, "38 boost theta form (DSETP, FSEL hi, DFMA, count)", out, in, cyc);
+        run<39>(sms, blk, "39 boost |u| form as shipped (2 DFMA + DADD)", out, in, cyc);
         if (getenv("ALLFORMS")) {
         run<18>(sms, blk, "18 P3: ISETP hi + DFMA x0 + @P DFMA d", out, in, cyc);
         run<19>(sms, blk, "19 P3 grouped per column (PTX)", out, in, cyc);
