@@ -155,9 +155,10 @@ typedef struct {
 
 /* TileParams (tiled_executor.hpp:11-15) on the GPU:
  *   kc      K-segment depth. kc <= 0 or kc >= K: one pass over K. Otherwise
- *           the K range is cut into ceil(K/kc) segments computed in parallel
- *           (split-K) and added to R in ascending segment order
- *           (deterministic), the GPU form of the reference's kc loop.
+ *           kc is rounded up to a multiple of 16 and the K range is cut
+ *           into ceil(K/kc) segments computed in parallel (split-K) and added
+ *           to R in ascending segment order (deterministic), the GPU form of
+ *           the reference's kc loop.
  *   nc      column-tile width: picks the registered tile variant whose CTA
  *           width is the largest <= nc (nc <= 0: planner default).
  *   pack    accepted for interface parity; operands are always staged

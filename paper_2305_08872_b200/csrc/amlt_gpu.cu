@@ -537,9 +537,11 @@ Dispatch plan_dispatch(const amlt_ctx* ctx, const amlt_plan* plan, const amlt_ti
     if (tile && tile->kc > 0 && tile->kc < rv.K && (!vdesc(dp.variant).run || vdesc(dp.variant).splittable)) {
         // (variants with their own staging run the whole K range unless they
         // take K segments)
-        // Segment starts stay multiples of 32 elements so every segment's
-        // operand rows keep the 16-byte alignment the staged copies need.
-        const int64_t kc = (tile->kc + 31) / 32 * 32;
+        // Segment starts stay multiples of 16 elements (one f64 k-tile, half
+        // an f32 one) so every segment's operand rows keep the 16-byte
+        // alignment the staged copies need and packed operands (4 k per
+        // word) stay whole.
+        const int64_t kc = (tile->kc + 15) / 16 * 16;
         dp.splits = static_cast<int>((rv.K + kc - 1) / kc);
         dp.kslice = kc;
         if (dp.splits > 65535) fail(AMLT_ERR_INVALID_ARGUMENT, "kc too small: more than 65535 K segments");
@@ -849,7 +851,7 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
             for (int64_t splits : counts) {
                 splits = std::min<int64_t>(splits, whole.K / 128);
                 if (splits < 2) continue;
-                const int64_t kc = ((whole.K + splits - 1) / splits + 31) / 32 * 32;
+                const int64_t kc = ((whole.K + splits - 1) / splits + 15) / 16 * 16;
                 if (std::find(kcs.begin(), kcs.end(), kc) == kcs.end()) kcs.push_back(kc);
             }
             for (int64_t kc : kcs) trials.push_back({v, kc});
@@ -1007,7 +1009,7 @@ void adaptive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops, co
             const int64_t slots = int64_t(ctx->num_sms) * occ;
             if (ctas > 0 && ctas < slots && whole.K >= 512) {
                 int64_t splits = std::min<int64_t>((slots + ctas - 1) / ctas, whole.K / 256);
-                if (splits > 1) kc = ((whole.K + splits - 1) / splits + 31) / 32 * 32;
+                if (splits > 1) kc = ((whole.K + splits - 1) / splits + 15) / 16 * 16;
             }
         }
         rep->best_variant = v >= 0 ? plan_local_index(plan, v) : -1;

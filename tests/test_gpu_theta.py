@@ -234,7 +234,7 @@ def test_theta_split_k_bit_exact(gpu_ctx, kc):
         log = P.ExecLog(capacity=8)
         P.run_subtask(plan, P.Operands(dev(A), dev(B), R, dev(t), dev(d)), P.TileParams(kc=kc, variant=vi),
                       P.Bounds(*b), log=log)
-        assert log.records[0].splits == (936 + (kc + 31) // 32 * 32 - 1) // ((kc + 31) // 32 * 32)
+        assert log.records[0].splits == (936 + (kc + 15) // 16 * 16 - 1) // ((kc + 15) // 16 * 16)
         check("discount", "f64", R.cpu().numpy(), want, exact=True, what=f"{name} kc={kc}")
 
 
