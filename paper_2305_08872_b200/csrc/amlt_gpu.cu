@@ -871,9 +871,12 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
         else ensure_tc_ws(ctx, vdesc(dp.variant), rs.kp);
         // two runs, the faster scored: the first can pay one-off costs (cold
         // instruction cache, first launch of the kernel) the cached winner
-        // never pays again; both are charged to the call
+        // never pays again; all are charged to the call. Sub-millisecond
+        // tasks take five: their candidates sit within a few percent of each
+        // other (config 0), and two runs let launch jitter pick the winner.
         float ms = 0, ms_sum = 0;
-        for (int rep = 0; rep < 2; ++rep) {
+        int reps = 2;
+        for (int rep = 0; rep < reps; ++rep) {
             cuda_check(cudaEventRecord(ctx->ev0, ctx->stream), "cudaEventRecord");
             enqueue(ctx, plan, rs, dp);
             cuda_check(cudaEventRecord(ctx->ev1, ctx->stream), "cudaEventRecord");
@@ -882,6 +885,7 @@ void scratch_tune(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops
             cuda_check(cudaEventElapsedTime(&one, ctx->ev0, ctx->ev1), "cudaEventElapsedTime");
             ms = rep == 0 ? one : std::min(ms, one);
             ms_sum += one;
+            if (rep == 0 && one < 1.0f) reps = 5;
         }
         // the whole task: its B preparation is part of every call
         const double el = ms * 1e-3 + (rs.packed() ? 0.0 : prep_seconds(ctx, vdesc(dp.variant)));

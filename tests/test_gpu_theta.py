@@ -279,5 +279,7 @@ def test_scratch_trials_are_charged(gpu_ctx):
     rep = P.adaptive_execute(plan, P.Operands(dev(A), dev(B), R, dev(t), dev(d)), P.Bounds(0, M, 0, N, 0, K))
     assert rep.scratch_tuned and rep.tuning_fraction == 0.0
     trials = sum(tr.elapsed for tr in rep.trials)
-    assert trials <= rep.tuning_seconds <= 2.5 * trials  # each candidate runs twice, the faster scored
+    # each candidate runs twice (five times for sub-millisecond tasks, as
+    # here), the fastest scored; every run is charged
+    assert trials <= rep.tuning_seconds <= 6.0 * trials
     assert rep.total_seconds > rep.tuning_seconds
