@@ -542,6 +542,9 @@ def main():
                          "used to pin the tuned winner under ncu, whose serialised launches "
                          "change the trial timings")
     ap.add_argument("--kc", type=int, default=0, help="with --tile: the K-segment depth (split-K)")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="value leg: plain enqueue per step instead of replaying the step from a "
+                         "CUDA graph (amlt_gpu_graph_capture)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-verify", action="store_true")
@@ -688,6 +691,15 @@ def main():
     variants = plan.variants()
     win_name = variants[win.variant].name if win.variant is not None and win.variant >= 0 else ""
     split = bool(last and last.best_kc < K)
+    # the step as a CUDA graph: every kernel of it, replayed with no
+    # per-launch host work (the capture runs one plain step first)
+    graph = None
+    if not args.no_graph:
+        try:
+            graph = P.capture_graph(plan, ops, win, bounds)
+        except P.EngineError as e:
+            log(f"bench.py: graph capture failed ({e}); timing plain enqueues")
+    step_launch = "cuda-graph replay" if graph is not None else "enqueue"
     barrier()
     torch.cuda.synchronize()
     sampler.start()
@@ -700,7 +712,10 @@ def main():
         if flush:
             flush_buf.zero_()  # evict L2 (outside the step's events)
         ev[s][0].record(stream)
-        P.enqueue(plan, ops, win, bounds)
+        if graph is not None:
+            graph.launch()
+        else:
+            P.enqueue(plan, ops, win, bounds)
         ev[s][1].record(stream)
         launches += launches_of(win_name, split)
     t1.record(stream)
@@ -772,6 +787,9 @@ def main():
         e_B = B[:, cdx].double().cpu().numpy()
         e_th = th[cdx].double().cpu().numpy() if th is not None else None
         e_ds = ds[cdx].double().cpu().numpy() if ds is not None else None
+        if graph is not None:
+            graph.close()  # (it holds the value leg's operands)
+            graph = None
         del A, B, R, ops
         torch.cuda.empty_cache()
         bcast = ws > 1
@@ -891,6 +909,7 @@ def main():
                               if flush else "inputs larger than L2 (no flush)"),
                        "tile": tile,
                        "split_k_kc": win.kc or None,
+                       "step_launch": step_launch,
                        "tuning": ("pinned by --tile" if args.tile else
                                   "row-band trials" if tuned and tuned.tuned else
                                   "whole-task trials on scratch R" if tuned and tuned.scratch_tuned

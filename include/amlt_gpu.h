@@ -363,6 +363,21 @@ amlt_status amlt_gpu_run_naive(amlt_ctx* ctx, const amlt_plan* plan, const amlt_
 amlt_status amlt_gpu_enqueue(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops,
                              const amlt_tile_params* tile, const amlt_bounds* bounds);
 
+/* One enqueue of (plan, ops, tile, bounds) captured into a CUDA graph on the
+ * context's stream, for repeated identical steps (launch-bound small tasks:
+ * the graph replays every kernel of the step, preparation and split-K
+ * reduction included, with no per-launch host work). The operand pointers,
+ * shapes and the chosen variant are fixed at capture; amlt_gpu_graph_launch
+ * enqueues a replay on the context's current stream and fails with
+ * AMLT_ERR_INVALID_ARGUMENT if the context's workspaces were reallocated
+ * since the capture (capture again then). */
+typedef struct amlt_graph amlt_graph;
+amlt_status amlt_gpu_graph_capture(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops,
+                                   const amlt_tile_params* tile, const amlt_bounds* bounds,
+                                   amlt_graph** out);
+amlt_status amlt_gpu_graph_launch(amlt_graph* graph);
+void amlt_gpu_graph_destroy(amlt_graph* graph);
+
 /* adaptive_execute: measured choice of the tile variant on row bands of the
  * real task (each band contributes its rows of R; coverage exactly once),
  * then the remainder with the winner. */

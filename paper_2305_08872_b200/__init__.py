@@ -12,7 +12,7 @@ from .engine import (Bounds, Clock, Context, CoverRect, EngineError, ExecLog, Ex
                      NonPositiveTime, Operands, SteadyClock, TileParams, Trial, TuneReport,
                      UnsupportedExpression, adaptive_execute, bounds_of, enqueue, operands_of,
                      run_adaptive, run_fixed, run_host, run_host_adaptive, run_naive, run_subtask,
-                     Shape, ShardedGroup, spr)
+                     Shape, ShardedGroup, spr, Graph, capture_graph)
 from .task import TaskPlan, compile_task  # noqa: F401
 from .taskdata import (TaskData, VerifyResult, bind_dims, load_operand_file,  # noqa: F401
                        make_task_data, verify_against_naive)

@@ -145,7 +145,7 @@ EXPORTS = [
     "amlt_gpu_comm_unique_id", "amlt_gpu_comm_attach", "amlt_gpu_comm_detach", "amlt_gpu_comm_size",
     "amlt_gpu_last_host_layout",
     "amlt_sharded_create", "amlt_sharded_destroy", "amlt_sharded_run", "amlt_sharded_size",
-    "amlt_sharded_last_error",
+    "amlt_sharded_last_error", "amlt_gpu_graph_capture", "amlt_gpu_graph_launch", "amlt_gpu_graph_destroy",
 ]
 HOST_LAYOUT_FIELDS = 7
 HOST_R_ZERO = 1
@@ -188,6 +188,11 @@ def lib():
                                       C.POINTER(C.c_double)]
     L.amlt_gpu_enqueue.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(TileParamsC),
                                    C.POINTER(BoundsC)]
+    L.amlt_gpu_graph_capture.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(TileParamsC),
+                                         C.POINTER(BoundsC), C.POINTER(P)]
+    L.amlt_gpu_graph_launch.argtypes = [P]
+    L.amlt_gpu_graph_destroy.argtypes = [P]
+    L.amlt_gpu_graph_destroy.restype = None
     L.amlt_gpu_adaptive_execute.argtypes = [P, P, C.POINTER(OperandsC), C.POINTER(BoundsC),
                                             C.c_int, CLOCK_FN, P, C.POINTER(ExecLogC),
                                             C.POINTER(TuneReportC)]

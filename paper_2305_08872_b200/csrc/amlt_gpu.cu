@@ -2207,6 +2207,74 @@ amlt_status amlt_gpu_enqueue(amlt_ctx* ctx, const amlt_plan* plan, const amlt_op
     });
 }
 
+struct amlt_graph {
+    amlt_ctx* ctx = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    // the workspaces baked into the graph's kernel parameters
+    void* work = nullptr;
+    void* tc_ws = nullptr;
+    void* pack_ws = nullptr;
+};
+
+amlt_status amlt_gpu_graph_capture(amlt_ctx* ctx, const amlt_plan* plan, const amlt_operands* ops,
+                                   const amlt_tile_params* tile, const amlt_bounds* bounds,
+                                   amlt_graph** out) {
+    if (!ctx || !plan || !out) return AMLT_ERR_INVALID_ARGUMENT;
+    *out = nullptr;
+    return guarded(ctx, [&] {
+        if (ctx->dry()) fail(AMLT_ERR_NO_DEVICE, "amlt_gpu_graph_capture needs a device context");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        Resolved rv = resolve(plan, ops, bounds);
+        Dispatch dp = plan_dispatch(ctx, plan, tile, rv);
+        // one plain step first: every workspace the step needs is allocated
+        // (no allocation may happen inside the capture)
+        enqueue(ctx, plan, rv, dp);
+        cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+        ++ctx->call_gen;  // the captured step prepares its own B, as every enqueue does
+        cudaGraph_t graph = nullptr;
+        cuda_check(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal),
+                   "cudaStreamBeginCapture");
+        try {
+            enqueue(ctx, plan, rv, dp);
+        } catch (...) {
+            cudaGraph_t g = nullptr;
+            (void)cudaStreamEndCapture(ctx->stream, &g);
+            if (g) cudaGraphDestroy(g);
+            (void)cudaGetLastError();
+            throw;
+        }
+        cuda_check(cudaStreamEndCapture(ctx->stream, &graph), "cudaStreamEndCapture");
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t e = cudaGraphInstantiate(&exec, graph, 0);
+        cudaGraphDestroy(graph);
+        cuda_check(e, "cudaGraphInstantiate");
+        auto* g = new amlt_graph;
+        g->ctx = ctx;
+        g->exec = exec;
+        g->work = ctx->work;
+        g->tc_ws = ctx->tc_ws;
+        g->pack_ws = ctx->pack_ws;
+        *out = g;
+    });
+}
+
+amlt_status amlt_gpu_graph_launch(amlt_graph* g) {
+    if (!g || !g->ctx) return AMLT_ERR_INVALID_ARGUMENT;
+    amlt_ctx* ctx = g->ctx;
+    return guarded(ctx, [&] {
+        if (ctx->work != g->work || ctx->tc_ws != g->tc_ws || ctx->pack_ws != g->pack_ws)
+            fail(AMLT_ERR_INVALID_ARGUMENT,
+                 "graph invalidated: the context's workspaces were reallocated after the capture");
+        cuda_check(cudaGraphLaunch(g->exec, ctx->stream), "cudaGraphLaunch");
+    });
+}
+
+void amlt_gpu_graph_destroy(amlt_graph* g) {
+    if (!g) return;
+    if (g->exec) cudaGraphExecDestroy(g->exec);
+    delete g;
+}
+
 amlt_status amlt_gpu_adaptive_execute(amlt_ctx* ctx, const amlt_plan* plan,
                                       const amlt_operands* ops, const amlt_bounds* bounds,
                                       int pack, amlt_clock_fn clock, void* clock_user,

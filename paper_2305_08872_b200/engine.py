@@ -563,6 +563,44 @@ def enqueue(plan: GpuPlan, ops: Operands, params: TileParams, bounds: Bounds) ->
                                      C.byref(bc)), ctx.handle)
 
 
+class Graph:
+    """One enqueue of (plan, ops, params, bounds) captured into a CUDA graph
+    (amlt_gpu_graph_capture): launch() replays every kernel of the step on
+    the context's current stream with no per-launch host work. The operands
+    (pointers and shapes) and the variant are fixed at capture."""
+
+    def __init__(self, plan: GpuPlan, ops: Operands, params: TileParams, bounds: Bounds):
+        self.plan = plan
+        self._ops = ops  # keeps the operand tensors alive while the graph exists
+        ctx = plan.ctx
+        oc = ops._c(True)
+        tp = params._c() if params is not None else TileParams()._c()
+        bc = bounds._c()
+        h = C.c_void_p()
+        _raise(ctx._lib.amlt_gpu_graph_capture(ctx.handle, plan.handle, C.byref(oc), C.byref(tp),
+                                               C.byref(bc), C.byref(h)), ctx.handle)
+        self.handle = h
+
+    def launch(self) -> None:
+        _raise(self.plan.ctx._lib.amlt_gpu_graph_launch(self.handle), self.plan.ctx.handle)
+
+    def close(self) -> None:
+        if self.handle:
+            self.plan.ctx._lib.amlt_gpu_graph_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 (interpreter shutdown)
+            pass
+
+
+def capture_graph(plan: GpuPlan, ops: Operands, params: TileParams, bounds: Bounds) -> Graph:
+    """amlt_gpu_graph_capture: the step enqueue() would run, as a CUDA graph."""
+    return Graph(plan, ops, params, bounds)
+
+
 def _report(rc: N.TuneReportC) -> TuneReport:
     rep = TuneReport()
     rep.trials = [Trial(rc.trials[i].value, rc.trials[i].rows, rc.trials[i].elapsed,

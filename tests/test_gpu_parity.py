@@ -775,3 +775,53 @@ def test_empty_bounds_generated_assign_naive_host(gpu_ctx, stmt):
         hR = to_host(R0)
         P.run_host_adaptive(plan, operands(hR, to_host), b)
         assert np.array_equal(hR.numpy(), R0), ("host", stmt, b)
+
+
+@pytest.mark.parametrize("body,dtype,variant,kc", [
+    ("discount", "f64", "discount_f64_48x128_theta_t6x4_w8x1", 208),  # B preparation + split-K reduce
+    ("discount", "f64", "discount_f64_32x128_t4x4_w8x1", 0),
+    ("gemm", "f32", "gemm_f32_128x256_tcgen05_3xtf32", 0),  # operand split pre-pass
+    ("eqcount", "i32", "eqcount_i32_32x128_swar_t4x4_w8x1", 0),  # packing pre-pass + guarded pair
+    ("gemm", "f64", "gemm_f64_64x128_dmma_w32x32_c2x4", 256)])
+def test_graph_replay_matches_enqueue(gpu_ctx, body, dtype, variant, kc):
+    """amlt_gpu_graph_capture: a captured step replayed N times gives what N
+    plain enqueues give (bit-exact on IntValued data), and a launch after the
+    context's workspaces were reallocated is refused, not run on freed
+    memory."""
+    import paper_2305_08872_b200 as P
+
+    M, K, N = 300, 1024, 520
+    A, B, t, d = make_inputs(body, M, K, N, "int", seed=12)
+    if body == "eqcount":
+        A, B = np.abs(A), np.abs(B)
+    plan = gpu_ctx.plan(body, dtype)
+    vi = [v.name for v in plan.variants()].index(variant)
+    tp = P.TileParams(kc=kc, variant=vi)
+    bnd = P.Bounds(0, M, 0, N, 0, K)
+    R1, R2 = dev(np.zeros((M, N)), dtype), dev(np.zeros((M, N)), dtype)
+    ops1 = P.Operands(dev(A, dtype), dev(B, dtype), R1, dev(t, dtype), dev(d, dtype))
+    ops2 = P.Operands(ops1.a, ops1.b, R2, ops1.thres, ops1.dis)
+    g = P.capture_graph(plan, ops2, tp, bnd)  # runs one plain step on R2 first
+    for _ in range(3):
+        P.enqueue(plan, ops1, tp, bnd)
+        g.launch()
+    P.enqueue(plan, ops1, tp, bnd)  # R1: 4 steps, R2: 1 (capture) + 3 replays
+    got1, got2 = R1.cpu().numpy(), R2.cpu().numpy()
+    assert np.array_equal(got1, got2), variant
+    want = oracle(body, A, B, t, d)
+    check(body, dtype, got2 / 4, want, exact=True, what=f"graph {variant}")
+    # workspaces reallocated (a bigger split-K / preparation need): refused
+    big = 4 * M
+    Ab = np.tile(A, (4, 1))
+    Rb = dev(np.zeros((big, N)), dtype)
+    P.run_subtask(plan, P.Operands(dev(Ab, dtype), ops1.b, Rb, ops1.thres, ops1.dis),
+                  P.TileParams(kc=64, variant=vi), P.Bounds(0, big, 0, N, 0, K))
+    gpu_ctx_ws_grew = True
+    try:
+        g.launch()
+        gpu_ctx_ws_grew = False  # nothing was reallocated: the replay is still valid
+    except P.EngineError as e:
+        assert "reallocated" in str(e)
+    if not gpu_ctx_ws_grew:
+        assert np.array_equal(R2.cpu().numpy(), got2 + got2 / 4)
+    g.close()
