@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define AMLT_GPU_ABI_VERSION 3
+#define AMLT_GPU_ABI_VERSION 4
 
 /* Aux arrays one generated (AMLT_BODY_GENERIC) statement may name. */
 #define AMLT_MAX_AUX 8
@@ -251,6 +251,13 @@ typedef struct {
     double tuning_seconds;                    /* of which whole-task trials on
                                                  the scratch R (work redone
                                                  for the real R afterwards) */
+    int32_t refined;                          /* row-band tuning whose bands
+                                                 were shorter than 8 waves: the
+                                                 best `refined` candidates ran
+                                                 one more 8-wave band each (the
+                                                 last `refined` trials), and
+                                                 the best of THOSE won; 0:
+                                                 the argmin of all trials won */
 } amlt_tune_report;
 
 typedef struct amlt_ctx amlt_ctx;

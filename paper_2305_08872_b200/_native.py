@@ -12,7 +12,7 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "lib", "libamlt_gpu.so")
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 MAX_AUX = 8
 
 # amlt_status
@@ -92,7 +92,7 @@ class TuneReportC(C.Structure):
                 ("best_variant", C.c_int32), ("best_kc", C.c_int64), ("tuned", C.c_int32),
                 ("from_cache", C.c_int32), ("scratch_tuned", C.c_int32), ("n_cover", C.c_int32),
                 ("coverage", CoverRectC * MAX_COVER), ("tuning_fraction", C.c_double),
-                ("total_seconds", C.c_double), ("tuning_seconds", C.c_double)]
+                ("total_seconds", C.c_double), ("tuning_seconds", C.c_double), ("refined", C.c_int32)]
 
 
 MAX_REF_TRIALS = 64

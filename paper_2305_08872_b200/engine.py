@@ -225,6 +225,7 @@ class TuneReport:
     tuning_fraction: float = 0.0
     total_seconds: float = 0.0
     tuning_seconds: float = 0.0  # whole-task trials on the scratch R (included in total_seconds)
+    refined: int = 0  # > 0: the winner is the best of the last `refined` (8-wave) trials
 
 
 @dataclass
@@ -615,6 +616,7 @@ def _report(rc: N.TuneReportC) -> TuneReport:
     rep.tuning_fraction = rc.tuning_fraction
     rep.total_seconds = rc.total_seconds
     rep.tuning_seconds = rc.tuning_seconds
+    rep.refined = rc.refined
     return rep
 
 
