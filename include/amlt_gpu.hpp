@@ -138,6 +138,7 @@ struct TuneReport {
     double tuning_fraction = 0.0;
     double total_seconds = 0.0;
     double tuning_seconds = 0.0;  // scratch (whole-task) trials, included in total_seconds
+    int refined = 0;              // > 0: the winner is the best of the last `refined` (8-wave) trials
 };
 
 // A MatrixBuffer-like view (device memory for run_subtask / adaptive_execute,
@@ -309,6 +310,7 @@ inline TuneReport adaptive_execute(const Plan& plan, const Operands& ops, const 
     rep.tuning_fraction = r.tuning_fraction;
     rep.total_seconds = r.total_seconds;
     rep.tuning_seconds = r.tuning_seconds;
+    rep.refined = r.refined;
     return rep;
 }
 
@@ -325,6 +327,7 @@ inline TuneReport report_of(const amlt_tune_report& r) {
     rep.tuning_fraction = r.tuning_fraction;
     rep.total_seconds = r.total_seconds;
     rep.tuning_seconds = r.tuning_seconds;
+    rep.refined = r.refined;
     return rep;
 }
 }  // namespace detail
