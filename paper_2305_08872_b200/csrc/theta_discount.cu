@@ -116,7 +116,7 @@ __device__ __forceinline__ bool pred(double x, double b, double t) {
 // pred, so the maximum found is the same double up to the sign of a zero,
 // which no compare a > theta can tell apart).
 __device__ double theta_of(double b, double t) {
-    double x = __ddiv_rn(t, b);
+    double x = __dmul_rn(t, __drcp_rn(b));  // within ~2 ulps of t / b: the walk finishes it
     if (x != x) x = 0.0;
     long long kx = okey(x);
 #pragma unroll 1
